@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the BP message-scheduling hot path (BASELINE.json configs[1]).
+
+Workload ("step"): one complete bpsched::run (schedulers.cpp:293-353) of RnBP
+(low_p 0.5, high_p 1.0, EdgeRatio threshold 0.9, epsilon 1e-5, 10,000-iteration
+cap) on the 1000 x 1000 Ising grid, C = 2.5, generated bit-identically to the
+reference's generate_ising (seed = step index + rank * 1000).
+
+  value  = committed edge-message updates / second (sum |F| / device time of the
+           runs, graph resident in HBM, CUDA events on the engine stream)
+  e2e    = the same metric through the public API with host buffers: every step
+           uploads the graph from host arrays (bp_graph_create: validation, CSR,
+           H2D), runs, and copies the beliefs back (D2H)
+
+Other schedulers (LBP, RBP p=1/256) on the same instance, the 100^2 C=2.5
+convergence suite (seeds 500-524) and an HBM-bound 4096^2 LBP sweep are
+reported as extra keys.  The reference arm (--impl reference) times the
+reference's own bpsched::run compiled from /root/reference (oracle/_ref) on the
+host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GRID = 1000
+C_COUPLING = 2.5
+CAP = 10000
+METRIC = "edge-message updates/sec (RnBP, Ising 1000x1000 C=2.5, run to convergence or 10k-iteration cap)"
+UNIT = "updates/s"
+REF_SAMPLE_ITERS = 5  # bounded CPU sample: reference run capped at 5 iterations
+
+
+def rnbp_kw(seed):
+    return dict(low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5, max_iterations=CAP,
+                time_limit=1e9, seed=seed)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 8:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].strip() == "Active"})
+        loaded = [x for x in sm if mx and x > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def flush_l2(torch, buf):
+    buf.zero_()  # 256 MiB > 126 MB L2
+    torch.cuda.synchronize()
+
+
+# bytes moved by one vertex-update launch per processed vertex / incident edge
+# (binary log-odds layout): in_off(8) + unary(4) per vertex;
+# per incident edge adj(4) + pair(8) + params(16) + candidate write(4) +
+# residual read+write(8) [LBP sweep: no residual traffic, message write(4)]
+def update_bytes(visits, evals, with_res=True):
+    return 12 * visits + (40 if with_res else 32) * evals
+
+
+def run_b200(args):
+    import torch
+
+    import paper_1909_11469_b200 as bp
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    K, W = args.steps, args.warmup
+
+    graphs = {}
+
+    def graph_for(seed):
+        if seed not in graphs:
+            graphs[seed] = bp.generate_ising(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=seed), device=local)
+        return graphs[seed]
+
+    seeds = [rank * 1000 + s for s in range(K)]
+    for s in seeds:
+        graph_for(s)
+    kind = bp.SchedulerKind.rnbp
+    # warmup
+    for w in range(W):
+        bp.run(graph_for(seeds[w % K]), bp.SchedulerConfig(kind=kind, **rnbp_kw(seeds[w % K])))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    results = []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        dev_ms = 0.0
+        for i, s in enumerate(seeds):
+            flush_l2(torch, flush)
+            r = bp.run(graph_for(s), bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
+            dev_ms += r.device_ms
+            results.append(r)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if dist:
+        dist.barrier()
+    updates = sum(r.messages_updated_total for r in results)
+    t_dev = dev_ms / 1e3
+    if dist:
+        tt = torch.tensor([t_dev, float(updates)], dtype=torch.float64, device="cuda")
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        t_dev = float(mx[0])
+        updates = float(tt[1])
+    value = updates / t_dev
+    ms_per_step = t_dev / K * 1e3
+    launches = sum(r.gpu_launches for r in results)
+
+    # ---- e2e: public API with host buffers (graph upload + run + beliefs D2H)
+    e2e_updates, e2e_t = 0, 0.0
+    h2d = d2h = 0
+    host_arrays = {}
+    for s in seeds[: min(K, 3)]:
+        host_arrays[s] = bp.generate_ising_arrays(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=s))
+    for s in seeds[: min(K, 3)]:
+        cards, un, ep, tb = host_arrays[s]
+        flush_l2(torch, flush)
+        t1 = time.perf_counter()
+        g = bp.PairwiseMRF.from_arrays(cards, un, ep, tb, device=local)
+        r = bp.run(g, bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
+        _ = r.beliefs.values.sum()
+        e2e_t += time.perf_counter() - t1
+        e2e_updates += r.messages_updated_total
+        h2d = cards.nbytes + un.nbytes + ep.nbytes + tb.nbytes
+        d2h = r.beliefs.values.nbytes + 32 * len(r.trace)
+        del g
+
+    out = {}
+    if rank == 0:
+        # ---- roofline of the dominant kernel (instrumented run after the timed region)
+        peak, peak_kind = measured_peaks()
+        g0 = graph_for(seeds[0])
+        ri = bp.run_ex(g0, bp.SchedulerConfig(kind=kind, **rnbp_kw(seeds[0])), kernel_timing=True)
+        ks = ri.kernel_stats
+        dom = max(ks, key=lambda k: ks[k]["ms"])
+        upd_bytes = update_bytes(ri.vertex_visits, ri.message_evaluations)
+        upd_ms = ks["update"]["ms"]
+        achieved = upd_bytes / (upd_ms / 1e3) / 1e9 if upd_ms else 0.0
+        traffic = _read_traffic()
+        shares = {k: round(v["ms"] / sum(x["ms"] for x in ks.values()), 4) for k, v in ks.items() if v["launches"]}
+
+        # ---- HBM-bound reference point: LBP sweeps on a 4096^2 grid (working set >> L2)
+        g4 = bp.generate_ising(bp.IsingParams(n=4096, c=C_COUPLING, seed=0), device=local)
+        r4 = bp.run_ex(g4, bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=20), kernel_timing=True)
+        k4 = r4.kernel_stats["update"]
+        b4 = update_bytes(r4.vertex_visits, r4.message_evaluations, with_res=False)
+        hbm_ach = b4 / (k4["ms"] / 1e3) / 1e9
+        del g4
+
+        # ---- other schedulers on the workload instance + convergence suite
+        extra = {}
+        for name, cfg in (("lbp", bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=CAP, time_limit=1e9)),
+                          ("rbp", bp.SchedulerConfig(kind=bp.SchedulerKind.rbp, p=1 / 256, max_iterations=CAP,
+                                                     time_limit=1e9))):
+            bp.run(g0, cfg)
+            rr = bp.run(g0, cfg)
+            extra[name] = {"value": rr.messages_updated_total / (rr.device_ms / 1e3), "unit": UNIT,
+                           "iterations": rr.iterations, "converged": rr.converged,
+                           "ms": round(rr.device_ms, 3)}
+        suite = _convergence_suite(bp, local)
+
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (log-domain messages)", "data": "synthetic (generate_ising, bit-identical to the reference generator)",
+            "config": {"workload": "ising1000_c2.5_rnbp", "n": N_GRID, "c": C_COUPLING, "scheduler": "rnbp",
+                       "low_p": 0.5, "high_p": 1.0, "edge_ratio_threshold": 0.9, "epsilon": 1e-5,
+                       "max_iterations": CAP, "seeds": f"{seeds[0]}..{seeds[-1]}",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "steps_detail": [{"seed": s, "converged": r.converged, "iterations": r.iterations,
+                              "updates": r.messages_updated_total, "ms": round(r.device_ms, 3)}
+                             for s, r in zip(seeds, results)],
+            "time_to_convergence_s": _ttc(results),
+            "wall_s": wall,
+            "gpu_launches": launches,
+            "e2e": {"value": e2e_updates / e2e_t if e2e_t else None, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": min(K, 3),
+                    "includes": "bp_graph_create from host arrays (validation + CSR + H2D) + run + beliefs D2H"},
+            "roofline": {"bound": "hbm", "kernel": "k_vertex_update (refresh)", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_kind, "algorithmic_bytes": upd_bytes, "kernel_ms": upd_ms,
+                         "launches": ks["update"]["launches"], "dominant_kernel_class": dom,
+                         "kernel_shares": shares,
+                         "note": "1000^2 working set (~100 MB) is L2-resident; roofline_hbm is the HBM-bound point"},
+            "roofline_hbm": {"kernel": "k_vertex_update (LBP sweep) on Ising 4096^2", "achieved": hbm_ach,
+                             "peak": peak, "unit": "GB/s", "frac": hbm_ach / peak, "algorithmic_bytes": b4,
+                             "kernel_ms": k4["ms"], "launches": k4["launches"],
+                             "updates_per_s": r4.messages_updated_total / (k4["ms"] / 1e3)},
+            "schedulers": extra,
+            "convergence_suite_100x100": suite,
+            "clocks": clk.summary(),
+        }
+        if ws == 1:
+            out["cpu_baseline"] = _cpu_baseline(sample_iters=REF_SAMPLE_ITERS)
+        print(json.dumps(out))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _ttc(results):
+    conv = [r.wall_time for r in results if r.converged]
+    return {"converged_steps": len(conv), "steps": len(results),
+            "median_s": statistics.median(conv) if conv else None}
+
+
+def _read_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def _convergence_suite(bp, device):
+    """BASELINE config 1: Ising 100^2 C=2.5, seeds 500-524, eps 1e-5, cap 10k."""
+    out = {}
+    for name, cfg_kw in (("lbp", dict(kind=bp.SchedulerKind.lbp)),
+                         ("rnbp_low0.5", dict(kind=bp.SchedulerKind.rnbp, low_p=0.5, high_p=1.0)),
+                         ("rnbp_low0.7", dict(kind=bp.SchedulerKind.rnbp, low_p=0.7, high_p=1.0))):
+        conv, times, iters = 0, [], []
+        t0 = time.perf_counter()
+        for s in range(500, 525):
+            g = bp.generate_ising(bp.IsingParams(n=100, c=2.5, seed=s), device=device)
+            kw = dict(cfg_kw)
+            if kw["kind"] == bp.SchedulerKind.rnbp:
+                kw["seed"] = s - 500
+            r = bp.run(g, bp.SchedulerConfig(max_iterations=CAP, time_limit=1e9, **kw))
+            conv += r.converged
+            if r.converged:
+                times.append(r.wall_time)
+                iters.append(r.iterations)
+        out[name] = {"converged": conv, "of": 25, "median_time_s": statistics.median(times) if times else None,
+                     "median_iterations": statistics.median(iters) if iters else None,
+                     "suite_wall_s": round(time.perf_counter() - t0, 3)}
+    return out
+
+
+def _cpu_baseline(sample_iters):
+    """The reference's bpsched::run (oracle/_ref, compiled from /root/reference)
+    on this host, bounded sample of the workload."""
+    from oracle import pyoracle as po
+    try:
+        ref = po.load("ref")
+        kind = "reference"
+    except FileNotFoundError:
+        ref = po.load("orc")
+        kind = "port"
+    cores = os.cpu_count() or 1
+    g = po.Graph.ising(ref, N_GRID, C_COUPLING, 0)
+    cfg = po.make_config("rnbp", low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5,
+                         max_iterations=sample_iters, time_limit=1e9, seed=0, worker_count=cores)
+    r = po.run(g, cfg)
+    return {"value": r.messages_updated_total / r.wall_time, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"RnBP Ising {N_GRID}^2 C={C_COUPLING} seed 0, first {sample_iters} iterations "
+                      f"(EngineState ctor + loop, {r.wall_time:.2f} s, {r.messages_updated_total} updates)",
+            "wall_s": r.wall_time}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import pyoracle as po
+    try:
+        ref = po.load("ref")
+        kind = "reference"
+    except FileNotFoundError:
+        ref = po.load("orc")
+        kind = "port"
+    cores = os.cpu_count() or 1
+    K, W = args.steps, args.warmup
+    graphs = [po.Graph.ising(ref, N_GRID, C_COUPLING, s) for s in range(min(K, 2))]
+    def cfg(s):
+        return po.make_config("rnbp", low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5,
+                              max_iterations=REF_SAMPLE_ITERS, time_limit=1e9, seed=s, worker_count=cores)
+    for w in range(W):
+        po.run(graphs[w % len(graphs)], cfg(w))
+    upd, t = 0, 0.0
+    for k in range(K):
+        r = po.run(graphs[k % len(graphs)], cfg(k))
+        upd += r.messages_updated_total
+        t += r.wall_time
+    v = upd / t
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+           "ms_per_step": t / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (generate_ising)",
+           "config": {"workload": "ising1000_c2.5_rnbp", "n": N_GRID, "c": C_COUPLING, "scheduler": "rnbp",
+                      "low_p": 0.5, "sample_iterations": REF_SAMPLE_ITERS},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                            "sample": f"first {REF_SAMPLE_ITERS} RnBP iterations per step (incl. EngineState ctor)"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

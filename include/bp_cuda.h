@@ -1,0 +1,215 @@
+/*
+ * bp_cuda.h -- C ABI of the B200 belief-propagation scheduling engine
+ * (libbp_b200.so, built from paper_1909_11469_b200/csrc).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/core, "bpsched"): a PairwiseMRF (mrf.hpp:31-87) plus a
+ * SchedulerConfig (schedulers.hpp:26-41) go in, a RunResult
+ * (schedulers.hpp:43-57) comes out.  Plain pointers and sizes only; no C++ or
+ * torch types cross it.  Each entry point names the reference interface it
+ * replaces.  Error convention (schedulers.cpp:78-90, errors.hpp:10-38): every
+ * function returns a bp_status; the message of the last failure on the calling
+ * thread is available from bp_last_error().  Iteration / time caps are NOT
+ * errors (schedulers.cpp:307-309): they yield converged == 0.
+ *
+ * Threading (mrf.hpp:24-25, schedulers.hpp:59-60): a bp_graph is immutable and
+ * may be shared by concurrent runs on its device; a run is synchronous on the
+ * calling thread and owns its engine; a bp_engine is not re-entrant.
+ */
+#ifndef BP_CUDA_H
+#define BP_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BP_CUDA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define BP_API __attribute__((visibility("default")))
+#else
+#define BP_API
+#endif
+
+typedef enum {
+  BP_OK = 0,
+  BP_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (SchedulerConfig::validate, schedulers.cpp:78-90) */
+  BP_ERR_MODEL = 2,            /* bpsched::model_error (errors.hpp:17)   */
+  BP_ERR_NUMERIC = 3,          /* bpsched::numeric_error (errors.hpp:23) */
+  BP_ERR_CUDA = 4,
+  BP_ERR_NCCL = 5,
+  BP_ERR_OOM = 6,
+  BP_ERR_UNSUPPORTED = 7
+} bp_status;
+
+/* bpsched::SchedulerKind (schedulers.hpp:21-24), same numbering. */
+typedef enum { BP_LBP = 0, BP_SERIAL_RBP = 1, BP_RBP = 2, BP_RS = 3, BP_RNBP = 4 } bp_scheduler_kind;
+
+/* Inputs of bpsched::build_graph (mrf.hpp:94-96), flattened:
+ *   unary_values    = concat over v of unary_tables[v]          (sum card)
+ *   edge_endpoints  = (i, j) per edge, i < j, edge-id order      (2 E)
+ *   pairwise_values = concat over e of the row-major |A_i|x|A_j| table.
+ * Arrays are borrowed for the duration of the call only. */
+typedef struct {
+  uint32_t num_vertices;
+  uint32_t num_edges;
+  const uint32_t* cardinalities;
+  const double* unary_values;
+  const uint32_t* edge_endpoints;
+  const double* pairwise_values;
+} bp_graph_desc;
+
+typedef struct {
+  int32_t device;   /* CUDA ordinal, -1 = current */
+  uint32_t flags;   /* BP_GRAPH_* */
+} bp_device_opts;
+
+#define BP_GRAPH_TRUSTED 1u /* skip the O(E log E) duplicate-edge scan (generated inputs) */
+
+/* bpsched::SchedulerConfig (schedulers.hpp:26-41); worker_count is accepted
+ * and ignored (the CUDA grid replaces ThreadPool, thread_pool.hpp:17-45). */
+typedef struct {
+  int32_t kind;
+  uint32_t splash_depth;
+  double epsilon;
+  double p;
+  double low_p;
+  double high_p;
+  double edge_ratio_threshold;
+  uint64_t max_iterations;
+  double time_limit;
+  uint64_t seed;
+  uint32_t worker_count;
+  uint32_t _pad;
+} bp_sched_config;
+
+/* bpsched::IterationRecord (schedulers.hpp:43-48). */
+typedef struct {
+  uint64_t iteration;
+  uint64_t frontier_size;
+  uint32_t unconverged;
+  uint32_t _pad;
+  double elapsed_seconds;
+} bp_iter_record;
+
+/* bpsched::RunResult scalars (schedulers.hpp:50-57) + device statistics. */
+typedef struct {
+  int32_t converged;
+  int32_t _pad;
+  uint64_t iterations;
+  double wall_time;                /* host steady clock, same span as schedulers.cpp:297-350 */
+  uint64_t messages_updated_total; /* sum of frontier sizes (schedulers.cpp:343)            */
+  uint64_t trace_len;              /* records produced (may exceed trace_cap)               */
+  double device_ms;                /* CUDA-event time of the same span on the run's stream  */
+  uint64_t message_evaluations;    /* candidate / message recomputations on the device     */
+  uint64_t gpu_launches;           /* kernels launched by this run (incl. early-exit ones)  */
+  uint64_t vertex_visits;          /* vertices processed by update kernels                  */
+} bp_run_result;
+
+typedef struct {
+  uint32_t num_vertices;
+  uint32_t num_edges;
+  uint32_t max_cardinality;
+  uint32_t state_stride;  /* floats per message on device (1 = binary log-odds) */
+  uint64_t device_bytes;  /* graph bytes resident in HBM */
+  int32_t device;
+  uint32_t layout;        /* 0 = binary log-odds, 1 = generic log-domain */
+} bp_graph_info;
+
+/* Per-kernel-class device time, filled when BP_RUN_KERNEL_TIMING is set. */
+typedef struct {
+  double ms[8];          /* 0 sweep/refresh, 1 select, 2 radix/top-k, 3 splash, 4 init, 5 beliefs, 6 other */
+  uint64_t launches[8];
+  uint64_t bytes[8];     /* algorithmic bytes moved by the timed launches */
+} bp_kernel_stats;
+
+typedef struct {
+  uint32_t flags;        /* BP_RUN_* */
+  uint32_t batch;        /* iterations per device batch (0 = adaptive) */
+  bp_kernel_stats* stats;/* optional */
+  double* beliefs_device;/* optional: write beliefs (fp64) to this DEVICE pointer instead */
+} bp_run_opts;
+
+#define BP_RUN_KERNEL_TIMING 1u /* CUDA events around every kernel (adds overhead) */
+#define BP_RUN_NO_GRAPHS 2u     /* launch kernels directly instead of CUDA-graph batches */
+#define BP_RUN_NO_BELIEFS 4u    /* skip beliefs */
+
+BP_API const char* bp_last_error(void);
+BP_API int bp_abi_version(void);
+
+/* build_graph (mrf.cpp:25-106): validates exactly like the reference (model
+ * errors for zero cardinality, table-size mismatch, non-positive / non-finite
+ * potentials, self loops, i >= j, duplicates) and uploads to HBM. */
+BP_API int bp_graph_create(const bp_graph_desc* desc, const bp_device_opts* opts, struct bp_graph** out);
+
+/* generate_ising / generate_chain (generators.cpp:24-71), bit-identical
+ * mt19937_64 streams, built straight into the device layout (no PairwiseMRF
+ * on the host: 16384^2 fits).  Potts / Erdos-Renyi: DESIGN.md section 3. */
+BP_API int bp_graph_generate_ising(uint32_t n, double c, uint64_t seed, const bp_device_opts* opts,
+                            struct bp_graph** out);
+BP_API int bp_graph_generate_chain(uint32_t length, double c, uint64_t seed, const bp_device_opts* opts,
+                            struct bp_graph** out);
+BP_API int bp_graph_generate_potts(uint32_t n, uint32_t q, double c, uint64_t seed,
+                            const bp_device_opts* opts, struct bp_graph** out);
+BP_API int bp_graph_generate_er(uint32_t n, uint32_t m, double c, uint64_t seed,
+                         const bp_device_opts* opts, struct bp_graph** out);
+
+/* Host-side generate_ising in build_graph's input layout (no device work):
+ * cards[n*n], unary[2 n*n], endpoints[2E], tables[4E] with E = 2 n (n - 1). */
+BP_API int bp_generate_ising_arrays(uint32_t n, double c, uint64_t seed, uint32_t* cardinalities,
+                                    double* unary_values, uint32_t* edge_endpoints,
+                                    double* pairwise_values);
+
+BP_API void bp_graph_destroy(struct bp_graph* g);
+BP_API int bp_graph_info_get(const struct bp_graph* g, bp_graph_info* info);
+
+/* bpsched::run (schedulers.hpp:156, schedulers.cpp:293-353).  beliefs_out:
+ * sum(card) doubles in vertex order (BeliefTable, messages.hpp:83-107) or NULL;
+ * trace_out: trace_cap records or NULL.  kind == BP_SERIAL_RBP returns
+ * BP_ERR_UNSUPPORTED: serial RBP is strictly sequential and is
+ * not offloaded; the C++ facade routes it to the reference's run_serial_rbp. */
+BP_API int bp_run(const struct bp_graph* g, const bp_sched_config* cfg, bp_run_result* result,
+           double* beliefs_out, bp_iter_record* trace_out, uint64_t trace_cap);
+BP_API int bp_run_ex(const struct bp_graph* g, const bp_sched_config* cfg, const bp_run_opts* opts,
+              bp_run_result* result, double* beliefs_out, bp_iter_record* trace_out,
+              uint64_t trace_cap);
+
+/* SchedulerConfig::validate (schedulers.cpp:78-90) and select_parallelism
+ * (schedulers.cpp:218-224), exported for parity tests. */
+BP_API int bp_validate_config(const bp_sched_config* cfg);
+BP_API double bp_select_parallelism(uint32_t prev_unconverged, uint32_t new_unconverged,
+                             const bp_sched_config* cfg);
+
+/* ---- Lockstep engine: EngineState + per-phase API (schedulers.hpp:61-151) ---- */
+BP_API int bp_engine_create(const struct bp_graph* g, const bp_sched_config* cfg, struct bp_engine** out);
+BP_API void bp_engine_destroy(struct bp_engine* e);
+BP_API int bp_engine_unconverged(const struct bp_engine* e, uint32_t* out);
+/* Live messages / candidates as fp64 probabilities, concatenated per directed
+ * edge (MessageStore::view, messages.hpp:24-26); residuals fp64 [2E]. */
+BP_API int bp_engine_messages(const struct bp_engine* e, double* out);
+BP_API int bp_engine_candidates(const struct bp_engine* e, double* out);
+BP_API int bp_engine_residuals(const struct bp_engine* e, double* out);
+BP_API int bp_engine_beliefs(const struct bp_engine* e, double* out);
+/* apply_frontier (schedulers.cpp:226-251): Jacobi commit + touched refresh. */
+BP_API int bp_engine_apply_frontier(struct bp_engine* e, const uint32_t* frontier, uint64_t n);
+/* apply_splash_frontier (schedulers.cpp:253-291). */
+BP_API int bp_engine_apply_splashes(struct bp_engine* e, uint64_t num_splashes, const uint32_t* roots,
+                             const uint64_t* edge_offsets, const uint32_t* edges);
+/* Device frontier builders; out: capacity 2E ids, ascending id order.
+ * rnbp: Philox4x32-10 keyed (seed, iteration, attempt, edge id). */
+BP_API int bp_engine_rnbp_frontier(struct bp_engine* e, double p, uint32_t* out, uint64_t* n);
+BP_API int bp_engine_rbp_frontier(struct bp_engine* e, double p, uint32_t* out, uint64_t* n);
+BP_API int bp_engine_rs_frontier(struct bp_engine* e, double p, uint32_t h, uint32_t* roots,
+                          uint64_t* edge_offsets, uint32_t* edges, uint64_t* num_splashes);
+/* One full iteration of the configured scheduler (frontier + apply), exactly
+ * as one pass of the run loop; *frontier_size receives |F|. */
+BP_API int bp_engine_step(struct bp_engine* e, uint64_t* frontier_size);
+BP_API int bp_engine_iteration(const struct bp_engine* e, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BP_CUDA_H */

@@ -1,0 +1,203 @@
+// Device-side data layout, numerics and RNG of the B200 BP engine.
+//
+// Layout in HBM:
+//   * directed edge d of undirected edge e = d >> 1: 2e = lo->hi, 2e+1 = hi->lo
+//     (mrf.cpp:89-90); src(d) = ep[d], tgt(d) = ep[d ^ 1] with ep = (lo, hi)
+//     pairs, so the reference's DirectedEdge table (mrf.hpp:14-18) is implicit.
+//   * incoming CSR in edge-id order (mrf.cpp:93-104): in_off[V+1], in_adj[D].
+//   * messages are stored per directed edge in id order, so the two directions
+//     of one undirected edge are adjacent ("edge pair"): a vertex update loads
+//     one pair and gets both the incoming message and the old outgoing message
+//     it needs for the residual.
+//   * binary graphs (all cardinalities 2): one fp32 log-odds per message,
+//     log(m(1)/m(0)); unary log-odds per vertex; per edge float4 of log-table
+//     differences.  Generic graphs: qs fp32 log-probabilities per message
+//     (qs = padded max cardinality), qs x qs max-scaled linear tables.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bpb {
+
+constexpr int kBlock = 256;
+
+struct DevGraph {
+  uint32_t V, E, D;
+  uint32_t qs;                            // floats per message (1 = binary log-odds)
+  const uint32_t* __restrict__ in_off;    // V+1
+  const uint32_t* __restrict__ in_adj;    // D
+  const uint32_t* __restrict__ ep;        // 2E (lo, hi)
+  // binary
+  const float* __restrict__ unary_lo;     // V: log psi(1) - log psi(0)
+  const float4* __restrict__ epar;        // E: (alpha, beta, g-alpha, g-beta), see graph.cu
+  // generic
+  const uint32_t* __restrict__ card;      // V
+  const float* __restrict__ unary_log;    // V*qs
+  const float* __restrict__ table;        // E*qs*qs, row = lo state, max-scaled linear
+  const uint32_t* __restrict__ bel_off;   // V+1 belief offsets (generic)
+};
+
+// Per-run control block in device memory.  Written only by single threads
+// (finalizers) or by atomics; read by every kernel at entry.
+struct TraceRec {
+  unsigned long long iteration;
+  unsigned long long frontier_size;
+  unsigned int unconverged;
+  unsigned int pad;
+  double elapsed_seconds;
+};
+
+constexpr unsigned kTraceRing = 4096;
+
+enum StopReason : unsigned { kStopNone = 0, kStopConverged = 1, kStopMaxIter = 2, kStopTime = 3, kStopNumeric = 4 };
+
+// Per-block contributions are accumulated into kSlots cache-line-separated
+// slots (block b adds into slot b % kSlots) so no single address sees more
+// than gridDim/kSlots atomics; a one-block finalize kernel reduces them.
+constexpr int kSlots = 128;
+struct alignas(128) Accum {
+  long long delta;                // unconverged-count change
+  unsigned long long count;       // r >= eps count (LBP sweep / init)
+  unsigned long long frontier;    // committed edges
+  unsigned long long survivors;   // r >= eps seen by the RnBP filter
+  unsigned long long evals;       // messages recomputed
+  unsigned long long visits;      // vertices updated
+};
+
+struct Ctl {
+  unsigned int done;
+  unsigned int converged;
+  unsigned int numeric_error;
+  unsigned int has_prev;
+  unsigned int unconverged;
+  unsigned int prev_unconverged;
+  unsigned int nflag;         // vertices queued in vlist this iteration (sparse mode)
+  unsigned int dense;         // this iteration flags vertices without a list
+  unsigned long long iteration;
+  unsigned long long sweeps;  // LBP sweeps completed
+  unsigned long long max_iterations;
+  unsigned long long msgs_total;
+  unsigned long long evals_total;
+  unsigned long long vertex_visits;
+  unsigned long long t0_ns;
+  unsigned long long time_limit_ns;
+  unsigned long long frontier;    // reduced by the retry kernel (RnBP)
+  unsigned long long survivors;
+  // radix select (RBP top-k): prefix of the k-th key found so far, and how
+  // many keys are strictly above it
+  unsigned int rx_prefix;
+  unsigned int rx_need;
+  unsigned long long rx_above;
+  unsigned long long rx_ties;
+  unsigned int stamp;         // vflag generation
+  unsigned int splashes;
+  unsigned long long splash_edges;
+  unsigned int rs_pending;
+  unsigned int rs_built;
+  unsigned long long trace_len;
+  unsigned long long cond_handle;  // cudaGraphConditionalHandle of the WHILE loop (0 = none)
+  unsigned int stop_reason;
+  unsigned int cl_cur;        // candidate list (RnBP): current buffer
+  unsigned int cl_n[2];       // candidate list sizes
+  unsigned int use_clist;
+  unsigned int pad2_;
+  Accum acc[kSlots];
+  TraceRec trace[kTraceRing];
+};
+
+// ---------------------------------------------------------------------------
+// numerics
+
+__device__ __forceinline__ float softplusf(float x) {
+  // log(1 + e^x) = max(x, 0) + log1p(e^-|x|)
+  return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x)));
+}
+
+__device__ __forceinline__ float sigmoidf(float x) { return __frcp_rn(1.f + __expf(-x)); }
+
+// Binary sum-product update (Eq. 2, messages.hpp:114-151) in log-odds form:
+// with cavity log-odds h of the source and the 2x2 table A oriented source x
+// target, out = log(A01 + A11 e^h) - log(A00 + A10 e^h)
+//             = c + softplus(h + a) - softplus(h + b).
+// par = (alpha, beta, g - alpha, g - beta) with alpha = lT01 - lT00,
+// beta = lT10 - lT00, g = lT11 - lT00 (T row = lo state).  Even d (lo -> hi):
+// c = alpha, a = g - alpha, b = beta.  Odd d: c = beta, a = g - beta, b = alpha.
+__device__ __forceinline__ float binary_update(float h, float4 par, bool odd) {
+  const float c = odd ? par.y : par.x;
+  const float a = odd ? par.w : par.z;
+  const float b = odd ? par.x : par.y;
+  return c + softplusf(h + a) - softplusf(h + b);
+}
+
+// L-inf residual in linear probability space (messages.cpp:56-65): for binary
+// messages |m'(1) - m(1)| = |m'(0) - m(0)|.
+__device__ __forceinline__ float binary_residual(float lnew, float lold) {
+  return fabsf(sigmoidf(lnew) - sigmoidf(lold));
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11), counter-based: the RnBP Bernoulli draw
+// for edge d in (iteration, attempt) is a pure function of (seed, iteration,
+// attempt, d), independent of launch shape and GPU count.
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, ctr.x), lo0 = M0 * ctr.x;
+    const uint32_t hi1 = __umulhi(M1, ctr.z), lo1 = M1 * ctr.z;
+    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+    if (r < 9) {  // key schedule between rounds (Random123 philox4x32_R)
+      key.x += W0;
+      key.y += W1;
+    }
+  }
+  return ctr;
+}
+
+// 53-bit uniform integer; u = value * 2^-53 in [0, 1) like uniform_unit (rng.hpp:11-13).
+__device__ __forceinline__ unsigned long long philox_u53(unsigned long long seed,
+                                                         unsigned long long iteration,
+                                                         unsigned attempt, unsigned long long d) {
+  const uint4 ctr = make_uint4(static_cast<uint32_t>(d), static_cast<uint32_t>(d >> 32),
+                               static_cast<uint32_t>(iteration),
+                               (static_cast<uint32_t>(iteration >> 32) & 0x3FFFFFFFu) | (attempt << 30));
+  const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+  const uint4 r = philox4x32_10(ctr, key);
+  return ((static_cast<unsigned long long>(r.x) << 32) | r.y) >> 11;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// block reductions
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over the block; valid in thread 0.  `sh` must hold blockDim/32 entries.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  T r = 0;
+  if (wid == 0) {
+    r = lane < static_cast<int>(blockDim.x >> 5) ? sh[lane] : T(0);
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+}  // namespace bpb

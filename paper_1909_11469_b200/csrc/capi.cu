@@ -1,0 +1,227 @@
+// extern "C" boundary (include/bp_cuda.h): exceptions -> bp_status codes,
+// message kept per thread (errors.hpp:10-38 -> return codes).
+#include <cstring>
+#include <string>
+
+#include "engine.hpp"
+#include "graph.hpp"
+
+struct bp_graph {
+  std::unique_ptr<bpb::GraphImpl> impl;
+};
+struct bp_engine {
+  std::unique_ptr<bpb::EngineBase> e;
+  const bp_graph* g;
+  bp_sched_config cfg;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BP_OK;
+  } catch (const bpb::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = std::string("host allocation failed: ") + e.what();
+    return BP_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return BP_ERR_INVALID_ARGUMENT;
+  }
+}
+
+int wrap_graph(std::unique_ptr<bpb::GraphImpl> g, bp_graph** out) {
+  *out = new bp_graph{std::move(g)};
+  return BP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bp_last_error(void) { return g_last_error.c_str(); }
+int bp_abi_version(void) { return BP_CUDA_ABI_VERSION; }
+
+int bp_graph_create(const bp_graph_desc* desc, const bp_device_opts* opts, bp_graph** out) {
+  if (!out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] { wrap_graph(bpb::build_from_desc(desc, opts), out); });
+}
+
+int bp_graph_generate_ising(uint32_t n, double c, uint64_t seed, const bp_device_opts* opts, bp_graph** out) {
+  if (!out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] { wrap_graph(bpb::build_lattice_binary(n, n, bpb::ising_streams(n, c, seed), opts), out); });
+}
+
+int bp_graph_generate_chain(uint32_t length, double c, uint64_t seed, const bp_device_opts* opts, bp_graph** out) {
+  if (!out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    wrap_graph(bpb::build_lattice_binary(length ? 1 : 0, length, bpb::chain_streams(length, c, seed), opts), out);
+  });
+}
+
+int bp_graph_generate_potts(uint32_t n, uint32_t q, double c, uint64_t seed, const bp_device_opts* opts,
+                            bp_graph** out) {
+  if (!out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] { wrap_graph(bpb::build_potts(n, q, bpb::potts_streams(n, q, c, seed), opts), out); });
+}
+
+int bp_graph_generate_er(uint32_t n, uint32_t m, double c, uint64_t seed, const bp_device_opts* opts,
+                         bp_graph** out) {
+  if (!out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] { wrap_graph(bpb::build_er(n, bpb::er_instance(n, m, c, seed), opts), out); });
+}
+
+int bp_generate_ising_arrays(uint32_t n, double c, uint64_t seed, uint32_t* cards, double* unary, uint32_t* ep,
+                             double* tables) {
+  if (!cards || !unary || (n > 1 && (!ep || !tables))) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    std::vector<uint32_t> cv, ev;
+    std::vector<double> uv, tv;
+    bpb::ising_desc_arrays(n, n, c, seed, cv, uv, ev, tv);
+    std::memcpy(cards, cv.data(), cv.size() * 4);
+    std::memcpy(unary, uv.data(), uv.size() * 8);
+    if (!ev.empty()) std::memcpy(ep, ev.data(), ev.size() * 4);
+    if (!tv.empty()) std::memcpy(tables, tv.data(), tv.size() * 8);
+  });
+}
+
+void bp_graph_destroy(bp_graph* g) { delete g; }
+
+int bp_graph_info_get(const bp_graph* g, bp_graph_info* info) {
+  if (!g || !info) return BP_ERR_INVALID_ARGUMENT;
+  const auto& G = *g->impl;
+  info->num_vertices = G.V;
+  info->num_edges = G.E;
+  info->max_cardinality = G.maxq;
+  info->state_stride = G.qs;
+  info->device_bytes = G.device_bytes();
+  info->device = G.device;
+  info->layout = G.binary ? 0u : 1u;
+  return BP_OK;
+}
+
+int bp_validate_config(const bp_sched_config* cfg) {
+  if (!cfg) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { bpb::validate_config(*cfg); });
+}
+
+double bp_select_parallelism(uint32_t prev, uint32_t now, const bp_sched_config* cfg) {
+  return bpb::select_parallelism_host(prev, now, *cfg);
+}
+
+int bp_run_ex(const bp_graph* g, const bp_sched_config* cfg, const bp_run_opts* opts, bp_run_result* result,
+              double* beliefs_out, bp_iter_record* trace_out, uint64_t trace_cap) {
+  if (!g || !cfg || !result) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    bpb::validate_config(*cfg);
+    if (cfg->kind == BP_SERIAL_RBP)
+      throw bpb::Error(BP_ERR_UNSUPPORTED,
+                       "serial RBP is strictly sequential and is not offloaded (use the reference run_serial_rbp)");
+    if (cfg->kind == BP_RS) throw bpb::Error(BP_ERR_UNSUPPORTED, "residual splash is not available in this build");
+    auto e = bpb::make_engine(*g->impl, *cfg);
+    e->run(opts, result, beliefs_out, trace_out, trace_cap);
+  });
+}
+
+int bp_run(const bp_graph* g, const bp_sched_config* cfg, bp_run_result* result, double* beliefs_out,
+           bp_iter_record* trace_out, uint64_t trace_cap) {
+  return bp_run_ex(g, cfg, nullptr, result, beliefs_out, trace_out, trace_cap);
+}
+
+int bp_engine_create(const bp_graph* g, const bp_sched_config* cfg, bp_engine** out) {
+  if (!g || !cfg || !out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    bpb::validate_config(*cfg);
+    auto e = bpb::make_engine(*g->impl, *cfg);
+    e->lockstep_init();
+    *out = new bp_engine{std::move(e), g, *cfg};
+  });
+}
+
+void bp_engine_destroy(bp_engine* e) { delete e; }
+
+int bp_engine_unconverged(const bp_engine* e, uint32_t* out) {
+  if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { *out = e->e->unconverged(); });
+}
+int bp_engine_iteration(const bp_engine* e, uint64_t* out) {
+  if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { *out = e->e->iteration(); });
+}
+int bp_engine_messages(const bp_engine* e, double* out) {
+  if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->messages(out, false); });
+}
+int bp_engine_candidates(const bp_engine* e, double* out) {
+  if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->messages(out, true); });
+}
+int bp_engine_residuals(const bp_engine* e, double* out) {
+  if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->residuals(out); });
+}
+int bp_engine_beliefs(const bp_engine* e, double* out) {
+  if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->beliefs(out); });
+}
+int bp_engine_apply_frontier(bp_engine* e, const uint32_t* frontier, uint64_t n) {
+  if (!e || (n && !frontier)) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->apply_frontier(frontier, n); });
+}
+int bp_engine_apply_splashes(bp_engine* e, uint64_t ns, const uint32_t* roots, const uint64_t* eoff,
+                             const uint32_t* edges) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->apply_splashes(ns, roots, eoff, edges); });
+}
+int bp_engine_rnbp_frontier(bp_engine* e, double p, uint32_t* out, uint64_t* n) {
+  if (!e || !out || !n) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    std::vector<uint32_t> f;
+    e->e->rnbp_frontier(p, f);
+    std::memcpy(out, f.data(), f.size() * 4);
+    *n = f.size();
+  });
+}
+int bp_engine_rbp_frontier(bp_engine* e, double p, uint32_t* out, uint64_t* n) {
+  if (!e || !out || !n) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    std::vector<uint32_t> f;
+    e->e->rbp_frontier(p, f);
+    std::memcpy(out, f.data(), f.size() * 4);
+    *n = f.size();
+  });
+}
+int bp_engine_rs_frontier(bp_engine* e, double p, uint32_t h, uint32_t* roots, uint64_t* eoff, uint32_t* edges,
+                          uint64_t* ns) {
+  if (!e || !roots || !eoff || !edges || !ns) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    std::vector<uint32_t> r, ed;
+    std::vector<uint64_t> o;
+    e->e->rs_frontier(p, h, r, o, ed);
+    std::memcpy(roots, r.data(), r.size() * 4);
+    std::memcpy(eoff, o.data(), o.size() * 8);
+    std::memcpy(edges, ed.data(), ed.size() * 4);
+    *ns = r.size();
+  });
+}
+int bp_engine_step(bp_engine* e, uint64_t* frontier_size) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    const uint64_t f = e->e->step();
+    if (frontier_size) *frontier_size = f;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// Host-side engine: owns the per-run device state and drives the kernels.
+// Restates EngineState (schedulers.hpp:61-90) and run() (schedulers.cpp:293-353).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "graph.hpp"
+
+namespace bpb {
+
+class EngineBase {
+ public:
+  virtual ~EngineBase() = default;
+  // full run (bp_run_ex)
+  virtual void run(const bp_run_opts* opts, bp_run_result* res, double* beliefs_host,
+                   bp_iter_record* trace, uint64_t trace_cap) = 0;
+  // lockstep API
+  virtual void lockstep_init() = 0;
+  virtual uint32_t unconverged() = 0;
+  virtual uint64_t iteration() = 0;
+  virtual void messages(double* out, bool candidates) = 0;
+  virtual void residuals(double* out) = 0;
+  virtual void beliefs(double* out) = 0;
+  virtual void apply_frontier(const uint32_t* f, uint64_t n) = 0;
+  virtual void rnbp_frontier(double p, std::vector<uint32_t>& out) = 0;
+  virtual void rbp_frontier(double p, std::vector<uint32_t>& out) = 0;
+  virtual void rs_frontier(double p, uint32_t h, std::vector<uint32_t>& roots,
+                           std::vector<uint64_t>& eoff, std::vector<uint32_t>& edges) = 0;
+  virtual void apply_splashes(uint64_t ns, const uint32_t* roots, const uint64_t* eoff,
+                              const uint32_t* edges) = 0;
+  virtual uint64_t step() = 0;
+};
+
+std::unique_ptr<EngineBase> make_engine(const GraphImpl& g, const bp_sched_config& cfg);
+
+void validate_config(const bp_sched_config& c);
+double select_parallelism_host(uint32_t prev, uint32_t now, const bp_sched_config& c);
+
+}  // namespace bpb

@@ -1,0 +1,406 @@
+// Graph construction and upload: the device counterpart of build_graph
+// (mrf.cpp:25-106) and of the generators (generators.cpp:24-71).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <thread>
+
+#include "bp_device.cuh"
+#include "graph.hpp"
+
+namespace bpb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) throw Error(BP_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  throw Error(BP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+DevBuf::~DevBuf() { reset(); }
+void DevBuf::reset() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+void DevBuf::alloc(size_t n) {
+  reset();
+  if (n == 0) n = 16;
+  cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+  bytes = n;
+}
+void DevBuf::upload(const void* src, size_t n) {
+  alloc(n);
+  if (src && n) cuda_check(cudaMemcpy(p, src, n, cudaMemcpyHostToDevice), "upload");
+}
+
+DevGraph GraphImpl::dev() const {
+  DevGraph g{};
+  g.V = V;
+  g.E = E;
+  g.D = D;
+  g.qs = qs;
+  g.in_off = in_off.as<uint32_t>();
+  g.in_adj = in_adj.as<uint32_t>();
+  g.ep = ep.as<uint32_t>();
+  g.unary_lo = unary_lo.as<float>();
+  g.epar = epar.as<float4>();
+  g.card = card.as<uint32_t>();
+  g.unary_log = unary_log.as<float>();
+  g.table = table.as<float>();
+  g.bel_off = bel_off.as<uint32_t>();
+  return g;
+}
+
+uint64_t GraphImpl::device_bytes() const {
+  return in_off.bytes + in_adj.bytes + ep.bytes + unary_lo.bytes + epar.bytes + card.bytes +
+         unary_log.bytes + table.bytes + bel_off.bytes;
+}
+
+namespace {
+
+int select_device(const bp_device_opts* opts) {
+  int dev = 0;
+  if (opts && opts->device >= 0) {
+    cuda_check(cudaSetDevice(opts->device), "cudaSetDevice");
+    dev = opts->device;
+  } else {
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  }
+  return dev;
+}
+
+uint32_t stride_for(uint32_t maxq) {
+  if (maxq <= 4) return 4;
+  if (maxq <= 8) return 8;
+  if (maxq <= 16) return 16;
+  if (maxq <= 32) return 32;
+  throw Error(BP_ERR_UNSUPPORTED, "cardinalities above 32 are not supported by the device kernels (max " +
+                                      std::to_string(maxq) + ")");
+}
+
+// CSR of incoming directed edges in edge-id order (mrf.cpp:93-104)
+void build_csr(uint32_t V, uint32_t E, const uint32_t* ep, std::vector<uint32_t>& off,
+               std::vector<uint32_t>& adj) {
+  const uint64_t D = 2ull * E;
+  off.assign(static_cast<size_t>(V) + 1, 0);
+  for (uint64_t d = 0; d < D; ++d) off[ep[d ^ 1ull] + 1]++;  // tgt(d) = ep[d ^ 1]
+  for (uint32_t v = 0; v < V; ++v) off[v + 1] += off[v];
+  adj.resize(D);
+  std::vector<uint32_t> cur(off.begin(), off.end() - 1);
+  for (uint64_t d = 0; d < D; ++d) adj[cur[ep[d ^ 1ull]]++] = static_cast<uint32_t>(d);
+}
+
+// Lattice topology (rows x cols, row-major vertices; per vertex the right edge
+// then the down edge -- generators.cpp:37-43), written straight into HBM.
+__global__ void k_lattice_topology(uint32_t R, uint32_t C, uint32_t* in_off, uint32_t* in_adj,
+                                   uint32_t* ep) {
+  const uint64_t V = static_cast<uint64_t>(R) * C;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = v / C, c = v % C;
+    auto ebase = [&](uint64_t rr, uint64_t cc) -> uint64_t {
+      return rr + 1 < R ? rr * (2ull * C - 1) + 2 * cc : rr * (2ull * C - 1) + cc;
+    };
+    const uint64_t vert = (r > 0) + (r + 1 < R);
+    const uint64_t before_rows = 2ull * (C - 1) * r + static_cast<uint64_t>(C) *
+                                                          ((r > 0 ? r - 1 : 0) + (r < R - 1 ? r : R - 1));
+    const uint64_t within = c * vert + (c > 0 ? c - 1 : 0) + (c < C - 1 ? c : C - 1);
+    uint64_t o = before_rows + within;
+    in_off[v] = static_cast<uint32_t>(o);
+    if (v + 1 == V) in_off[V] = static_cast<uint32_t>(2ull * ((R - 1) * C + (C - 1) * R));
+    if (r > 0) in_adj[o++] = static_cast<uint32_t>(2 * (ebase(r - 1, c) + (c + 1 < C)));  // up: v is hi
+    if (c > 0) in_adj[o++] = static_cast<uint32_t>(2 * ebase(r, c - 1));                 // left: v is hi
+    if (c + 1 < C) {                                                                      // right: v is lo
+      const uint64_t e = ebase(r, c);
+      in_adj[o++] = static_cast<uint32_t>(2 * e + 1);
+      ep[2 * e] = static_cast<uint32_t>(v);
+      ep[2 * e + 1] = static_cast<uint32_t>(v + 1);
+    }
+    if (r + 1 < R) {  // down: v is lo
+      const uint64_t e = ebase(r, c) + (c + 1 < C);
+      in_adj[o++] = static_cast<uint32_t>(2 * e + 1);
+      ep[2 * e] = static_cast<uint32_t>(v);
+      ep[2 * e + 1] = static_cast<uint32_t>(v + C);
+    }
+  }
+}
+
+// Ising-style binary edge parameters from J = 2 lambda c: (alpha, beta, g-alpha, g-beta) = (-J, -J, J, J)
+__global__ void k_ising_params(const float* J, uint32_t E, float4* epar) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const float j = J[e];
+    epar[e] = make_float4(-j, -j, j, j);
+  }
+}
+
+// Potts tables from lambda*c: exp(lc) on the diagonal, exp(-lc) off it,
+// scaled by the larger of the two (normalisation makes the scale irrelevant).
+template <int QS>
+__global__ void k_potts_tables(const float* lc, uint32_t E, uint32_t q, float* table) {
+  const size_t n = static_cast<size_t>(E) * QS * QS;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = static_cast<uint32_t>(i / (QS * QS));
+    const uint32_t a = static_cast<uint32_t>((i / QS) % QS), b = static_cast<uint32_t>(i % QS);
+    const double l = lc[e];
+    const double agree = exp(l - fabs(l)), disagree = exp(-l - fabs(l));
+    table[i] = (a < q && b < q) ? static_cast<float>(a == b ? agree : disagree) : 0.f;
+  }
+}
+
+__global__ void k_fill_u32(uint32_t* p, size_t n, uint32_t v) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_iota_mul(uint32_t* p, size_t n, uint32_t mul) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = static_cast<uint32_t>(i * mul);
+}
+
+unsigned grid_for(size_t n) {
+  return static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148ull * 32));
+}
+
+}  // namespace
+
+std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_device_opts* opts) {
+  if (!d) throw_invalid("null graph descriptor");
+  const uint32_t V = d->num_vertices, E = d->num_edges;
+  if (E > (1u << 31) - 1) throw_model("too many edges for 32-bit directed edge ids");
+  if (V && !d->cardinalities) throw_invalid("null cardinalities");
+  // --- validation (mrf.cpp:28-91) ---
+  uint32_t maxq = 0;
+  size_t usz = 0;
+  for (uint32_t v = 0; v < V; ++v) {
+    if (d->cardinalities[v] == 0) throw_model("vertex " + std::to_string(v) + " has cardinality 0");
+    maxq = std::max(maxq, d->cardinalities[v]);
+    usz += d->cardinalities[v];
+  }
+  if (usz && !d->unary_values) throw_invalid("null unary values");
+  for (uint32_t v = 0, o = 0; v < V; o += d->cardinalities[v], ++v)
+    for (uint32_t x = 0; x < d->cardinalities[v]; ++x) {
+      const double u = d->unary_values[o + x];
+      if (!(u > 0.0) || !std::isfinite(u))
+        throw_model("unary(" + std::to_string(v) + ") entries must be strictly positive and finite");
+    }
+  if (E && (!d->edge_endpoints || !d->pairwise_values)) throw_invalid("null edge arrays");
+  std::vector<size_t> poff(static_cast<size_t>(E) + 1, 0);
+  for (uint32_t e = 0; e < E; ++e) {
+    const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
+    if (i >= V || j >= V) throw_model("edge " + std::to_string(e) + " references a vertex out of range");
+    if (i == j) throw_model("edge " + std::to_string(e) + " is a self-loop on vertex " + std::to_string(i));
+    if (i > j) throw_model("edge " + std::to_string(e) + " endpoints must satisfy i < j");
+    poff[e + 1] = poff[e] + static_cast<size_t>(d->cardinalities[i]) * d->cardinalities[j];
+  }
+  for (uint32_t e = 0; e < E; ++e)
+    for (size_t k = poff[e]; k < poff[e + 1]; ++k) {
+      const double t = d->pairwise_values[k];
+      if (!(t > 0.0) || !std::isfinite(t))
+        throw_model("pairwise(" + std::to_string(d->edge_endpoints[2 * e]) + "," +
+                    std::to_string(d->edge_endpoints[2 * e + 1]) + ") entries must be strictly positive and finite");
+    }
+  std::vector<uint32_t> off, adj;
+  build_csr(V, E, d->edge_endpoints, off, adj);
+  if (!(opts && (opts->flags & BP_GRAPH_TRUSTED))) {
+    // duplicate edges: two incoming edges of one vertex from the same source
+    std::vector<uint32_t> mark(V, std::numeric_limits<uint32_t>::max());
+    for (uint32_t v = 0; v < V; ++v)
+      for (uint32_t a = off[v]; a < off[v + 1]; ++a) {
+        const uint32_t s = d->edge_endpoints[adj[a]];
+        if (mark[s] == v) {
+          const uint32_t lo = std::min(s, v), hi = std::max(s, v);
+          throw_model("duplicate edge (" + std::to_string(lo) + ", " + std::to_string(hi) + ")");
+        }
+        mark[s] = v;
+      }
+  }
+  auto g = std::make_unique<GraphImpl>();
+  g->device = select_device(opts);
+  g->V = V;
+  g->E = E;
+  g->D = 2 * E;
+  g->maxq = maxq;
+  g->binary = V > 0 && maxq == 2 && usz == 2ull * V;
+  bool uniform = true;
+  for (uint32_t v = 1; v < V; ++v) uniform = uniform && d->cardinalities[v] == d->cardinalities[0];
+  if (uniform && V) g->uniform_q = d->cardinalities[0];
+  else g->cards_host.assign(d->cardinalities, d->cardinalities + V);
+  g->in_off.upload(off.data(), off.size() * 4);
+  g->in_adj.upload(adj.data(), adj.size() * 4);
+  g->ep.upload(d->edge_endpoints, static_cast<size_t>(E) * 8);
+  if (g->binary || V == 0) {
+    g->binary = true;
+    g->qs = 1;
+    std::vector<float> ulo(V);
+    for (uint32_t v = 0; v < V; ++v)
+      ulo[v] = static_cast<float>(std::log(d->unary_values[2 * v + 1]) - std::log(d->unary_values[2 * v]));
+    std::vector<float4> par(E);
+    for (uint32_t e = 0; e < E; ++e) {
+      const double* t = d->pairwise_values + 4ull * e;
+      const double l00 = std::log(t[0]), l01 = std::log(t[1]), l10 = std::log(t[2]), l11 = std::log(t[3]);
+      const double alpha = l01 - l00, beta = l10 - l00, gg = l11 - l00;
+      par[e] = make_float4(static_cast<float>(alpha), static_cast<float>(beta), static_cast<float>(gg - alpha),
+                           static_cast<float>(gg - beta));
+    }
+    g->unary_lo.upload(ulo.data(), ulo.size() * 4);
+    g->epar.upload(par.data(), par.size() * 16);
+  } else {
+    const uint32_t qs = stride_for(maxq);
+    g->qs = qs;
+    std::vector<float> ul(static_cast<size_t>(V) * qs, 0.f);
+    std::vector<uint32_t> bo(static_cast<size_t>(V) + 1, 0);
+    for (uint32_t v = 0, o = 0; v < V; o += d->cardinalities[v], ++v) {
+      bo[v + 1] = bo[v] + d->cardinalities[v];
+      for (uint32_t x = 0; x < d->cardinalities[v]; ++x)
+        ul[static_cast<size_t>(v) * qs + x] = static_cast<float>(std::log(d->unary_values[o + x]));
+    }
+    std::vector<float> tb(static_cast<size_t>(E) * qs * qs, 0.f);
+    for (uint32_t e = 0; e < E; ++e) {
+      const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
+      const uint32_t ci = d->cardinalities[i], cj = d->cardinalities[j];
+      const double* t = d->pairwise_values + poff[e];
+      double mx = 0.0;
+      for (size_t k = 0; k < static_cast<size_t>(ci) * cj; ++k) mx = std::max(mx, t[k]);
+      for (uint32_t a = 0; a < ci; ++a)
+        for (uint32_t b = 0; b < cj; ++b) {
+          // max-scaled linear fp32; clamped so no entry underflows to 0
+          const double s = t[static_cast<size_t>(a) * cj + b] / mx;
+          tb[static_cast<size_t>(e) * qs * qs + static_cast<size_t>(a) * qs + b] =
+              static_cast<float>(std::max(s, 1e-30));
+        }
+    }
+    g->card.upload(d->cardinalities, static_cast<size_t>(V) * 4);
+    g->unary_log.upload(ul.data(), ul.size() * 4);
+    g->table.upload(tb.data(), tb.size() * 4);
+    g->bel_off.upload(bo.data(), bo.size() * 4);
+  }
+  cuda_check(cudaDeviceSynchronize(), "graph upload");
+  return g;
+}
+
+std::unique_ptr<GraphImpl> build_lattice_binary(uint32_t rows, uint32_t cols, const BinaryStreams& s,
+                                                const bp_device_opts* opts) {
+  auto g = std::make_unique<GraphImpl>();
+  g->device = select_device(opts);
+  const uint64_t V = static_cast<uint64_t>(rows) * cols;
+  const uint64_t E = s.coupling.size();
+  if (2 * E >= (1ull << 32)) throw_model("too many edges for 32-bit directed edge ids");
+  g->V = static_cast<uint32_t>(V);
+  g->E = static_cast<uint32_t>(E);
+  g->D = static_cast<uint32_t>(2 * E);
+  g->maxq = V ? 2 : 0;
+  g->binary = true;
+  g->qs = 1;
+  g->uniform_q = 2;
+  g->in_off.alloc((V + 1) * 4);
+  g->in_adj.alloc(2 * E * 4);
+  g->ep.alloc(2 * E * 4);
+  if (V) {
+    k_lattice_topology<<<grid_for(V), 256>>>(rows, cols, g->in_off.as<uint32_t>(), g->in_adj.as<uint32_t>(),
+                                             g->ep.as<uint32_t>());
+    cuda_check(cudaGetLastError(), "lattice topology");
+  } else {
+    cuda_check(cudaMemset(g->in_off.p, 0, 4), "memset");
+  }
+  g->unary_lo.upload(s.unary_lo.data(), V * 4);
+  DevBuf J;
+  J.upload(s.coupling.data(), E * 4);
+  g->epar.alloc(E * 16);
+  if (E) k_ising_params<<<grid_for(E), 256>>>(J.as<float>(), g->E, g->epar.as<float4>());
+  cuda_check(cudaDeviceSynchronize(), "lattice build");
+  return g;
+}
+
+std::unique_ptr<GraphImpl> build_potts(uint32_t n, uint32_t q, const PottsStreams& s,
+                                       const bp_device_opts* opts) {
+  if (q < 2) throw_invalid("potts: q must be >= 2");
+  auto g = std::make_unique<GraphImpl>();
+  g->device = select_device(opts);
+  const uint64_t V = static_cast<uint64_t>(n) * n;
+  const uint64_t E = s.lambda_c.size();
+  if (2 * E >= (1ull << 32)) throw_model("too many edges for 32-bit directed edge ids");
+  g->V = static_cast<uint32_t>(V);
+  g->E = static_cast<uint32_t>(E);
+  g->D = static_cast<uint32_t>(2 * E);
+  g->maxq = q;
+  g->uniform_q = q;
+  g->binary = false;
+  const uint32_t qs = stride_for(q);
+  g->qs = qs;
+  g->in_off.alloc((V + 1) * 4);
+  g->in_adj.alloc(2 * E * 4);
+  g->ep.alloc(2 * E * 4);
+  if (V) {
+    k_lattice_topology<<<grid_for(V), 256>>>(n, n, g->in_off.as<uint32_t>(), g->in_adj.as<uint32_t>(),
+                                             g->ep.as<uint32_t>());
+    cuda_check(cudaGetLastError(), "lattice topology");
+  }
+  std::vector<float> ul(V * qs, 0.f);
+  for (uint64_t v = 0; v < V; ++v)
+    for (uint32_t x = 0; x < q; ++x) ul[v * qs + x] = s.unary_log[v * q + x];
+  g->unary_log.upload(ul.data(), ul.size() * 4);
+  g->card.alloc(V * 4);
+  if (V) k_fill_u32<<<grid_for(V), 256>>>(g->card.as<uint32_t>(), V, q);
+  g->bel_off.alloc((V + 1) * 4);
+  k_iota_mul<<<grid_for(V + 1), 256>>>(g->bel_off.as<uint32_t>(), V + 1, q);
+  DevBuf LC;
+  LC.upload(s.lambda_c.data(), E * 4);
+  g->table.alloc(E * qs * qs * 4);
+  if (E) {
+    const size_t n_el = E * qs * qs;
+    switch (qs) {
+      case 4: k_potts_tables<4><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
+      case 8: k_potts_tables<8><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
+      case 16: k_potts_tables<16><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
+      default: k_potts_tables<32><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
+    }
+  }
+  cuda_check(cudaDeviceSynchronize(), "potts build");
+  return g;
+}
+
+std::unique_ptr<GraphImpl> build_er(uint32_t n, const ErInstance& inst, const bp_device_opts* opts) {
+  auto g = std::make_unique<GraphImpl>();
+  g->device = select_device(opts);
+  const uint32_t E = static_cast<uint32_t>(inst.coupling.size());
+  g->V = n;
+  g->E = E;
+  g->D = 2 * E;
+  g->maxq = n ? 2 : 0;
+  g->uniform_q = 2;
+  g->binary = true;
+  g->qs = 1;
+  std::vector<uint32_t> off, adj;
+  build_csr(n, E, inst.endpoints.data(), off, adj);
+  g->in_off.upload(off.data(), off.size() * 4);
+  g->in_adj.upload(adj.data(), adj.size() * 4);
+  g->ep.upload(inst.endpoints.data(), static_cast<size_t>(E) * 8);
+  g->unary_lo.upload(inst.unary_lo.data(), static_cast<size_t>(n) * 4);
+  DevBuf J;
+  J.upload(inst.coupling.data(), static_cast<size_t>(E) * 4);
+  g->epar.alloc(static_cast<size_t>(E) * 16);
+  if (E) k_ising_params<<<grid_for(E), 256>>>(J.as<float>(), E, g->epar.as<float4>());
+  cuda_check(cudaDeviceSynchronize(), "er build");
+  return g;
+}
+
+// Host copies needed only by the lockstep API (message conversion).
+const std::vector<uint32_t>& GraphImpl::host_ep() const {
+  std::lock_guard<std::mutex> lk(host_mu);
+  if (ep_host.size() != 2ull * E) {
+    ep_host.resize(2ull * E);
+    if (E) cuda_check(cudaMemcpy(ep_host.data(), ep.p, 8ull * E, cudaMemcpyDeviceToHost), "ep download");
+  }
+  return ep_host;
+}
+
+uint32_t GraphImpl::card_of(uint32_t v) const {
+  if (uniform_q) return uniform_q;
+  return cards_host[v];
+}
+
+}  // namespace bpb

@@ -1,0 +1,63 @@
+// Device-resident graph (host handle).  See bp_device.cuh for the layout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "bp_device.cuh"
+#include "bp_internal.hpp"
+
+namespace bpb {
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf();
+  void alloc(size_t n);
+  void upload(const void* src, size_t n);
+  void reset();
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct GraphImpl {
+  int device = 0;
+  uint32_t V = 0, E = 0, D = 0, maxq = 0, qs = 1;
+  uint32_t uniform_q = 0;  // all cardinalities equal to this (0 = mixed)
+  bool binary = true;
+  DevBuf in_off, in_adj, ep, unary_lo, epar, card, unary_log, table, bel_off;
+  std::vector<uint32_t> cards_host;  // mixed cardinalities only
+
+  DevGraph dev() const;
+  uint64_t device_bytes() const;
+  uint64_t unary_size() const {
+    if (uniform_q) return static_cast<uint64_t>(V) * uniform_q;
+    uint64_t n = 0;
+    for (uint32_t c : cards_host) n += c;
+    return n;
+  }
+  uint32_t card_of(uint32_t v) const;
+  const std::vector<uint32_t>& host_ep() const;
+
+  mutable std::mutex host_mu;
+  mutable std::vector<uint32_t> ep_host;
+};
+
+std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_device_opts* opts);
+std::unique_ptr<GraphImpl> build_lattice_binary(uint32_t rows, uint32_t cols, const BinaryStreams& s,
+                                                const bp_device_opts* opts);
+std::unique_ptr<GraphImpl> build_potts(uint32_t n, uint32_t q, const PottsStreams& s,
+                                       const bp_device_opts* opts);
+std::unique_ptr<GraphImpl> build_er(uint32_t n, const ErInstance& inst, const bp_device_opts* opts);
+
+}  // namespace bpb

@@ -1,0 +1,1053 @@
+// CUDA kernels of the B200 BP engine (sm_100a).  See DESIGN.md section 5 for
+// the roofline of each kernel and its algorithmic bytes.
+//
+// Reference correspondence (paths relative to /root/reference/proj/core):
+//   vertex_update  <- refresh_residuals (src/residuals.cpp:26-59) calling
+//                     update_message_into (include/bpsched/messages.hpp:114-151)
+//                     + residual (src/messages.cpp:56-65), and one LBP sweep
+//                     (apply_frontier fast path, src/schedulers.cpp:243-245)
+//   rnbp_select    <- rnbp_frontier (src/schedulers.cpp:194-216) fused with the
+//                     commit loop of apply_frontier (src/schedulers.cpp:231-241)
+//                     and collect_touched (src/schedulers.cpp:31-42)
+//   radix_*        <- select_top_k (src/schedulers.cpp:105-116)
+//   finalize       <- the loop control of run() (src/schedulers.cpp:301-347)
+//   beliefs        <- compute_beliefs (src/messages.cpp:82-105)
+#pragma once
+
+#include "bp_device.cuh"
+
+namespace bpb {
+
+enum UpdateMode : int {
+  kModeCount = 0,  // LBP sweep: write next messages, count r >= eps
+  kModeInit = 1,   // first refresh: write candidates + residuals, count r >= eps
+  kModeDelta = 2,  // refresh: write candidates + residuals, count (now - was)
+};
+
+enum FinMode : int { kFinNone = 0, kFinLbp = 1, kFinInit = 2, kFinIter = 3, kFinApply = 4 };
+
+constexpr int kSinkCap = 4096;
+
+// Block-level staging of list appends: pushes go to shared memory (spilling
+// straight to the global list when full), flushes reserve the block's range
+// with one global atomic.
+struct Stager {
+  uint32_t* sbuf;     // shared, cap entries
+  unsigned* scount;   // shared
+  unsigned* sbase;    // shared
+  unsigned cap;
+  uint32_t* gdst;     // global list
+  unsigned* gcount;   // global counter
+
+  __device__ __forceinline__ void init() {
+    if (threadIdx.x == 0) *scount = 0;
+    __syncthreads();
+  }
+  // any thread, any time (shared atomic per push)
+  __device__ __forceinline__ void push(uint32_t x) {
+    const unsigned i = atomicAdd(scount, 1u);
+    if (i < cap)
+      sbuf[i] = x;
+    else
+      gdst[atomicAdd(gcount, 1u)] = x;
+  }
+  // warp-aggregated push; all lanes of the warp must call it
+  __device__ __forceinline__ void push_warp(bool pred, uint32_t x) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (mask == 0) return;
+    const unsigned leader = __ffs(mask) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(scount, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) {
+      const unsigned i = base + __popc(mask & ((1u << lane) - 1u));
+      if (i < cap)
+        sbuf[i] = x;
+      else
+        gdst[atomicAdd(gcount, 1u)] = x;
+    }
+  }
+  // block-uniform: flush when fewer than `room` slots remain (room == 0: always)
+  __device__ __forceinline__ void flush(unsigned room) {
+    __syncthreads();
+    const unsigned n0 = *scount;
+    const unsigned n = n0 < cap ? n0 : cap;
+    if (n == 0 || (room && n0 + room <= cap)) return;
+    __syncthreads();
+    if (threadIdx.x == 0) *sbase = atomicAdd(gcount, n);
+    __syncthreads();
+    const unsigned gb = *sbase;
+    for (unsigned i = threadIdx.x; i < n; i += blockDim.x) gdst[gb + i] = sbuf[i];
+    __syncthreads();
+    if (threadIdx.x == 0) *scount = 0;
+    __syncthreads();
+  }
+};
+
+#define BPB_STAGER(name, capacity, dst, counter)          \
+  __shared__ uint32_t name##_buf[capacity];               \
+  __shared__ unsigned name##_cnt, name##_base;            \
+  Stager name{name##_buf, &name##_cnt, &name##_base, capacity, dst, counter}
+
+
+// ---------------------------------------------------------------------------
+// accumulation: block reduction, then <= 6 atomics into slot blockIdx % kSlots
+
+struct Contrib {
+  long long delta = 0;
+  unsigned long long count = 0, frontier = 0, survivors = 0, evals = 0, visits = 0;
+};
+
+__device__ __forceinline__ void block_accumulate(Ctl* ctl, const Contrib& c) {
+  __shared__ unsigned long long sh[6][32];
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  unsigned long long v[6] = {static_cast<unsigned long long>(c.delta), c.count, c.frontier, c.survivors,
+                             c.evals, c.visits};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) sh[k][wid] = v[k];
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned nw = blockDim.x >> 5;
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      unsigned long long x = lane < nw ? sh[k][lane] : 0ull;
+      x = warp_sum(x);
+      if (static_cast<int>(lane) == k) mine = x;
+    }
+    if (lane < 6 && mine) {
+      Accum& a = ctl->acc[blockIdx.x % kSlots];
+      unsigned long long* f = lane == 0 ? reinterpret_cast<unsigned long long*>(&a.delta)
+                              : lane == 1 ? &a.count
+                              : lane == 2 ? &a.frontier
+                              : lane == 3 ? &a.survivors
+                              : lane == 4 ? &a.evals
+                                          : &a.visits;
+      atomicAdd(f, mine);
+    }
+  }
+}
+
+// Early exit of every loop kernel once the run is over; inside the device-side
+// WHILE loop it also clears the loop condition.
+__device__ __forceinline__ bool run_done(Ctl* c) {
+  if (!c->done) return false;
+  if (c->cond_handle && blockIdx.x == 0 && threadIdx.x == 0)
+    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(c->cond_handle), 0u);
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// finalize: one block reduces the slots and restates the loop control of
+// run() (schedulers.cpp:301-347).
+
+__device__ __forceinline__ void fin_record(Ctl* c, unsigned long long it, unsigned long long fs,
+                                           unsigned un) {
+  TraceRec& r = c->trace[it % kTraceRing];
+  r.iteration = it;
+  r.frontier_size = fs;
+  r.unconverged = un;
+  r.elapsed_seconds = 1e-9 * static_cast<double>(globaltimer_ns() - c->t0_ns);
+  c->trace_len = it + 1;
+}
+
+// top of the loop: converged check BEFORE the cap check (schedulers.cpp:302-309)
+__device__ __forceinline__ void fin_check_top(Ctl* c) {
+  if (c->numeric_error) {
+    c->done = 1;
+    c->stop_reason = kStopNumeric;
+    return;
+  }
+  if (c->unconverged == 0) {
+    c->converged = 1;
+    c->done = 1;
+    c->stop_reason = kStopConverged;
+    return;
+  }
+  if (c->iteration >= c->max_iterations) {
+    c->done = 1;
+    c->stop_reason = kStopMaxIter;
+  } else if (globaltimer_ns() - c->t0_ns >= c->time_limit_ns) {
+    c->done = 1;
+    c->stop_reason = kStopTime;
+  }
+}
+
+__device__ __forceinline__ void fin_reset_scratch(Ctl* c) {
+  c->frontier = 0;
+  c->survivors = 0;
+  c->nflag = 0;
+  c->dense = 0;
+  c->stamp += 1;
+  c->rx_prefix = 0;
+  c->rx_above = 0;
+}
+
+// <<<1, kSlots>>>
+__global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D) {
+  if (run_done(c)) return;
+  const int t = threadIdx.x;
+  const Accum a = c->acc[t];
+  c->acc[t] = Accum{};
+  __shared__ unsigned long long sh[6][kSlots / 32];
+  unsigned long long v[6] = {static_cast<unsigned long long>(a.delta), a.count, a.frontier, a.survivors,
+                             a.evals, a.visits};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[k] = warp_sum(v[k]);
+  if ((t & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) sh[k][t >> 5] = v[k];
+  __syncthreads();
+  if (t != 0) return;
+  for (int k = 0; k < 6; ++k) {
+    v[k] = 0;
+    for (int w = 0; w < kSlots / 32; ++w) v[k] += sh[k][w];
+  }
+  const long long delta = static_cast<long long>(v[0]);
+  const unsigned long long count = v[1], frontier = v[2] + c->frontier;
+  c->evals_total += v[4];
+  c->vertex_visits += v[5];
+  switch (mode) {
+    case kFinLbp: {  // sweep s computed r(m_s): it closes iteration s-1
+      const unsigned long long s = c->sweeps;
+      if (s > 0) {
+        fin_record(c, s - 1, D, static_cast<unsigned>(count));
+        c->msgs_total += D;
+      }
+      c->iteration = s;
+      c->unconverged = static_cast<unsigned>(count);
+      c->sweeps = s + 1;
+      fin_reset_scratch(c);
+      fin_check_top(c);
+      break;
+    }
+    case kFinInit:
+      c->unconverged = static_cast<unsigned>(count);
+      c->iteration = 0;
+      fin_reset_scratch(c);
+      fin_check_top(c);
+      break;
+    case kFinIter: {
+      const unsigned start = c->unconverged;
+      c->unconverged = static_cast<unsigned>(static_cast<long long>(start) + delta);
+      fin_record(c, c->iteration, frontier, c->unconverged);
+      c->msgs_total += frontier;
+      c->prev_unconverged = start;  // set_prev_unconverged (schedulers.cpp:327)
+      c->has_prev = 1;
+      c->iteration += 1;
+      if (c->use_clist) {
+        c->cl_cur ^= 1u;
+        c->cl_n[c->cl_cur ^ 1u] = 0;
+      }
+      fin_reset_scratch(c);
+      fin_check_top(c);
+      break;
+    }
+    case kFinApply:
+      c->unconverged = static_cast<unsigned>(static_cast<long long>(c->unconverged) + delta);
+      fin_reset_scratch(c);
+      break;
+    default:
+      break;
+  }
+  if (c->cond_handle && mode != kFinApply)
+    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(c->cond_handle), c->done ? 0u : 1u);
+}
+
+// ---------------------------------------------------------------------------
+// vertex-centric sum-product update.  One thread owns vertex v: it reads every
+// incoming message of v once (edge pair loads), forms the vertex total in log
+// space, and for each incoming edge `in` produces the outgoing message
+// out = in ^ 1 from the cavity (total minus the message on `in`).  This is
+// refresh_residuals over the outgoing edges of v: each message is read once
+// per vertex and written once, instead of deg times as in the edge-parallel
+// reference loop.
+
+// CL: candidate-list maintenance (RnBP): an outgoing edge whose residual is
+// >= eps and that is not in the list yet is pushed to `cl`.
+template <int MODE, bool CL>
+__device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t v,
+                                                    const float* __restrict__ A,
+                                                    float* __restrict__ B, float* __restrict__ res,
+                                                    float eps, unsigned* numeric_flag,
+                                                    unsigned long long& evals, uint8_t* inlist,
+                                                    Stager* cl) {
+  const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
+  float T = g.unary_lo[v];
+  const float2* __restrict__ A2 = reinterpret_cast<const float2*>(A);
+  for (uint32_t a = b; a < e; ++a) {
+    const uint32_t in = g.in_adj[a];
+    const float2 pr = __ldg(&A2[in >> 1]);
+    T += (in & 1u) ? pr.y : pr.x;
+  }
+  int cnt = 0;
+  for (uint32_t a = b; a < e; ++a) {
+    const uint32_t in = g.in_adj[a];
+    const uint32_t out = in ^ 1u;
+    const float2 pr = __ldg(&A2[in >> 1]);
+    const float4 par = __ldg(&g.epar[in >> 1]);
+    const float r_was = MODE == kModeDelta ? res[out] : 0.f;
+    const float m_in = (in & 1u) ? pr.y : pr.x;
+    const float m_old = (in & 1u) ? pr.x : pr.y;
+    const float lnew = binary_update(T - m_in, par, (out & 1u) != 0u);
+    const float r = binary_residual(lnew, m_old);
+    if (!(fabsf(lnew) < INFINITY)) *numeric_flag = 1u;
+    B[out] = lnew;
+    const int now = r >= eps;
+    if (MODE == kModeDelta) {
+      cnt += now - (r_was >= eps);
+      res[out] = r;
+    } else {
+      if (MODE == kModeInit) res[out] = r;
+      cnt += now;
+    }
+    if (CL && now && !inlist[out]) {
+      inlist[out] = 1;
+      cl->push(out);
+    }
+  }
+  evals += e - b;
+  return cnt;
+}
+
+template <int QS, int MODE, bool CL>
+__device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t v,
+                                                     const float* __restrict__ A,
+                                                     float* __restrict__ B, float* __restrict__ res,
+                                                     float eps, unsigned* numeric_flag,
+                                                     unsigned long long& evals, uint8_t* inlist,
+                                                     Stager* cl) {
+  const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
+  const uint32_t ci = g.card[v];
+  float T[QS];
+#pragma unroll
+  for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
+  for (uint32_t a = b; a < e; ++a) {
+    const float* m = A + static_cast<size_t>(g.in_adj[a]) * QS;
+#pragma unroll
+    for (int x = 0; x < QS; ++x) T[x] += __ldg(&m[x]);
+  }
+  int cnt = 0;
+  for (uint32_t a = b; a < e; ++a) {
+    const uint32_t in = g.in_adj[a];
+    const uint32_t out = in ^ 1u;
+    const uint32_t edge = in >> 1;
+    const uint32_t tgt = g.ep[in];  // source of `in` = target of `out`
+    const uint32_t cj = g.card[tgt];
+    const float* m_in = A + static_cast<size_t>(in) * QS;
+    const float r_was = MODE == kModeDelta ? res[out] : 0.f;
+    float p[QS];
+    float M = -INFINITY;
+#pragma unroll
+    for (int x = 0; x < QS; ++x) {
+      p[x] = T[x] - __ldg(&m_in[x]);
+      if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
+    }
+#pragma unroll
+    for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
+    const float* tab = g.table + static_cast<size_t>(edge) * QS * QS;
+    float o[QS];
+    float s = 0.f;
+    if ((out & 1u) == 0u) {  // v is lo: A(xs, xt) = T[xs][xt]
+#pragma unroll
+      for (int xt = 0; xt < QS; ++xt) o[xt] = 0.f;
+#pragma unroll
+      for (int xs = 0; xs < QS; ++xs) {
+#pragma unroll
+        for (int xt = 0; xt < QS; ++xt) o[xt] = fmaf(__ldg(&tab[xs * QS + xt]), p[xs], o[xt]);
+      }
+    } else {  // v is hi: A(xs, xt) = T[xt][xs]
+#pragma unroll
+      for (int xt = 0; xt < QS; ++xt) {
+        float acc = 0.f;
+#pragma unroll
+        for (int xs = 0; xs < QS; ++xs) acc = fmaf(__ldg(&tab[xt * QS + xs]), p[xs], acc);
+        o[xt] = acc;
+      }
+    }
+#pragma unroll
+    for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
+    const float inv = __frcp_rn(s);
+    const float* m_old = A + static_cast<size_t>(out) * QS;
+    float* dst = B + static_cast<size_t>(out) * QS;
+    float r = 0.f;
+#pragma unroll
+    for (int xt = 0; xt < QS; ++xt) {
+      if (xt < static_cast<int>(cj)) {
+        const float pn = o[xt] * inv;
+        const float po = __expf(__ldg(&m_old[xt]));
+        r = fmaxf(r, fabsf(pn - po));
+        dst[xt] = __logf(pn);
+      }
+    }
+    if (!(s > 0.f) || !(s < INFINITY)) *numeric_flag = 1u;
+    const int now = r >= eps;
+    if (MODE == kModeDelta) {
+      cnt += now - (r_was >= eps);
+      res[out] = r;
+    } else {
+      if (MODE == kModeInit) res[out] = r;
+      cnt += now;
+    }
+    if (CL && now && !inlist[out]) {
+      inlist[out] = 1;
+      cl->push(out);
+    }
+  }
+  evals += e - b;
+  return cnt;
+}
+
+// QS == 1 selects the binary layout.
+template <int QS, int MODE, bool CL>
+__device__ __forceinline__ int vertex_update(const DevGraph& g, uint32_t v, const float* A, float* B,
+                                             float* res, float eps, unsigned* nf,
+                                             unsigned long long& evals, uint8_t* inlist, Stager* cl) {
+  if constexpr (QS == 1)
+    return vertex_update_binary<MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl);
+  else
+    return vertex_update_generic<QS, MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl);
+}
+
+// Sweep over all vertices (LIST = false) or over the vertices flagged this
+// iteration (collect_touched): sparse iterations walk vlist, dense ones scan
+// vflag in vertex order so the accesses stay coalesced.
+// For the LBP sweep the source/destination buffers alternate with the sweep
+// index held on the device (A = buf[s & 1], B = buf[(s + 1) & 1]).
+// CL: maintain the RnBP candidate list (init appends to list cl_cur, the
+// refresh to list cl_cur ^ 1, which the select of this iteration is filling).
+struct CandList {
+  uint32_t* list[2];
+  uint8_t* inlist;
+};
+
+template <int QS, int MODE, bool LIST, bool PINGPONG, bool CL>
+__global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const float* A0, float* B0,
+                                                          float* res, const uint32_t* vlist,
+                                                          const uint32_t* vflag, Ctl* ctl, float eps,
+                                                          CandList cand_list) {
+  if (run_done(ctl)) return;
+  const float* A = A0;
+  float* B = B0;
+  if (PINGPONG) {
+    if (ctl->sweeps & 1ull) {
+      A = B0;
+      B = const_cast<float*>(A0);
+    }
+  }
+  const bool dense = !LIST || ctl->dense;
+  const uint32_t n = dense ? g.V : ctl->nflag;
+  const uint32_t stamp = LIST ? ctl->stamp : 0u;
+  const unsigned tgt_list = CL ? (MODE == kModeInit ? ctl->cl_cur : ctl->cl_cur ^ 1u) : 0u;
+  BPB_STAGER(cl, CL ? 2048 : 1, CL ? (tgt_list ? cand_list.list[1] : cand_list.list[0]) : nullptr, &ctl->cl_n[tgt_list]);
+  if (CL) cl.init();
+  int cnt = 0;
+  unsigned long long evals = 0, visits = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    const uint32_t i = base + threadIdx.x;
+    if (i < n) {
+      uint32_t v = i;
+      bool go = true;
+      if (LIST) {
+        if (dense)
+          go = vflag[i] == stamp;
+        else
+          v = vlist[i];
+      }
+      if (go) {
+        cnt += vertex_update<QS, MODE, CL>(g, v, A, B, res, eps, &ctl->numeric_error, evals, cand_list.inlist, &cl);
+        ++visits;
+      }
+    }
+    if (CL) cl.flush(1024);
+  }
+  if (CL) cl.flush(0);
+  Contrib c;
+  if (MODE == kModeDelta)
+    c.delta = cnt;
+  else
+    c.count = static_cast<unsigned long long>(cnt);
+  c.evals = evals;
+  c.visits = visits;
+  block_accumulate(ctl, c);
+}
+
+// ---------------------------------------------------------------------------
+// initial messages (init_messages, messages.cpp:23-39): uniform over the
+// target's states; binary log-odds 0.
+
+template <int QS>
+__global__ void k_init_messages(DevGraph g, float* M, Ctl* ctl, int set_t0) {
+  if (set_t0 && blockIdx.x == 0 && threadIdx.x == 0) ctl->t0_ns = globaltimer_ns();
+  const size_t n = static_cast<size_t>(g.D) * QS;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (QS == 1) {
+      M[i] = 0.f;
+    } else {
+      const uint32_t d = static_cast<uint32_t>(i / QS);
+      const uint32_t x = static_cast<uint32_t>(i % QS);
+      const uint32_t q = g.card[g.ep[d ^ 1u]];
+      M[i] = x < q ? -__logf(static_cast<float>(q)) : 0.f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Frontier commit and touched-vertex flagging.
+//
+// commit: live <- candidate (MessageStore::write, messages.cpp:11-13) and
+// r <- 0 (the candidate of d is unchanged unless its source is touched, in
+// which case the refresh recomputes it); its target joins the touched set
+// (collect_touched: every outgoing edge of tgt(d)).  Dense iterations mark
+// vflag with plain stores; sparse ones dedupe with atomicMax and stage new
+// vertices in shared memory, one global append per block flush.
+
+template <int QS>
+__device__ __forceinline__ void commit_edge(const DevGraph& g, uint32_t d, float r, float* live,
+                                            const float* cand, float* res, float eps,
+                                            uint32_t* vflag, uint32_t stamp, bool dense, Contrib& c,
+                                            bool& new_flag, uint32_t& tgt) {
+  c.delta -= (r >= eps) ? 1 : 0;
+  c.frontier += 1;
+  res[d] = 0.f;
+#pragma unroll
+  for (int x = 0; x < QS; ++x) live[static_cast<size_t>(d) * QS + x] = cand[static_cast<size_t>(d) * QS + x];
+  tgt = g.ep[d ^ 1u];
+  if (dense) {
+    vflag[tgt] = stamp;
+    new_flag = false;
+  } else {
+    new_flag = atomicMax(&vflag[tgt], stamp) < stamp;
+  }
+}
+
+// select_parallelism (schedulers.cpp:218-224)
+__device__ __forceinline__ double device_p_now(const Ctl* c, double low_p, double high_p,
+                                               double thr) {
+  if (!c->has_prev || c->prev_unconverged == 0) return high_p;
+  const double ratio = static_cast<double>(c->unconverged) / static_cast<double>(c->prev_unconverged);
+  return ratio > thr ? low_p : high_p;
+}
+
+struct RnbpParams {
+  unsigned long long seed;
+  double low_p, high_p, thr;
+  double fixed_p;  // >= 0: lockstep override of p_now
+  int commit;      // 0: only mark `sel` (lockstep frontier query)
+};
+
+// rnbp_frontier (schedulers.cpp:194-216) attempt 0, fused with the commit of
+// apply_frontier: filter 1 (r >= eps), filter 2 Bernoulli(p_now) with Philox.
+//
+// CL = false: scan every residual (4 per thread per trip, one 16-byte load;
+// res is padded to a multiple of 4 with zeros).
+// CL = true: scan the candidate list (a superset of the edges with r >= eps,
+// maintained by the refresh): converged entries and committed edges leave the
+// list, surviving unselected ones are kept in the next list, so the cost of an
+// iteration follows the unconverged count instead of 2|E|.  The Bernoulli draw
+// is keyed by the edge id, so list order does not matter.
+template <int QS, bool CL>
+__global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live, const float* cand,
+                                                        float* res, uint32_t* vflag, uint32_t* vlist,
+                                                        uint8_t* sel, Ctl* ctl, float eps,
+                                                        RnbpParams prm, CandList cl) {
+  if (run_done(ctl)) return;
+  const double p = prm.fixed_p >= 0.0 ? prm.fixed_p : device_p_now(ctl, prm.low_p, prm.high_p, prm.thr);
+  const unsigned long long thresh = static_cast<unsigned long long>(ceil(ldexp(p, 53)));
+  const unsigned long long it = ctl->iteration;
+  const uint32_t stamp = ctl->stamp;
+  // dense iterations (expected frontier > V/16) flag without a list
+  const bool dense =
+      prm.commit && static_cast<double>(ctl->unconverged) * p > static_cast<double>(g.V) / 16.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dense = dense ? 1u : 0u;
+  BPB_STAGER(fl, 2048, vlist, &ctl->nflag);
+  const unsigned cur = CL ? ctl->cl_cur : 0u;
+  BPB_STAGER(keep, CL ? 2048 : 1, CL ? (cur ? cl.list[0] : cl.list[1]) : nullptr, &ctl->cl_n[cur ^ 1u]);
+  fl.init();
+  if (CL) keep.init();
+  Contrib c;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  if (!CL) {
+    const uint32_t D4 = (g.D + 3) / 4;
+    const float4* res4 = reinterpret_cast<const float4*>(res);
+    for (uint32_t base = blockIdx.x * blockDim.x; base < D4; base += stride) {
+      const uint32_t q = base + threadIdx.x;
+      bool nf[4] = {false, false, false, false};
+      uint32_t tg[4] = {0, 0, 0, 0};
+      if (q < D4) {
+        const float4 r4 = res4[q];
+        const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t d = 4 * q + k;
+          if (rr[k] >= eps) {  // padding entries are 0
+            c.survivors += 1;
+            if (philox_u53(prm.seed, it, 0u, d) < thresh) {
+              if (prm.commit) {
+                commit_edge<QS>(g, d, rr[k], live, cand, res, eps, vflag, stamp, dense, c, nf[k], tg[k]);
+              } else {
+                sel[d] = 1;
+                c.frontier += 1;
+              }
+            }
+          }
+        }
+      }
+      if (prm.commit && !dense) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fl.push_warp(nf[k], tg[k]);
+        fl.flush(4 * kBlock);
+      }
+    }
+  } else {
+    const uint32_t n = ctl->cl_n[cur];
+    const uint32_t* list = cur ? cl.list[1] : cl.list[0];
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+      const uint32_t i = base + threadIdx.x;
+      bool nf = false, kept = false;
+      uint32_t tg = 0, d = 0;
+      if (i < n) {
+        d = list[i];
+        const float r = res[d];
+        if (r >= eps) {
+          c.survivors += 1;
+          if (philox_u53(prm.seed, it, 0u, d) < thresh) {
+            cl.inlist[d] = 0;
+            commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, dense, c, nf, tg);
+          } else {
+            kept = true;
+          }
+        } else {
+          cl.inlist[d] = 0;
+        }
+      }
+      keep.push_warp(kept, d);
+      keep.flush(kBlock);
+      if (!dense) {
+        fl.push_warp(nf, tg);
+        fl.flush(kBlock);
+      }
+    }
+    keep.flush(0);
+  }
+  if (prm.commit && !dense) fl.flush(0);
+  block_accumulate(ctl, c);
+}
+
+// Retry + fallback of rnbp_frontier (schedulers.cpp:204-214), single block:
+// reduces the attempt-0 frontier and survivor counts; when the frontier came
+// back empty it redraws every survivor once (attempt 1) and, if still empty,
+// commits survivors[min(S-1, floor(u*S))] in ascending id order.  The redraw
+// runs only on that rare path, so one block suffices.  With the candidate
+// list the survivors are exactly the kept list.
+template <int QS, bool CL>
+__global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, const float* cand,
+                                                     float* res, uint32_t* vflag, uint32_t* vlist,
+                                                     uint8_t* sel, Ctl* ctl, float eps, RnbpParams prm,
+                                                     CandList cl) {
+  if (run_done(ctl)) return;
+  __shared__ unsigned long long s_front, s_surv;
+  __shared__ unsigned warp_tot[32];
+  __shared__ unsigned long long running_s;
+  __shared__ int found;
+  if (threadIdx.x < 32) {
+    unsigned long long f = 0, s = 0;
+    for (int k = threadIdx.x; k < kSlots; k += 32) {
+      f += ctl->acc[k].frontier;
+      s += ctl->acc[k].survivors;
+    }
+    f = warp_sum(f);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) {
+      s_front = f;
+      s_surv = s;
+      ctl->survivors = s;
+    }
+  }
+  __syncthreads();
+  if (s_front > 0 || s_surv == 0) return;
+  const double p = prm.fixed_p >= 0.0 ? prm.fixed_p : device_p_now(ctl, prm.low_p, prm.high_p, prm.thr);
+  const unsigned long long thresh = static_cast<unsigned long long>(ceil(ldexp(p, 53)));
+  const unsigned long long it = ctl->iteration;
+  const uint32_t stamp = ctl->stamp;
+  if (threadIdx.x == 0) {
+    ctl->dense = 0;
+    found = 0;
+    running_s = 0;
+  }
+  __syncthreads();
+  // attempt 1: every survivor redrawn
+  unsigned long long fr = 0;
+  long long delta = 0;
+  const uint32_t n = CL ? ctl->cl_n[ctl->cl_cur ^ 1u] : g.D;
+  const uint32_t* list = CL ? (ctl->cl_cur ? cl.list[0] : cl.list[1]) : nullptr;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t d = CL ? list[i] : i;
+    const float r = res[d];
+    if (r >= eps && philox_u53(prm.seed, it, 1u, d) < thresh) {
+      ++fr;
+      if (prm.commit) {
+        Contrib c;
+        bool nf = false;
+        uint32_t tg = 0;
+        commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, false, c, nf, tg);
+        delta += c.delta;
+        if (nf) vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
+      } else {
+        sel[d] = 1;
+      }
+    }
+  }
+  __shared__ unsigned long long sh_f[32];
+  __shared__ long long sh_d[32];
+  fr = block_sum(fr, sh_f);
+  delta = block_sum(delta, sh_d);
+  if (threadIdx.x == 0) {
+    ctl->frontier = fr;  // counted here; the attempt-0 slots hold 0
+    if (delta)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->acc[0].delta), static_cast<unsigned long long>(delta));
+    s_front = fr;
+  }
+  __syncthreads();
+  if (s_front > 0) return;
+  // fallback: one uniformly chosen survivor, ascending id order
+  const unsigned long long S = s_surv;
+  const double u = static_cast<double>(philox_u53(prm.seed, it, 2u, 0ull)) * 0x1.0p-53;
+  unsigned long long pick = static_cast<unsigned long long>(u * static_cast<double>(S));
+  if (pick > S - 1) pick = S - 1;
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  for (size_t base = 0; base < g.D; base += blockDim.x) {
+    const size_t di = base + threadIdx.x;
+    const bool f = di < g.D && res[di] >= eps;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) warp_tot[wid] = __popc(m);
+    __syncthreads();
+    unsigned before = 0, total = 0;
+    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
+      if (w < wid) before += warp_tot[w];
+      total += warp_tot[w];
+    }
+    const unsigned long long rank = running_s + before + __popc(m & ((1u << lane) - 1u));
+    if (f && rank == pick) {
+      const uint32_t d = static_cast<uint32_t>(di);
+      if (prm.commit) {
+        Contrib c;
+        bool nf = false;
+        uint32_t tg = 0;
+        commit_edge<QS>(g, d, res[d], live, cand, res, eps, vflag, stamp, false, c, nf, tg);
+        if (nf) vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->acc[0].delta),
+                  static_cast<unsigned long long>(c.delta));
+      } else {
+        sel[d] = 1;
+      }
+      ctl->frontier = 1;
+      found = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) running_s += total;
+    __syncthreads();
+    if (found) break;
+  }
+}
+
+// Commit of a host-supplied frontier (lockstep apply_frontier).
+template <int QS>
+__global__ void __launch_bounds__(kBlock) k_commit_list(DevGraph g, const uint32_t* list, uint32_t n,
+                                                        float* live, const float* cand, float* res,
+                                                        uint32_t* vflag, uint32_t* vlist, Ctl* ctl,
+                                                        float eps, int dense) {
+  BPB_STAGER(fl, 2048, vlist, &ctl->nflag);
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dense = dense;
+  fl.init();
+  const uint32_t stamp = ctl->stamp;
+  Contrib c;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    bool nf = false;
+    uint32_t tgt = 0;
+    if (i < n) {
+      const uint32_t d = list[i];
+      commit_edge<QS>(g, d, res[d], live, cand, res, eps, vflag, stamp, dense != 0, c, nf, tgt);
+    }
+    if (!dense) {
+      fl.push_warp(nf, tgt);
+      fl.flush(kBlock);
+    }
+  }
+  if (!dense) fl.flush(0);
+  block_accumulate(ctl, c);
+}
+
+// ---------------------------------------------------------------------------
+// RBP top-k (select_top_k, schedulers.cpp:105-116): exact radix select of the
+// k-th largest residual over the 32-bit float pattern (residuals are >= +0,
+// so the unsigned order equals the float order), three passes of 12/12/8
+// bits, then a commit pass; ties at the threshold go to the lowest ids via
+// per-chunk tie counts.
+
+constexpr int kRadixBins = 4096;
+
+__device__ __forceinline__ uint32_t float_key(float r) { return __float_as_uint(r); }
+
+// pass 0: bins key>>20; pass 1: (key>>8)&0xfff for key>>20 == prefix;
+// pass 2: key&0xff for key>>8 == prefix
+__global__ void __launch_bounds__(kBlock) k_radix_hist(const float* res, uint32_t D, int pass,
+                                                       unsigned* hist, Ctl* ctl) {
+  if (run_done(ctl)) return;
+  __shared__ unsigned sh[kRadixBins];
+  const int nb = pass == 2 ? 256 : kRadixBins;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t prefix = ctl->rx_prefix;
+  const uint32_t D4 = (D + 3) / 4;
+  const float4* res4 = reinterpret_cast<const float4*>(res);
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < D4; q += gridDim.x * blockDim.x) {
+    const float4 r4 = res4[q];
+    const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (4 * q + k >= D) break;
+      const uint32_t key = float_key(rr[k]);
+      if (pass == 0) {
+        atomicAdd(&sh[key >> 20], 1u);
+      } else if (pass == 1) {
+        if ((key >> 20) == prefix) atomicAdd(&sh[(key >> 8) & 0xfffu], 1u);
+      } else {
+        if ((key >> 8) == prefix) atomicAdd(&sh[key & 0xffu], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// Single block of 1024: find the bin holding the k-th largest key (counting
+// from the top), extend the prefix, accumulate the count strictly above it and
+// clear the histogram for the next use.
+__global__ void __launch_bounds__(1024) k_radix_scan(unsigned* hist, int pass, unsigned long long k,
+                                                     Ctl* ctl) {
+  if (run_done(ctl)) return;
+  __shared__ unsigned long long wsum[32];
+  const int nb = pass == 2 ? 256 : kRadixBins;
+  const int per = nb / 1024 > 0 ? nb / 1024 : 1;
+  const int t = threadIdx.x;
+  // thread t owns bins [lo, lo+per) counted from the TOP: bin index nb-1-(t*per+j)
+  unsigned long long mine = 0;
+  if (t * per < nb)
+    for (int j = 0; j < per; ++j) mine += hist[nb - 1 - (t * per + j)];
+  // exclusive scan of `mine` across the block (in top-down order)
+  unsigned long long v = mine;
+  const unsigned lane = t & 31, wid = t >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= static_cast<unsigned>(o)) v += n;
+  }
+  if (lane == 31) wsum[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long n = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= static_cast<unsigned>(o)) w += n;
+    }
+    wsum[lane] = w;  // inclusive
+  }
+  __syncthreads();
+  const unsigned long long excl = v - mine + (wid ? wsum[wid - 1] : 0ull);
+  const unsigned long long above0 = ctl->rx_above;
+  const unsigned long long need = k - above0;  // >= 1
+  if (t * per < nb && excl < need && need <= excl + mine) {
+    unsigned long long acc = excl;
+    for (int j = 0; j < per; ++j) {
+      const int bin = nb - 1 - (t * per + j);
+      const unsigned c = hist[bin];
+      if (acc < need && need <= acc + c) {
+        const int bits = pass == 2 ? 8 : 12;
+        ctl->rx_prefix = (pass == 0 ? 0u : (ctl->rx_prefix << bits)) | static_cast<unsigned>(bin);
+        ctl->rx_above = above0 + acc;
+        ctl->rx_ties = c;
+        ctl->rx_need = static_cast<unsigned>(need - acc);
+        break;
+      }
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int i = t; i < nb; i += blockDim.x) hist[i] = 0;
+}
+
+constexpr uint32_t kTieChunk = 8192;
+
+// per-chunk count of keys equal to the threshold (only when not all ties are taken)
+__global__ void __launch_bounds__(kBlock) k_tie_count(const float* res, uint32_t D, unsigned* chunk_cnt,
+                                                      Ctl* ctl) {
+  if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
+  const uint32_t key = ctl->rx_prefix;
+  const size_t c0 = static_cast<size_t>(blockIdx.x) * kTieChunk;
+  unsigned n = 0;
+  for (size_t d = c0 + threadIdx.x; d < c0 + kTieChunk && d < D; d += blockDim.x)
+    n += float_key(res[d]) == key;
+  __shared__ unsigned sh[kBlock / 32];
+  const unsigned tot = block_sum(n, sh);
+  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = tot;
+}
+
+// exclusive prefix over chunk counts (single block)
+__global__ void __launch_bounds__(1024) k_tie_scan(unsigned* chunk_cnt, uint32_t nchunks, Ctl* ctl) {
+  if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
+  __shared__ unsigned wsum[32];
+  __shared__ unsigned carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < nchunks; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const unsigned c = i < nchunks ? chunk_cnt[i] : 0u;
+    unsigned v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= static_cast<unsigned>(o)) v += n;
+    }
+    if (lane == 31) wsum[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned n = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= static_cast<unsigned>(o)) w += n;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const unsigned excl = v - c + (wid ? wsum[wid - 1] : 0u) + carry;
+    if (i < nchunks) chunk_cnt[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+}
+
+// Commit the top-k: key > K*, or key == K* with tie rank < need.
+// One block per tie chunk so tie ranks follow ascending edge id.
+template <int QS>
+__global__ void __launch_bounds__(kBlock) k_rbp_commit(DevGraph g, float* live, const float* cand,
+                                                       float* res, uint32_t* vflag, uint32_t* vlist,
+                                                       uint8_t* sel, const unsigned* chunk_off,
+                                                       Ctl* ctl, float eps, int select_all,
+                                                       int commit, int dense) {
+  if (run_done(ctl)) return;
+  BPB_STAGER(fl, 2048, vlist, &ctl->nflag);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && commit) ctl->dense = dense;
+  fl.init();
+  const uint32_t key = ctl->rx_prefix;
+  const bool rank_ties = !select_all && ctl->rx_need != ctl->rx_ties;
+  const unsigned need = ctl->rx_need;
+  const uint32_t stamp = ctl->stamp;
+  __shared__ unsigned wt[kBlock / 32];
+  __shared__ unsigned running;
+  if (threadIdx.x == 0) running = rank_ties ? chunk_off[blockIdx.x] : 0u;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  Contrib c;
+  const size_t c0 = static_cast<size_t>(blockIdx.x) * kTieChunk;
+  for (size_t base = c0; base < c0 + kTieChunk && base < g.D; base += blockDim.x) {
+    const size_t di = base + threadIdx.x;
+    const bool valid = di < g.D && di < c0 + kTieChunk;
+    const float r = valid ? res[di] : 0.f;
+    const uint32_t k = float_key(r);
+    bool take = valid && (select_all || k > key);
+    const bool tie = valid && !select_all && k == key;
+    if (rank_ties) {
+      const unsigned m = __ballot_sync(0xffffffffu, tie);
+      if (lane == 0) wt[wid] = __popc(m);
+      __syncthreads();
+      unsigned before = 0, total = 0;
+      for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
+        if (w < wid) before += wt[w];
+        total += wt[w];
+      }
+      const unsigned rank = running + before + __popc(m & ((1u << lane) - 1u));
+      if (tie && rank < need) take = true;
+      __syncthreads();
+      if (threadIdx.x == 0) running += total;
+    } else if (tie) {
+      take = true;
+    }
+    bool nf = false;
+    uint32_t tgt = 0;
+    if (take) {
+      if (commit) {
+        commit_edge<QS>(g, static_cast<uint32_t>(di), r, live, cand, res, eps, vflag, stamp, dense != 0, c, nf,
+                        tgt);
+      } else {
+        sel[di] = 1;
+        c.frontier += 1;
+      }
+    }
+    if (commit && !dense) {
+      fl.push_warp(nf, tgt);
+      fl.flush(kBlock);
+    }
+  }
+  if (commit && !dense) fl.flush(0);
+  block_accumulate(ctl, c);
+}
+
+// ---------------------------------------------------------------------------
+// beliefs (compute_beliefs, messages.cpp:82-105): normalize(psi_v * prod m_in)
+
+template <int QS>
+__global__ void k_beliefs(DevGraph g, const float* A0, const float* A1, int pingpong, Ctl* ctl,
+                          double* out) {
+  const float* A = (pingpong && (ctl->iteration & 1ull)) ? A1 : A0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.V; v += gridDim.x * blockDim.x) {
+    const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
+    if (QS == 1) {
+      float T = g.unary_lo[v];
+      for (uint32_t a = b; a < e; ++a) T += A[g.in_adj[a]];
+      const double t = static_cast<double>(T);
+      out[2 * static_cast<size_t>(v)] = 1.0 / (1.0 + exp(t));
+      out[2 * static_cast<size_t>(v) + 1] = 1.0 / (1.0 + exp(-t));
+    } else {
+      const uint32_t q = g.card[v];
+      float T[QS];
+#pragma unroll
+      for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
+      for (uint32_t a = b; a < e; ++a) {
+        const float* m = A + static_cast<size_t>(g.in_adj[a]) * QS;
+#pragma unroll
+        for (int x = 0; x < QS; ++x) T[x] += m[x];
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int x = 0; x < QS; ++x)
+        if (x < static_cast<int>(q)) M = fmaxf(M, T[x]);
+      double p[QS];
+      double s = 0.0;
+#pragma unroll
+      for (int x = 0; x < QS; ++x) {
+        p[x] = x < static_cast<int>(q) ? exp(static_cast<double>(T[x] - M)) : 0.0;
+        s += p[x];
+      }
+      double* o = out + g.bel_off[v];
+#pragma unroll
+      for (int x = 0; x < QS; ++x)
+        if (x < static_cast<int>(q)) o[x] = p[x] / s;
+    }
+  }
+}
+
+}  // namespace bpb
