@@ -751,6 +751,20 @@ static void build_splash(const orc_engine* e, uint32_t root, uint32_t h, uint32_
   }
 }
 
+int orc_engine_build_splash(const orc_engine* e, uint32_t root, uint32_t h, uint32_t* claimed,
+                            uint32_t* edges, uint64_t* n) {
+  const uint32_t V = e->g->V;
+  if (root >= V) return fail(ORC_INVALID_ARGUMENT, "root out of range");
+  if (claimed[root] != UINT32_MAX) return fail(ORC_INVALID_ARGUMENT, "splash root %u is already claimed", root);
+  uint32_t* qv = (uint32_t*)malloc(sizeof(uint32_t) * V);
+  uint32_t* qd = (uint32_t*)malloc(sizeof(uint32_t) * V);
+  *n = 0;
+  build_splash(e, root, h, claimed, qv, qd, edges, n);
+  free(qv);
+  free(qd);
+  return ORC_OK;
+}
+
 /* rs_frontier: schedulers.cpp:169-192 */
 int orc_engine_rs_frontier(orc_engine* e, double p, uint32_t h, uint32_t* roots,
                            uint64_t* eoff, uint32_t* edges, uint64_t* num) {

@@ -119,6 +119,11 @@ int orc_engine_rs_frontier(orc_engine* e, double p, uint32_t h, uint32_t* roots,
 int orc_engine_apply_splashes(orc_engine* e, uint64_t num_splashes, const uint32_t* roots,
                               const uint64_t* edge_offsets, const uint32_t* edges);
 int orc_engine_beliefs(const orc_engine* e, double* out);
+/* build_splash (schedulers.cpp:136-167) with an explicit root; claimed[V]
+ * (UINT32_MAX = unclaimed) is updated; edges capacity 2E. Returns
+ * ORC_INVALID_ARGUMENT when the root is already claimed. */
+int orc_engine_build_splash(const orc_engine* e, uint32_t root, uint32_t h, uint32_t* claimed,
+                            uint32_t* edges, uint64_t* n);
 /* One-off update of message d against the live store (messages.cpp:67-73). */
 int orc_engine_update_message(const orc_engine* e, uint32_t d, double* out);
 /* select_top_k (schedulers.cpp:105-116) over an arbitrary residual array. */

@@ -128,6 +128,7 @@ class Lib:
         f("engine_rs_frontier", C.c_int, [_P, C.c_double, C.c_uint32, _u32p, _u64p, _u32p, C.POINTER(C.c_uint64)])
         f("engine_apply_splashes", C.c_int, [_P, C.c_uint64, _u32p, _u64p, _u32p])
         f("engine_beliefs", C.c_int, [_P, _f64p])
+        f("engine_build_splash", C.c_int, [_P, C.c_uint32, C.c_uint32, _u32p, _u32p, C.POINTER(C.c_uint64)])
         f("engine_update_message", C.c_int, [_P, C.c_uint32, _f64p])
         f("select_top_k", None, [_f64p, C.c_uint64, C.c_uint64, _u32p, C.POINTER(C.c_uint64)])
 
@@ -376,6 +377,13 @@ class Engine:
         self.lib.check(self.lib.engine_apply_splashes(
             self.h, roots.size, roots if roots.size else np.zeros(1, np.uint32), eoff,
             edges if edges.size else np.zeros(1, np.uint32)))
+
+    def build_splash(self, root, h, claimed):
+        """build_splash with an explicit root; `claimed` (uint32[V]) is updated in place."""
+        edges = np.zeros(max(self.D, 1), np.uint32)
+        n = C.c_uint64()
+        self.lib.check(self.lib.engine_build_splash(self.h, root, h, claimed, edges, C.byref(n)))
+        return edges[: n.value].copy()
 
     def beliefs(self):
         n = int(self.lib.graph_unary_size(self.g.h))

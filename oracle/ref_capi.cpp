@@ -296,6 +296,17 @@ int ref_engine_update_message(const ref_engine* e, uint32_t d, double* out) {
     std::memcpy(out, m.data(), sizeof(double) * m.size());
   });
 }
+int ref_engine_build_splash(const ref_engine* e, uint32_t root, uint32_t h, uint32_t* claimed,
+                            uint32_t* edges, uint64_t* n) {
+  return guarded([&] {
+    std::vector<vertex_id> cl(claimed, claimed + e->st->graph().num_vertices());
+    const Splash s = build_splash(*e->st, root, h, cl);
+    std::memcpy(claimed, cl.data(), cl.size() * 4);
+    std::memcpy(edges, s.edges.data(), s.edges.size() * 4);
+    *n = s.edges.size();
+  });
+}
+
 void ref_select_top_k(const double* r, uint64_t m, uint64_t k, uint32_t* out, uint64_t* n) {
   const auto f = select_top_k(std::span<const double>(r, m), k);
   std::memcpy(out, f.data(), sizeof(uint32_t) * f.size());
