@@ -128,7 +128,6 @@ int bp_run_ex(const bp_graph* g, const bp_sched_config* cfg, const bp_run_opts* 
     if (cfg->kind == BP_SERIAL_RBP)
       throw bpb::Error(BP_ERR_UNSUPPORTED,
                        "serial RBP is strictly sequential and is not offloaded (use the reference run_serial_rbp)");
-    if (cfg->kind == BP_RS) throw bpb::Error(BP_ERR_UNSUPPORTED, "residual splash is not available in this build");
     auto e = bpb::make_engine(*g->impl, *cfg);
     e->run(opts, result, beliefs_out, trace_out, trace_cap);
   });

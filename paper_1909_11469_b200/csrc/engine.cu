@@ -9,6 +9,7 @@
 
 #include "engine.hpp"
 #include "kernels.cuh"
+#include "kernels_rs.cuh"
 
 namespace bpb {
 
@@ -89,6 +90,7 @@ class EngineT final : public EngineBase {
       const long long kr = std::llround(cfg.p * static_cast<double>(g.D));  // schedulers.cpp:124
       k_ = kr < 1 ? 1 : static_cast<uint64_t>(kr);
     }
+    if (cfg.kind == BP_RS) ensure_rs(cfg.splash_depth);
     prm_.seed = cfg.seed;
     prm_.low_p = cfg.low_p;
     prm_.high_p = cfg.high_p;
@@ -259,12 +261,77 @@ class EngineT final : public EngineBase {
     enqueue_topk(k, /*commit=*/0);
     collect_sel(out);
   }
-  void rs_frontier(double, uint32_t, std::vector<uint32_t>&, std::vector<uint64_t>&,
-                   std::vector<uint32_t>&) override {
-    throw Error(BP_ERR_UNSUPPORTED, "residual splash is not available in this build");
+  // rs_frontier (schedulers.cpp:169-192): the device builds the splashes;
+  // the host only serialises them in the reference's layout (roots in
+  // priority order, edges in BFS visit order, schedulers.cpp:160-165).
+  void rs_frontier(double p, uint32_t h, std::vector<uint32_t>& roots, std::vector<uint64_t>& eoff,
+                   std::vector<uint32_t>& edges) override {
+    roots.clear();
+    edges.clear();
+    eoff.assign(1, 0);
+    if (g_.V == 0) return;
+    ensure_rs(h);
+    force_not_done();
+    launch_rs(rs_k(p), h, /*apply=*/0);
+    sync();
+    RsCtl rc{};
+    cuda_check(cudaMemcpy(&rc, rs_ctl_.p, sizeof(RsCtl), cudaMemcpyDeviceToHost), "d2h");
+    std::vector<uint32_t> kept(rc.nkept), qnext(g_.V);
+    std::vector<float> vres(g_.V);
+    if (rc.nkept) cuda_check(cudaMemcpy(kept.data(), rs_klist_.p, 4ull * rc.nkept, cudaMemcpyDeviceToHost), "d2h");
+    cuda_check(cudaMemcpy(qnext.data(), rs_qnext_.p, 4ull * g_.V, cudaMemcpyDeviceToHost), "d2h");
+    cuda_check(cudaMemcpy(vres.data(), rs_vres_.p, 4ull * g_.V, cudaMemcpyDeviceToHost), "d2h");
+    std::sort(kept.begin(), kept.end(), [&](uint32_t a, uint32_t b) {
+      if (vres[a] != vres[b]) return vres[a] > vres[b];
+      return a < b;
+    });
+    const auto& off = g_.host_in_off();
+    const auto& adj = g_.host_in_adj();
+    for (uint32_t r : kept) {
+      roots.push_back(r);
+      for (uint32_t v = r; v != kUncl; v = qnext[v])
+        for (uint32_t a = off[v]; a < off[v + 1]; ++a) edges.push_back(adj[a] ^ 1u);
+      eoff.push_back(edges.size());
+    }
   }
-  void apply_splashes(uint64_t, const uint32_t*, const uint64_t*, const uint32_t*) override {
-    throw Error(BP_ERR_UNSUPPORTED, "residual splash is not available in this build");
+  // apply_splash_frontier (schedulers.cpp:253-291) for host-supplied splashes
+  void apply_splashes(uint64_t ns, const uint32_t* roots, const uint64_t* eoff, const uint32_t* edges) override {
+    (void)roots;
+    if (ns == 0 || eoff[ns] == eoff[0]) return;
+    const uint64_t n = eoff[ns] - eoff[0];
+    std::vector<uint32_t> all(edges + eoff[0], edges + eoff[ns]);
+    for (uint32_t d : all)
+      if (d >= g_.D) throw_invalid("splash edge out of range");
+    {
+      std::vector<uint32_t> check(all);
+      std::sort(check.begin(), check.end());
+      if (std::adjacent_find(check.begin(), check.end()) != check.end())
+        throw_model("overlapping splashes: an edge is updated by two splashes");  // schedulers.cpp:262-268
+    }
+    ensure_rs(0);
+    if (!rs_written_.p) {
+      rs_written_.alloc(static_cast<size_t>(g_.D) * 4);
+      cuda_check(cudaMemset(rs_written_.p, 0, rs_written_.bytes), "memset");
+    }
+    std::vector<unsigned long long> off(ns + 1);
+    for (uint64_t i = 0; i <= ns; ++i) off[i] = eoff[i] - eoff[0];
+    DevBuf doff, dedges;
+    doff.upload(off.data(), off.size() * 8);
+    dedges.upload(all.data(), all.size() * 4);
+    force_not_done();
+    k_splash_apply_edges<QS><<<static_cast<unsigned>((ns + kBlock - 1) / kBlock), kBlock, 0, s_>>>(
+        dg_, live(), rs_shadow_.as<float>(), rs_written_.as<uint32_t>(), doff.as<unsigned long long>(),
+        dedges.as<uint32_t>(), static_cast<uint32_t>(ns), rs_stamp_ + 1, &ctl()->numeric_error);
+    rs_stamp_ += static_cast<uint32_t>(ns);
+    launch_check();
+    k_splash_commit_edges<QS><<<static_cast<unsigned>((n + kBlock - 1) / kBlock), kBlock, 0, s_>>>(
+        dg_, live(), rs_shadow_.as<float>(), dedges.as<uint32_t>(), static_cast<uint32_t>(n),
+        vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl());
+    launch_check();
+    enqueue_refresh(kFinApply);
+    sync();
+    fetch_ctl_header();
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
   }
   uint64_t step() override {
     force_not_done();
@@ -535,6 +602,10 @@ class EngineT final : public EngineBase {
         enqueue_topk(k_, 1);
         enqueue_refresh(kFinIter);
         break;
+      case BP_RS:
+        timed(kKSplash, [&] { launch_rs(rs_k(cfg_.p), cfg_.splash_depth, 1); });
+        enqueue_refresh(kFinIter);
+        break;
       default:
         throw Error(BP_ERR_UNSUPPORTED, "scheduler not available on the device");
     }
@@ -613,6 +684,68 @@ class EngineT final : public EngineBase {
     sync();
   }
 
+  // ---- Residual Splash state (kernels_rs.cuh)
+  static unsigned long long rs_k_of(double p, uint32_t V) {  // schedulers.cpp:172-173
+    const long long kr = std::llround(p * static_cast<double>(V));
+    return kr < 1 ? 1ull : static_cast<unsigned long long>(kr);
+  }
+  unsigned long long rs_k(double p) const { return rs_k_of(p, g_.V); }
+  void ensure_rs(uint32_t h) {
+    if (h > kRsMaxDepth)
+      throw Error(BP_ERR_UNSUPPORTED, "splash_depth above " + std::to_string(kRsMaxDepth) +
+                                          " is not supported by the device splash builder");
+    if (rs_vres_.p) return;
+    const size_t V = std::max<size_t>(g_.V, 1);
+    for (DevBuf* b : {&rs_vres_, &rs_state_, &rs_claimed_, &rs_qnext_, &rs_spos_, &rs_depth_, &rs_clist_,
+                      &rs_blist_, &rs_rlist_, &rs_klist_})
+      b->alloc(V * 4);
+    rs_ballmax_.alloc(V * 8);
+    rs_hist_.alloc(4096 * 4);
+    cuda_check(cudaMemset(rs_hist_.p, 0, 4096 * 4), "memset");
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rs_iteration<QS>, kRsBlock, 0),
+               "occupancy");
+    rs_grid_ = static_cast<unsigned>(std::max(1, per_sm) * sm_count());
+    rs_blk_.alloc(static_cast<size_t>(rs_grid_) * 4);
+    rs_ctl_.alloc(sizeof(RsCtl));
+    cuda_check(cudaMemset(rs_ctl_.p, 0, sizeof(RsCtl)), "memset");
+    rs_shadow_.alloc(std::max<size_t>(static_cast<size_t>(g_.D) * QS * 4, 16));
+  }
+  RsBufs rs_bufs() {
+    RsBufs b{};
+    b.vres = rs_vres_.as<float>();
+    b.state = rs_state_.as<uint32_t>();
+    b.claimed = rs_claimed_.as<uint32_t>();
+    b.qnext = rs_qnext_.as<uint32_t>();
+    b.spos = rs_spos_.as<uint32_t>();
+    b.depth = rs_depth_.as<uint32_t>();
+    b.ballmax = rs_ballmax_.as<unsigned long long>();
+    b.clist = rs_clist_.as<uint32_t>();
+    b.blist = rs_blist_.as<uint32_t>();
+    b.rlist = rs_rlist_.as<uint32_t>();
+    b.klist = rs_klist_.as<uint32_t>();
+    b.hist = rs_hist_.as<unsigned>();
+    b.blk = rs_blk_.as<unsigned>();
+    b.rc = rs_ctl_.as<RsCtl>();
+    b.shadow = rs_shadow_.as<float>();
+    return b;
+  }
+  void launch_rs(unsigned long long k, uint32_t h, int apply) {
+    RsParams prm{k, h, apply};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(rs_grid_);
+    lc.blockDim = dim3(kRsBlock);
+    lc.stream = s_;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&lc, k_rs_iteration<QS>, dg_, live(), static_cast<const float*>(res_.as<float>()),
+                                  vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), rs_bufs(), prm),
+               "cooperative splash launch");
+  }
+
   void ensure_beliefs_buf(size_t nb) {
     if (bel_.bytes < nb * 8) bel_.alloc(nb * 8);
   }
@@ -652,6 +785,10 @@ class EngineT final : public EngineBase {
   cudaStream_t s_ = nullptr;
   DevBuf bufA_, bufB_, res_, vflag_, vlist_, ctl_, hist_, chunk_, sel_, bel_, inlist_;
   DevBuf clist_[2];
+  DevBuf rs_vres_, rs_state_, rs_claimed_, rs_qnext_, rs_spos_, rs_depth_, rs_clist_, rs_blist_, rs_rlist_,
+      rs_klist_, rs_ballmax_, rs_hist_, rs_blk_, rs_ctl_, rs_shadow_, rs_written_;
+  unsigned rs_grid_ = 1;
+  uint32_t rs_stamp_ = 0;
   bool use_clist_ = false;
   Ctl* hctl_ = nullptr;
   uint32_t nchunks_ = 1;

@@ -398,6 +398,24 @@ const std::vector<uint32_t>& GraphImpl::host_ep() const {
   return ep_host;
 }
 
+const std::vector<uint32_t>& GraphImpl::host_in_off() const {
+  std::lock_guard<std::mutex> lk(host_mu);
+  if (in_off_host.size() != static_cast<size_t>(V) + 1) {
+    in_off_host.resize(static_cast<size_t>(V) + 1);
+    cuda_check(cudaMemcpy(in_off_host.data(), in_off.p, 4ull * (V + 1), cudaMemcpyDeviceToHost), "csr download");
+  }
+  return in_off_host;
+}
+
+const std::vector<uint32_t>& GraphImpl::host_in_adj() const {
+  std::lock_guard<std::mutex> lk(host_mu);
+  if (in_adj_host.size() != static_cast<size_t>(D)) {
+    in_adj_host.resize(D);
+    if (D) cuda_check(cudaMemcpy(in_adj_host.data(), in_adj.p, 4ull * D, cudaMemcpyDeviceToHost), "csr download");
+  }
+  return in_adj_host;
+}
+
 uint32_t GraphImpl::card_of(uint32_t v) const {
   if (uniform_q) return uniform_q;
   return cards_host[v];

@@ -48,9 +48,11 @@ struct GraphImpl {
   }
   uint32_t card_of(uint32_t v) const;
   const std::vector<uint32_t>& host_ep() const;
+  const std::vector<uint32_t>& host_in_off() const;
+  const std::vector<uint32_t>& host_in_adj() const;
 
   mutable std::mutex host_mu;
-  mutable std::vector<uint32_t> ep_host;
+  mutable std::vector<uint32_t> ep_host, in_off_host, in_adj_host;
 };
 
 std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_device_opts* opts);
