@@ -36,7 +36,39 @@ struct DevGraph {
   const float* __restrict__ unary_log;    // V*qs
   const float* __restrict__ table;        // E*qs*qs, row = lo state, max-scaled linear
   const uint32_t* __restrict__ bel_off;   // V+1 belief offsets (generic)
+  // Structured fast paths (uniform-branch flags, no extra template axes):
+  //   lattice topology: rows x cols row-major grid with the generator's edge
+  //   order (generators.cpp:37-43) -> incoming edges by arithmetic, no CSR reads;
+  //   par_mode 1: binary Ising tables {a, d, d, a} -> one coupling J per edge
+  //   (jcoup), generic Potts tables (a on the diagonal, d off it) -> one
+  //   w1 = a/d - 1 per edge (pw).  0: float4 epar / dense q x q tables.
+  uint32_t lat_rows, lat_cols;
+  uint32_t par_mode;
+  uint32_t uniform_q;                     // all cardinalities equal (0 = mixed)
+  const float* __restrict__ jcoup;        // E  (binary, par_mode 1)
+  const float* __restrict__ pw;           // E  (generic, par_mode 1)
 };
+
+// Incoming directed edges of v in CSR order (mrf.cpp:93-104).  Lattice: up,
+// left, right, down, from the edge numbering of generate_ising
+// (generators.cpp:37-43): per row the right edge then the down edge of each
+// vertex; the last row has right edges only.
+template <class F>
+__device__ __forceinline__ void for_each_in(const DevGraph& g, uint32_t v, F&& f) {
+  if (g.lat_cols) {
+    const uint32_t C = g.lat_cols, R = g.lat_rows;
+    const uint32_t r = v / C, c = v - r * C;
+    const uint32_t row = r * (2u * C - 1u);
+    const bool last = r + 1u == R;
+    if (r > 0u) f(2u * ((r - 1u) * (2u * C - 1u) + 2u * c + (c + 1u < C ? 1u : 0u)));
+    if (c > 0u) f(2u * (last ? row + c - 1u : row + 2u * (c - 1u)));
+    if (c + 1u < C) f(2u * (last ? row + c : row + 2u * c) + 1u);
+    if (!last) f(2u * (row + 2u * c + (c + 1u < C ? 1u : 0u)) + 1u);
+  } else {
+    const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
+    for (uint32_t a = b; a < e; ++a) f(g.in_adj[a]);
+  }
+}
 
 // Per-run control block in device memory.  Written only by single threads
 // (finalizers) or by atomics; read by every kernel at entry.
@@ -128,6 +160,49 @@ __device__ __forceinline__ float binary_update(float h, float4 par, bool odd) {
   const float a = odd ? par.w : par.z;
   const float b = odd ? par.x : par.y;
   return c + softplusf(h + a) - softplusf(h + b);
+}
+
+// Outgoing binary message on directed edge `out` from the cavity log-odds h.
+__device__ __forceinline__ float binary_msg(const DevGraph& g, float h, uint32_t out) {
+  if (g.par_mode) {  // Ising table: par = (-J, -J, J, J) in both directions
+    const float j = __ldg(&g.jcoup[out >> 1]);
+    return -j + softplusf(h + j) - softplusf(h - j);
+  }
+  return binary_update(h, __ldg(&g.epar[out >> 1]), (out & 1u) != 0u);
+}
+
+// Unnormalised outgoing q-vector on `out` from the source distribution p
+// (p[x] = 0 for x >= |A_src|): the contraction of messages.hpp:134-149, row
+// orientation by out & 1.  Potts tables contract in O(q): o = S + w1 p.
+template <int QS>
+__device__ __forceinline__ void generic_matvec(const DevGraph& g, uint32_t out, const float* p, float* o) {
+  if (g.par_mode) {
+    const float w1 = __ldg(&g.pw[out >> 1]);
+    float S = 0.f;
+#pragma unroll
+    for (int x = 0; x < QS; ++x) S += p[x];
+#pragma unroll
+    for (int x = 0; x < QS; ++x) o[x] = fmaf(w1, p[x], S);
+    return;
+  }
+  const float* tab = g.table + static_cast<size_t>(out >> 1) * QS * QS;
+  if ((out & 1u) == 0u) {  // source is lo: A(xs, xt) = T[xs][xt]
+#pragma unroll
+    for (int xt = 0; xt < QS; ++xt) o[xt] = 0.f;
+#pragma unroll
+    for (int xs = 0; xs < QS; ++xs) {
+#pragma unroll
+      for (int xt = 0; xt < QS; ++xt) o[xt] = fmaf(__ldg(&tab[xs * QS + xt]), p[xs], o[xt]);
+    }
+  } else {  // source is hi: A(xs, xt) = T[xt][xs]
+#pragma unroll
+    for (int xt = 0; xt < QS; ++xt) {
+      float acc = 0.f;
+#pragma unroll
+      for (int xs = 0; xs < QS; ++xs) acc = fmaf(__ldg(&tab[xt * QS + xs]), p[xs], acc);
+      o[xt] = acc;
+    }
+  }
 }
 
 // L-inf residual in linear probability space (messages.cpp:56-65): for binary

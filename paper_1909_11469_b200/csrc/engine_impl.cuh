@@ -1,0 +1,791 @@
+// EngineT<QS>: per-run device state + the scheduler loop of run()
+// (schedulers.cpp:293-353), executed as a device-side CUDA-graph WHILE loop so
+// no host round trip happens per iteration.  Instantiated once per message
+// stride in engine_q*.cu (parallel builds).
+#pragma once
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "engine.hpp"
+#include "kernels.cuh"
+#include "kernels_rs.cuh"
+
+namespace bpb {
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+// smallest float >= eps: r (fp32) >= eps (fp64) <=> r >= eps_ceil
+float eps_ceil(double eps) {
+  float f = static_cast<float>(eps);
+  if (static_cast<double>(f) < eps) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+  return f;
+}
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, c = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c > 0 ? c : 148;
+  }();
+  return n;
+}
+
+unsigned grid_cap(size_t n, int per_sm = 8) {
+  const size_t want = (n + kBlock - 1) / kBlock;
+  const size_t cap = static_cast<size_t>(sm_count()) * per_sm;
+  return static_cast<unsigned>(std::max<size_t>(1, std::min(want, cap)));
+}
+
+enum KClass { kKUpdate = 0, kKSelect = 1, kKTopk = 2, kKSplash = 3, kKInit = 4, kKBeliefs = 5, kKOther = 6 };
+
+template <int QS>
+class EngineT final : public EngineBase {
+ public:
+  EngineT(const GraphImpl& g, const bp_sched_config& cfg) : g_(g), cfg_(cfg) {
+    cuda_check(cudaSetDevice(g.device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+    dg_ = g.dev();
+    eps_ = eps_ceil(cfg.epsilon);
+    const size_t msz = static_cast<size_t>(g.D) * QS * sizeof(float);
+    bufA_.alloc(msz);
+    bufB_.alloc(msz);
+    res_.alloc((static_cast<size_t>(g.D) + 3) / 4 * 16);  // padded to float4, tail stays 0
+    cuda_check(cudaMemset(res_.p, 0, res_.bytes), "memset res");
+    vflag_.alloc(static_cast<size_t>(g.V) * 4);
+    if (cfg.kind == BP_RNBP) {  // candidate list (run mode)
+      clist_[0].alloc(static_cast<size_t>(g.D) * 4);
+      clist_[1].alloc(static_cast<size_t>(g.D) * 4);
+      inlist_.alloc(g.D ? g.D : 1);
+    }
+    vlist_.alloc(static_cast<size_t>(g.V) * 4);
+    ctl_.alloc(sizeof(Ctl));
+    cuda_check(cudaMallocHost(&hctl_, sizeof(Ctl)), "cudaMallocHost");
+    std::memset(hctl_, 0, sizeof(Ctl));
+    if (cfg.kind == BP_RBP) {
+      hist_.alloc(kRadixBins * 4);
+      cuda_check(cudaMemset(hist_.p, 0, kRadixBins * 4), "memset");
+      nchunks_ = std::max<uint32_t>(1, (g.D + kTieChunk - 1) / kTieChunk);
+      chunk_.alloc(static_cast<size_t>(nchunks_) * 4);
+      const long long kr = std::llround(cfg.p * static_cast<double>(g.D));  // schedulers.cpp:124
+      k_ = kr < 1 ? 1 : static_cast<uint64_t>(kr);
+    }
+    if (cfg.kind == BP_RS) ensure_rs(cfg.splash_depth);
+    prm_.seed = cfg.seed;
+    prm_.low_p = cfg.low_p;
+    prm_.high_p = cfg.high_p;
+    prm_.thr = cfg.edge_ratio_threshold;
+    prm_.fixed_p = -1.0;
+    prm_.commit = 1;
+  }
+
+  ~EngineT() override {
+    if (gexec_) cudaGraphExecDestroy(gexec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    for (auto& ev : evs_) cudaEventDestroy(ev);
+    if (hctl_) cudaFreeHost(hctl_);
+    if (s_) cudaStreamDestroy(s_);
+  }
+
+  // ------------------------------------------------------------------ run
+  void run(const bp_run_opts* opts, bp_run_result* res, double* beliefs_host, bp_iter_record* trace,
+           uint64_t trace_cap) override {
+    const uint32_t flags = opts ? opts->flags : 0u;
+    timing_ = (flags & BP_RUN_KERNEL_TIMING) != 0;
+    stats_ = opts ? opts->stats : nullptr;
+    if (stats_) std::memset(stats_, 0, sizeof(*stats_));
+    launches_ = 0;
+    const bool use_graph = !(flags & BP_RUN_NO_GRAPHS) && !timing_;
+    const Clock::time_point t0 = Clock::now();  // schedulers.cpp:297
+
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    cuda_check(cudaEventRecord(e0, s_), "event record");
+    reset_ctl(cfg_.max_iterations, cfg_.time_limit, cfg_.kind == BP_RNBP);
+    enqueue_init(cfg_.kind == BP_LBP);
+
+    uint64_t copied = 0;
+    // first look: did the initial sweep already converge / hit a cap?
+    fetch_ctl_header();
+    drain_trace(trace, trace_cap, copied);
+    if (!hctl_->done) {
+      if (use_graph) {
+        run_graph_loop(trace, trace_cap, copied);
+      } else {
+        uint32_t batch = opts && opts->batch ? opts->batch : 16;
+        while (!hctl_->done) {
+          for (uint32_t b = 0; b < batch; ++b) enqueue_iteration();
+          fetch_ctl_header();
+          drain_trace(trace, trace_cap, copied);
+          if (!(opts && opts->batch)) batch = std::min<uint32_t>(batch * 2, 256);
+        }
+      }
+    }
+    fetch_ctl_header();
+    drain_trace(trace, trace_cap, copied);
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
+
+    const size_t nb = g_.unary_size();
+    if (!(flags & BP_RUN_NO_BELIEFS) && (beliefs_host || (opts && opts->beliefs_device))) {
+      double* dst = opts && opts->beliefs_device ? opts->beliefs_device : nullptr;
+      if (!dst) {
+        ensure_beliefs_buf(nb);
+        dst = bel_.as<double>();
+      }
+      enqueue_beliefs(dst, cfg_.kind == BP_LBP);
+      if (beliefs_host) cuda_check(cudaMemcpyAsync(beliefs_host, dst, nb * 8, cudaMemcpyDeviceToHost, s_), "beliefs d2h");
+    }
+    cuda_check(cudaEventRecord(e1, s_), "event record");
+    cuda_check(cudaStreamSynchronize(s_), "run");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    collect_timing();
+
+    std::memset(res, 0, sizeof(*res));
+    res->converged = hctl_->converged ? 1 : 0;
+    res->iterations = hctl_->iteration;
+    res->messages_updated_total = hctl_->msgs_total;
+    res->trace_len = hctl_->trace_len;
+    res->device_ms = ms;
+    res->message_evaluations = hctl_->evals_total;
+    res->vertex_visits = hctl_->vertex_visits;
+    res->gpu_launches = launches_;
+    res->wall_time = std::chrono::duration<double>(Clock::now() - t0).count();
+  }
+
+  // ------------------------------------------------------------- lockstep
+  void lockstep_init() override {
+    reset_ctl(std::numeric_limits<uint64_t>::max(), 1e300);
+    enqueue_init(false);
+    sync();
+  }
+  uint32_t unconverged() override {
+    fetch_ctl_header();
+    return hctl_->unconverged;
+  }
+  uint64_t iteration() override {
+    fetch_ctl_header();
+    return hctl_->iteration;
+  }
+  void messages(double* out, bool candidates) override {
+    std::vector<float> raw(static_cast<size_t>(g_.D) * QS);
+    const DevBuf& src = candidates ? bufB_ : bufA_;
+    if (!raw.empty()) cuda_check(cudaMemcpy(raw.data(), src.p, raw.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+    const auto& ep = g_.host_ep();
+    size_t o = 0;
+    for (uint32_t d = 0; d < g_.D; ++d) {
+      if (QS == 1) {
+        const double l = raw[d];
+        out[o++] = 1.0 / (1.0 + std::exp(l));
+        out[o++] = 1.0 / (1.0 + std::exp(-l));
+      } else {
+        const uint32_t q = g_.card_of(ep[d ^ 1u]);
+        for (uint32_t x = 0; x < q; ++x) out[o++] = std::exp(static_cast<double>(raw[static_cast<size_t>(d) * QS + x]));
+      }
+    }
+  }
+  void residuals(double* out) override {
+    std::vector<float> raw(g_.D);
+    if (g_.D) cuda_check(cudaMemcpy(raw.data(), res_.p, raw.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+    for (uint32_t d = 0; d < g_.D; ++d) out[d] = raw[d];
+  }
+  void beliefs(double* out) override {
+    const size_t nb = g_.unary_size();
+    ensure_beliefs_buf(nb);
+    enqueue_beliefs(bel_.as<double>(), false);
+    cuda_check(cudaMemcpyAsync(out, bel_.p, nb * 8, cudaMemcpyDeviceToHost, s_), "d2h");
+    sync();
+  }
+  void apply_frontier(const uint32_t* f, uint64_t n) override {
+    if (n == 0) return;  // schedulers.cpp:230
+    std::vector<uint32_t> u(f, f + n);
+    for (uint32_t d : u)
+      if (d >= g_.D) throw_invalid("frontier edge out of range");
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    DevBuf list;
+    list.upload(u.data(), u.size() * 4);
+    force_not_done();
+    const int dense = u.size() > g_.V / 16 ? 1 : 0;
+    k_commit_list<QS><<<grid_cap(u.size()), kBlock, 0, s_>>>(dg_, list.as<uint32_t>(), static_cast<uint32_t>(u.size()),
+                                                            live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
+                                                            vlist_.as<uint32_t>(), ctl(), eps_, dense);
+    launch_check();
+    enqueue_refresh(kFinApply);
+    sync();
+  }
+  void rnbp_frontier(double p, std::vector<uint32_t>& out) override {
+    ensure_sel();
+    force_not_done();
+    RnbpParams q = prm_;
+    q.fixed_p = p;
+    q.commit = 0;
+    k_rnbp_select<QS, false><<<grid_cap(g_.D / 4 + 1), kBlock, 0, s_>>>(
+        dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), sel_.as<uint8_t>(),
+        ctl(), eps_, q, cand_list());
+    k_rnbp_retry<QS, false><<<1, 1024, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
+                                                vlist_.as<uint32_t>(), sel_.as<uint8_t>(), ctl(), eps_, q,
+                                                cand_list());
+    launch_check();
+    collect_sel(out);
+  }
+  void rbp_frontier(double p, std::vector<uint32_t>& out) override {
+    ensure_sel();
+    force_not_done();
+    const long long kr = std::llround(p * static_cast<double>(g_.D));
+    const uint64_t k = kr < 1 ? 1 : static_cast<uint64_t>(kr);
+    ensure_rbp_scratch();
+    enqueue_topk(k, /*commit=*/0);
+    collect_sel(out);
+  }
+  // rs_frontier (schedulers.cpp:169-192): the device builds the splashes;
+  // the host only serialises them in the reference's layout (roots in
+  // priority order, edges in BFS visit order, schedulers.cpp:160-165).
+  void rs_frontier(double p, uint32_t h, std::vector<uint32_t>& roots, std::vector<uint64_t>& eoff,
+                   std::vector<uint32_t>& edges) override {
+    roots.clear();
+    edges.clear();
+    eoff.assign(1, 0);
+    if (g_.V == 0) return;
+    ensure_rs(h);
+    force_not_done();
+    launch_rs(rs_k(p), h, /*apply=*/0);
+    sync();
+    RsCtl rc{};
+    cuda_check(cudaMemcpy(&rc, rs_ctl_.p, sizeof(RsCtl), cudaMemcpyDeviceToHost), "d2h");
+    std::vector<uint32_t> kept(rc.nkept), qnext(g_.V);
+    std::vector<float> vres(g_.V);
+    if (rc.nkept) cuda_check(cudaMemcpy(kept.data(), rs_klist_.p, 4ull * rc.nkept, cudaMemcpyDeviceToHost), "d2h");
+    cuda_check(cudaMemcpy(qnext.data(), rs_qnext_.p, 4ull * g_.V, cudaMemcpyDeviceToHost), "d2h");
+    cuda_check(cudaMemcpy(vres.data(), rs_vres_.p, 4ull * g_.V, cudaMemcpyDeviceToHost), "d2h");
+    std::sort(kept.begin(), kept.end(), [&](uint32_t a, uint32_t b) {
+      if (vres[a] != vres[b]) return vres[a] > vres[b];
+      return a < b;
+    });
+    const auto& off = g_.host_in_off();
+    const auto& adj = g_.host_in_adj();
+    for (uint32_t r : kept) {
+      roots.push_back(r);
+      for (uint32_t v = r; v != kUncl; v = qnext[v])
+        for (uint32_t a = off[v]; a < off[v + 1]; ++a) edges.push_back(adj[a] ^ 1u);
+      eoff.push_back(edges.size());
+    }
+  }
+  // apply_splash_frontier (schedulers.cpp:253-291) for host-supplied splashes
+  void apply_splashes(uint64_t ns, const uint32_t* roots, const uint64_t* eoff, const uint32_t* edges) override {
+    (void)roots;
+    if (ns == 0 || eoff[ns] == eoff[0]) return;
+    const uint64_t n = eoff[ns] - eoff[0];
+    std::vector<uint32_t> all(edges + eoff[0], edges + eoff[ns]);
+    for (uint32_t d : all)
+      if (d >= g_.D) throw_invalid("splash edge out of range");
+    {
+      std::vector<uint32_t> check(all);
+      std::sort(check.begin(), check.end());
+      if (std::adjacent_find(check.begin(), check.end()) != check.end())
+        throw_model("overlapping splashes: an edge is updated by two splashes");  // schedulers.cpp:262-268
+    }
+    ensure_rs(0);
+    if (!rs_written_.p) {
+      rs_written_.alloc(static_cast<size_t>(g_.D) * 4);
+      cuda_check(cudaMemset(rs_written_.p, 0, rs_written_.bytes), "memset");
+    }
+    std::vector<unsigned long long> off(ns + 1);
+    for (uint64_t i = 0; i <= ns; ++i) off[i] = eoff[i] - eoff[0];
+    DevBuf doff, dedges;
+    doff.upload(off.data(), off.size() * 8);
+    dedges.upload(all.data(), all.size() * 4);
+    force_not_done();
+    k_splash_apply_edges<QS><<<static_cast<unsigned>((ns + kBlock - 1) / kBlock), kBlock, 0, s_>>>(
+        dg_, live(), rs_shadow_.as<float>(), rs_written_.as<uint32_t>(), doff.as<unsigned long long>(),
+        dedges.as<uint32_t>(), static_cast<uint32_t>(ns), rs_stamp_ + 1, &ctl()->numeric_error);
+    rs_stamp_ += static_cast<uint32_t>(ns);
+    launch_check();
+    k_splash_commit_edges<QS><<<static_cast<unsigned>((n + kBlock - 1) / kBlock), kBlock, 0, s_>>>(
+        dg_, live(), rs_shadow_.as<float>(), dedges.as<uint32_t>(), static_cast<uint32_t>(n),
+        vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl());
+    launch_check();
+    enqueue_refresh(kFinApply);
+    sync();
+    fetch_ctl_header();
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
+  }
+  uint64_t step() override {
+    force_not_done();
+    fetch_ctl_header();
+    const uint64_t before = hctl_->msgs_total;
+    if (cfg_.kind == BP_LBP) {
+      // lockstep LBP = frontier_lbp + apply_frontier (commit all + refresh all)
+      ensure_rbp_scratch();
+      enqueue_topk_all();
+      enqueue_refresh(kFinIter);
+      sync();
+    } else {
+      enqueue_iteration();
+    }
+    fetch_ctl_header();
+    return hctl_->msgs_total - before;
+  }
+
+ private:
+  float* live() { return bufA_.as<float>(); }
+  float* cand() { return bufB_.as<float>(); }
+  Ctl* ctl() { return ctl_.as<Ctl>(); }
+
+  void sync() { cuda_check(cudaStreamSynchronize(s_), "stream sync"); }
+  void launch_check() { cuda_check(cudaGetLastError(), "kernel launch"); }
+
+  CandList cand_list() {
+    CandList c{};
+    c.list[0] = clist_[0].as<uint32_t>();
+    c.list[1] = clist_[1].as<uint32_t>();
+    c.inlist = inlist_.as<uint8_t>();
+    return c;
+  }
+
+  void reset_ctl(uint64_t max_iter, double time_limit, bool use_clist = false) {
+    use_clist_ = use_clist && clist_[0].p != nullptr;
+    std::memset(hctl_, 0, offsetof(Ctl, trace));
+    hctl_->use_clist = use_clist_ ? 1u : 0u;
+    if (use_clist_) cuda_check(cudaMemsetAsync(inlist_.p, 0, inlist_.bytes, s_), "memset inlist");
+    hctl_->max_iterations = max_iter;
+    const double ns = time_limit * 1e9;
+    hctl_->time_limit_ns = ns >= 1.8e19 ? std::numeric_limits<unsigned long long>::max()
+                                        : static_cast<unsigned long long>(ns);
+    hctl_->stamp = 1;
+    cuda_check(cudaMemcpyAsync(ctl_.p, hctl_, offsetof(Ctl, trace), cudaMemcpyHostToDevice, s_), "ctl h2d");
+    cuda_check(cudaMemsetAsync(vflag_.p, 0, static_cast<size_t>(g_.V) * 4, s_), "memset vflag");
+  }
+
+  void fetch_ctl_header() {
+    cuda_check(cudaMemcpyAsync(hctl_, ctl_.p, offsetof(Ctl, trace), cudaMemcpyDeviceToHost, s_), "ctl d2h");
+    sync();
+  }
+
+  void force_not_done() {
+    const unsigned zero = 0;
+    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, done), &zero, 4,
+                               cudaMemcpyHostToDevice, s_),
+               "ctl h2d");
+    sync();
+  }
+
+  // copy trace records [copied, trace_len) from the device ring
+  void drain_trace(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
+    const uint64_t n = hctl_->trace_len;
+    if (n <= copied) return;
+    if (!trace || copied >= cap) {
+      copied = n;
+      return;
+    }
+    if (n - copied > kTraceRing) throw Error(BP_ERR_CUDA, "trace ring overrun");
+    std::vector<TraceRec> tmp(kTraceRing);
+    cuda_check(cudaMemcpy(tmp.data(), reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, trace),
+                          sizeof(TraceRec) * kTraceRing, cudaMemcpyDeviceToHost),
+               "trace d2h");
+    for (uint64_t it = copied; it < n && it < cap; ++it) {
+      const TraceRec& r = tmp[it % kTraceRing];
+      trace[it].iteration = r.iteration;
+      trace[it].frontier_size = r.frontier_size;
+      trace[it].unconverged = r.unconverged;
+      trace[it]._pad = 0;
+      trace[it].elapsed_seconds = r.elapsed_seconds;
+    }
+    copied = n;
+  }
+
+  // ---- kernel timing (BP_RUN_KERNEL_TIMING): an event pair per launch
+  struct Timed {
+    int cls;
+    cudaEvent_t a, b;
+    uint64_t bytes;
+  };
+  std::vector<Timed> pending_;
+  std::vector<cudaEvent_t> evs_;
+  size_t ev_next_ = 0;
+  cudaEvent_t next_event() {
+    if (ev_next_ == evs_.size()) {
+      cudaEvent_t ev;
+      cuda_check(cudaEventCreate(&ev), "event");
+      evs_.push_back(ev);
+    }
+    return evs_[ev_next_++];
+  }
+  template <class F>
+  void timed(int cls, F&& launch) {
+    ++launches_;
+    if (!timing_) {
+      launch();
+      return;
+    }
+    Timed t{cls, next_event(), next_event(), 0};
+    cudaEventRecord(t.a, s_);
+    launch();
+    cudaEventRecord(t.b, s_);
+    pending_.push_back(t);
+    if (ev_next_ > 4096) collect_timing();
+  }
+  void collect_timing() {
+    if (pending_.empty()) return;
+    sync();
+    for (auto& t : pending_) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t.a, t.b);
+      if (stats_) {
+        stats_->ms[t.cls] += ms;
+        stats_->launches[t.cls] += 1;
+      }
+    }
+    pending_.clear();
+    ev_next_ = 0;
+  }
+
+  // ---- launch sequences
+  void enqueue_finalize(int mode) {
+    timed(kKOther, [&] { k_finalize<<<1, kSlots, 0, s_>>>(ctl(), mode, g_.D); });
+    launch_check();
+  }
+
+  void enqueue_init(bool lbp) {
+    const unsigned gi = grid_cap(static_cast<size_t>(g_.D) * QS);
+    timed(kKInit, [&] { k_init_messages<QS><<<gi, kBlock, 0, s_>>>(dg_, live(), ctl(), 1); });
+    launch_check();
+    const unsigned gv = grid_cap(g_.V);
+    if (lbp) {  // sweep 0 (ResidualTracker ctor, residuals.cpp:9-24)
+      timed(kKUpdate, [&] {
+        k_vertex_update<QS, kModeCount, false, true, false>
+            <<<gv, kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+      });
+      launch_check();
+      enqueue_finalize(kFinLbp);
+    } else {
+      timed(kKUpdate, [&] {
+        if (use_clist_)
+          k_vertex_update<QS, kModeInit, false, false, true><<<gv, kBlock, 0, s_>>>(
+              dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
+        else
+          k_vertex_update<QS, kModeInit, false, false, false><<<gv, kBlock, 0, s_>>>(
+              dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
+      });
+      launch_check();
+      enqueue_finalize(kFinInit);
+    }
+  }
+
+  void enqueue_refresh(int fin) {
+    const unsigned gv = grid_cap(g_.V);
+    timed(kKUpdate, [&] {
+      if (use_clist_)
+        k_vertex_update<QS, kModeDelta, true, false, true><<<gv, kBlock, 0, s_>>>(
+            dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
+            cand_list());
+      else
+        k_vertex_update<QS, kModeDelta, true, false, false><<<gv, kBlock, 0, s_>>>(
+            dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
+            cand_list());
+    });
+    launch_check();
+    enqueue_finalize(fin);
+  }
+
+  void ensure_rbp_scratch() {
+    if (!hist_.p) {
+      hist_.alloc(kRadixBins * 4);
+      cuda_check(cudaMemset(hist_.p, 0, kRadixBins * 4), "memset");
+    }
+    if (!chunk_.p) {
+      nchunks_ = std::max<uint32_t>(1, (g_.D + kTieChunk - 1) / kTieChunk);
+      chunk_.alloc(static_cast<size_t>(nchunks_) * 4);
+    }
+  }
+
+  // select_all commit (|F| = 2|E|)
+  void enqueue_topk_all() {
+    timed(kKSelect, [&] {
+      k_rbp_commit<QS><<<nchunks_, kBlock, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
+                                                    vlist_.as<uint32_t>(), sel_.as<uint8_t>(), chunk_.as<unsigned>(),
+                                                    ctl(), eps_, 1, 1, 1);
+    });
+    launch_check();
+  }
+
+  void enqueue_topk(uint64_t k, int commit) {
+    const int dense = k > g_.V / 16 ? 1 : 0;
+    if (k >= g_.D) {
+      timed(kKSelect, [&] {
+        k_rbp_commit<QS><<<nchunks_, kBlock, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
+                                                      vlist_.as<uint32_t>(), sel_.as<uint8_t>(), chunk_.as<unsigned>(),
+                                                      ctl(), eps_, 1, commit, dense);
+      });
+      launch_check();
+      return;
+    }
+    const unsigned gh = grid_cap(g_.D / 4 + 1, 4);
+    for (int pass = 0; pass < 3; ++pass) {
+      timed(kKTopk, [&] {
+        k_radix_hist<<<gh, kBlock, 0, s_>>>(res_.as<float>(), g_.D, pass, hist_.as<unsigned>(), ctl());
+      });
+      timed(kKTopk, [&] { k_radix_scan<<<1, 1024, 0, s_>>>(hist_.as<unsigned>(), pass, k, ctl()); });
+    }
+    timed(kKTopk, [&] { k_tie_count<<<nchunks_, kBlock, 0, s_>>>(res_.as<float>(), g_.D, chunk_.as<unsigned>(), ctl()); });
+    timed(kKTopk, [&] { k_tie_scan<<<1, 1024, 0, s_>>>(chunk_.as<unsigned>(), nchunks_, ctl()); });
+    timed(kKSelect, [&] {
+      k_rbp_commit<QS><<<nchunks_, kBlock, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
+                                                    vlist_.as<uint32_t>(), sel_.as<uint8_t>(), chunk_.as<unsigned>(),
+                                                    ctl(), eps_, 0, commit, dense);
+    });
+    launch_check();
+  }
+
+  // one iteration of the loop body (schedulers.cpp:311-346) for the configured scheduler
+  void enqueue_iteration() {
+    switch (cfg_.kind) {
+      case BP_LBP: {
+        const unsigned gv = grid_cap(g_.V);
+        timed(kKUpdate, [&] {
+          k_vertex_update<QS, kModeCount, false, true, false>
+              <<<gv, kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+        });
+        launch_check();
+        enqueue_finalize(kFinLbp);
+        break;
+      }
+      case BP_RNBP: {
+        timed(kKSelect, [&] {
+          if (use_clist_)
+            k_rnbp_select<QS, true><<<grid_cap(g_.D), kBlock, 0, s_>>>(
+                dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), nullptr, ctl(),
+                eps_, prm_, cand_list());
+          else
+            k_rnbp_select<QS, false><<<grid_cap(g_.D / 4 + 1), kBlock, 0, s_>>>(
+                dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), nullptr, ctl(),
+                eps_, prm_, cand_list());
+        });
+        timed(kKSelect, [&] {
+          if (use_clist_)
+            k_rnbp_retry<QS, true><<<1, 1024, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
+                                                       vlist_.as<uint32_t>(), nullptr, ctl(), eps_, prm_, cand_list());
+          else
+            k_rnbp_retry<QS, false><<<1, 1024, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
+                                                        vlist_.as<uint32_t>(), nullptr, ctl(), eps_, prm_,
+                                                        cand_list());
+        });
+        launch_check();
+        enqueue_refresh(kFinIter);
+        break;
+      }
+      case BP_RBP:
+        ensure_rbp_scratch();
+        enqueue_topk(k_, 1);
+        enqueue_refresh(kFinIter);
+        break;
+      case BP_RS:
+        timed(kKSplash, [&] { launch_rs(rs_k(cfg_.p), cfg_.splash_depth, 1); });
+        enqueue_refresh(kFinIter);
+        break;
+      default:
+        throw Error(BP_ERR_UNSUPPORTED, "scheduler not available on the device");
+    }
+  }
+
+  // Device-side loop: WHILE(cond) { iteration } as one CUDA graph launch; the
+  // last block of each iteration sets cond = !done.
+  void run_graph_loop(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
+    if (!gexec_) {
+      cuda_check(cudaGraphCreate(&graph_, 0), "graph create");
+      cuda_check(cudaGraphConditionalHandleCreate(&cond_, graph_, 1, cudaGraphCondAssignDefault), "cond handle");
+      cudaGraphNodeParams p{};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = cond_;
+      p.conditional.type = cudaGraphCondTypeWhile;
+      p.conditional.size = 1;
+      cudaGraphNode_t node;
+      cuda_check(cudaGraphAddNode(&node, graph_, nullptr, 0, &p), "graph add conditional");
+      cudaGraph_t body = p.conditional.phGraph_out[0];
+      cuda_check(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
+                 "begin capture");
+      const uint64_t l0 = launches_;
+      enqueue_iteration();
+      body_launches_ = launches_ - l0;
+      launches_ = l0;
+      cudaGraph_t out_body;
+      cuda_check(cudaStreamEndCapture(s_, &out_body), "end capture");
+      cuda_check(cudaGraphInstantiate(&gexec_, graph_, 0), "graph instantiate");
+    }
+    set_cond_handle(static_cast<unsigned long long>(cond_));
+    const uint64_t it0 = hctl_->iteration;
+    // The device loop stops itself (converged / max_iterations / time_limit
+    // via %globaltimer).  The trace ring holds kTraceRing records, so long
+    // runs are split into chunks that the host drains in between.
+    for (;;) {
+      const uint64_t start_it = hctl_->iteration;
+      set_iteration_budget(start_it + kTraceRing / 2);
+      cuda_check(cudaGraphLaunch(gexec_, s_), "graph launch");
+      fetch_ctl_header();
+      drain_trace(trace, cap, copied);
+      if (hctl_->done) {
+        if (hctl_->stop_reason == kStopMaxIter && hctl_->iteration < cfg_.max_iterations && budget_stop_) {
+          // stopped by the chunk budget, not by the run: continue
+          clear_budget_stop();
+          continue;
+        }
+        break;
+      }
+    }
+    launches_ += (hctl_->iteration - it0) * body_launches_;
+    set_cond_handle(0);
+  }
+
+  // Chunking of the device loop: temporarily lower max_iterations so the ring
+  // never overruns; a stop caused by it is undone before continuing.
+  bool budget_stop_ = false;
+  void set_iteration_budget(uint64_t limit) {
+    const uint64_t eff = std::min<uint64_t>(limit, cfg_.max_iterations);
+    budget_stop_ = eff < cfg_.max_iterations;
+    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, max_iterations), &eff, 8,
+                               cudaMemcpyHostToDevice, s_),
+               "ctl h2d");
+    sync();
+  }
+  void clear_budget_stop() {
+    const unsigned zero = 0;
+    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, done), &zero, 4,
+                               cudaMemcpyHostToDevice, s_),
+               "ctl h2d");
+    sync();
+  }
+  void set_cond_handle(unsigned long long h) {
+    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, cond_handle), &h, 8,
+                               cudaMemcpyHostToDevice, s_),
+               "ctl h2d");
+    sync();
+  }
+
+  // ---- Residual Splash state (kernels_rs.cuh)
+  static unsigned long long rs_k_of(double p, uint32_t V) {  // schedulers.cpp:172-173
+    const long long kr = std::llround(p * static_cast<double>(V));
+    return kr < 1 ? 1ull : static_cast<unsigned long long>(kr);
+  }
+  unsigned long long rs_k(double p) const { return rs_k_of(p, g_.V); }
+  void ensure_rs(uint32_t h) {
+    if (h > kRsMaxDepth)
+      throw Error(BP_ERR_UNSUPPORTED, "splash_depth above " + std::to_string(kRsMaxDepth) +
+                                          " is not supported by the device splash builder");
+    if (rs_vres_.p) return;
+    const size_t V = std::max<size_t>(g_.V, 1);
+    for (DevBuf* b : {&rs_vres_, &rs_state_, &rs_claimed_, &rs_qnext_, &rs_spos_, &rs_depth_, &rs_clist_,
+                      &rs_blist_, &rs_rlist_, &rs_klist_})
+      b->alloc(V * 4);
+    rs_ballmax_.alloc(V * 8);
+    rs_hist_.alloc(4096 * 4);
+    cuda_check(cudaMemset(rs_hist_.p, 0, 4096 * 4), "memset");
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rs_iteration<QS>, kRsBlock, 0),
+               "occupancy");
+    rs_grid_ = static_cast<unsigned>(std::max(1, per_sm) * sm_count());
+    rs_blk_.alloc(static_cast<size_t>(rs_grid_) * 4);
+    rs_ctl_.alloc(sizeof(RsCtl));
+    cuda_check(cudaMemset(rs_ctl_.p, 0, sizeof(RsCtl)), "memset");
+    rs_shadow_.alloc(std::max<size_t>(static_cast<size_t>(g_.D) * QS * 4, 16));
+  }
+  RsBufs rs_bufs() {
+    RsBufs b{};
+    b.vres = rs_vres_.as<float>();
+    b.state = rs_state_.as<uint32_t>();
+    b.claimed = rs_claimed_.as<uint32_t>();
+    b.qnext = rs_qnext_.as<uint32_t>();
+    b.spos = rs_spos_.as<uint32_t>();
+    b.depth = rs_depth_.as<uint32_t>();
+    b.ballmax = rs_ballmax_.as<unsigned long long>();
+    b.clist = rs_clist_.as<uint32_t>();
+    b.blist = rs_blist_.as<uint32_t>();
+    b.rlist = rs_rlist_.as<uint32_t>();
+    b.klist = rs_klist_.as<uint32_t>();
+    b.hist = rs_hist_.as<unsigned>();
+    b.blk = rs_blk_.as<unsigned>();
+    b.rc = rs_ctl_.as<RsCtl>();
+    b.shadow = rs_shadow_.as<float>();
+    return b;
+  }
+  void launch_rs(unsigned long long k, uint32_t h, int apply) {
+    RsParams prm{k, h, apply};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(rs_grid_);
+    lc.blockDim = dim3(kRsBlock);
+    lc.stream = s_;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&lc, k_rs_iteration<QS>, dg_, live(), static_cast<const float*>(res_.as<float>()),
+                                  vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), rs_bufs(), prm),
+               "cooperative splash launch");
+  }
+
+  void ensure_beliefs_buf(size_t nb) {
+    if (bel_.bytes < nb * 8) bel_.alloc(nb * 8);
+  }
+  void enqueue_beliefs(double* dst, bool pingpong) {
+    timed(kKBeliefs, [&] {
+      k_beliefs<QS><<<grid_cap(g_.V), kBlock, 0, s_>>>(dg_, live(), cand(), pingpong ? 1 : 0, ctl(), dst);
+    });
+    launch_check();
+  }
+
+  void ensure_sel() {
+    if (!sel_.p) sel_.alloc(g_.D ? g_.D : 1);
+    cuda_check(cudaMemsetAsync(sel_.p, 0, g_.D ? g_.D : 1, s_), "memset sel");
+  }
+  void collect_sel(std::vector<uint32_t>& out) {
+    std::vector<uint8_t> h(g_.D);
+    if (g_.D) cuda_check(cudaMemcpyAsync(h.data(), sel_.p, g_.D, cudaMemcpyDeviceToHost, s_), "d2h");
+    sync();
+    out.clear();
+    for (uint32_t d = 0; d < g_.D; ++d)
+      if (h[d]) out.push_back(d);
+    // the queries do not change the state: clear the per-iteration counters
+    fetch_ctl_header();
+    hctl_->frontier = 0;
+    hctl_->survivors = 0;
+    hctl_->rx_prefix = 0;
+    hctl_->rx_above = 0;
+    std::memset(hctl_->acc, 0, sizeof(hctl_->acc));
+    cuda_check(cudaMemcpyAsync(ctl_.p, hctl_, offsetof(Ctl, trace), cudaMemcpyHostToDevice, s_), "ctl h2d");
+    sync();
+  }
+
+  const GraphImpl& g_;
+  bp_sched_config cfg_;
+  DevGraph dg_{};
+  float eps_ = 0.f;
+  cudaStream_t s_ = nullptr;
+  DevBuf bufA_, bufB_, res_, vflag_, vlist_, ctl_, hist_, chunk_, sel_, bel_, inlist_;
+  DevBuf clist_[2];
+  DevBuf rs_vres_, rs_state_, rs_claimed_, rs_qnext_, rs_spos_, rs_depth_, rs_clist_, rs_blist_, rs_rlist_,
+      rs_klist_, rs_ballmax_, rs_hist_, rs_blk_, rs_ctl_, rs_shadow_, rs_written_;
+  unsigned rs_grid_ = 1;
+  uint32_t rs_stamp_ = 0;
+  bool use_clist_ = false;
+  Ctl* hctl_ = nullptr;
+  uint32_t nchunks_ = 1;
+  uint64_t k_ = 1;
+  RnbpParams prm_{};
+  bool timing_ = false;
+  bp_kernel_stats* stats_ = nullptr;
+  uint64_t launches_ = 0;
+  uint64_t body_launches_ = 0;
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t gexec_ = nullptr;
+  cudaGraphConditionalHandle cond_{};
+};
+
+}  // namespace
+}  // namespace bpb

@@ -1,0 +1,8 @@
+// EngineT<16> instantiation (see engine_impl.cuh).
+#include "engine_impl.cuh"
+
+namespace bpb {
+std::unique_ptr<EngineBase> make_engine_q16(const GraphImpl& g, const bp_sched_config& cfg) {
+  return std::make_unique<EngineT<16>>(g, cfg);
+}
+}  // namespace bpb

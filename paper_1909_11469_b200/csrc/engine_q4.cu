@@ -1,0 +1,8 @@
+// EngineT<4> instantiation (see engine_impl.cuh).
+#include "engine_impl.cuh"
+
+namespace bpb {
+std::unique_ptr<EngineBase> make_engine_q4(const GraphImpl& g, const bp_sched_config& cfg) {
+  return std::make_unique<EngineT<4>>(g, cfg);
+}
+}  // namespace bpb

@@ -49,12 +49,18 @@ DevGraph GraphImpl::dev() const {
   g.unary_log = unary_log.as<float>();
   g.table = table.as<float>();
   g.bel_off = bel_off.as<uint32_t>();
+  g.lat_rows = lat_rows;
+  g.lat_cols = lat_cols;
+  g.par_mode = par_mode;
+  g.uniform_q = uniform_q;
+  g.jcoup = jcoup.as<float>();
+  g.pw = pw.as<float>();
   return g;
 }
 
 uint64_t GraphImpl::device_bytes() const {
   return in_off.bytes + in_adj.bytes + ep.bytes + unary_lo.bytes + epar.bytes + card.bytes +
-         unary_log.bytes + table.bytes + bel_off.bytes;
+         unary_log.bytes + table.bytes + bel_off.bytes + jcoup.bytes + pw.bytes;
 }
 
 namespace {
@@ -126,29 +132,6 @@ __global__ void k_lattice_topology(uint32_t R, uint32_t C, uint32_t* in_off, uin
   }
 }
 
-// Ising-style binary edge parameters from J = 2 lambda c: (alpha, beta, g-alpha, g-beta) = (-J, -J, J, J)
-__global__ void k_ising_params(const float* J, uint32_t E, float4* epar) {
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-    const float j = J[e];
-    epar[e] = make_float4(-j, -j, j, j);
-  }
-}
-
-// Potts tables from lambda*c: exp(lc) on the diagonal, exp(-lc) off it,
-// scaled by the larger of the two (normalisation makes the scale irrelevant).
-template <int QS>
-__global__ void k_potts_tables(const float* lc, uint32_t E, uint32_t q, float* table) {
-  const size_t n = static_cast<size_t>(E) * QS * QS;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const uint32_t e = static_cast<uint32_t>(i / (QS * QS));
-    const uint32_t a = static_cast<uint32_t>((i / QS) % QS), b = static_cast<uint32_t>(i % QS);
-    const double l = lc[e];
-    const double agree = exp(l - fabs(l)), disagree = exp(-l - fabs(l));
-    table[i] = (a < q && b < q) ? static_cast<float>(a == b ? agree : disagree) : 0.f;
-  }
-}
-
 __global__ void k_fill_u32(uint32_t* p, size_t n, uint32_t v) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -163,6 +146,28 @@ __global__ void k_iota_mul(uint32_t* p, size_t n, uint32_t mul) {
 
 unsigned grid_for(size_t n) {
   return static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148ull * 32));
+}
+
+// Does the edge list equal generate_ising's lattice numbering for some
+// rows x cols (generators.cpp:37-43)?  Then the device derives incoming
+// edges arithmetically.  Returns cols (0 = not a lattice).
+uint32_t detect_lattice(uint32_t V, uint32_t E, const uint32_t* ep) {
+  if (V < 2 || E == 0) return 0;
+  uint32_t C = V;  // a single row (also covers a single column)
+  if (E >= 2 && ep[0] == 0 && ep[1] == 1 && ep[2] == 0 && ep[3] > 1) C = ep[3];
+  if (V % C) return 0;
+  const uint64_t R = V / C;
+  if (static_cast<uint64_t>(E) != R * (C - 1) + (R - 1) * C) return 0;
+  uint64_t e = 0;
+  for (uint64_t r = 0; r < R; ++r)
+    for (uint64_t c = 0; c < C; ++c) {
+      const uint64_t v = r * C + c;
+      if (c + 1 < C && (ep[2 * e] != v || ep[2 * e + 1] != v + 1)) return 0;
+      if (c + 1 < C) ++e;
+      if (r + 1 < R && (ep[2 * e] != v || ep[2 * e + 1] != v + C)) return 0;
+      if (r + 1 < R) ++e;
+    }
+  return C;
 }
 
 }  // namespace
@@ -247,7 +252,23 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
                            static_cast<float>(gg - beta));
     }
     g->unary_lo.upload(ulo.data(), ulo.size() * 4);
-    g->epar.upload(par.data(), par.size() * 16);
+    // Ising tables {a, d, d, a} (generators.cpp:18-22): one coupling per edge
+    bool ising = E > 0;
+    for (uint32_t e = 0; e < E && ising; ++e) {
+      const double* t = d->pairwise_values + 4ull * e;
+      ising = t[0] == t[3] && t[1] == t[2];
+    }
+    if (ising) {
+      std::vector<float> J(E);
+      for (uint32_t e = 0; e < E; ++e) {
+        const double* t = d->pairwise_values + 4ull * e;
+        J[e] = static_cast<float>(std::log(t[0]) - std::log(t[1]));
+      }
+      g->jcoup.upload(J.data(), J.size() * 4);
+      g->par_mode = 1;
+    } else {
+      g->epar.upload(par.data(), par.size() * 16);
+    }
   } else {
     const uint32_t qs = stride_for(maxq);
     g->qs = qs;
@@ -258,8 +279,28 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
       for (uint32_t x = 0; x < d->cardinalities[v]; ++x)
         ul[static_cast<size_t>(v) * qs + x] = static_cast<float>(std::log(d->unary_values[o + x]));
     }
-    std::vector<float> tb(static_cast<size_t>(E) * qs * qs, 0.f);
-    for (uint32_t e = 0; e < E; ++e) {
+    // Potts tables (a on the diagonal, d off it, square): one weight per edge
+    bool potts = E > 0;
+    std::vector<float> w1(potts ? E : 0);
+    for (uint32_t e = 0; e < E && potts; ++e) {
+      const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
+      const uint32_t ci = d->cardinalities[i], cj = d->cardinalities[j];
+      const double* t = d->pairwise_values + poff[e];
+      if (ci != cj || ci < 2) {
+        potts = false;
+        break;
+      }
+      const double a = t[0], dd = t[1];
+      for (uint32_t x = 0; x < ci && potts; ++x)
+        for (uint32_t y = 0; y < cj && potts; ++y) potts = t[static_cast<size_t>(x) * cj + y] == (x == y ? a : dd);
+      if (potts) w1[e] = static_cast<float>(a / dd - 1.0);
+    }
+    std::vector<float> tb(potts ? 0 : static_cast<size_t>(E) * qs * qs, 0.f);
+    if (potts) {
+      g->pw.upload(w1.data(), w1.size() * 4);
+      g->par_mode = 1;
+    }
+    for (uint32_t e = 0; e < E && !potts; ++e) {
       const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
       const uint32_t ci = d->cardinalities[i], cj = d->cardinalities[j];
       const double* t = d->pairwise_values + poff[e];
@@ -275,9 +316,11 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     }
     g->card.upload(d->cardinalities, static_cast<size_t>(V) * 4);
     g->unary_log.upload(ul.data(), ul.size() * 4);
-    g->table.upload(tb.data(), tb.size() * 4);
+    if (!potts) g->table.upload(tb.data(), tb.size() * 4);
     g->bel_off.upload(bo.data(), bo.size() * 4);
   }
+  g->lat_cols = detect_lattice(V, E, d->edge_endpoints);
+  g->lat_rows = g->lat_cols ? V / g->lat_cols : 0;
   cuda_check(cudaDeviceSynchronize(), "graph upload");
   return g;
 }
@@ -307,10 +350,12 @@ std::unique_ptr<GraphImpl> build_lattice_binary(uint32_t rows, uint32_t cols, co
     cuda_check(cudaMemset(g->in_off.p, 0, 4), "memset");
   }
   g->unary_lo.upload(s.unary_lo.data(), V * 4);
-  DevBuf J;
-  J.upload(s.coupling.data(), E * 4);
-  g->epar.alloc(E * 16);
-  if (E) k_ising_params<<<grid_for(E), 256>>>(J.as<float>(), g->E, g->epar.as<float4>());
+  g->jcoup.upload(s.coupling.data(), E * 4);  // J = 2 lambda c: par = (-J, -J, J, J)
+  g->par_mode = 1;
+  if (V > 1) {
+    g->lat_rows = rows;
+    g->lat_cols = cols;
+  }
   cuda_check(cudaDeviceSynchronize(), "lattice build");
   return g;
 }
@@ -347,17 +392,14 @@ std::unique_ptr<GraphImpl> build_potts(uint32_t n, uint32_t q, const PottsStream
   if (V) k_fill_u32<<<grid_for(V), 256>>>(g->card.as<uint32_t>(), V, q);
   g->bel_off.alloc((V + 1) * 4);
   k_iota_mul<<<grid_for(V + 1), 256>>>(g->bel_off.as<uint32_t>(), V + 1, q);
-  DevBuf LC;
-  LC.upload(s.lambda_c.data(), E * 4);
-  g->table.alloc(E * qs * qs * 4);
-  if (E) {
-    const size_t n_el = E * qs * qs;
-    switch (qs) {
-      case 4: k_potts_tables<4><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
-      case 8: k_potts_tables<8><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
-      case 16: k_potts_tables<16><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
-      default: k_potts_tables<32><<<grid_for(n_el), 256>>>(LC.as<float>(), g->E, q, g->table.as<float>()); break;
-    }
+  // table: exp(lc) on the diagonal, exp(-lc) off it -> w1 = exp(2 lc) - 1
+  std::vector<float> w1(E);
+  for (uint64_t e = 0; e < E; ++e) w1[e] = static_cast<float>(std::expm1(2.0 * static_cast<double>(s.lambda_c[e])));
+  g->pw.upload(w1.data(), E * 4);
+  g->par_mode = 1;
+  if (V > 1) {
+    g->lat_rows = n;
+    g->lat_cols = n;
   }
   cuda_check(cudaDeviceSynchronize(), "potts build");
   return g;
@@ -380,10 +422,8 @@ std::unique_ptr<GraphImpl> build_er(uint32_t n, const ErInstance& inst, const bp
   g->in_adj.upload(adj.data(), adj.size() * 4);
   g->ep.upload(inst.endpoints.data(), static_cast<size_t>(E) * 8);
   g->unary_lo.upload(inst.unary_lo.data(), static_cast<size_t>(n) * 4);
-  DevBuf J;
-  J.upload(inst.coupling.data(), static_cast<size_t>(E) * 4);
-  g->epar.alloc(static_cast<size_t>(E) * 16);
-  if (E) k_ising_params<<<grid_for(E), 256>>>(J.as<float>(), E, g->epar.as<float4>());
+  g->jcoup.upload(inst.coupling.data(), static_cast<size_t>(E) * 4);
+  g->par_mode = 1;
   cuda_check(cudaDeviceSynchronize(), "er build");
   return g;
 }

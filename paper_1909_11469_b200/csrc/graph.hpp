@@ -35,7 +35,9 @@ struct GraphImpl {
   uint32_t V = 0, E = 0, D = 0, maxq = 0, qs = 1;
   uint32_t uniform_q = 0;  // all cardinalities equal to this (0 = mixed)
   bool binary = true;
-  DevBuf in_off, in_adj, ep, unary_lo, epar, card, unary_log, table, bel_off;
+  DevBuf in_off, in_adj, ep, unary_lo, epar, card, unary_log, table, bel_off, jcoup, pw;
+  uint32_t lat_rows = 0, lat_cols = 0;  // lattice topology detected / generated (0 = CSR only)
+  uint32_t par_mode = 0;                // 1: Ising couplings (binary) / Potts weights (generic)
   std::vector<uint32_t> cards_host;  // mixed cardinalities only
 
   DevGraph dev() const;

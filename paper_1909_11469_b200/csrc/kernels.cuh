@@ -189,7 +189,7 @@ __device__ __forceinline__ void fin_reset_scratch(Ctl* c) {
 }
 
 // <<<1, kSlots>>>
-__global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D) {
+static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D) {
   if (run_done(c)) return;
   const int t = threadIdx.x;
   const Accum a = c->acc[t];
@@ -277,24 +277,18 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
                                                     float eps, unsigned* numeric_flag,
                                                     unsigned long long& evals, uint8_t* inlist,
                                                     Stager* cl) {
-  const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
   float T = g.unary_lo[v];
   const float2* __restrict__ A2 = reinterpret_cast<const float2*>(A);
-  for (uint32_t a = b; a < e; ++a) {
-    const uint32_t in = g.in_adj[a];
-    const float2 pr = __ldg(&A2[in >> 1]);
-    T += (in & 1u) ? pr.y : pr.x;
-  }
+  // incoming messages and (same edge pair) the old outgoing ones, kept in
+  // registers between the two passes (lattice: exactly 4; CSR: re-read)
   int cnt = 0;
-  for (uint32_t a = b; a < e; ++a) {
-    const uint32_t in = g.in_adj[a];
+  uint32_t deg = 0;
+  auto emit = [&](uint32_t in, float2 pr) {
     const uint32_t out = in ^ 1u;
-    const float2 pr = __ldg(&A2[in >> 1]);
-    const float4 par = __ldg(&g.epar[in >> 1]);
     const float r_was = MODE == kModeDelta ? res[out] : 0.f;
     const float m_in = (in & 1u) ? pr.y : pr.x;
     const float m_old = (in & 1u) ? pr.x : pr.y;
-    const float lnew = binary_update(T - m_in, par, (out & 1u) != 0u);
+    const float lnew = binary_msg(g, T - m_in, out);
     const float r = binary_residual(lnew, m_old);
     if (!(fabsf(lnew) < INFINITY)) *numeric_flag = 1u;
     B[out] = lnew;
@@ -310,8 +304,28 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
       inlist[out] = 1;
       cl->push(out);
     }
+  };
+  if (g.lat_cols) {
+    uint32_t ins[4];
+    float2 prs[4];
+    for_each_in(g, v, [&](uint32_t in) {
+      ins[deg] = in;
+      prs[deg] = __ldg(&A2[in >> 1]);
+      T += (in & 1u) ? prs[deg].y : prs[deg].x;
+      ++deg;
+    });
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < static_cast<int>(deg)) emit(ins[k], prs[k]);
+  } else {
+    for_each_in(g, v, [&](uint32_t in) {
+      const float2 pr = __ldg(&A2[in >> 1]);
+      T += (in & 1u) ? pr.y : pr.x;
+      ++deg;
+    });
+    for_each_in(g, v, [&](uint32_t in) { emit(in, __ldg(&A2[in >> 1])); });
   }
-  evals += e - b;
+  evals += deg;
   return cnt;
 }
 
@@ -322,23 +336,21 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
                                                      float eps, unsigned* numeric_flag,
                                                      unsigned long long& evals, uint8_t* inlist,
                                                      Stager* cl) {
-  const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
   const uint32_t ci = g.card[v];
   float T[QS];
 #pragma unroll
   for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
-  for (uint32_t a = b; a < e; ++a) {
-    const float* m = A + static_cast<size_t>(g.in_adj[a]) * QS;
+  uint32_t deg = 0;
+  for_each_in(g, v, [&](uint32_t in) {
+    const float* m = A + static_cast<size_t>(in) * QS;
 #pragma unroll
     for (int x = 0; x < QS; ++x) T[x] += __ldg(&m[x]);
-  }
+    ++deg;
+  });
   int cnt = 0;
-  for (uint32_t a = b; a < e; ++a) {
-    const uint32_t in = g.in_adj[a];
+  for_each_in(g, v, [&](uint32_t in) {
     const uint32_t out = in ^ 1u;
-    const uint32_t edge = in >> 1;
-    const uint32_t tgt = g.ep[in];  // source of `in` = target of `out`
-    const uint32_t cj = g.card[tgt];
+    const uint32_t cj = g.uniform_q ? g.uniform_q : g.card[g.ep[in]];  // target of `out` = source of `in`
     const float* m_in = A + static_cast<size_t>(in) * QS;
     const float r_was = MODE == kModeDelta ? res[out] : 0.f;
     float p[QS];
@@ -350,26 +362,9 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
     }
 #pragma unroll
     for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
-    const float* tab = g.table + static_cast<size_t>(edge) * QS * QS;
     float o[QS];
+    generic_matvec<QS>(g, out, p, o);
     float s = 0.f;
-    if ((out & 1u) == 0u) {  // v is lo: A(xs, xt) = T[xs][xt]
-#pragma unroll
-      for (int xt = 0; xt < QS; ++xt) o[xt] = 0.f;
-#pragma unroll
-      for (int xs = 0; xs < QS; ++xs) {
-#pragma unroll
-        for (int xt = 0; xt < QS; ++xt) o[xt] = fmaf(__ldg(&tab[xs * QS + xt]), p[xs], o[xt]);
-      }
-    } else {  // v is hi: A(xs, xt) = T[xt][xs]
-#pragma unroll
-      for (int xt = 0; xt < QS; ++xt) {
-        float acc = 0.f;
-#pragma unroll
-        for (int xs = 0; xs < QS; ++xs) acc = fmaf(__ldg(&tab[xt * QS + xs]), p[xs], acc);
-        o[xt] = acc;
-      }
-    }
 #pragma unroll
     for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
     const float inv = __frcp_rn(s);
@@ -398,8 +393,8 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
       inlist[out] = 1;
       cl->push(out);
     }
-  }
-  evals += e - b;
+  });
+  evals += deg;
   return cnt;
 }
 
@@ -799,7 +794,7 @@ __device__ __forceinline__ uint32_t float_key(float r) { return __float_as_uint(
 
 // pass 0: bins key>>20; pass 1: (key>>8)&0xfff for key>>20 == prefix;
 // pass 2: key&0xff for key>>8 == prefix
-__global__ void __launch_bounds__(kBlock) k_radix_hist(const float* res, uint32_t D, int pass,
+static __global__ void __launch_bounds__(kBlock) k_radix_hist(const float* res, uint32_t D, int pass,
                                                        unsigned* hist, Ctl* ctl) {
   if (run_done(ctl)) return;
   __shared__ unsigned sh[kRadixBins];
@@ -833,7 +828,7 @@ __global__ void __launch_bounds__(kBlock) k_radix_hist(const float* res, uint32_
 // Single block of 1024: find the bin holding the k-th largest key (counting
 // from the top), extend the prefix, accumulate the count strictly above it and
 // clear the histogram for the next use.
-__global__ void __launch_bounds__(1024) k_radix_scan(unsigned* hist, int pass, unsigned long long k,
+static __global__ void __launch_bounds__(1024) k_radix_scan(unsigned* hist, int pass, unsigned long long k,
                                                      Ctl* ctl) {
   if (run_done(ctl)) return;
   __shared__ unsigned long long wsum[32];
@@ -890,7 +885,7 @@ __global__ void __launch_bounds__(1024) k_radix_scan(unsigned* hist, int pass, u
 constexpr uint32_t kTieChunk = 8192;
 
 // per-chunk count of keys equal to the threshold (only when not all ties are taken)
-__global__ void __launch_bounds__(kBlock) k_tie_count(const float* res, uint32_t D, unsigned* chunk_cnt,
+static __global__ void __launch_bounds__(kBlock) k_tie_count(const float* res, uint32_t D, unsigned* chunk_cnt,
                                                       Ctl* ctl) {
   if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
   const uint32_t key = ctl->rx_prefix;
@@ -904,7 +899,7 @@ __global__ void __launch_bounds__(kBlock) k_tie_count(const float* res, uint32_t
 }
 
 // exclusive prefix over chunk counts (single block)
-__global__ void __launch_bounds__(1024) k_tie_scan(unsigned* chunk_cnt, uint32_t nchunks, Ctl* ctl) {
+static __global__ void __launch_bounds__(1024) k_tie_scan(unsigned* chunk_cnt, uint32_t nchunks, Ctl* ctl) {
   if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
   __shared__ unsigned wsum[32];
   __shared__ unsigned carry;
@@ -1014,10 +1009,9 @@ __global__ void k_beliefs(DevGraph g, const float* A0, const float* A1, int ping
                           double* out) {
   const float* A = (pingpong && (ctl->iteration & 1ull)) ? A1 : A0;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.V; v += gridDim.x * blockDim.x) {
-    const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
     if (QS == 1) {
       float T = g.unary_lo[v];
-      for (uint32_t a = b; a < e; ++a) T += A[g.in_adj[a]];
+      for_each_in(g, v, [&](uint32_t in) { T += A[in]; });
       const double t = static_cast<double>(T);
       out[2 * static_cast<size_t>(v)] = 1.0 / (1.0 + exp(t));
       out[2 * static_cast<size_t>(v) + 1] = 1.0 / (1.0 + exp(-t));
@@ -1026,11 +1020,11 @@ __global__ void k_beliefs(DevGraph g, const float* A0, const float* A1, int ping
       float T[QS];
 #pragma unroll
       for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
-      for (uint32_t a = b; a < e; ++a) {
-        const float* m = A + static_cast<size_t>(g.in_adj[a]) * QS;
+      for_each_in(g, v, [&](uint32_t in) {
+        const float* m = A + static_cast<size_t>(in) * QS;
 #pragma unroll
         for (int x = 0; x < QS; ++x) T[x] += m[x];
-      }
+      });
       float M = -INFINITY;
 #pragma unroll
       for (int x = 0; x < QS; ++x)

@@ -304,7 +304,7 @@ __device__ __forceinline__ void splash_vertex_update(const DevGraph& g, uint32_t
     for (uint32_t a = b0; a < e0; ++a) T += *src_of(g.in_adj[a]);
     for (uint32_t a = b0; a < e0; ++a) {
       const uint32_t in = g.in_adj[a], out = in ^ 1u;
-      const float lnew = binary_update(T - *src_of(in), __ldg(&g.epar[in >> 1]), (out & 1u) != 0u);
+      const float lnew = binary_msg(g, T - *src_of(in), out);
       if (!(fabsf(lnew) < INFINITY)) *nf = 1u;
       shadow[out] = lnew;
     }
@@ -330,24 +330,8 @@ __device__ __forceinline__ void splash_vertex_update(const DevGraph& g, uint32_t
       }
 #pragma unroll
       for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
-      const float* tab = g.table + static_cast<size_t>(in >> 1) * QS * QS;
       float o[QS], s = 0.f;
-      if ((out & 1u) == 0u) {
-#pragma unroll
-        for (int xt = 0; xt < QS; ++xt) o[xt] = 0.f;
-#pragma unroll
-        for (int xs = 0; xs < QS; ++xs)
-#pragma unroll
-          for (int xt = 0; xt < QS; ++xt) o[xt] = fmaf(__ldg(&tab[xs * QS + xt]), p[xs], o[xt]);
-      } else {
-#pragma unroll
-        for (int xt = 0; xt < QS; ++xt) {
-          float acc = 0.f;
-#pragma unroll
-          for (int xs = 0; xs < QS; ++xs) acc = fmaf(__ldg(&tab[xt * QS + xs]), p[xs], acc);
-          o[xt] = acc;
-        }
-      }
+      generic_matvec<QS>(g, out, p, o);
 #pragma unroll
       for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
       if (!(s > 0.f) || !(s < INFINITY)) *nf = 1u;
@@ -605,7 +589,7 @@ __global__ void __launch_bounds__(kBlock) k_splash_apply_edges(DevGraph g, const
         const uint32_t in = g.in_adj[a];
         if (in != back) T += *src_of(in);
       }
-      const float lnew = binary_update(T, __ldg(&g.epar[d >> 1]), (d & 1u) != 0u);
+      const float lnew = binary_msg(g, T, d);
       if (!(fabsf(lnew) < INFINITY)) *nf = 1u;
       shadow[d] = lnew;
     } else {
@@ -625,24 +609,8 @@ __global__ void __launch_bounds__(kBlock) k_splash_apply_edges(DevGraph g, const
         if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
 #pragma unroll
       for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
-      const float* tab = g.table + static_cast<size_t>(d >> 1) * QS * QS;
       float o[QS], s2 = 0.f;
-      if ((d & 1u) == 0u) {
-#pragma unroll
-        for (int xt = 0; xt < QS; ++xt) o[xt] = 0.f;
-#pragma unroll
-        for (int xs = 0; xs < QS; ++xs)
-#pragma unroll
-          for (int xt = 0; xt < QS; ++xt) o[xt] = fmaf(tab[xs * QS + xt], p[xs], o[xt]);
-      } else {
-#pragma unroll
-        for (int xt = 0; xt < QS; ++xt) {
-          float acc = 0.f;
-#pragma unroll
-          for (int xs = 0; xs < QS; ++xs) acc = fmaf(tab[xt * QS + xs], p[xs], acc);
-          o[xt] = acc;
-        }
-      }
+      generic_matvec<QS>(g, d, p, o);
 #pragma unroll
       for (int xt = 0; xt < QS; ++xt) s2 += xt < static_cast<int>(cj) ? o[xt] : 0.f;
       if (!(s2 > 0.f) || !(s2 < INFINITY)) *nf = 1u;
