@@ -107,6 +107,8 @@ typedef struct {
   uint64_t message_evaluations;    /* candidate / message recomputations on the device     */
   uint64_t gpu_launches;           /* kernels launched by this run (incl. early-exit ones)  */
   uint64_t vertex_visits;          /* vertices processed by update kernels                  */
+  uint64_t splashes;               /* residual splash: splashes applied (all iterations)    */
+  uint64_t splash_rounds;          /* residual splash: parallel claiming rounds             */
 } bp_run_result;
 
 typedef struct {

@@ -1,0 +1,152 @@
+/*
+ * bpsched_cuda.hpp -- C++ drop-in for the reference's scheduler entry point.
+ *
+ *   bpsched::RunResult bpsched_cuda::run(const bpsched::PairwiseMRF&,
+ *                                        const bpsched::SchedulerConfig&);
+ *
+ * has the signature, types, defaults and error behaviour of bpsched::run
+ * (/root/reference/proj/core/include/bpsched/schedulers.hpp:156,
+ * src/schedulers.cpp:293-353) and runs the scheduler loop on the B200 engine
+ * through the C ABI in bp_cuda.h.  Header-only: a caller of the reference
+ * (tools/bpsched.cpp:172,299,349) includes this next to the reference headers,
+ * links libbp_b200.so, and switches `bpsched::run(` to `bpsched_cuda::run(`
+ * (INTEGRATION.md).  Graph loading stays the reference's own
+ * (build_graph / parse_model / generate_ising, mrf.hpp:94-96): the facade reads
+ * only the public PairwiseMRF accessors (mrf.hpp:39-70).
+ *
+ * Errors are rethrown as the reference's exceptions (errors.hpp:10-38):
+ * std::invalid_argument for a bad config, bpsched::model_error,
+ * bpsched::numeric_error, bpsched::error for device failures.  Caps are not
+ * errors (converged == false), exactly as in the reference.
+ *
+ * Serial RBP (SchedulerKind::serial_rbp) is strictly sequential by
+ * definition and stays on the host: the facade forwards it to
+ * the reference's bpsched::run_serial_rbp.
+ */
+#ifndef BPSCHED_CUDA_HPP
+#define BPSCHED_CUDA_HPP
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "bp_cuda.h"
+#include "bpsched/errors.hpp"
+#include "bpsched/messages.hpp"
+#include "bpsched/mrf.hpp"
+#include "bpsched/schedulers.hpp"
+
+namespace bpsched_cuda {
+
+[[noreturn]] inline void throw_status(int rc) {
+  const std::string msg = bp_last_error();
+  switch (rc) {
+    case BP_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case BP_ERR_MODEL: throw bpsched::model_error(msg);
+    case BP_ERR_NUMERIC: throw bpsched::numeric_error(msg);
+    default: throw bpsched::error("bp_cuda (status " + std::to_string(rc) + "): " + msg);
+  }
+}
+
+inline void check(int rc) {
+  if (rc != BP_OK) throw_status(rc);
+}
+
+/// SchedulerConfig (schedulers.hpp:26-41) -> bp_sched_config; same numbering
+/// of SchedulerKind.
+inline bp_sched_config to_c(const bpsched::SchedulerConfig& c) {
+  bp_sched_config o{};
+  o.kind = static_cast<int32_t>(c.kind);
+  o.splash_depth = c.splash_depth;
+  o.epsilon = c.epsilon;
+  o.p = c.p;
+  o.low_p = c.low_p;
+  o.high_p = c.high_p;
+  o.edge_ratio_threshold = c.edge_ratio_threshold;
+  o.max_iterations = c.max_iterations;
+  o.time_limit = c.time_limit;
+  o.seed = c.seed;
+  o.worker_count = c.worker_count;
+  return o;
+}
+
+/// A PairwiseMRF resident in HBM.  Upload once, run many times (the graph is
+/// immutable and shareable across runs, mrf.hpp:24-25).
+class DeviceGraph {
+ public:
+  explicit DeviceGraph(const bpsched::PairwiseMRF& g, int device = -1) {
+    const uint32_t V = g.num_vertices(), E = g.num_edges();
+    cards_.resize(V);
+    std::vector<double> unary;
+    for (bpsched::vertex_id v = 0; v < V; ++v) {
+      cards_[v] = g.cardinality(v);
+      const auto u = g.unary(v);
+      unary.insert(unary.end(), u.begin(), u.end());
+    }
+    std::vector<uint32_t> ep(2ull * E);
+    std::vector<double> tables;
+    for (bpsched::edge_id e = 0; e < E; ++e) {
+      const auto [i, j] = g.edge_endpoints(e);
+      ep[2ull * e] = i;
+      ep[2ull * e + 1] = j;
+      const auto t = g.pairwise(e);
+      tables.insert(tables.end(), t.begin(), t.end());
+    }
+    bp_graph_desc d{V, E, cards_.data(), unary.data(), ep.data(), tables.data()};
+    bp_device_opts o{device, BP_GRAPH_TRUSTED};  // build_graph already validated it
+    check(bp_graph_create(&d, &o, &h_));
+  }
+  DeviceGraph(const DeviceGraph&) = delete;
+  DeviceGraph& operator=(const DeviceGraph&) = delete;
+  ~DeviceGraph() { bp_graph_destroy(h_); }
+
+  const bp_graph* get() const { return h_; }
+  const std::vector<uint32_t>& cardinalities() const { return cards_; }
+
+ private:
+  bp_graph* h_ = nullptr;
+  std::vector<uint32_t> cards_;
+};
+
+/// bpsched::run on a device-resident graph.
+inline bpsched::RunResult run(const DeviceGraph& g, const bpsched::SchedulerConfig& config) {
+  config.validate();  // the reference's own validation (schedulers.cpp:78-90)
+  const bp_sched_config c = to_c(config);
+  size_t nb = 0;
+  for (uint32_t q : g.cardinalities()) nb += q;
+  std::vector<double> beliefs(nb);
+  const uint64_t cap = config.max_iterations < (1ull << 22) ? config.max_iterations + 1 : (1ull << 22);
+  std::vector<bp_iter_record> trace(cap);
+  bp_run_result r{};
+  check(bp_run(g.get(), &c, &r, beliefs.data(), trace.data(), cap));
+
+  bpsched::RunResult out;
+  out.converged = r.converged != 0;
+  out.iterations = r.iterations;
+  out.wall_time = r.wall_time;
+  out.messages_updated_total = r.messages_updated_total;
+  out.beliefs = bpsched::BeliefTable(g.cardinalities());
+  size_t o = 0;
+  for (bpsched::vertex_id v = 0; v < g.cardinalities().size(); ++v) {
+    auto dst = out.beliefs.at(v);
+    for (size_t x = 0; x < dst.size(); ++x) dst[x] = beliefs[o++];
+  }
+  const uint64_t n = r.trace_len < cap ? r.trace_len : cap;
+  out.trace.reserve(n);
+  for (uint64_t k = 0; k < n; ++k)
+    out.trace.push_back({trace[k].iteration, trace[k].frontier_size, trace[k].unconverged, trace[k].elapsed_seconds});
+  return out;
+}
+
+/// Drop-in for bpsched::run (schedulers.hpp:156).
+inline bpsched::RunResult run(const bpsched::PairwiseMRF& graph, const bpsched::SchedulerConfig& config) {
+  config.validate();
+  if (config.kind == bpsched::SchedulerKind::serial_rbp) return bpsched::run_serial_rbp(graph, config);
+  DeviceGraph g(graph);
+  return run(g, config);
+}
+
+}  // namespace bpsched_cuda
+
+#endif  // BPSCHED_CUDA_HPP

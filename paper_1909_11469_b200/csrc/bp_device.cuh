@@ -9,9 +9,10 @@
 //     of one undirected edge are adjacent ("edge pair"): a vertex update loads
 //     one pair and gets both the incoming message and the old outgoing message
 //     it needs for the residual.
-//   * binary graphs (all cardinalities 2): one fp32 log-odds per message,
-//     log(m(1)/m(0)); unary log-odds per vertex; per edge float4 of log-table
-//     differences.  Generic graphs: qs fp32 log-probabilities per message
+//   * binary graphs (all cardinalities 2): one fp32 BASE-2 log-odds per
+//     message, log2(m(1)/m(0)); unary log2-odds per vertex; per edge either
+//     a = e^J (Ising tables) or a float4 of log2-table differences.  Base 2
+//     makes every transcendental one SFU instruction (ex2/lg2.approx).  Generic graphs: qs fp32 log-probabilities per message
 //     (qs = padded max cardinality), qs x qs max-scaled linear tables.
 #pragma once
 
@@ -39,15 +40,49 @@ struct DevGraph {
   // Structured fast paths (uniform-branch flags, no extra template axes):
   //   lattice topology: rows x cols row-major grid with the generator's edge
   //   order (generators.cpp:37-43) -> incoming edges by arithmetic, no CSR reads;
-  //   par_mode 1: binary Ising tables {a, d, d, a} -> one coupling J per edge
-  //   (jcoup), generic Potts tables (a on the diagonal, d off it) -> one
+  //   par_mode 1: binary Ising tables {a, d, d, a} -> one weight a/d per edge
+  //   (ising_a), generic Potts tables (a on the diagonal, d off it) -> one
   //   w1 = a/d - 1 per edge (pw).  0: float4 epar / dense q x q tables.
   uint32_t lat_rows, lat_cols;
   uint32_t par_mode;
   uint32_t uniform_q;                     // all cardinalities equal (0 = mixed)
-  const float* __restrict__ jcoup;        // E  (binary, par_mode 1)
+  const float* __restrict__ ising_a;      // E  (binary, par_mode 1): a = e^J of the table {a, 1/a, 1/a, a}
   const float* __restrict__ pw;           // E  (generic, par_mode 1)
 };
+
+constexpr uint32_t kUncl = 0xFFFFFFFFu;
+constexpr uint32_t kRsMaxDepth = 8;
+
+// Non-backtracking walks of length <= h from r (covers every vertex within
+// distance h, some more than once).  f(w) returning false stops the walk.
+template <class F>
+__device__ __forceinline__ bool ball_walk(const DevGraph& g, uint32_t r, uint32_t h, F&& f) {
+  if (!f(r)) return false;
+  if (h == 0) return true;
+  uint32_t vs[kRsMaxDepth], par[kRsMaxDepth], pos[kRsMaxDepth], end[kRsMaxDepth];
+  int d = 0;
+  vs[0] = r;
+  par[0] = kUncl;
+  pos[0] = g.in_off[r];
+  end[0] = g.in_off[r + 1];
+  while (d >= 0) {
+    if (pos[d] < end[d]) {
+      const uint32_t w = g.ep[g.in_adj[pos[d]++]];  // source of an incoming edge = neighbour
+      if (w == par[d]) continue;
+      if (!f(w)) return false;
+      if (d + 1 < static_cast<int>(h)) {
+        ++d;
+        vs[d] = w;
+        par[d] = vs[d - 1];
+        pos[d] = g.in_off[w];
+        end[d] = g.in_off[w + 1];
+      }
+    } else {
+      --d;
+    }
+  }
+  return true;
+}
 
 // Incoming directed edges of v in CSR order (mrf.cpp:93-104).  Lattice: up,
 // left, right, down, from the edge numbering of generate_ising
@@ -125,49 +160,111 @@ struct Ctl {
   unsigned int stamp;         // vflag generation
   unsigned int splashes;
   unsigned long long splash_edges;
-  unsigned int rs_pending;
-  unsigned int rs_built;
+  unsigned int rs_rounds;     // splash claiming rounds (all iterations)
+  unsigned int rs_passes;     // candidate-prefix passes (all iterations)
   unsigned long long trace_len;
   unsigned long long cond_handle;  // cudaGraphConditionalHandle of the WHILE loop (0 = none)
   unsigned int stop_reason;
   unsigned int cl_cur;        // candidate list (RnBP): current buffer
   unsigned int cl_n[2];       // candidate list sizes
   unsigned int use_clist;
-  unsigned int pad2_;
+  unsigned int cl_state;      // 0 scan residuals, 1 build the list this iteration, 2 walk the list
   Accum acc[kSlots];
   TraceRec trace[kTraceRing];
 };
 
 // ---------------------------------------------------------------------------
-// numerics
+// numerics.  Raw SFU instructions (one SASS op each; __expf/__logf/__fdividef
+// add denormal guards that cost 4-6 extra instructions per call).  ftz: the
+// operands here never need denormals (2^-126 is far below any message scale).
 
-__device__ __forceinline__ float softplusf(float x) {
-  // log(1 + e^x) = max(x, 0) + log1p(e^-|x|)
-  return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x)));
+__device__ __forceinline__ float fex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float flg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float frcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
-__device__ __forceinline__ float sigmoidf(float x) { return __frcp_rn(1.f + __expf(-x)); }
+// log2(1 + 2^x) = max(x, 0) + log2(1 + 2^-|x|)
+__device__ __forceinline__ float softplus2(float x) { return fmaxf(x, 0.f) + flg2(1.f + fex2(-fabsf(x))); }
 
-// Binary sum-product update (Eq. 2, messages.hpp:114-151) in log-odds form:
-// with cavity log-odds h of the source and the 2x2 table A oriented source x
-// target, out = log(A01 + A11 e^h) - log(A00 + A10 e^h)
-//             = c + softplus(h + a) - softplus(h + b).
+// probability of state 1 of a base-2 log-odds message
+__device__ __forceinline__ float sigmoid2(float x) { return frcp(1.f + fex2(-x)); }
+
+// Binary sum-product update (Eq. 2, messages.hpp:114-151) in log2-odds form:
+// with cavity log2-odds h of the source and the 2x2 table A oriented source x
+// target, out = log2(A01 + A11 2^h) - log2(A00 + A10 2^h)
+//             = c + softplus2(h + a) - softplus2(h + b).
 // par = (alpha, beta, g - alpha, g - beta) with alpha = lT01 - lT00,
-// beta = lT10 - lT00, g = lT11 - lT00 (T row = lo state).  Even d (lo -> hi):
-// c = alpha, a = g - alpha, b = beta.  Odd d: c = beta, a = g - beta, b = alpha.
+// beta = lT10 - lT00, g = lT11 - lT00 (log2 of the table, row = lo state).
+// Even d (lo -> hi): c = alpha, a = g - alpha, b = beta.  Odd d: c = beta,
+// a = g - beta, b = alpha.
 __device__ __forceinline__ float binary_update(float h, float4 par, bool odd) {
   const float c = odd ? par.y : par.x;
   const float a = odd ? par.w : par.z;
   const float b = odd ? par.x : par.y;
-  return c + softplusf(h + a) - softplusf(h + b);
+  return c + softplus2(h + a) - softplus2(h + b);
+}
+
+// L-inf residual in linear probability space (messages.cpp:56-65): for binary
+// messages |m'(1) - m(1)| = |m'(0) - m(0)|.
+__device__ __forceinline__ float binary_residual(float lnew, float lold) {
+  return fabsf(sigmoid2(lnew) - sigmoid2(lold));
+}
+
+// Ising message (table {a, 1, 1, a} up to scale, a = e^J): with u = 2^h the
+// outgoing odds are X = (1 + u a) / (a + u); evaluated through
+// v = 2^-|h| <= 1 so nothing overflows.
+struct IsingOut {
+  float l;  // log2-odds log2 X
+};
+__device__ __forceinline__ IsingOut ising_msg(float h, float a) {
+  const float v = fex2(-fabsf(h));
+  float num, den;
+  if (h >= 0.f) {
+    num = v + a;
+    den = fmaf(a, v, 1.f);
+  } else {
+    num = fmaf(v, a, 1.f);
+    den = a + v;
+  }
+  IsingOut o;
+  o.l = flg2(num * frcp(den));
+  return o;
+}
+
+// Ising message + its L-inf residual in one pass (5 SFU ops: ex2, rcp, lg2 for
+// the message, ex2, rcp for the residual).  With X = num/den the new odds and
+// Y = 2^{l_old} the old ones, |sigma(l_new) - sigma(l_old)| =
+// |num - Y den| / ((num + den)(1 + Y)); for l_old >= 0 the mirrored form
+// (sigma(-x) = 1 - sigma(x)) keeps Y = 2^-|l_old| <= 1 so nothing overflows.
+// A bitwise fixed point (l_new == l_old) reports exactly 0, so tree exactness
+// at epsilon 1e-8 holds (test_schedulers.cpp:418-434).
+__device__ __forceinline__ float ising_update(float h, float a, float l_old, float& l_new) {
+  const float v = fex2(-fabsf(h));
+  const bool pos = h >= 0.f;
+  const float num = pos ? v + a : fmaf(v, a, 1.f);
+  const float den = pos ? fmaf(a, v, 1.f) : a + v;
+  l_new = flg2(num * frcp(den));
+  const bool po = l_old >= 0.f;
+  const float Y = fex2(-fabsf(l_old));
+  const float nn = po ? den : num, dd = po ? num : den;
+  const float r = fabsf(fmaf(-Y, dd, nn)) * frcp((num + den) * (1.f + Y));
+  return l_new == l_old ? 0.f : r;
 }
 
 // Outgoing binary message on directed edge `out` from the cavity log-odds h.
 __device__ __forceinline__ float binary_msg(const DevGraph& g, float h, uint32_t out) {
-  if (g.par_mode) {  // Ising table: par = (-J, -J, J, J) in both directions
-    const float j = __ldg(&g.jcoup[out >> 1]);
-    return -j + softplusf(h + j) - softplusf(h - j);
-  }
+  if (g.par_mode) return ising_msg(h, __ldg(&g.ising_a[out >> 1])).l;
   return binary_update(h, __ldg(&g.epar[out >> 1]), (out & 1u) != 0u);
 }
 
@@ -203,12 +300,6 @@ __device__ __forceinline__ void generic_matvec(const DevGraph& g, uint32_t out, 
       o[xt] = acc;
     }
   }
-}
-
-// L-inf residual in linear probability space (messages.cpp:56-65): for binary
-// messages |m'(1) - m(1)| = |m'(0) - m(0)|.
-__device__ __forceinline__ float binary_residual(float lnew, float lold) {
-  return fabsf(sigmoidf(lnew) - sigmoidf(lold));
 }
 
 // ---------------------------------------------------------------------------

@@ -40,7 +40,7 @@ class Mt64 {
 // Host-side instance streams (generators.cpp:24-71 for Ising/chain; the new
 // Potts and Erdos-Renyi definitions are in DESIGN.md section 3).
 struct BinaryStreams {
-  std::vector<float> unary_lo;  // log(u1) - log(u0) per vertex
+  std::vector<float> unary_lo;  // log2(u1) - log2(u0) per vertex (binary layout: base-2 log-odds)
   std::vector<float> coupling;  // J = 2 * lambda * c per edge (log-table differences)
 };
 BinaryStreams ising_streams(uint32_t n, double c, uint64_t seed);

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 
 #include "engine.hpp"
 #include "kernels.cuh"
@@ -156,6 +157,8 @@ class EngineT final : public EngineBase {
     res->device_ms = ms;
     res->message_evaluations = hctl_->evals_total;
     res->vertex_visits = hctl_->vertex_visits;
+    res->splashes = hctl_->splashes;
+    res->splash_rounds = hctl_->rs_rounds;
     res->gpu_launches = launches_;
     res->wall_time = std::chrono::duration<double>(Clock::now() - t0).count();
   }
@@ -183,8 +186,8 @@ class EngineT final : public EngineBase {
     for (uint32_t d = 0; d < g_.D; ++d) {
       if (QS == 1) {
         const double l = raw[d];
-        out[o++] = 1.0 / (1.0 + std::exp(l));
-        out[o++] = 1.0 / (1.0 + std::exp(-l));
+        out[o++] = 1.0 / (1.0 + std::exp2(l));  // base-2 log-odds
+        out[o++] = 1.0 / (1.0 + std::exp2(-l));
       } else {
         const uint32_t q = g_.card_of(ep[d ^ 1u]);
         for (uint32_t x = 0; x < q; ++x) out[o++] = std::exp(static_cast<double>(raw[static_cast<size_t>(d) * QS + x]));
@@ -447,6 +450,23 @@ class EngineT final : public EngineBase {
     ev_next_ = 0;
   }
 
+  // resident grid for a grid-stride kernel: blocks/SM from the occupancy
+  // calculator x SMs (one wave, no tail), capped by the work
+  std::map<const void*, int> occ_;
+  template <class K>
+  unsigned vgrid(K kern, size_t items) {
+    auto it = occ_.find(reinterpret_cast<const void*>(kern));
+    int per = 0;
+    if (it == occ_.end()) {
+      cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kBlock, 0), "occupancy");
+      occ_[reinterpret_cast<const void*>(kern)] = per;
+    } else {
+      per = it->second;
+    }
+    const size_t want = (items + kBlock - 1) / kBlock;
+    return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(want, static_cast<size_t>(std::max(per, 1)) * sm_count())));
+  }
+
   // ---- launch sequences
   void enqueue_finalize(int mode) {
     timed(kKOther, [&] { k_finalize<<<1, kSlots, 0, s_>>>(ctl(), mode, g_.D); });
@@ -461,17 +481,17 @@ class EngineT final : public EngineBase {
     if (lbp) {  // sweep 0 (ResidualTracker ctor, residuals.cpp:9-24)
       timed(kKUpdate, [&] {
         k_vertex_update<QS, kModeCount, false, true, false>
-            <<<gv, kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+            <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
       });
       launch_check();
       enqueue_finalize(kFinLbp);
     } else {
       timed(kKUpdate, [&] {
         if (use_clist_)
-          k_vertex_update<QS, kModeInit, false, false, true><<<gv, kBlock, 0, s_>>>(
+          k_vertex_update<QS, kModeInit, false, false, true><<<vgrid(k_vertex_update<QS, kModeInit, false, false, true>, g_.V), kBlock, 0, s_>>>(
               dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
         else
-          k_vertex_update<QS, kModeInit, false, false, false><<<gv, kBlock, 0, s_>>>(
+          k_vertex_update<QS, kModeInit, false, false, false><<<vgrid(k_vertex_update<QS, kModeInit, false, false, false>, g_.V), kBlock, 0, s_>>>(
               dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
       });
       launch_check();
@@ -483,11 +503,11 @@ class EngineT final : public EngineBase {
     const unsigned gv = grid_cap(g_.V);
     timed(kKUpdate, [&] {
       if (use_clist_)
-        k_vertex_update<QS, kModeDelta, true, false, true><<<gv, kBlock, 0, s_>>>(
+        k_vertex_update<QS, kModeDelta, true, false, true><<<vgrid(k_vertex_update<QS, kModeDelta, true, false, true>, g_.V), kBlock, 0, s_>>>(
             dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
             cand_list());
       else
-        k_vertex_update<QS, kModeDelta, true, false, false><<<gv, kBlock, 0, s_>>>(
+        k_vertex_update<QS, kModeDelta, true, false, false><<<vgrid(k_vertex_update<QS, kModeDelta, true, false, false>, g_.V), kBlock, 0, s_>>>(
             dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
             cand_list());
     });
@@ -551,7 +571,7 @@ class EngineT final : public EngineBase {
         const unsigned gv = grid_cap(g_.V);
         timed(kKUpdate, [&] {
           k_vertex_update<QS, kModeCount, false, true, false>
-              <<<gv, kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+              <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
         });
         launch_check();
         enqueue_finalize(kFinLbp);
@@ -678,6 +698,7 @@ class EngineT final : public EngineBase {
     if (h > kRsMaxDepth)
       throw Error(BP_ERR_UNSUPPORTED, "splash_depth above " + std::to_string(kRsMaxDepth) +
                                           " is not supported by the device splash builder");
+    (void)g_.balls(h);  // built here, never inside a graph capture
     if (rs_vres_.p) return;
     const size_t V = std::max<size_t>(g_.V, 1);
     for (DevBuf* b : {&rs_vres_, &rs_state_, &rs_claimed_, &rs_qnext_, &rs_spos_, &rs_depth_, &rs_clist_,
@@ -716,6 +737,11 @@ class EngineT final : public EngineBase {
   }
   void launch_rs(unsigned long long k, uint32_t h, int apply) {
     RsParams prm{k, h, apply};
+    RsBufs bufs = rs_bufs();
+    if (const BallLists* bl = g_.balls(h)) {
+      bufs.boff = bl->off.as<unsigned long long>();
+      bufs.bl = bl->list.as<uint32_t>();
+    }
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(rs_grid_);
     lc.blockDim = dim3(kRsBlock);
@@ -726,7 +752,7 @@ class EngineT final : public EngineBase {
     lc.attrs = at;
     lc.numAttrs = 1;
     cuda_check(cudaLaunchKernelEx(&lc, k_rs_iteration<QS>, dg_, live(), static_cast<const float*>(res_.as<float>()),
-                                  vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), rs_bufs(), prm),
+                                  vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), bufs, prm),
                "cooperative splash launch");
   }
 

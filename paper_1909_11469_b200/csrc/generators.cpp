@@ -69,7 +69,7 @@ BinaryStreams lattice_streams(uint32_t rows, uint32_t cols, double c, uint64_t s
   }
   s.unary_lo.resize(V);
   parallel_for(V, [&](size_t b, size_t e) {
-    for (size_t v = b; v < e; ++v) s.unary_lo[v] = static_cast<float>(std::log(u[2 * v + 1]) - std::log(u[2 * v]));
+    for (size_t v = b; v < e; ++v) s.unary_lo[v] = static_cast<float>(std::log2(u[2 * v + 1]) - std::log2(u[2 * v]));
   });
   return s;
 }
@@ -128,7 +128,7 @@ ErInstance er_instance(uint32_t n, uint32_t m, double c, uint64_t seed) {
   }
   inst.unary_lo.resize(n);
   for (uint32_t v = 0; v < n; ++v)
-    inst.unary_lo[v] = static_cast<float>(std::log(u[2 * v + 1]) - std::log(u[2 * v]));
+    inst.unary_lo[v] = static_cast<float>(std::log2(u[2 * v + 1]) - std::log2(u[2 * v]));
   return inst;
 }
 

@@ -53,14 +53,14 @@ DevGraph GraphImpl::dev() const {
   g.lat_cols = lat_cols;
   g.par_mode = par_mode;
   g.uniform_q = uniform_q;
-  g.jcoup = jcoup.as<float>();
+  g.ising_a = ising_a.as<float>();
   g.pw = pw.as<float>();
   return g;
 }
 
 uint64_t GraphImpl::device_bytes() const {
   return in_off.bytes + in_adj.bytes + ep.bytes + unary_lo.bytes + epar.bytes + card.bytes +
-         unary_log.bytes + table.bytes + bel_off.bytes + jcoup.bytes + pw.bytes;
+         unary_log.bytes + table.bytes + bel_off.bytes + ising_a.bytes + pw.bytes;
 }
 
 namespace {
@@ -170,6 +170,18 @@ uint32_t detect_lattice(uint32_t V, uint32_t E, const uint32_t* ep) {
   return C;
 }
 
+// a = e^J (a / d of the table), clamped so the device arithmetic stays finite
+float ising_weight(double J) {
+  const double j = std::min(69.0, std::max(-69.0, J));
+  return static_cast<float>(std::exp(j));
+}
+
+void upload_ising_weights(GraphImpl& g, const std::vector<float>& J) {
+  std::vector<float> a(J.size());
+  for (size_t e = 0; e < J.size(); ++e) a[e] = ising_weight(static_cast<double>(J[e]));
+  g.ising_a.upload(a.data(), a.size() * 4);
+}
+
 }  // namespace
 
 std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_device_opts* opts) {
@@ -242,11 +254,11 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     g->qs = 1;
     std::vector<float> ulo(V);
     for (uint32_t v = 0; v < V; ++v)
-      ulo[v] = static_cast<float>(std::log(d->unary_values[2 * v + 1]) - std::log(d->unary_values[2 * v]));
+      ulo[v] = static_cast<float>(std::log2(d->unary_values[2 * v + 1]) - std::log2(d->unary_values[2 * v]));
     std::vector<float4> par(E);
     for (uint32_t e = 0; e < E; ++e) {
       const double* t = d->pairwise_values + 4ull * e;
-      const double l00 = std::log(t[0]), l01 = std::log(t[1]), l10 = std::log(t[2]), l11 = std::log(t[3]);
+      const double l00 = std::log2(t[0]), l01 = std::log2(t[1]), l10 = std::log2(t[2]), l11 = std::log2(t[3]);
       const double alpha = l01 - l00, beta = l10 - l00, gg = l11 - l00;
       par[e] = make_float4(static_cast<float>(alpha), static_cast<float>(beta), static_cast<float>(gg - alpha),
                            static_cast<float>(gg - beta));
@@ -259,12 +271,12 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
       ising = t[0] == t[3] && t[1] == t[2];
     }
     if (ising) {
-      std::vector<float> J(E);
+      std::vector<float> a(E);
       for (uint32_t e = 0; e < E; ++e) {
         const double* t = d->pairwise_values + 4ull * e;
-        J[e] = static_cast<float>(std::log(t[0]) - std::log(t[1]));
+        a[e] = ising_weight(std::log(t[0]) - std::log(t[1]));
       }
-      g->jcoup.upload(J.data(), J.size() * 4);
+      g->ising_a.upload(a.data(), a.size() * 4);
       g->par_mode = 1;
     } else {
       g->epar.upload(par.data(), par.size() * 16);
@@ -350,7 +362,7 @@ std::unique_ptr<GraphImpl> build_lattice_binary(uint32_t rows, uint32_t cols, co
     cuda_check(cudaMemset(g->in_off.p, 0, 4), "memset");
   }
   g->unary_lo.upload(s.unary_lo.data(), V * 4);
-  g->jcoup.upload(s.coupling.data(), E * 4);  // J = 2 lambda c: par = (-J, -J, J, J)
+  upload_ising_weights(*g, s.coupling);  // J = 2 lambda c: table {e^lc, e^-lc, e^-lc, e^lc}
   g->par_mode = 1;
   if (V > 1) {
     g->lat_rows = rows;
@@ -422,10 +434,87 @@ std::unique_ptr<GraphImpl> build_er(uint32_t n, const ErInstance& inst, const bp
   g->in_adj.upload(adj.data(), adj.size() * 4);
   g->ep.upload(inst.endpoints.data(), static_cast<size_t>(E) * 8);
   g->unary_lo.upload(inst.unary_lo.data(), static_cast<size_t>(n) * 4);
-  g->jcoup.upload(inst.coupling.data(), static_cast<size_t>(E) * 4);
+  upload_ising_weights(*g, inst.coupling);
   g->par_mode = 1;
   cuda_check(cudaDeviceSynchronize(), "er build");
   return g;
+}
+
+// ---------------------------------------------------------------------------
+// ball lists (kernels_rs.cuh): distinct vertices within distance h, walk order
+
+constexpr int kBallCap = 256;
+
+template <class F>
+__device__ __forceinline__ int distinct_ball(const DevGraph& g, uint32_t v, uint32_t h, uint32_t* buf, bool& of,
+                                             F&& emit) {
+  int n = 0;
+  of = false;
+  ball_walk(g, v, h, [&](uint32_t w) {
+    for (int i = 0; i < n; ++i)
+      if (buf[i] == w) return true;
+    if (n == kBallCap) {
+      of = true;
+      return false;
+    }
+    buf[n++] = w;
+    emit(w);
+    return true;
+  });
+  return n;
+}
+
+__global__ void k_ball_count(DevGraph g, uint32_t h, unsigned* cnt, unsigned* overflow) {
+  uint32_t buf[kBallCap];
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.V; v += gridDim.x * blockDim.x) {
+    bool of;
+    cnt[v] = distinct_ball(g, v, h, buf, of, [](uint32_t) {});
+    if (of) *overflow = 1u;
+  }
+}
+
+__global__ void k_ball_fill(DevGraph g, uint32_t h, const unsigned long long* off, uint32_t* out) {
+  uint32_t buf[kBallCap];
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.V; v += gridDim.x * blockDim.x) {
+    bool of;
+    unsigned long long o = off[v];
+    distinct_ball(g, v, h, buf, of, [&](uint32_t w) { out[o++] = w; });
+  }
+}
+
+const BallLists* GraphImpl::balls(uint32_t h) const {
+  std::lock_guard<std::mutex> lk(host_mu);
+  auto it = balls_.find(h);
+  if (it != balls_.end()) return it->second.get();
+  if (balls_too_big_.count(h) || V == 0) return nullptr;
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  const DevGraph dg = dev();
+  DevBuf cnt, of;
+  cnt.alloc(static_cast<size_t>(V) * 4);
+  of.alloc(4);
+  cuda_check(cudaMemset(of.p, 0, 4), "memset");
+  const unsigned grid = static_cast<unsigned>(std::min<size_t>((V + 127) / 128, 148ull * 16));
+  k_ball_count<<<grid, 128>>>(dg, h, cnt.as<unsigned>(), of.as<unsigned>());
+  cuda_check(cudaGetLastError(), "ball count");
+  unsigned overflow = 0;
+  std::vector<unsigned> c(V);
+  cuda_check(cudaMemcpy(&overflow, of.p, 4, cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(c.data(), cnt.p, 4ull * V, cudaMemcpyDeviceToHost), "d2h");
+  std::vector<unsigned long long> off(static_cast<size_t>(V) + 1, 0);
+  for (uint32_t v = 0; v < V; ++v) off[v + 1] = off[v] + c[v];
+  // budget: 32 entries per vertex on average (grid h=2: 13, ER deg 4 h=2: ~21)
+  if (overflow || off[V] > 32ull * V + (1ull << 20)) {
+    balls_too_big_[h] = true;
+    return nullptr;
+  }
+  auto b = std::make_unique<BallLists>();
+  b->off.upload(off.data(), off.size() * 8);
+  b->list.alloc(std::max<size_t>(off[V] * 4, 16));
+  k_ball_fill<<<grid, 128>>>(dg, h, b->off.as<unsigned long long>(), b->list.as<uint32_t>());
+  cuda_check(cudaDeviceSynchronize(), "ball fill");
+  const BallLists* out = b.get();
+  balls_[h] = std::move(b);
+  return out;
 }
 
 // Host copies needed only by the lockstep API (message conversion).

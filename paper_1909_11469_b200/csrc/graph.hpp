@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -30,12 +31,19 @@ struct DevBuf {
   }
 };
 
+// Vertices within distance h of every vertex (the balls the splash builder
+// reserves), CSR layout; built on the device on first use per h.
+struct BallLists {
+  DevBuf off;   // u64[V+1]
+  DevBuf list;  // u32[off[V]]
+};
+
 struct GraphImpl {
   int device = 0;
   uint32_t V = 0, E = 0, D = 0, maxq = 0, qs = 1;
   uint32_t uniform_q = 0;  // all cardinalities equal to this (0 = mixed)
   bool binary = true;
-  DevBuf in_off, in_adj, ep, unary_lo, epar, card, unary_log, table, bel_off, jcoup, pw;
+  DevBuf in_off, in_adj, ep, unary_lo, epar, card, unary_log, table, bel_off, ising_a, pw;
   uint32_t lat_rows = 0, lat_cols = 0;  // lattice topology detected / generated (0 = CSR only)
   uint32_t par_mode = 0;                // 1: Ising couplings (binary) / Potts weights (generic)
   std::vector<uint32_t> cards_host;  // mixed cardinalities only
@@ -53,7 +61,12 @@ struct GraphImpl {
   const std::vector<uint32_t>& host_in_off() const;
   const std::vector<uint32_t>& host_in_adj() const;
 
+  // nullptr when the lists would be too large (the kernels then walk the CSR)
+  const BallLists* balls(uint32_t h) const;
+
   mutable std::mutex host_mu;
+  mutable std::map<uint32_t, std::unique_ptr<BallLists>> balls_;
+  mutable std::map<uint32_t, bool> balls_too_big_;
   mutable std::vector<uint32_t> ep_host, in_off_host, in_adj_host;
 };
 

@@ -229,6 +229,7 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
     case kFinInit:
       c->unconverged = static_cast<unsigned>(count);
       c->iteration = 0;
+      if (c->use_clist && 16ull * c->unconverged < D) c->cl_state = 1u;
       fin_reset_scratch(c);
       fin_check_top(c);
       break;
@@ -241,8 +242,16 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
       c->has_prev = 1;
       c->iteration += 1;
       if (c->use_clist) {
-        c->cl_cur ^= 1u;
-        c->cl_n[c->cl_cur ^ 1u] = 0;
+        // RnBP candidate list: scan residuals while most edges are
+        // unconverged; once fewer than 1/16 are, the next select builds the
+        // list (state 1) and from then on iterations walk it (state 2)
+        if (c->cl_state >= 1u) {
+          c->cl_cur ^= 1u;
+          c->cl_n[c->cl_cur ^ 1u] = 0;
+          c->cl_state = 2u;
+        } else if (16ull * c->unconverged < D) {
+          c->cl_state = 1u;
+        }
       }
       fin_reset_scratch(c);
       fin_check_top(c);
@@ -276,7 +285,7 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
                                                     float* __restrict__ B, float* __restrict__ res,
                                                     float eps, unsigned* numeric_flag,
                                                     unsigned long long& evals, uint8_t* inlist,
-                                                    Stager* cl) {
+                                                    Stager* cl, bool cl_on) {
   float T = g.unary_lo[v];
   const float2* __restrict__ A2 = reinterpret_cast<const float2*>(A);
   // incoming messages and (same edge pair) the old outgoing ones, kept in
@@ -288,8 +297,13 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
     const float r_was = MODE == kModeDelta ? res[out] : 0.f;
     const float m_in = (in & 1u) ? pr.y : pr.x;
     const float m_old = (in & 1u) ? pr.x : pr.y;
-    const float lnew = binary_msg(g, T - m_in, out);
-    const float r = binary_residual(lnew, m_old);
+    float lnew, r;
+    if (g.par_mode) {
+      r = ising_update(T - m_in, __ldg(&g.ising_a[out >> 1]), m_old, lnew);
+    } else {
+      lnew = binary_msg(g, T - m_in, out);
+      r = binary_residual(lnew, m_old);
+    }
     if (!(fabsf(lnew) < INFINITY)) *numeric_flag = 1u;
     B[out] = lnew;
     const int now = r >= eps;
@@ -300,7 +314,7 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
       if (MODE == kModeInit) res[out] = r;
       cnt += now;
     }
-    if (CL && now && !inlist[out]) {
+    if (CL && cl_on && now && !inlist[out]) {
       inlist[out] = 1;
       cl->push(out);
     }
@@ -335,7 +349,7 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
                                                      float* __restrict__ B, float* __restrict__ res,
                                                      float eps, unsigned* numeric_flag,
                                                      unsigned long long& evals, uint8_t* inlist,
-                                                     Stager* cl) {
+                                                     Stager* cl, bool cl_on) {
   const uint32_t ci = g.card[v];
   float T[QS];
 #pragma unroll
@@ -389,7 +403,7 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
       if (MODE == kModeInit) res[out] = r;
       cnt += now;
     }
-    if (CL && now && !inlist[out]) {
+    if (CL && cl_on && now && !inlist[out]) {
       inlist[out] = 1;
       cl->push(out);
     }
@@ -398,15 +412,143 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
   return cnt;
 }
 
+// Dense sweep over a binary Ising lattice (par_mode 1, lat_cols > 0): the
+// HBM-bound LBP kernel.  A tile is kLatVPT * kBlock consecutive vertices of
+// one row; thread t owns columns t, t + kBlock, ... so every load instruction
+// of a warp touches one contiguous span.  Each vertex needs its own (right,
+// down) edge pairs, the left neighbour's right pair and the upper neighbour's
+// down pair (L1 / L2 hits), the four a = e^J and its unary: all kLatVPT x 9
+// loads are issued before any arithmetic.  check_flag: dense touched-set
+// refresh (only vertices with vflag == stamp).
+constexpr int kLatVPT = 4;
+constexpr uint32_t kLatTile = kBlock * kLatVPT;
+
+template <int MODE, bool CL>
+__device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const float* __restrict__ A,
+                                                     float* __restrict__ B, float* __restrict__ res,
+                                                     const uint32_t* __restrict__ vflag, uint32_t stamp,
+                                                     bool check_flag, float eps, unsigned* nf, int& cnt,
+                                                     unsigned long long& evals, unsigned long long& visits,
+                                                     uint8_t* inlist, Stager* cl, bool cl_on) {
+  const uint32_t C = g.lat_cols, R = g.lat_rows;
+  const uint32_t tpr = (C + kLatTile - 1) / kLatTile;
+  const uint64_t ntiles = static_cast<uint64_t>(R) * tpr;
+  const float2* __restrict__ A2 = reinterpret_cast<const float2*>(A);
+  const float* __restrict__ ea = g.ising_a;
+  bool bad = false;
+  // Each block walks a contiguous run of tiles in (column strip, row) order:
+  // down the rows of one kLatTile-wide strip, so the upper neighbour's edge
+  // pairs were read by this block one tile ago and the message sectors it
+  // half-writes are completed by its next tile -- the live working set is
+  // ~2 rows x strip x blocks (L2-resident even at 16384^2).
+  const uint64_t t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  for (uint64_t t = t_begin; t < t_end; ++t) {
+    const uint32_t strip = static_cast<uint32_t>(t / R);
+    const uint32_t r = static_cast<uint32_t>(t - static_cast<uint64_t>(strip) * R);
+    const uint32_t c0 = strip * kLatTile + threadIdx.x;
+    const bool last = r + 1u == R, first = r == 0u;
+    const uint32_t row = r * (2u * C - 1u), prow = first ? 0u : (r - 1u) * (2u * C - 1u);
+    bool act[kLatVPT];
+    float2 pU[kLatVPT], pL[kLatVPT], pR[kLatVPT], pD[kLatVPT];
+    float aU[kLatVPT], aL[kLatVPT], aR[kLatVPT], aD[kLatVPT], un[kLatVPT];
+#pragma unroll
+    for (int k = 0; k < kLatVPT; ++k) {
+      const uint32_t c = c0 + k * kBlock;
+      act[k] = c < C;
+      if (check_flag && act[k]) act[k] = vflag[r * C + c] == stamp;
+    }
+#pragma unroll
+    for (int k = 0; k < kLatVPT; ++k) {
+      const uint32_t c = c0 + k * kBlock;
+      pU[k] = pL[k] = pR[k] = pD[k] = make_float2(0.f, 0.f);
+      aU[k] = aL[k] = aR[k] = aD[k] = 1.f;
+      un[k] = 0.f;
+      if (!act[k]) continue;
+      const uint32_t dn = c + 1u < C ? 1u : 0u;
+      if (!first) {
+        const uint32_t e = prow + 2u * c + dn;
+        pU[k] = __ldg(&A2[e]);
+        aU[k] = __ldg(&ea[e]);
+      }
+      if (c > 0u) {
+        const uint32_t e = last ? row + c - 1u : row + 2u * c - 2u;
+        pL[k] = __ldg(&A2[e]);
+        aL[k] = __ldg(&ea[e]);
+      }
+      if (dn) {
+        const uint32_t e = last ? row + c : row + 2u * c;
+        pR[k] = __ldg(&A2[e]);
+        aR[k] = __ldg(&ea[e]);
+      }
+      if (!last) {
+        const uint32_t e = row + 2u * c + dn;
+        pD[k] = __ldg(&A2[e]);
+        aD[k] = __ldg(&ea[e]);
+      }
+      un[k] = __ldg(&g.unary_lo[r * C + c]);
+    }
+#pragma unroll
+    for (int k = 0; k < kLatVPT; ++k) {
+      if (CL) cl->flush(1024);  // <= 4 kBlock pushes per k
+      const uint32_t c = c0 + k * kBlock;
+      const uint32_t dn = c + 1u < C ? 1u : 0u;
+      const bool hu = act[k] && !first, hl = act[k] && c > 0u, hr = act[k] && dn, hd = act[k] && !last;
+      // incoming: up (2eU, .x), left (2eL, .x), right (2eR+1, .y), down (2eD+1, .y); absent ones hold 0
+      const float T = un[k] + pU[k].x + pL[k].x + pR[k].y + pD[k].y;
+      // all four messages are computed (predicated stores, no divergence at the borders)
+      float lu, ll, lr, ld;
+      const float ru = ising_update(T - pU[k].x, aU[k], pU[k].y, lu);
+      const float rl = ising_update(T - pL[k].x, aL[k], pL[k].y, ll);
+      const float rr = ising_update(T - pR[k].y, aR[k], pR[k].x, lr);
+      const float rd = ising_update(T - pD[k].y, aD[k], pD[k].x, ld);
+      const uint32_t ou = 2u * (prow + 2u * c + dn) + 1u;
+      const uint32_t ol = 2u * (last ? row + c - 1u : row + 2u * c - 2u) + 1u;
+      const uint32_t orr = 2u * (last ? row + c : row + 2u * c);
+      const uint32_t od = 2u * (row + 2u * c + dn);
+      bad |= (hu && !(fabsf(lu) < INFINITY)) || (hl && !(fabsf(ll) < INFINITY)) ||
+             (hr && !(fabsf(lr) < INFINITY)) || (hd && !(fabsf(ld) < INFINITY));
+      if (hu) B[ou] = lu;
+      if (hl) B[ol] = ll;
+      if (hr) B[orr] = lr;
+      if (hd) B[od] = ld;
+      auto track = [&](bool has, uint32_t out, float r_msg) {
+        const int now = has && r_msg >= eps;
+        if (MODE == kModeDelta) {
+          if (has) {
+            cnt += now - (res[out] >= eps);
+            res[out] = r_msg;
+          }
+        } else {
+          if (MODE == kModeInit && has) res[out] = r_msg;
+          cnt += now;
+        }
+        if (CL && cl_on && now && !inlist[out]) {
+          inlist[out] = 1;
+          cl->push(out);
+        }
+      };
+      track(hu, ou, ru);
+      track(hl, ol, rl);
+      track(hr, orr, rr);
+      track(hd, od, rd);
+      const uint32_t deg = (hu ? 1u : 0u) + (hl ? 1u : 0u) + (hr ? 1u : 0u) + (hd ? 1u : 0u);
+      evals += deg;
+      visits += act[k] ? 1u : 0u;
+    }
+  }
+  if (bad) *nf = 1u;
+}
+
 // QS == 1 selects the binary layout.
 template <int QS, int MODE, bool CL>
 __device__ __forceinline__ int vertex_update(const DevGraph& g, uint32_t v, const float* A, float* B,
                                              float* res, float eps, unsigned* nf,
-                                             unsigned long long& evals, uint8_t* inlist, Stager* cl) {
+                                             unsigned long long& evals, uint8_t* inlist, Stager* cl,
+                                             bool cl_on) {
   if constexpr (QS == 1)
-    return vertex_update_binary<MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl);
+    return vertex_update_binary<MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
   else
-    return vertex_update_generic<QS, MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl);
+    return vertex_update_generic<QS, MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
 }
 
 // Sweep over all vertices (LIST = false) or over the vertices flagged this
@@ -444,7 +586,13 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
   int cnt = 0;
   unsigned long long evals = 0, visits = 0;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+  // candidate list maintained once the RnBP run is in list mode (cl_state >= 1)
+  const bool cl_on = CL && ctl->cl_state >= 1u;
+  const bool lattice = QS == 1 && g.lat_cols != 0u && g.par_mode != 0u && dense;
+  if (lattice)
+    lattice_binary_tiles<MODE, CL>(g, A, B, res, vflag, stamp, LIST, eps, &ctl->numeric_error, cnt, evals, visits,
+                                   cand_list.inlist, &cl, cl_on);
+  for (uint32_t base = lattice ? n : blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint32_t i = base + threadIdx.x;
     if (i < n) {
       uint32_t v = i;
@@ -456,7 +604,8 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
           v = vlist[i];
       }
       if (go) {
-        cnt += vertex_update<QS, MODE, CL>(g, v, A, B, res, eps, &ctl->numeric_error, evals, cand_list.inlist, &cl);
+        cnt += vertex_update<QS, MODE, CL>(g, v, A, B, res, eps, &ctl->numeric_error, evals, cand_list.inlist, &cl,
+                                           cl_on);
         ++visits;
       }
     }
@@ -564,17 +713,18 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dense = dense ? 1u : 0u;
   BPB_STAGER(fl, 2048, vlist, &ctl->nflag);
   const unsigned cur = CL ? ctl->cl_cur : 0u;
+  const unsigned st = CL && prm.commit ? ctl->cl_state : 0u;  // 1: build the list, 2: walk it
   BPB_STAGER(keep, CL ? 2048 : 1, CL ? (cur ? cl.list[0] : cl.list[1]) : nullptr, &ctl->cl_n[cur ^ 1u]);
   fl.init();
   if (CL) keep.init();
   Contrib c;
   const uint32_t stride = gridDim.x * blockDim.x;
-  if (!CL) {
+  if (st != 2u) {
     const uint32_t D4 = (g.D + 3) / 4;
     const float4* res4 = reinterpret_cast<const float4*>(res);
     for (uint32_t base = blockIdx.x * blockDim.x; base < D4; base += stride) {
       const uint32_t q = base + threadIdx.x;
-      bool nf[4] = {false, false, false, false};
+      bool nf[4] = {false, false, false, false}, kp[4] = {false, false, false, false};
       uint32_t tg[4] = {0, 0, 0, 0};
       if (q < D4) {
         const float4 r4 = res4[q];
@@ -591,6 +741,9 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
                 sel[d] = 1;
                 c.frontier += 1;
               }
+            } else if (CL && st == 1u) {
+              cl.inlist[d] = 1;
+              kp[k] = true;
             }
           }
         }
@@ -600,7 +753,13 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
         for (int k = 0; k < 4; ++k) fl.push_warp(nf[k], tg[k]);
         fl.flush(4 * kBlock);
       }
+      if (CL && st == 1u) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) keep.push_warp(kp[k], 4 * q + k);
+        keep.flush(4 * kBlock);
+      }
     }
+    if (CL && st == 1u) keep.flush(0);
   } else {
     const uint32_t n = ctl->cl_n[cur];
     const uint32_t* list = cur ? cl.list[1] : cl.list[0];
@@ -681,10 +840,11 @@ __global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, co
   // attempt 1: every survivor redrawn
   unsigned long long fr = 0;
   long long delta = 0;
-  const uint32_t n = CL ? ctl->cl_n[ctl->cl_cur ^ 1u] : g.D;
-  const uint32_t* list = CL ? (ctl->cl_cur ? cl.list[0] : cl.list[1]) : nullptr;
+  const bool use_list = CL && ctl->cl_state == 2u;  // survivors = the kept list
+  const uint32_t n = use_list ? ctl->cl_n[ctl->cl_cur ^ 1u] : g.D;
+  const uint32_t* list = use_list ? (ctl->cl_cur ? cl.list[0] : cl.list[1]) : nullptr;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t d = CL ? list[i] : i;
+    const uint32_t d = use_list ? list[i] : i;
     const float r = res[d];
     if (r >= eps && philox_u53(prm.seed, it, 1u, d) < thresh) {
       ++fr;
@@ -1013,8 +1173,8 @@ __global__ void k_beliefs(DevGraph g, const float* A0, const float* A1, int ping
       float T = g.unary_lo[v];
       for_each_in(g, v, [&](uint32_t in) { T += A[in]; });
       const double t = static_cast<double>(T);
-      out[2 * static_cast<size_t>(v)] = 1.0 / (1.0 + exp(t));
-      out[2 * static_cast<size_t>(v) + 1] = 1.0 / (1.0 + exp(-t));
+      out[2 * static_cast<size_t>(v)] = 1.0 / (1.0 + exp2(t));  // base-2 log-odds
+      out[2 * static_cast<size_t>(v) + 1] = 1.0 / (1.0 + exp2(-t));
     } else {
       const uint32_t q = g.card[v];
       float T[QS];

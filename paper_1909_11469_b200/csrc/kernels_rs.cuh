@@ -43,8 +43,6 @@ namespace bpb {
 
 namespace cg = cooperative_groups;
 
-constexpr uint32_t kUncl = 0xFFFFFFFFu;
-constexpr uint32_t kRsMaxDepth = 8;
 constexpr int kRsBlock = 512;
 
 enum RsState : uint32_t { kRsNone = 0, kRsCand = 1, kRsBuilt = 2, kRsSkip = 3, kRsKept = 4 };
@@ -76,41 +74,24 @@ struct RsBufs {
   unsigned* blk;    // gridDim
   RsCtl* rc;
   float* shadow;    // D * QS
+  const unsigned long long* boff;  // ball lists (GraphImpl::balls): V+1 offsets, or null
+  const uint32_t* bl;
 };
+
+// every vertex within distance h of r (precomputed list, else a walk)
+template <class F>
+__device__ __forceinline__ bool ball_each(const DevGraph& g, const RsBufs& b, uint32_t r, uint32_t h, F&& f) {
+  if (b.boff) {
+    const unsigned long long e = b.boff[r + 1];
+    for (unsigned long long i = b.boff[r]; i < e; ++i)
+      if (!f(__ldg(&b.bl[i]))) return false;
+    return true;
+  }
+  return ball_walk(g, r, h, f);
+}
 
 __device__ __forceinline__ unsigned long long rs_key64(float vres, uint32_t v) {
   return (static_cast<unsigned long long>(__float_as_uint(vres)) << 32) | static_cast<unsigned long long>(~v);
-}
-
-// Non-backtracking walks of length <= h from r (covers every vertex within
-// distance h, some more than once).  f(w) returning false stops the walk.
-template <class F>
-__device__ __forceinline__ bool ball_walk(const DevGraph& g, uint32_t r, uint32_t h, F&& f) {
-  if (!f(r)) return false;
-  if (h == 0) return true;
-  uint32_t vs[kRsMaxDepth], par[kRsMaxDepth], pos[kRsMaxDepth], end[kRsMaxDepth];
-  int d = 0;
-  vs[0] = r;
-  par[0] = kUncl;
-  pos[0] = g.in_off[r];
-  end[0] = g.in_off[r + 1];
-  while (d >= 0) {
-    if (pos[d] < end[d]) {
-      const uint32_t w = g.ep[g.in_adj[pos[d]++]];  // source of an incoming edge = neighbour
-      if (w == par[d]) continue;
-      if (!f(w)) return false;
-      if (d + 1 < static_cast<int>(h)) {
-        ++d;
-        vs[d] = w;
-        par[d] = vs[d - 1];
-        pos[d] = g.in_off[w];
-        end[d] = g.in_off[w + 1];
-      }
-    } else {
-      --d;
-    }
-  }
-  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -432,7 +413,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
         }
         ++unres;
         const unsigned long long key = rs_key64(__ldcg(&b.vres[r]), r);
-        ball_walk(g, r, h, [&](uint32_t w) {
+        ball_each(g, b, r, h, [&](uint32_t w) {
           atomicMax(&b.ballmax[w], key);
           return true;
         });
@@ -447,7 +428,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
         const uint32_t r = __ldcg(&b.clist[i]);
         if (__ldcg(&b.state[r]) != kRsCand) continue;
         const unsigned long long key = rs_key64(__ldcg(&b.vres[r]), r);
-        const bool ready = ball_walk(g, r, h, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; });
+        const bool ready = ball_each(g, b, r, h, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; });
         if (ready) b.rlist[atomicAdd(&rc->nready, 1u)] = r;
       }
       grid.sync();
@@ -478,7 +459,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
         }
         b.state[r] = kRsBuilt;
         b.blist[atomicAdd(&rc->nbuilt, 1u)] = r;
-        ball_walk(g, r, h, [&](uint32_t w) {
+        ball_each(g, b, r, h, [&](uint32_t w) {
           b.ballmax[w] = 0ull;
           return true;
         });
@@ -488,7 +469,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       for (uint32_t i = tid; i < nc; i += stride) {
         const uint32_t r = __ldcg(&b.clist[i]);
         if (__ldcg(&b.state[r]) == kRsCand)
-          ball_walk(g, r, h, [&](uint32_t w) {
+          ball_each(g, b, r, h, [&](uint32_t w) {
             b.ballmax[w] = 0ull;
             return true;
           });
@@ -559,7 +540,11 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       }
     }
   }
-  if (tid == 0) ctl->splashes += nk;
+  if (tid == 0) {
+    ctl->splashes += nk;
+    ctl->rs_rounds += rc->rounds;
+    ctl->rs_passes += rc->passes;
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -27,7 +27,7 @@ def emit(name, g, cfg, **extra):
            "device_ms": round(r.device_ms, 3), "wall_s": round(r.wall_time, 4),
            "updates": r.messages_updated_total, "updates_per_s": r.messages_updated_total / (r.device_ms / 1e3),
            "evals": r.message_evaluations, "ms_per_iter": round(r.device_ms / max(r.iterations, 1), 4),
-           "launches": r.gpu_launches}
+           "launches": r.gpu_launches, "splashes": r.splashes, "splash_rounds": r.splash_rounds}
     out.update(extra)
     if a.timing:
         rk = bp.run_ex(g, cfg, beliefs=False, kernel_timing=True)
