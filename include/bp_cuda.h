@@ -138,6 +138,7 @@ typedef struct {
 #define BP_RUN_KERNEL_TIMING 1u /* CUDA events around every kernel (adds overhead) */
 #define BP_RUN_NO_GRAPHS 2u     /* launch kernels directly instead of CUDA-graph batches */
 #define BP_RUN_NO_BELIEFS 4u    /* skip beliefs */
+#define BP_RUN_NO_PERSIST 8u    /* RnBP: keep the per-kernel graph loop in candidate-list mode */
 
 BP_API const char* bp_last_error(void);
 BP_API int bp_abi_version(void);

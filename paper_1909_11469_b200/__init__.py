@@ -107,10 +107,11 @@ class _Info(C.Structure):
 class KernelStats(C.Structure):
     _fields_ = [("ms", C.c_double * 8), ("launches", C.c_uint64 * 8), ("bytes", C.c_uint64 * 8)]
 
-    CLASSES = ("update", "select", "topk", "splash", "init", "beliefs", "other")
+    CLASSES = ("update", "select", "topk", "splash", "init", "beliefs", "other", "persist")
 
     def as_dict(self):
-        return {n: {"ms": self.ms[i], "launches": int(self.launches[i])} for i, n in enumerate(self.CLASSES)}
+        return {n: {"ms": self.ms[i], "launches": int(self.launches[i]), "bytes": int(self.bytes[i])}
+                for i, n in enumerate(self.CLASSES)}
 
 
 class _RunOpts(C.Structure):
@@ -121,6 +122,7 @@ class _RunOpts(C.Structure):
 RUN_KERNEL_TIMING = 1
 RUN_NO_GRAPHS = 2
 RUN_NO_BELIEFS = 4
+RUN_NO_PERSIST = 8
 GRAPH_TRUSTED = 1
 
 

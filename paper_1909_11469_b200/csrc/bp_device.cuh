@@ -169,6 +169,16 @@ struct Ctl {
   unsigned int cl_n[2];       // candidate list sizes
   unsigned int use_clist;
   unsigned int cl_state;      // 0 scan residuals, 1 build the list this iteration, 2 walk the list
+  unsigned int persist_ok;    // RnBP: hand list mode over to the persistent kernel (graph loop exits)
+  unsigned int pad3_;
+  // persistent kernel: per-iteration sums (delta, count, frontier, survivors,
+  // evals, visits), triple-buffered by iteration; touched-list counters,
+  // double-buffered; the time-limit verdict of CTA 0
+  unsigned long long pacc3[3][6];
+  unsigned int nfl2[2];
+  unsigned int time_stop;
+  unsigned int pad4_;
+  unsigned long long persist_bytes;  // algorithmic bytes moved by the persistent kernel
   Accum acc[kSlots];
   TraceRec trace[kTraceRing];
 };
@@ -276,26 +286,26 @@ __device__ __forceinline__ void generic_matvec(const DevGraph& g, uint32_t out, 
   if (g.par_mode) {
     const float w1 = __ldg(&g.pw[out >> 1]);
     float S = 0.f;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int x = 0; x < QS; ++x) S += p[x];
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int x = 0; x < QS; ++x) o[x] = fmaf(w1, p[x], S);
     return;
   }
   const float* tab = g.table + static_cast<size_t>(out >> 1) * QS * QS;
   if ((out & 1u) == 0u) {  // source is lo: A(xs, xt) = T[xs][xt]
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) o[xt] = 0.f;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int xs = 0; xs < QS; ++xs) {
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt) o[xt] = fmaf(__ldg(&tab[xs * QS + xt]), p[xs], o[xt]);
     }
   } else {  // source is hi: A(xs, xt) = T[xt][xs]
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) {
       float acc = 0.f;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int xs = 0; xs < QS; ++xs) acc = fmaf(__ldg(&tab[xt * QS + xs]), p[xs], acc);
       o[xt] = acc;
     }
@@ -338,6 +348,18 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// warp-aggregated append of x (pred) to list[*counter]
+__device__ __forceinline__ void warp_append(bool pred, uint32_t x, uint32_t* list, unsigned* counter) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned mask = __ballot_sync(0xffffffffu, pred);
+  if (!mask) return;
+  const unsigned leader = __ffs(mask) - 1;
+  unsigned base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = x;
 }
 
 // ---------------------------------------------------------------------------

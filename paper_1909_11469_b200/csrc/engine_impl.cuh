@@ -8,11 +8,14 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 
 #include "engine.hpp"
 #include "kernels.cuh"
 #include "kernels_rs.cuh"
+#include "kernels_persist.cuh"
 
 namespace bpb {
 namespace {
@@ -42,7 +45,8 @@ unsigned grid_cap(size_t n, int per_sm = 8) {
   return static_cast<unsigned>(std::max<size_t>(1, std::min(want, cap)));
 }
 
-enum KClass { kKUpdate = 0, kKSelect = 1, kKTopk = 2, kKSplash = 3, kKInit = 4, kKBeliefs = 5, kKOther = 6 };
+enum KClass { kKUpdate = 0, kKSelect = 1, kKTopk = 2, kKSplash = 3, kKInit = 4, kKBeliefs = 5, kKOther = 6,
+              kKPersist = 7 };
 
 template <int QS>
 class EngineT final : public EngineBase {
@@ -101,13 +105,14 @@ class EngineT final : public EngineBase {
     if (stats_) std::memset(stats_, 0, sizeof(*stats_));
     launches_ = 0;
     const bool use_graph = !(flags & BP_RUN_NO_GRAPHS) && !timing_;
+    persist_ = cfg_.kind == BP_RNBP && !(flags & BP_RUN_NO_PERSIST);
     const Clock::time_point t0 = Clock::now();  // schedulers.cpp:297
 
     cudaEvent_t e0, e1;
     cuda_check(cudaEventCreate(&e0), "event");
     cuda_check(cudaEventCreate(&e1), "event");
     cuda_check(cudaEventRecord(e0, s_), "event record");
-    reset_ctl(cfg_.max_iterations, cfg_.time_limit, cfg_.kind == BP_RNBP);
+    reset_ctl(cfg_.max_iterations, cfg_.time_limit, cfg_.kind == BP_RNBP, persist_);
     enqueue_init(cfg_.kind == BP_LBP);
 
     uint64_t copied = 0;
@@ -119,13 +124,14 @@ class EngineT final : public EngineBase {
         run_graph_loop(trace, trace_cap, copied);
       } else {
         uint32_t batch = opts && opts->batch ? opts->batch : 16;
-        while (!hctl_->done) {
+        while (!hctl_->done && !handover()) {
           for (uint32_t b = 0; b < batch; ++b) enqueue_iteration();
           fetch_ctl_header();
           drain_trace(trace, trace_cap, copied);
           if (!(opts && opts->batch)) batch = std::min<uint32_t>(batch * 2, 256);
         }
       }
+      if (!hctl_->done && handover()) run_persist_loop(trace, trace_cap, copied);
     }
     fetch_ctl_header();
     drain_trace(trace, trace_cap, copied);
@@ -148,6 +154,7 @@ class EngineT final : public EngineBase {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     collect_timing();
+    if (stats_) stats_->bytes[kKPersist] = hctl_->persist_bytes;
 
     std::memset(res, 0, sizeof(*res));
     res->converged = hctl_->converged ? 1 : 0;
@@ -353,10 +360,11 @@ class EngineT final : public EngineBase {
     return c;
   }
 
-  void reset_ctl(uint64_t max_iter, double time_limit, bool use_clist = false) {
+  void reset_ctl(uint64_t max_iter, double time_limit, bool use_clist = false, bool persist = false) {
     use_clist_ = use_clist && clist_[0].p != nullptr;
     std::memset(hctl_, 0, offsetof(Ctl, trace));
     hctl_->use_clist = use_clist_ ? 1u : 0u;
+    hctl_->persist_ok = use_clist_ && persist ? 1u : 0u;
     if (use_clist_) cuda_check(cudaMemsetAsync(inlist_.p, 0, inlist_.bytes, s_), "memset inlist");
     hctl_->max_iterations = max_iter;
     const double ns = time_limit * 1e9;
@@ -650,6 +658,7 @@ class EngineT final : public EngineBase {
       cuda_check(cudaGraphLaunch(gexec_, s_), "graph launch");
       fetch_ctl_header();
       drain_trace(trace, cap, copied);
+      if (!hctl_->done && handover()) break;  // RnBP list mode -> persistent kernel
       if (hctl_->done) {
         if (hctl_->stop_reason == kStopMaxIter && hctl_->iteration < cfg_.max_iterations && budget_stop_) {
           // stopped by the chunk budget, not by the run: continue
@@ -686,6 +695,70 @@ class EngineT final : public EngineBase {
                                cudaMemcpyHostToDevice, s_),
                "ctl h2d");
     sync();
+  }
+
+  // ---- persistent RnBP tail (kernels_persist.cuh)
+  bool persist_ = false;
+  unsigned persist_grid_ = 0;
+  bool handover() const { return hctl_->persist_ok && hctl_->cl_state == 2u; }
+  // The tail runs on one 16-CTA cluster (hardware cluster barrier, ~sub-us)
+  // while the candidate list is small, else on a cooperative grid of all SMs.
+  // BPB_PERSIST_GRID / BPB_PERSIST_CLUSTER override the choice (tuning).
+  void run_persist_loop(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
+    if (!persist_grid_) {
+      int per_sm = 0;
+      cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rnbp_persist<QS, false>, kPersistBlock, 0),
+                 "occupancy");
+      persist_grid_ = static_cast<unsigned>(std::max(1, per_sm) * sm_count());
+      cuda_check(cudaFuncSetAttribute(k_rnbp_persist<QS, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                 "cluster attribute");
+    }
+    const char* eg = std::getenv("BPB_PERSIST_GRID");
+    const char* ec = std::getenv("BPB_PERSIST_CLUSTER");
+    for (;;) {
+      set_iteration_budget(hctl_->iteration + kTraceRing / 2);
+      const uint32_t list_n = hctl_->cl_n[hctl_->cl_cur];
+      bool cluster = list_n < (1u << 16);
+      if (ec) cluster = std::atoi(ec) != 0;
+      unsigned grid = cluster ? 16u : persist_grid_;
+      if (eg && !cluster) grid = std::min<unsigned>(persist_grid_, std::max(1, std::atoi(eg)));
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(kPersistBlock);
+      lc.stream = s_;
+      cudaLaunchAttribute at[1];
+      if (cluster) {
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = grid;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+      } else {
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+      }
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      timed(kKPersist, [&] {
+        if (cluster)
+          cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, true>, dg_, live(), cand(), res_.as<float>(),
+                                        vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
+                     "persistent cluster launch");
+        else
+          cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, false>, dg_, live(), cand(), res_.as<float>(),
+                                        vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
+                     "persistent launch");
+      });
+      fetch_ctl_header();
+      drain_trace(trace, cap, copied);
+      if (hctl_->done) {
+        if (hctl_->stop_reason == kStopMaxIter && hctl_->iteration < cfg_.max_iterations && budget_stop_) {
+          clear_budget_stop();
+          continue;
+        }
+        break;
+      }
+      if (!handover()) break;  // not reached: list mode is final
+    }
   }
 
   // ---- Residual Splash state (kernels_rs.cuh)

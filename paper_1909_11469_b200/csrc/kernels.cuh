@@ -43,9 +43,15 @@ struct Stager {
     if (threadIdx.x == 0) *scount = 0;
     __syncthreads();
   }
-  // any thread, any time (shared atomic per push)
+  // any thread, any time: one shared atomic per group of converged lanes
   __device__ __forceinline__ void push(uint32_t x) {
-    const unsigned i = atomicAdd(scount, 1u);
+    const unsigned m = __activemask();
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(scount, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    const unsigned i = base + __popc(m & ((1u << lane) - 1u));
     if (i < cap)
       sbuf[i] = x;
     else
@@ -188,6 +194,31 @@ __device__ __forceinline__ void fin_reset_scratch(Ctl* c) {
   c->rx_above = 0;
 }
 
+// end of one iteration of the run loop (schedulers.cpp:326-346)
+__device__ __forceinline__ void fin_iter(Ctl* c, long long delta, unsigned long long frontier, uint32_t D) {
+  const unsigned start = c->unconverged;
+  c->unconverged = static_cast<unsigned>(static_cast<long long>(start) + delta);
+  fin_record(c, c->iteration, frontier, c->unconverged);
+  c->msgs_total += frontier;
+  c->prev_unconverged = start;  // set_prev_unconverged (schedulers.cpp:327)
+  c->has_prev = 1;
+  c->iteration += 1;
+  if (c->use_clist) {
+    // RnBP candidate list: scan residuals while most edges are unconverged;
+    // once fewer than 1/16 are, the next select builds the list (state 1) and
+    // from then on iterations walk it (state 2)
+    if (c->cl_state >= 1u) {
+      c->cl_cur ^= 1u;
+      c->cl_n[c->cl_cur ^ 1u] = 0;
+      c->cl_state = 2u;
+    } else if (16ull * c->unconverged < D) {
+      c->cl_state = 1u;
+    }
+  }
+  fin_reset_scratch(c);
+  fin_check_top(c);
+}
+
 // <<<1, kSlots>>>
 static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D) {
   if (run_done(c)) return;
@@ -233,30 +264,9 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
       fin_reset_scratch(c);
       fin_check_top(c);
       break;
-    case kFinIter: {
-      const unsigned start = c->unconverged;
-      c->unconverged = static_cast<unsigned>(static_cast<long long>(start) + delta);
-      fin_record(c, c->iteration, frontier, c->unconverged);
-      c->msgs_total += frontier;
-      c->prev_unconverged = start;  // set_prev_unconverged (schedulers.cpp:327)
-      c->has_prev = 1;
-      c->iteration += 1;
-      if (c->use_clist) {
-        // RnBP candidate list: scan residuals while most edges are
-        // unconverged; once fewer than 1/16 are, the next select builds the
-        // list (state 1) and from then on iterations walk it (state 2)
-        if (c->cl_state >= 1u) {
-          c->cl_cur ^= 1u;
-          c->cl_n[c->cl_cur ^ 1u] = 0;
-          c->cl_state = 2u;
-        } else if (16ull * c->unconverged < D) {
-          c->cl_state = 1u;
-        }
-      }
-      fin_reset_scratch(c);
-      fin_check_top(c);
+    case kFinIter:
+      fin_iter(c, delta, frontier, D);
       break;
-    }
     case kFinApply:
       c->unconverged = static_cast<unsigned>(static_cast<long long>(c->unconverged) + delta);
       fin_reset_scratch(c);
@@ -264,8 +274,10 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
     default:
       break;
   }
+  // the graph loop also hands RnBP list mode over to the persistent kernel
+  const bool handover = c->persist_ok && c->cl_state == 2u;
   if (c->cond_handle && mode != kFinApply)
-    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(c->cond_handle), c->done ? 0u : 1u);
+    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(c->cond_handle), c->done || handover ? 0u : 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -279,7 +291,16 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
 
 // CL: candidate-list maintenance (RnBP): an outgoing edge whose residual is
 // >= eps and that is not in the list yet is pushed to `cl`.
-template <int MODE, bool CL>
+// ldm<NC>: read-only-path load (__ldg) inside normal kernels; a plain
+// coherent load inside persistent kernels, where the data changes between
+// grid barriers of the same launch.
+template <bool NC, class T>
+__device__ __forceinline__ T ldm(const T* p) {
+  if constexpr (NC) return __ldg(p);
+  else return *p;
+}
+
+template <int MODE, bool CL, bool NC = true>
 __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t v,
                                                     const float* __restrict__ A,
                                                     float* __restrict__ B, float* __restrict__ res,
@@ -319,31 +340,71 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
       cl->push(out);
     }
   };
+  // emit with prefetched residual / in-list flag
+  auto emit_pre = [&](uint32_t in, float2 pr, float r_was, bool in_list) {
+    const uint32_t out = in ^ 1u;
+    const float m_in = (in & 1u) ? pr.y : pr.x;
+    const float m_old = (in & 1u) ? pr.x : pr.y;
+    float lnew, r;
+    if (g.par_mode) {
+      r = ising_update(T - m_in, __ldg(&g.ising_a[out >> 1]), m_old, lnew);
+    } else {
+      lnew = binary_msg(g, T - m_in, out);
+      r = binary_residual(lnew, m_old);
+    }
+    if (!(fabsf(lnew) < INFINITY)) *numeric_flag = 1u;
+    B[out] = lnew;
+    const int now = r >= eps;
+    if (MODE == kModeDelta) {
+      cnt += now - (r_was >= eps);
+      res[out] = r;
+    } else {
+      if (MODE == kModeInit) res[out] = r;
+      cnt += now;
+    }
+    if (CL && cl_on && now && !in_list) {
+      inlist[out] = 1;
+      cl->push(out);
+    }
+  };
   if (g.lat_cols) {
     uint32_t ins[4];
     float2 prs[4];
+    float rw[4];
+    uint8_t il[4];
     for_each_in(g, v, [&](uint32_t in) {
       ins[deg] = in;
-      prs[deg] = __ldg(&A2[in >> 1]);
+      prs[deg] = ldm<NC>(&A2[in >> 1]);
       T += (in & 1u) ? prs[deg].y : prs[deg].x;
       ++deg;
     });
+    // prefetch the per-message state so the four updates do not serialise
+    // on (possibly aliasing) loads between their stores
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      rw[k] = 0.f;
+      il[k] = 1;
+      if (k < static_cast<int>(deg)) {
+        if (MODE == kModeDelta) rw[k] = res[ins[k] ^ 1u];
+        if (CL && cl_on) il[k] = inlist[ins[k] ^ 1u];
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (k < static_cast<int>(deg)) emit(ins[k], prs[k]);
+      if (k < static_cast<int>(deg)) emit_pre(ins[k], prs[k], rw[k], il[k] != 0);
   } else {
     for_each_in(g, v, [&](uint32_t in) {
-      const float2 pr = __ldg(&A2[in >> 1]);
+      const float2 pr = ldm<NC>(&A2[in >> 1]);
       T += (in & 1u) ? pr.y : pr.x;
       ++deg;
     });
-    for_each_in(g, v, [&](uint32_t in) { emit(in, __ldg(&A2[in >> 1])); });
+    for_each_in(g, v, [&](uint32_t in) { emit(in, ldm<NC>(&A2[in >> 1])); });
   }
   evals += deg;
   return cnt;
 }
 
-template <int QS, int MODE, bool CL>
+template <int QS, int MODE, bool CL, bool NC = true>
 __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t v,
                                                      const float* __restrict__ A,
                                                      float* __restrict__ B, float* __restrict__ res,
@@ -352,13 +413,13 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
                                                      Stager* cl, bool cl_on) {
   const uint32_t ci = g.card[v];
   float T[QS];
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
   for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
   uint32_t deg = 0;
   for_each_in(g, v, [&](uint32_t in) {
     const float* m = A + static_cast<size_t>(in) * QS;
-#pragma unroll
-    for (int x = 0; x < QS; ++x) T[x] += __ldg(&m[x]);
+#pragma unroll (QS <= 8 ? QS : 2)
+    for (int x = 0; x < QS; ++x) T[x] += ldm<NC>(&m[x]);
     ++deg;
   });
   int cnt = 0;
@@ -369,27 +430,27 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
     const float r_was = MODE == kModeDelta ? res[out] : 0.f;
     float p[QS];
     float M = -INFINITY;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int x = 0; x < QS; ++x) {
-      p[x] = T[x] - __ldg(&m_in[x]);
+      p[x] = T[x] - ldm<NC>(&m_in[x]);
       if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
     }
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
     float o[QS];
     generic_matvec<QS>(g, out, p, o);
     float s = 0.f;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
     const float inv = __frcp_rn(s);
     const float* m_old = A + static_cast<size_t>(out) * QS;
     float* dst = B + static_cast<size_t>(out) * QS;
     float r = 0.f;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) {
       if (xt < static_cast<int>(cj)) {
         const float pn = o[xt] * inv;
-        const float po = __expf(__ldg(&m_old[xt]));
+        const float po = __expf(ldm<NC>(&m_old[xt]));
         r = fmaxf(r, fabsf(pn - po));
         dst[xt] = __logf(pn);
       }
@@ -540,15 +601,15 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
 }
 
 // QS == 1 selects the binary layout.
-template <int QS, int MODE, bool CL>
+template <int QS, int MODE, bool CL, bool NC = true>
 __device__ __forceinline__ int vertex_update(const DevGraph& g, uint32_t v, const float* A, float* B,
                                              float* res, float eps, unsigned* nf,
                                              unsigned long long& evals, uint8_t* inlist, Stager* cl,
                                              bool cl_on) {
   if constexpr (QS == 1)
-    return vertex_update_binary<MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
+    return vertex_update_binary<MODE, CL, NC>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
   else
-    return vertex_update_generic<QS, MODE, CL>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
+    return vertex_update_generic<QS, MODE, CL, NC>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
 }
 
 // Sweep over all vertices (LIST = false) or over the vertices flagged this
@@ -661,7 +722,7 @@ __device__ __forceinline__ void commit_edge(const DevGraph& g, uint32_t d, float
   c.delta -= (r >= eps) ? 1 : 0;
   c.frontier += 1;
   res[d] = 0.f;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
   for (int x = 0; x < QS; ++x) live[static_cast<size_t>(d) * QS + x] = cand[static_cast<size_t>(d) * QS + x];
   tgt = g.ep[d ^ 1u];
   if (dense) {
@@ -734,7 +795,7 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
           const uint32_t d = 4 * q + k;
           if (rr[k] >= eps) {  // padding entries are 0
             c.survivors += 1;
-            if (philox_u53(prm.seed, it, 0u, d) < thresh) {
+            if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d) < thresh)) {
               if (prm.commit) {
                 commit_edge<QS>(g, d, rr[k], live, cand, res, eps, vflag, stamp, dense, c, nf[k], tg[k]);
               } else {
@@ -772,7 +833,7 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
         const float r = res[d];
         if (r >= eps) {
           c.survivors += 1;
-          if (philox_u53(prm.seed, it, 0u, d) < thresh) {
+          if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d) < thresh)) {
             cl.inlist[d] = 0;
             commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, dense, c, nf, tg);
           } else {
@@ -801,32 +862,19 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
 // commits survivors[min(S-1, floor(u*S))] in ascending id order.  The redraw
 // runs only on that rare path, so one block suffices.  With the candidate
 // list the survivors are exactly the kept list.
+// Attempt 1 + fallback of rnbp_frontier (schedulers.cpp:204-214) by one
+// block, called only when attempt 0 selected nothing and survivors exist.
+// The commits' count change goes to *delta_out (atomic).
 template <int QS, bool CL>
-__global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, const float* cand,
-                                                     float* res, uint32_t* vflag, uint32_t* vlist,
-                                                     uint8_t* sel, Ctl* ctl, float eps, RnbpParams prm,
-                                                     CandList cl) {
-  if (run_done(ctl)) return;
+__device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live, const float* cand, float* res,
+                                                 uint32_t* vflag, uint32_t* vlist, uint8_t* sel, Ctl* ctl,
+                                                 float eps, const RnbpParams& prm, const CandList& cl,
+                                                 unsigned long long surv, long long* delta_out) {
   __shared__ unsigned long long s_front, s_surv;
   __shared__ unsigned warp_tot[32];
   __shared__ unsigned long long running_s;
   __shared__ int found;
-  if (threadIdx.x < 32) {
-    unsigned long long f = 0, s = 0;
-    for (int k = threadIdx.x; k < kSlots; k += 32) {
-      f += ctl->acc[k].frontier;
-      s += ctl->acc[k].survivors;
-    }
-    f = warp_sum(f);
-    s = warp_sum(s);
-    if (threadIdx.x == 0) {
-      s_front = f;
-      s_surv = s;
-      ctl->survivors = s;
-    }
-  }
-  __syncthreads();
-  if (s_front > 0 || s_surv == 0) return;
+  if (threadIdx.x == 0) s_surv = surv;
   const double p = prm.fixed_p >= 0.0 ? prm.fixed_p : device_p_now(ctl, prm.low_p, prm.high_p, prm.thr);
   const unsigned long long thresh = static_cast<unsigned long long>(ceil(ldexp(p, 53)));
   const unsigned long long it = ctl->iteration;
@@ -866,8 +914,7 @@ __global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, co
   delta = block_sum(delta, sh_d);
   if (threadIdx.x == 0) {
     ctl->frontier = fr;  // counted here; the attempt-0 slots hold 0
-    if (delta)
-      atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->acc[0].delta), static_cast<unsigned long long>(delta));
+    if (delta) atomicAdd(reinterpret_cast<unsigned long long*>(delta_out), static_cast<unsigned long long>(delta));
     s_front = fr;
   }
   __syncthreads();
@@ -898,8 +945,7 @@ __global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, co
         uint32_t tg = 0;
         commit_edge<QS>(g, d, res[d], live, cand, res, eps, vflag, stamp, false, c, nf, tg);
         if (nf) vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
-        atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->acc[0].delta),
-                  static_cast<unsigned long long>(c.delta));
+        atomicAdd(reinterpret_cast<unsigned long long*>(delta_out), static_cast<unsigned long long>(c.delta));
       } else {
         sel[d] = 1;
       }
@@ -911,6 +957,32 @@ __global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, co
     __syncthreads();
     if (found) break;
   }
+}
+
+template <int QS, bool CL>
+__global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, const float* cand,
+                                                     float* res, uint32_t* vflag, uint32_t* vlist,
+                                                     uint8_t* sel, Ctl* ctl, float eps, RnbpParams prm,
+                                                     CandList cl) {
+  if (run_done(ctl)) return;
+  __shared__ unsigned long long s_f, s_s;
+  if (threadIdx.x < 32) {
+    unsigned long long f = 0, s = 0;
+    for (int k = threadIdx.x; k < kSlots; k += 32) {
+      f += ctl->acc[k].frontier;
+      s += ctl->acc[k].survivors;
+    }
+    f = warp_sum(f);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) {
+      s_f = f;
+      s_s = s;
+      ctl->survivors = s;
+    }
+  }
+  __syncthreads();
+  if (s_f > 0 || s_s == 0) return;
+  rnbp_retry_block<QS, CL>(g, live, cand, res, vflag, vlist, sel, ctl, eps, prm, cl, s_s, &ctl->acc[0].delta);
 }
 
 // Commit of a host-supplied frontier (lockstep apply_frontier).
@@ -1178,26 +1250,26 @@ __global__ void k_beliefs(DevGraph g, const float* A0, const float* A1, int ping
     } else {
       const uint32_t q = g.card[v];
       float T[QS];
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
       for_each_in(g, v, [&](uint32_t in) {
         const float* m = A + static_cast<size_t>(in) * QS;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
         for (int x = 0; x < QS; ++x) T[x] += m[x];
       });
       float M = -INFINITY;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x)
         if (x < static_cast<int>(q)) M = fmaxf(M, T[x]);
       double p[QS];
       double s = 0.0;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) {
         p[x] = x < static_cast<int>(q) ? exp(static_cast<double>(T[x] - M)) : 0.0;
         s += p[x];
       }
       double* o = out + g.bel_off[v];
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x)
         if (x < static_cast<int>(q)) o[x] = p[x] / s;
     }

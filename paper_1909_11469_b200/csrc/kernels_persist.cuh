@@ -1,0 +1,262 @@
+// Persistent RnBP tail (sm_100a, cooperative launch).
+//
+// Once the RnBP run walks its candidate list (cl_state 2: fewer than 1/16 of
+// the directed edges unconverged) an iteration is a few thousand message
+// updates, and four kernel launches per iteration would cost more than the
+// work.  k_rnbp_persist runs the iterations of run() (schedulers.cpp:301-347)
+// back to back inside one launch, with grid-wide barriers between the phases
+// of an iteration:
+//
+//   select   rnbp_frontier attempt 0 over the candidate list + the Jacobi
+//            commit of apply_frontier (schedulers.cpp:194-216, 231-241)
+//   retry    block 0: attempt 1 + single-survivor fallback (:204-214)
+//   refresh  refresh_residuals over the touched vertices (residuals.cpp:26-59)
+//   finalize block 0 / thread 0: the loop control of run() (fin_iter)
+//
+// It stops when the run is done (converged / max_iterations / time limit /
+// the host's trace-ring budget).  All data written inside the launch is read
+// with coherent loads (ldm<false>); __ldg only touches the immutable graph.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+
+namespace bpb {
+
+namespace cgp = cooperative_groups;
+
+constexpr int kPersistBlock = 512;
+
+// block reduction of the per-iteration contributions into acc[0..5]
+__device__ __forceinline__ void block_add_pacc(unsigned long long* accum, const Contrib& c) {
+  __shared__ unsigned long long sh[6][kPersistBlock / 32];
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  unsigned long long v[6] = {static_cast<unsigned long long>(c.delta), c.count, c.frontier, c.survivors,
+                             c.evals, c.visits};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) sh[k][wid] = v[k];
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      unsigned long long x = lane < nw ? sh[k][lane] : 0ull;
+      x = warp_sum(x);
+      if (lane == 0 && x) atomicAdd(&accum[k], x);
+    }
+  }
+}
+
+// CLUSTER: the whole grid is one thread-block cluster (<= 16 CTAs) and the
+// phases are separated by the hardware cluster barrier; otherwise a
+// cooperative grid barrier.
+//
+// The loop state of run() (iteration, unconverged count, previous count,
+// vflag stamp, current list) is REPLICATED in every CTA: after the refresh
+// barrier each CTA applies the finalize step itself from the reduced sums,
+// so an iteration needs two barriers and no global read-modify-write of the
+// control block.  Reductions and list counters are multi-buffered by
+// iteration so no CTA resets a value another CTA may still read.  CTA 0 / thread 0
+// mirrors the state into Ctl and writes the trace record for the host.
+template <int QS, bool CLUSTER>
+__global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, float* live, float* cand, float* res,
+                                                                uint32_t* vflag, uint32_t* vlist, Ctl* ctl,
+                                                                float eps, RnbpParams prm, CandList cl) {
+  auto sync_all = [] {
+    if constexpr (CLUSTER)
+      cgp::this_cluster().sync();
+    else
+      cgp::this_grid().sync();
+  };
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  // replicated loop state (identical in every thread of every CTA)
+  if (ctl->done || ctl->cl_state != 2u) return;
+  unsigned long long it = ctl->iteration;
+  unsigned unc = ctl->unconverged, prev = ctl->prev_unconverged, has_prev = ctl->has_prev;
+  uint32_t stamp = ctl->stamp;
+  unsigned cur = ctl->cl_cur;
+  const unsigned long long max_it = ctl->max_iterations;
+  // Bernoulli thresholds of both parallelism levels (uniform_unit < p <=> u53 < ceil(p 2^53))
+  const unsigned long long th_low = static_cast<unsigned long long>(ceil(ldexp(prm.low_p, 53)));
+  const unsigned long long th_high = static_cast<unsigned long long>(ceil(ldexp(prm.high_p, 53)));
+  unsigned long long msgs = ctl->msgs_total;
+  // buffers indexed by iteration: pacc3[it % 3], nfl2[it & 1]
+  unsigned long long* pacc3 = ctl->pacc3[0];
+  if (lead) {
+    for (int b = 0; b < 3; ++b)
+      for (int k = 0; k < 6; ++k) ctl->pacc3[b][k] = 0ull;
+    ctl->nfl2[0] = ctl->nfl2[1] = 0u;
+    ctl->time_stop = 0u;
+  }
+  sync_all();
+  for (;;) {
+    const unsigned pb = static_cast<unsigned>(it % 3ull), fb = static_cast<unsigned>(it & 1ull);
+    unsigned long long* acc = pacc3 + 6 * pb;
+    unsigned* nfl = &ctl->nfl2[fb];
+    // ---- select + commit over the candidate list (rnbp_frontier attempt 0)
+    {
+      const uint32_t n = ctl->cl_n[cur];
+      const uint32_t* list = cur ? cl.list[1] : cl.list[0];
+      uint32_t* keep = cur ? cl.list[0] : cl.list[1];
+      unsigned long long thresh = th_high;  // select_parallelism (schedulers.cpp:218-224)
+      if (has_prev && prev != 0u) {
+        const double ratio = static_cast<double>(unc) / static_cast<double>(prev);
+        thresh = ratio > prm.thr ? th_low : th_high;
+      }
+      if (lead) {  // buffers of the NEXT iteration: last read two barriers ago
+        unsigned long long* nx = pacc3 + 6 * static_cast<unsigned>((it + 1) % 3ull);
+        for (int k = 0; k < 6; ++k) nx[k] = 0ull;
+        ctl->nfl2[fb ^ 1u] = 0u;
+      }
+      BPB_STAGER(kp, 2048, keep, &ctl->cl_n[cur ^ 1u]);
+      BPB_STAGER(fl, 2048, vlist, nfl);
+      kp.init();
+      fl.init();
+      Contrib c;
+      for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+        const uint32_t i = base + threadIdx.x;
+        bool nf = false, kept = false;
+        uint32_t tg = 0, d = 0;
+        if (i < n) {
+          d = list[i];
+          const float r = res[d];
+          c.count += 8;  // algorithmic bytes: list entry + residual
+          if (r >= eps) {
+            c.survivors += 1;
+            if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d) < thresh)) {
+              cl.inlist[d] = 0;
+              commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, false, c, nf, tg);
+              c.count += 8 * QS + 12;  // candidate -> live, residual, target id, flag
+            } else {
+              kept = true;
+              c.count += 4;  // kept list entry
+            }
+          } else {
+            cl.inlist[d] = 0;
+          }
+        }
+        kp.push_warp(kept, d);
+        fl.push_warp(nf, tg);
+        kp.flush(kPersistBlock);
+        fl.flush(kPersistBlock);
+      }
+      kp.flush(0);
+      fl.flush(0);
+      block_add_pacc(acc, c);
+    }
+    sync_all();
+    // ---- retry / fallback (schedulers.cpp:204-214): uniform decision, one block
+    unsigned long long retry_front = 0;
+    if (acc[2] == 0ull && acc[3] > 0ull) {
+      if (blockIdx.x == 0) {
+        // rnbp_retry_block reads the loop state from Ctl: mirror it first
+        if (threadIdx.x == 0) {
+          ctl->iteration = it;
+          ctl->unconverged = unc;
+          ctl->prev_unconverged = prev;
+          ctl->has_prev = has_prev;
+          ctl->stamp = stamp;
+          ctl->cl_cur = cur;
+          ctl->nflag = *nfl;
+          ctl->frontier = 0;
+        }
+        __syncthreads();
+        rnbp_retry_block<QS, true>(g, live, cand, res, vflag, vlist, nullptr, ctl, eps, prm, cl, acc[3],
+                                   reinterpret_cast<long long*>(&acc[0]));
+        __syncthreads();
+        if (threadIdx.x == 0) *nfl = ctl->nflag;  // fallback / attempt-1 targets appended there
+      }
+      sync_all();
+      retry_front = ctl->frontier;
+    }
+    // ---- refresh over the touched vertices; new unconverged edges join the list
+    {
+      const uint32_t nv = *nfl;
+      if (lead) ctl->cl_n[cur] = 0u;  // the list just read is refilled next iteration
+      BPB_STAGER(st, 2048, cur ? cl.list[0] : cl.list[1], &ctl->cl_n[cur ^ 1u]);
+      st.init();
+      int cnt = 0;
+      unsigned long long evals = 0, visits = 0;
+      for (uint32_t base = blockIdx.x * blockDim.x; base < nv; base += stride) {
+        const uint32_t i = base + threadIdx.x;
+        if (i < nv) {
+          cnt += vertex_update<QS, kModeDelta, true, false>(g, vlist[i], live, cand, res, eps, &ctl->numeric_error,
+                                                            evals, cl.inlist, &st, true);
+          ++visits;
+        }
+        st.flush(1024);
+      }
+      st.flush(0);
+      Contrib c;
+      c.delta = cnt;
+      c.evals = evals;
+      c.visits = visits;
+      // per vertex: list id + unary; per message: edge pair (in + old out),
+      // coupling, candidate write, residual read + write
+      c.count = 8ull * visits + static_cast<unsigned long long>(8 * QS + 4 + 4 * QS + 8) * evals;
+      block_add_pacc(acc, c);
+      if (lead && globaltimer_ns() - ctl->t0_ns >= ctl->time_limit_ns) ctl->time_stop = 1u;
+    }
+    sync_all();
+    // ---- finalize (fin_iter), replicated: converged check before the caps
+    const long long delta = static_cast<long long>(acc[0]);
+    const unsigned long long frontier = acc[2] + retry_front;
+    const unsigned start = unc;
+    unc = static_cast<unsigned>(static_cast<long long>(start) + delta);
+    prev = start;  // set_prev_unconverged (schedulers.cpp:327)
+    has_prev = 1u;
+    msgs += frontier;
+    const bool numeric = ctl->numeric_error != 0u;
+    const bool tstop = ctl->time_stop != 0u;
+    if (lead) {
+      fin_record(ctl, it, frontier, unc);
+      ctl->evals_total += acc[4];
+      ctl->vertex_visits += acc[5];
+      ctl->persist_bytes += acc[1];
+      ctl->survivors = acc[3];
+    }
+    it += 1;
+    stamp += 1u;
+    cur ^= 1u;
+    bool done = false;
+    unsigned reason = kStopNone;
+    if (numeric) {
+      done = true;
+      reason = kStopNumeric;
+    } else if (unc == 0u) {
+      done = true;
+      reason = kStopConverged;
+    } else if (it >= max_it) {
+      done = true;
+      reason = kStopMaxIter;
+    } else if (tstop) {
+      done = true;
+      reason = kStopTime;
+    }
+    if (done) {
+      if (lead) {  // mirror the final state for the host
+        ctl->iteration = it;
+        ctl->unconverged = unc;
+        ctl->prev_unconverged = prev;
+        ctl->has_prev = has_prev;
+        ctl->stamp = stamp;
+        ctl->cl_cur = cur;
+        ctl->msgs_total = msgs;
+        ctl->frontier = 0;
+        ctl->nflag = 0;
+        ctl->done = 1u;
+        ctl->converged = reason == kStopConverged ? 1u : 0u;
+        ctl->stop_reason = reason;
+      }
+      return;
+    }
+  }
+}
+
+}  // namespace bpb

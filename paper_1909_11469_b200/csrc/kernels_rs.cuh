@@ -119,18 +119,6 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned x, unsigned* total)
   return before + v - x;
 }
 
-// warp-aggregated append of x (pred) to list[*counter]
-__device__ __forceinline__ void warp_append(bool pred, uint32_t x, uint32_t* list, unsigned* counter) {
-  const unsigned lane = threadIdx.x & 31u;
-  const unsigned mask = __ballot_sync(0xffffffffu, pred);
-  if (!mask) return;
-  const unsigned leader = __ffs(mask) - 1;
-  unsigned base = 0;
-  if (lane == leader) base = atomicAdd(counter, __popc(mask));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = x;
-}
-
 // ---------------------------------------------------------------------------
 // Grid-wide exact top-k of 32-bit keys, ties to the lower index
 // (select_top_k semantics, schedulers.cpp:105-116).  keyof(i, key) -> valid.
@@ -292,11 +280,11 @@ __device__ __forceinline__ void splash_vertex_update(const DevGraph& g, uint32_t
   } else {
     const uint32_t ci = g.card[v];
     float T[QS];
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
     for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
     for (uint32_t a = b0; a < e0; ++a) {
       const float* m = src_of(g.in_adj[a]);
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) T[x] += m[x];
     }
     for (uint32_t a = b0; a < e0; ++a) {
@@ -304,21 +292,21 @@ __device__ __forceinline__ void splash_vertex_update(const DevGraph& g, uint32_t
       const uint32_t cj = g.card[g.ep[in]];
       const float* m_in = src_of(in);
       float p[QS], M = -INFINITY;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) {
         p[x] = T[x] - m_in[x];
         if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
       }
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
       float o[QS], s = 0.f;
       generic_matvec<QS>(g, out, p, o);
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
       if (!(s > 0.f) || !(s < INFINITY)) *nf = 1u;
       const float inv = __frcp_rn(s);
       float* dst = shadow + static_cast<size_t>(out) * QS;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt)
         if (xt < static_cast<int>(cj)) dst[xt] = __logf(o[xt] * inv);
     }
@@ -533,7 +521,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       rs_flag(v, vflag, vlist, &ctl->nflag, stamp, dense);
       for (uint32_t a = g.in_off[v]; a < g.in_off[v + 1]; ++a) {
         const uint32_t in = g.in_adj[a], out = in ^ 1u;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
         for (int x = 0; x < QS; ++x)
           live[static_cast<size_t>(out) * QS + x] = b.shadow[static_cast<size_t>(out) * QS + x];
         rs_flag(g.ep[in], vflag, vlist, &ctl->nflag, stamp, dense);
@@ -580,27 +568,27 @@ __global__ void __launch_bounds__(kBlock) k_splash_apply_edges(DevGraph g, const
     } else {
       const uint32_t ci = g.card[v], cj = g.card[g.ep[back]];
       float p[QS], M = -INFINITY;
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) p[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
       for (uint32_t a = g.in_off[v]; a < g.in_off[v + 1]; ++a) {
         const uint32_t in = g.in_adj[a];
         if (in == back) continue;
         const float* m = src_of(in);
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
         for (int x = 0; x < QS; ++x) p[x] += m[x];
       }
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x)
         if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
       float o[QS], s2 = 0.f;
       generic_matvec<QS>(g, d, p, o);
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt) s2 += xt < static_cast<int>(cj) ? o[xt] : 0.f;
       if (!(s2 > 0.f) || !(s2 < INFINITY)) *nf = 1u;
       const float inv = __frcp_rn(s2);
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt)
         if (xt < static_cast<int>(cj)) shadow[static_cast<size_t>(d) * QS + xt] = __logf(o[xt] * inv);
     }
@@ -617,7 +605,7 @@ __global__ void __launch_bounds__(kBlock) k_splash_commit_edges(DevGraph g, floa
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dense = 0;
   if (i >= n) return;
   const uint32_t d = edges[i];
-#pragma unroll
+#pragma unroll (QS <= 8 ? QS : 2)
   for (int x = 0; x < QS; ++x) live[static_cast<size_t>(d) * QS + x] = shadow[static_cast<size_t>(d) * QS + x];
   const uint32_t stamp = ctl->stamp;
   rs_flag(g.ep[d], vflag, vlist, &ctl->nflag, stamp, false);

@@ -212,3 +212,16 @@ def test_zero_edge_graph(bp, orc):
         assert r.converged and r.iterations == 0
         assert abs(r.beliefs.at(0)[0] - 0.25) < 1e-6
         assert abs(r.beliefs.at(1)[2] - 0.5) < 1e-6
+
+
+@pytest.mark.parametrize("n,c,seed", [(100, 2.5, 500), (60, 3.0, 7)])
+def test_rnbp_persistent_tail_matches_graph_loop(bp, orc, n, c, seed):
+    """The persistent list-mode kernel runs the same iterations as the
+    per-kernel graph loop: identical traces (frontier sizes, counts)."""
+    g = bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed))
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=3000, seed=seed)
+    a = bp.run(g, cfg)
+    b = bp.run_ex(g, cfg, flags=bp.RUN_NO_PERSIST)
+    assert a.trace_signature() == b.trace_signature()
+    assert np.max(np.abs(a.beliefs.values - b.beliefs.values)) <= 1e-6
+    assert a.gpu_launches <= b.gpu_launches

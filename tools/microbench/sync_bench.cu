@@ -1,0 +1,107 @@
+// Microbenchmark of the per-iteration primitives of the persistent RnBP tail:
+// cluster barrier, cooperative grid barrier, contended global atomics, a
+// dependent L2 round trip, and %globaltimer.  nvcc -gencode
+// arch=compute_100a,code=sm_100a -O3 -o sync_bench sync_bench.cu
+#include <cooperative_groups.h>
+#include <cstdio>
+namespace cg = cooperative_groups;
+
+__device__ unsigned long long g_ctr[64];
+__device__ unsigned g_chain[1 << 20];
+
+template <int MODE>
+__global__ void bench(int iters, unsigned long long* out) {
+  unsigned long long t0 = clock64();
+  unsigned v = threadIdx.x;
+  for (int i = 0; i < iters; ++i) {
+    if (MODE == 0) cg::this_cluster().sync();
+    if (MODE == 1) cg::this_grid().sync();
+    if (MODE == 2) {  // one atomic per block + cluster barrier
+      if (threadIdx.x == 0) atomicAdd(&g_ctr[0], 1ull);
+      cg::this_cluster().sync();
+    }
+    if (MODE == 3) {  // dependent L2 load chain of 4 + cluster barrier
+      for (int k = 0; k < 4; ++k) v = *(volatile unsigned*)&g_chain[(v * 2654435761u) & ((1 << 20) - 1)];
+      cg::this_cluster().sync();
+    }
+    if (MODE == 4) {  // one atomic per WARP on one address + cluster barrier
+      if ((threadIdx.x & 31) == 0) atomicAdd(&g_ctr[0], 1ull);
+      cg::this_cluster().sync();
+    }
+    if (MODE == 5) __syncthreads();
+    if (MODE == 6) {  // %globaltimer read by one thread + cluster barrier
+      if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_ctr[1] += t & 1;
+      }
+      cg::this_cluster().sync();
+    }
+    if (MODE == 7) {  // double division by one thread + cluster barrier
+      if (threadIdx.x == 0) {
+        volatile double a = (double)v, b2 = 3.0 + i;
+        g_ctr[2] += (unsigned long long)ceil(ldexp(a / b2, 53));
+      }
+      cg::this_cluster().sync();
+    }
+  }
+  unsigned long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+  if (v == 0xFFFFFFFF) out[1] = v;
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 16);
+  const int iters = 20000;
+  for (int mode = 0; mode < 8; ++mode) {
+    for (int blocks : {16, 32, 148}) {
+      if (mode != 1 && mode != 5 && blocks > 16) continue;
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(blocks);
+      lc.blockDim = dim3(512);
+      cudaLaunchAttribute at[1];
+      if (mode == 1) {
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+      } else {
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = mode == 5 ? 1 : blocks;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+      }
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      cudaError_t e;
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a);
+      switch (mode) {
+        case 0: cudaFuncSetAttribute(bench<0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                e = cudaLaunchKernelEx(&lc, bench<0>, iters, d); break;
+        case 1: e = cudaLaunchKernelEx(&lc, bench<1>, iters, d); break;
+        case 2: cudaFuncSetAttribute(bench<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                e = cudaLaunchKernelEx(&lc, bench<2>, iters, d); break;
+        case 3: cudaFuncSetAttribute(bench<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                e = cudaLaunchKernelEx(&lc, bench<3>, iters, d); break;
+        case 4: cudaFuncSetAttribute(bench<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                e = cudaLaunchKernelEx(&lc, bench<4>, iters, d); break;
+        case 6: cudaFuncSetAttribute(bench<6>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                e = cudaLaunchKernelEx(&lc, bench<6>, iters, d); break;
+        case 7: cudaFuncSetAttribute(bench<7>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                e = cudaLaunchKernelEx(&lc, bench<7>, iters, d); break;
+        default: e = cudaLaunchKernelEx(&lc, bench<5>, iters, d); break;
+      }
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      unsigned long long cyc = 0;
+      cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+      printf("mode %d blocks %3d: %s  %.3f us/iter (event)  %llu cycles/iter\n", mode, blocks,
+             e == cudaSuccess ? "ok " : cudaGetErrorString(e), ms * 1e3 / iters, cyc);
+    }
+  }
+  return 0;
+}
