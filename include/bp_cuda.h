@@ -98,7 +98,7 @@ typedef struct {
 /* bpsched::RunResult scalars (schedulers.hpp:50-57) + device statistics. */
 typedef struct {
   int32_t converged;
-  int32_t _pad;
+  int32_t stopped;                 /* the run loop has ended (converged or a cap); bp_band_status */
   uint64_t iterations;
   double wall_time;                /* host steady clock, same span as schedulers.cpp:297-350 */
   uint64_t messages_updated_total; /* sum of frontier sizes (schedulers.cpp:343)            */
@@ -211,6 +211,42 @@ BP_API int bp_engine_rs_frontier(struct bp_engine* e, double p, uint32_t h, uint
  * as one pass of the run loop; *frontier_size receives |F|. */
 BP_API int bp_engine_step(struct bp_engine* e, uint64_t* frontier_size);
 BP_API int bp_engine_iteration(const struct bp_engine* e, uint64_t* out);
+
+/* ---- Row-band partition of a lattice across GPUs ----------
+ * Rank `part` of `nparts` owns rows [row0, row1) of generate_ising(n, c, seed)
+ * (generators.cpp:24-50); its band adds one ghost row per neighbouring band.
+ * Per LBP iteration the caller runs, in order on bp_band_stream():
+ *   bp_band_lbp_sweep   sweep of the band, boundary messages -> send_up /
+ *                       send_down, local unconverged count + time vote -> count[0..1]
+ *   (collectives)       send_up -> rank-1's recv_down, send_down -> rank+1's
+ *                       recv_up, all-reduce(sum) of count[0..1]
+ *   bp_band_lbp_finish  ghost messages <- recv_*, run() loop control on the
+ *                       GLOBAL count (every rank takes the same stop decision)
+ * Owned messages are bitwise identical to the unpartitioned run. */
+typedef struct {
+  uint32_t part, nparts;
+  uint32_t row0, row1;          /* owned global rows [row0, row1) */
+  uint32_t ghost_up, ghost_down;
+  uint32_t local_rows, cols;    /* band lattice: local_rows x cols */
+  uint64_t owned_directed;      /* directed edges whose source row is owned */
+} bp_band_info;
+
+typedef struct {                /* DEVICE pointers, owned by the caller */
+  float* send_up;               /* cols floats */
+  float* send_down;             /* cols floats */
+  const float* recv_up;         /* cols floats */
+  const float* recv_down;       /* cols floats */
+  unsigned long long* count;    /* 2 values, all-reduced (sum) in place between sweep and finish */
+} bp_halo_buffers;
+
+BP_API int bp_graph_generate_ising_band(uint32_t n, double c, uint64_t seed, uint32_t part, uint32_t nparts,
+                                        const bp_device_opts* opts, struct bp_graph** out, bp_band_info* info);
+BP_API int bp_band_engine_create(const struct bp_graph* g, const bp_sched_config* cfg, const bp_band_info* info,
+                                 const bp_halo_buffers* bufs, struct bp_engine** out);
+BP_API int bp_band_stream(const struct bp_engine* e, uint64_t* stream); /* cudaStream_t of the band */
+BP_API int bp_band_lbp_sweep(struct bp_engine* e);
+BP_API int bp_band_lbp_finish(struct bp_engine* e);
+BP_API int bp_band_status(struct bp_engine* e, bp_run_result* result); /* synchronises */
 
 #ifdef __cplusplus
 }

@@ -91,7 +91,7 @@ class _Record(C.Structure):
 
 
 class _Result(C.Structure):
-    _fields_ = [("converged", C.c_int32), ("_pad", C.c_int32), ("iterations", C.c_uint64),
+    _fields_ = [("converged", C.c_int32), ("stopped", C.c_int32), ("iterations", C.c_uint64),
                 ("wall_time", C.c_double), ("messages_updated_total", C.c_uint64),
                 ("trace_len", C.c_uint64), ("device_ms", C.c_double),
                 ("message_evaluations", C.c_uint64), ("gpu_launches", C.c_uint64),
@@ -163,6 +163,13 @@ def _load():
         "bp_engine_rbp_frontier": (C.c_int, [P, C.c_double, P, C.POINTER(C.c_uint64)]),
         "bp_engine_rs_frontier": (C.c_int, [P, C.c_double, C.c_uint32, P, P, P, C.POINTER(C.c_uint64)]),
         "bp_engine_step": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+        "bp_graph_generate_ising_band": (C.c_int, [C.c_uint32, C.c_double, C.c_uint64, C.c_uint32, C.c_uint32,
+                                                   C.POINTER(_DevOpts), C.POINTER(P), C.c_void_p]),
+        "bp_band_engine_create": (C.c_int, [P, C.POINTER(_Config), C.c_void_p, C.c_void_p, C.POINTER(P)]),
+        "bp_band_stream": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+        "bp_band_lbp_sweep": (C.c_int, [P]),
+        "bp_band_lbp_finish": (C.c_int, [P]),
+        "bp_band_status": (C.c_int, [P, C.POINTER(_Result)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

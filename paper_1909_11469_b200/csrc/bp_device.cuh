@@ -46,6 +46,7 @@ struct DevGraph {
   uint32_t lat_rows, lat_cols;
   uint32_t par_mode;
   uint32_t uniform_q;                     // all cardinalities equal (0 = mixed)
+  uint32_t cnt_row0, cnt_row1;            // lattice rows whose messages are owned (row-band partition)
   const float* __restrict__ ising_a;      // E  (binary, par_mode 1): a = e^J of the table {a, 1/a, 1/a, a}
   const float* __restrict__ pw;           // E  (generic, par_mode 1)
 };
@@ -179,8 +180,20 @@ struct Ctl {
   unsigned int time_stop;
   unsigned int pad4_;
   unsigned long long persist_bytes;  // algorithmic bytes moved by the persistent kernel
+  unsigned long long vote_limit_ns;  // row-band partition: time limit, decided by an all-reduced vote
   Accum acc[kSlots];
   TraceRec trace[kTraceRing];
+};
+
+// Halo buffers of a row-band partition (device pointers owned by the caller;
+// kernels.cuh: k_part_pack / k_part_count / k_part_unpack).
+struct PartHalo {
+  float* send_up;             // C: up messages of the first owned row (to the band above)
+  float* send_down;           // C: down messages of the last owned row (to the band below)
+  const float* recv_up;       // C: the band above's send_down
+  const float* recv_down;     // C: the band below's send_up
+  unsigned long long* count;  // [0] local unconverged count, [1] local time-limit vote (all-reduced in place)
+  uint32_t ghost_up, ghost_down;
 };
 
 // ---------------------------------------------------------------------------

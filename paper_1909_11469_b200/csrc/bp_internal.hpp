@@ -44,6 +44,7 @@ struct BinaryStreams {
   std::vector<float> coupling;  // J = 2 * lambda * c per edge (log-table differences)
 };
 BinaryStreams ising_streams(uint32_t n, double c, uint64_t seed);
+BinaryStreams ising_band_streams(uint32_t n, double c, uint64_t seed, uint32_t a, uint32_t b);
 BinaryStreams chain_streams(uint32_t length, double c, uint64_t seed);
 
 struct PottsStreams {

@@ -215,6 +215,64 @@ int bp_engine_rs_frontier(bp_engine* e, double p, uint32_t h, uint32_t* roots, u
     *ns = r.size();
   });
 }
+int bp_graph_generate_ising_band(uint32_t n, double c, uint64_t seed, uint32_t part, uint32_t nparts,
+                                 const bp_device_opts* opts, bp_graph** out, bp_band_info* info) {
+  if (!out || !info) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    if (nparts == 0 || part >= nparts || nparts > n) throw bpb::Error(BP_ERR_INVALID_ARGUMENT, "bad band partition");
+    const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(part) * n / nparts);
+    const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(part + 1) * n / nparts);
+    const uint32_t gu = part > 0 ? 1u : 0u, gd = part + 1 < nparts ? 1u : 0u;
+    auto g = bpb::build_lattice_binary(r1 + gd - (r0 - gu), n, bpb::ising_band_streams(n, c, seed, r0 - gu, r1 + gd),
+                                       opts);
+    g->cnt_row0 = gu;
+    g->cnt_row1 = gu + (r1 - r0);
+    uint64_t owned = 0;  // sum of degrees of the owned vertices in the full grid
+    for (uint32_t r = r0; r < r1; ++r)
+      owned += static_cast<uint64_t>(n) * ((r > 0) + (r + 1 < n)) + 2ull * (n - 1);
+    g->owned_directed = owned;
+    *info = bp_band_info{part, nparts, r0, r1, gu, gd, r1 + gd - (r0 - gu), n, owned};
+    wrap_graph(std::move(g), out);
+  });
+}
+
+int bp_band_engine_create(const bp_graph* g, const bp_sched_config* cfg, const bp_band_info* info,
+                          const bp_halo_buffers* bufs, bp_engine** out) {
+  if (!g || !cfg || !info || !bufs || !out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    bpb::validate_config(*cfg);
+    auto e = bpb::make_engine(*g->impl, *cfg);
+    bpb::PartHalo h{};
+    h.send_up = bufs->send_up;
+    h.send_down = bufs->send_down;
+    h.recv_up = bufs->recv_up;
+    h.recv_down = bufs->recv_down;
+    h.count = bufs->count;
+    e->band_config(h, info->owned_directed);
+    *out = new bp_engine{std::move(e), g, *cfg};
+  });
+}
+
+int bp_band_stream(const bp_engine* e, uint64_t* stream) {
+  if (!e || !stream) return BP_ERR_INVALID_ARGUMENT;
+  *stream = reinterpret_cast<uint64_t>(e->e->stream());
+  return BP_OK;
+}
+int bp_band_lbp_sweep(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_sweep(); });
+}
+int bp_band_lbp_finish(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_finish(); });
+}
+int bp_band_status(bp_engine* e, bp_run_result* r) {
+  if (!e || !r) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_status(r); });
+}
+
 int bp_engine_step(bp_engine* e, uint64_t* frontier_size) {
   if (!e) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] {

@@ -30,6 +30,12 @@ class EngineBase {
   virtual void apply_splashes(uint64_t ns, const uint32_t* roots, const uint64_t* eoff,
                               const uint32_t* edges) = 0;
   virtual uint64_t step() = 0;
+  // row-band partition (bp_band_*): LBP on a lattice band with ghost rows
+  virtual void band_config(const PartHalo& h, uint64_t owned_directed) = 0;
+  virtual void band_sweep() = 0;
+  virtual void band_finish() = 0;
+  virtual void band_status(bp_run_result* r) = 0;
+  virtual cudaStream_t stream() const = 0;
 };
 
 std::unique_ptr<EngineBase> make_engine(const GraphImpl& g, const bp_sched_config& cfg);

@@ -186,7 +186,13 @@ class EngineT final : public EngineBase {
   }
   void messages(double* out, bool candidates) override {
     std::vector<float> raw(static_cast<size_t>(g_.D) * QS);
-    const DevBuf& src = candidates ? bufB_ : bufA_;
+    // band engines ping-pong like run()'s LBP: m_t lives in buf[t & 1]
+    bool flip = false;
+    if (band_started_) {
+      fetch_ctl_header();
+      flip = (hctl_->iteration & 1ull) != 0;
+    }
+    const DevBuf& src = (candidates != flip) ? bufB_ : bufA_;
     if (!raw.empty()) cuda_check(cudaMemcpy(raw.data(), src.p, raw.size() * 4, cudaMemcpyDeviceToHost), "d2h");
     const auto& ep = g_.host_ep();
     size_t o = 0;
@@ -209,7 +215,7 @@ class EngineT final : public EngineBase {
   void beliefs(double* out) override {
     const size_t nb = g_.unary_size();
     ensure_beliefs_buf(nb);
-    enqueue_beliefs(bel_.as<double>(), false);
+    enqueue_beliefs(bel_.as<double>(), band_started_);
     cuda_check(cudaMemcpyAsync(out, bel_.p, nb * 8, cudaMemcpyDeviceToHost, s_), "d2h");
     sync();
   }
@@ -476,9 +482,69 @@ class EngineT final : public EngineBase {
   }
 
   // ---- launch sequences
-  void enqueue_finalize(int mode) {
-    timed(kKOther, [&] { k_finalize<<<1, kSlots, 0, s_>>>(ctl(), mode, g_.D); });
+  void enqueue_finalize(int mode, uint32_t D = 0xFFFFFFFFu, const unsigned long long* ext = nullptr) {
+    const uint32_t d = D == 0xFFFFFFFFu ? g_.D : D;
+    timed(kKOther, [&] { k_finalize<<<1, kSlots, 0, s_>>>(ctl(), mode, d, ext); });
     launch_check();
+  }
+
+  // ---- row-band partition: sweep -> pack halos + local count -> [caller's
+  // collectives on stream()] -> unpack ghosts -> finalize with the global count
+  PartHalo halo_{};
+  uint64_t band_owned_ = 0;
+  bool band_started_ = false;
+  cudaStream_t stream() const override { return s_; }
+  void band_config(const PartHalo& h, uint64_t owned_directed) override {
+    if (QS != 1 || !g_.lat_cols || g_.par_mode != 1)
+      throw Error(BP_ERR_UNSUPPORTED, "row-band partition needs a binary Ising lattice band");
+    if (cfg_.kind != BP_LBP) throw Error(BP_ERR_UNSUPPORTED, "row-band partition: LBP only in this build");
+    halo_ = h;
+    halo_.ghost_up = g_.cnt_row0 > 0 ? 1u : 0u;
+    halo_.ghost_down = g_.cnt_row1 < g_.lat_rows ? 1u : 0u;
+    band_owned_ = owned_directed;
+    band_started_ = false;
+  }
+  void band_sweep() override {
+    if (!band_started_) {
+      reset_ctl(cfg_.max_iterations, 1e300);  // the local clock never stops a band alone
+      const double ns = cfg_.time_limit * 1e9;
+      const unsigned long long lim = ns >= 1.8e19 ? ~0ull : static_cast<unsigned long long>(ns);
+      cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, vote_limit_ns), &lim, 8,
+                                 cudaMemcpyHostToDevice, s_), "ctl h2d");
+      const unsigned gi = grid_cap(static_cast<size_t>(g_.D) * QS);
+      k_init_messages<QS><<<gi, kBlock, 0, s_>>>(dg_, live(), ctl(), 1);
+      launch_check();
+      ++launches_;
+      band_started_ = true;
+    }
+    k_vertex_update<QS, kModeCount, false, true, false>
+        <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(
+            dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+    const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
+    k_part_pack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
+    k_part_count<<<1, kSlots, 0, s_>>>(ctl(), halo_);
+    launch_check();
+    launches_ += 3;
+  }
+  void band_finish() override {
+    const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
+    k_part_unpack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
+    launch_check();
+    ++launches_;
+    enqueue_finalize(kFinLbp, static_cast<uint32_t>(band_owned_), halo_.count);
+  }
+  void band_status(bp_run_result* r) override {
+    fetch_ctl_header();
+    std::memset(r, 0, sizeof(*r));
+    r->converged = hctl_->converged ? 1 : 0;
+    r->stopped = hctl_->done ? 1 : 0;
+    r->iterations = hctl_->iteration;
+    r->messages_updated_total = hctl_->msgs_total;
+    r->trace_len = hctl_->trace_len;
+    r->message_evaluations = hctl_->evals_total;
+    r->vertex_visits = hctl_->vertex_visits;
+    r->gpu_launches = launches_;
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
   }
 
   void enqueue_init(bool lbp) {

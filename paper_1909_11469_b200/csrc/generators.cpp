@@ -77,6 +77,25 @@ BinaryStreams lattice_streams(uint32_t rows, uint32_t cols, double c, uint64_t s
 }  // namespace
 
 BinaryStreams ising_streams(uint32_t n, double c, uint64_t seed) { return lattice_streams(n, n, c, seed); }
+
+// Rows [a, b) of generate_ising's n x n instance as a stand-alone
+// (b - a) x n lattice: same unaries and couplings; the band's last row keeps
+// only its right edges (its down edges lead out of the band).
+BinaryStreams ising_band_streams(uint32_t n, double c, uint64_t seed, uint32_t a, uint32_t b) {
+  if (a >= b || b > n) throw_invalid("ising band: need 0 <= a < b <= n");
+  const BinaryStreams full = lattice_streams(n, n, c, seed);
+  const size_t C = n, L = b - a, row = 2 * C - 1;
+  BinaryStreams s;
+  s.unary_lo.assign(full.unary_lo.begin() + a * C, full.unary_lo.begin() + b * C);
+  s.coupling.resize((L - 1) * row + (C - 1));
+  for (size_t lr = 0; lr + 1 < L; ++lr)
+    std::copy(full.coupling.begin() + (a + lr) * row, full.coupling.begin() + (a + lr + 1) * row,
+              s.coupling.begin() + lr * row);
+  const size_t r = b - 1;
+  for (size_t col = 0; col + 1 < C; ++col)
+    s.coupling[(L - 1) * row + col] = full.coupling[r * row + (r + 1 == n ? col : 2 * col)];
+  return s;
+}
 BinaryStreams chain_streams(uint32_t length, double c, uint64_t seed) {
   return lattice_streams(length ? 1 : 0, length, c, seed);
 }

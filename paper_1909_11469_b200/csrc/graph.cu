@@ -53,6 +53,8 @@ DevGraph GraphImpl::dev() const {
   g.lat_cols = lat_cols;
   g.par_mode = par_mode;
   g.uniform_q = uniform_q;
+  g.cnt_row0 = cnt_row0;
+  g.cnt_row1 = cnt_row1;
   g.ising_a = ising_a.as<float>();
   g.pw = pw.as<float>();
   return g;

@@ -46,6 +46,10 @@ struct GraphImpl {
   DevBuf in_off, in_adj, ep, unary_lo, epar, card, unary_log, table, bel_off, ising_a, pw;
   uint32_t lat_rows = 0, lat_cols = 0;  // lattice topology detected / generated (0 = CSR only)
   uint32_t par_mode = 0;                // 1: Ising couplings (binary) / Potts weights (generic)
+  // row-band partition (bp_graph_generate_ising_band): owned local rows
+  // [cnt_row0, cnt_row1); other rows are ghosts of the neighbouring bands
+  uint32_t cnt_row0 = 0, cnt_row1 = 0xFFFFFFFFu;
+  uint64_t owned_directed = 0;          // directed edges whose source is owned
   std::vector<uint32_t> cards_host;  // mixed cardinalities only
 
   DevGraph dev() const;

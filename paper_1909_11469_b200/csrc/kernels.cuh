@@ -219,8 +219,58 @@ __device__ __forceinline__ void fin_iter(Ctl* c, long long delta, unsigned long 
   fin_check_top(c);
 }
 
+// ---------------------------------------------------------------------------
+// row-band partition: halo rows of a lattice band.  The band
+// holds its owned rows plus one ghost row per neighbouring band.  After a
+// sweep writes the new messages into B, the band's boundary messages go to
+// the neighbours (send) and the neighbours' messages overwrite the ghost-row
+// messages that flow into owned rows (recv), so every owned vertex sees
+// exactly the messages of the unpartitioned sweep.
+
+__device__ __forceinline__ uint32_t lat_edge_down(uint32_t lr, uint32_t c, uint32_t C) {
+  return lr * (2u * C - 1u) + 2u * c + (c + 1u < C ? 1u : 0u);
+}
+
+// pack after the sweep: B = the buffer the sweep just wrote (ping-pong parity)
+static __global__ void k_part_pack(DevGraph g, const float* buf0, const float* buf1, Ctl* ctl, PartHalo h) {
+  const float* B = (ctl->sweeps & 1ull) ? buf0 : buf1;
+  const uint32_t C = g.lat_cols, L = g.lat_rows;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    if (h.ghost_up) h.send_up[c] = B[2u * lat_edge_down(0u, c, C) + 1u];     // (1, c) -> (0, c)
+    if (h.ghost_down) h.send_down[c] = B[2u * lat_edge_down(L - 2u, c, C)];  // (L-2, c) -> (L-1, c)
+  }
+}
+
+// local count of the sweep (slots) -> h.count[0]; time-limit vote -> h.count[1]
+static __global__ void __launch_bounds__(kSlots) k_part_count(Ctl* c, PartHalo h) {
+  unsigned long long v = c->acc[threadIdx.x].count;
+  __shared__ unsigned long long sh[kSlots / 32];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kSlots / 32; ++w) t += sh[w];
+    h.count[0] = t;
+    h.count[1] = (globaltimer_ns() - c->t0_ns >= c->vote_limit_ns) ? 1ull : 0ull;
+  }
+}
+
+static __global__ void k_part_unpack(DevGraph g, float* buf0, float* buf1, const Ctl* ctl, PartHalo h) {
+  float* B = (ctl->sweeps & 1ull) ? buf0 : buf1;
+  const uint32_t C = g.lat_cols, L = g.lat_rows;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    if (h.ghost_up) B[2u * lat_edge_down(0u, c, C)] = h.recv_up[c];               // (0, c) -> (1, c)
+    if (h.ghost_down) B[2u * lat_edge_down(L - 2u, c, C) + 1u] = h.recv_down[c];  // (L-1, c) -> (L-2, c)
+  }
+}
+
 // <<<1, kSlots>>>
-static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D) {
+// ext (row-band partition): {global unconverged count, time-limit votes},
+// all-reduced over the ranks, replaces the local count and the local clock so
+// every rank takes the same stop decision.
+static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D,
+                                                          const unsigned long long* ext = nullptr) {
   if (run_done(c)) return;
   const int t = threadIdx.x;
   const Accum a = c->acc[t];
@@ -240,7 +290,8 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
     for (int w = 0; w < kSlots / 32; ++w) v[k] += sh[k][w];
   }
   const long long delta = static_cast<long long>(v[0]);
-  const unsigned long long count = v[1], frontier = v[2] + c->frontier;
+  const unsigned long long count = ext ? ext[0] : v[1], frontier = v[2] + c->frontier;
+  if (ext && ext[1]) c->time_limit_ns = 0;  // some rank hit the time limit: stop everywhere
   c->evals_total += v[4];
   c->vertex_visits += v[5];
   switch (mode) {
@@ -554,6 +605,7 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       const uint32_t c = c0 + k * kBlock;
       const uint32_t dn = c + 1u < C ? 1u : 0u;
       const bool hu = act[k] && !first, hl = act[k] && c > 0u, hr = act[k] && dn, hd = act[k] && !last;
+      const bool owned = r >= g.cnt_row0 && r < g.cnt_row1;  // ghost rows of a band: computed, not counted
       // incoming: up (2eU, .x), left (2eL, .x), right (2eR+1, .y), down (2eD+1, .y); absent ones hold 0
       const float T = un[k] + pU[k].x + pL[k].x + pR[k].y + pD[k].y;
       // all four messages are computed (predicated stores, no divergence at the borders)
@@ -573,7 +625,7 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       if (hr) B[orr] = lr;
       if (hd) B[od] = ld;
       auto track = [&](bool has, uint32_t out, float r_msg) {
-        const int now = has && r_msg >= eps;
+        const int now = has && owned && r_msg >= eps;
         if (MODE == kModeDelta) {
           if (has) {
             cnt += now - (res[out] >= eps);
@@ -593,8 +645,8 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       track(hr, orr, rr);
       track(hd, od, rd);
       const uint32_t deg = (hu ? 1u : 0u) + (hl ? 1u : 0u) + (hr ? 1u : 0u) + (hd ? 1u : 0u);
-      evals += deg;
-      visits += act[k] ? 1u : 0u;
+      evals += owned ? deg : 0u;
+      visits += act[k] && owned ? 1u : 0u;
     }
   }
   if (bad) *nf = 1u;

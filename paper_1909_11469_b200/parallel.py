@@ -1,0 +1,209 @@
+"""Row-band partition of a lattice across GPUs.
+
+One process per GPU.  Rank g owns rows [g*n/P, (g+1)*n/P) of the
+generate_ising(n, c, seed) grid (generators.cpp:24-50) and every message whose
+source it owns; its band adds one ghost row per neighbouring band.  One LBP
+iteration (schedulers.cpp:301-347 with the LBP frontier) is
+
+    bp_band_lbp_sweep    sweep of the band on the device; boundary messages
+                         -> send_up / send_down; local unconverged count and
+                         time-limit vote -> count[0..1]
+    exchange             send_up -> rank g-1 (its recv_down), send_down ->
+                         rank g+1 (its recv_up); all-reduce(sum) of count
+    bp_band_lbp_finish   ghost messages <- recv_*; the loop control of run()
+                         on the GLOBAL count
+
+all enqueued on the band's own CUDA stream (torch.cuda.ExternalStream), so
+there is no host synchronisation inside the loop; the host polls the stop flag
+every `check_every` iterations (iterations after a stop are no-ops on the
+device).  Owned messages are bitwise identical to the unpartitioned run, so
+results do not depend on the GPU count (the determinism contract of
+thread_pool.hpp:13-16, restated for GPUs).
+
+The transport is torch.distributed: NCCL over NVLink between GPUs, gloo on
+CPU for the host-logic tests (tests/test_parallel_cpu.py), or `LocalExchange`
+for several bands inside one process on one device (parity tests).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import (_Config, _DevOpts, _Result, _check, _lib, GRAPH_TRUSTED, PairwiseMRF, SchedulerConfig,
+               SchedulerKind)
+
+__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "NcclExchange", "LocalExchange",
+           "run_band_lbp"]
+
+
+def band_rows(n: int, part: int, nparts: int):
+    """Owned rows [r0, r1) and ghost flags of band `part` (mirrors bp_graph_generate_ising_band)."""
+    if nparts < 1 or not 0 <= part < nparts or nparts > n:
+        raise ValueError("bad band partition")
+    r0, r1 = part * n // nparts, (part + 1) * n // nparts
+    return r0, r1, int(part > 0), int(part + 1 < nparts)
+
+
+def owned_directed_edges(n: int, r0: int, r1: int) -> int:
+    """Directed edges whose source lies in rows [r0, r1) of an n x n grid (sum of degrees)."""
+    return sum(n * ((r > 0) + (r + 1 < n)) + 2 * (n - 1) for r in range(r0, r1))
+
+
+class _BandInfoC(C.Structure):
+    _fields_ = [("part", C.c_uint32), ("nparts", C.c_uint32), ("row0", C.c_uint32), ("row1", C.c_uint32),
+                ("ghost_up", C.c_uint32), ("ghost_down", C.c_uint32), ("local_rows", C.c_uint32),
+                ("cols", C.c_uint32), ("owned_directed", C.c_uint64)]
+
+
+class _HaloC(C.Structure):
+    _fields_ = [("send_up", C.c_void_p), ("send_down", C.c_void_p), ("recv_up", C.c_void_p),
+                ("recv_down", C.c_void_p), ("count", C.c_void_p)]
+
+
+@dataclass
+class BandInfo:
+    part: int
+    nparts: int
+    row0: int
+    row1: int
+    ghost_up: int
+    ghost_down: int
+    local_rows: int
+    cols: int
+    owned_directed: int
+
+
+@dataclass
+class BandStatus:
+    stopped: bool
+    converged: bool
+    iterations: int
+    messages_updated_total: int  # this band's owned messages
+    gpu_launches: int
+
+
+class BandLBP:
+    """LBP on one band of the n x n Ising grid, on cuda:`device`."""
+
+    def __init__(self, n: int, c: float, seed: int, part: int, nparts: int, config: SchedulerConfig,
+                 device: int = 0):
+        import torch
+
+        if config.kind != SchedulerKind.lbp:
+            raise ValueError("row-band partition: LBP only")
+        info = _BandInfoC()
+        h = C.c_void_p()
+        _check(_lib.bp_graph_generate_ising_band(n, c, seed, part, nparts, C.byref(_DevOpts(device, GRAPH_TRUSTED)),
+                                                 C.byref(h), C.byref(info)))
+        self.graph = PairwiseMRF(h, None)
+        self.info = BandInfo(*(getattr(info, f) for f, _ in _BandInfoC._fields_))
+        dev = torch.device("cuda", device)
+        cols = self.info.cols
+        self.send_up = torch.zeros(cols, dtype=torch.float32, device=dev)
+        self.send_down = torch.zeros(cols, dtype=torch.float32, device=dev)
+        self.recv_up = torch.zeros(cols, dtype=torch.float32, device=dev)
+        self.recv_down = torch.zeros(cols, dtype=torch.float32, device=dev)
+        self.count = torch.zeros(2, dtype=torch.int64, device=dev)
+        halo = _HaloC(self.send_up.data_ptr(), self.send_down.data_ptr(), self.recv_up.data_ptr(),
+                      self.recv_down.data_ptr(), self.count.data_ptr())
+        self._cfg = config._c()
+        e = C.c_void_p()
+        torch.cuda.synchronize(dev)  # buffers initialised before the engine's stream uses them
+        _check(_lib.bp_band_engine_create(self.graph._h, C.byref(self._cfg), C.byref(info), C.byref(halo),
+                                          C.byref(e)))
+        self._e = e
+        s = C.c_uint64()
+        _check(_lib.bp_band_stream(e, C.byref(s)))
+        self.stream = torch.cuda.ExternalStream(s.value, device=dev)
+
+    def __del__(self):
+        e = getattr(self, "_e", None)
+        if e:
+            _lib.bp_engine_destroy(e)
+            self._e = None
+
+    def sweep(self):
+        _check(_lib.bp_band_lbp_sweep(self._e))
+
+    def finish(self):
+        _check(_lib.bp_band_lbp_finish(self._e))
+
+    def beliefs(self):
+        """Beliefs of every band vertex (ghost rows included) from the current messages."""
+        import numpy as np
+
+        out = np.zeros(2 * self.graph.num_vertices())
+        _check(_lib.bp_engine_beliefs(self._e, out.ctypes.data_as(C.c_void_p)))
+        return out.reshape(self.info.local_rows, self.info.cols, 2)
+
+    def owned_beliefs(self):
+        g = self.info.ghost_up
+        return self.beliefs()[g:g + self.info.row1 - self.info.row0]
+
+    def status(self) -> BandStatus:
+        r = _Result()
+        _check(_lib.bp_band_status(self._e, C.byref(r)))
+        return BandStatus(bool(r.stopped), bool(r.converged), int(r.iterations), int(r.messages_updated_total),
+                          int(r.gpu_launches))
+
+
+class NcclExchange:
+    """Halo exchange + count all-reduce through torch.distributed (NCCL on GPUs),
+    enqueued on the band's stream."""
+
+    def __init__(self, rank: int, world: int):
+        self.rank, self.world = rank, world
+
+    def __call__(self, band: BandLBP):
+        import torch.distributed as dist
+
+        ops = []
+        if band.info.ghost_up:
+            ops += [dist.P2POp(dist.isend, band.send_up, self.rank - 1),
+                    dist.P2POp(dist.irecv, band.recv_up, self.rank - 1)]
+        if band.info.ghost_down:
+            ops += [dist.P2POp(dist.isend, band.send_down, self.rank + 1),
+                    dist.P2POp(dist.irecv, band.recv_down, self.rank + 1)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        dist.all_reduce(band.count)
+
+
+class LocalExchange:
+    """All bands in one process (one device): the same data movement as
+    NcclExchange with device copies; host-synchronised (tests only)."""
+
+    def __init__(self, bands):
+        self.bands = bands
+
+    def exchange_all(self):
+        import torch
+
+        torch.cuda.synchronize()
+        bands = self.bands
+        for i, b in enumerate(bands):
+            if b.info.ghost_up:
+                b.recv_up.copy_(bands[i - 1].send_down)
+            if b.info.ghost_down:
+                b.recv_down.copy_(bands[i + 1].send_up)
+        total = sum(b.count.clone() for b in bands)
+        for b in bands:
+            b.count.copy_(total)
+        torch.cuda.synchronize()
+
+
+def run_band_lbp(band: BandLBP, exchange, max_iterations: int, check_every: int = 16) -> BandStatus:
+    """The run() loop of one band (all ranks call it with the same arguments)."""
+    import torch
+
+    with torch.cuda.stream(band.stream):
+        for it in range(max_iterations + 1):  # sweep 0 computes r(m_0) (ResidualTracker ctor)
+            band.sweep()
+            exchange(band)
+            band.finish()
+            if it % check_every == check_every - 1:
+                st = band.status()
+                if st.stopped:
+                    return st
+    return band.status()

@@ -1,0 +1,59 @@
+"""Row-band partition on one GPU: P bands in one process,
+halos moved by LocalExchange (the data movement NcclExchange does between
+GPUs).  Owned messages must be bitwise identical to the unpartitioned run for
+every P -- the GPU-count independence contract (thread_pool.hpp:13-16)."""
+import numpy as np
+import pytest
+
+from paper_1909_11469_b200 import parallel as par
+
+pytestmark = pytest.mark.gpu
+
+
+def _lockstep(bp, n, c, seed, nparts, iters, eps=1e-5):
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=iters, epsilon=eps)
+    bands = [par.BandLBP(n, c, seed, p, nparts, cfg, 0) for p in range(nparts)]
+    ex = par.LocalExchange(bands)
+    for _ in range(iters + 1):
+        for b in bands:
+            b.sweep()
+        ex.exchange_all()
+        for b in bands:
+            b.finish()
+    return bands, [b.status() for b in bands]
+
+
+@pytest.mark.parametrize("nparts", [2, 3, 5])
+def test_band_lbp_bitwise_equals_unpartitioned(bp, nparts):
+    n, c, seed, iters = 23, 2.5, 3, 17
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)),
+                  bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=iters))
+    want = full.beliefs.values.reshape(n, n, 2)
+    bands, st = _lockstep(bp, n, c, seed, nparts, iters)
+    for b, s in zip(bands, st):
+        assert s.stopped and s.iterations == full.iterations == iters and s.converged == full.converged
+        got = b.owned_beliefs()
+        assert np.array_equal(got, want[b.info.row0:b.info.row1]), b.info
+    # every directed edge is owned (and counted) by exactly one band
+    assert sum(s.messages_updated_total for s in st) == full.messages_updated_total
+
+
+def test_band_lbp_converges_like_unpartitioned(bp):
+    n, c, seed = 30, 1.0, 8
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)),
+                  bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=500))
+    assert full.converged
+    bands, st = _lockstep(bp, n, c, seed, 4, full.iterations + 5)
+    for b, s in zip(bands, st):
+        assert s.converged and s.iterations == full.iterations
+        assert np.array_equal(b.owned_beliefs(), full.beliefs.values.reshape(n, n, 2)[b.info.row0:b.info.row1])
+
+
+def test_band_rows_cover_grid():
+    for n in (7, 16, 1000):
+        for p in (1, 2, 3, 7):
+            rows = [par.band_rows(n, k, p) for k in range(p)]
+            assert rows[0][0] == 0 and rows[-1][1] == n
+            assert all(rows[k][1] == rows[k + 1][0] for k in range(p - 1))
+            total = sum(par.owned_directed_edges(n, r0, r1) for r0, r1, _, _ in rows)
+            assert total == 4 * n * (n - 1)
