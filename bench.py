@@ -9,14 +9,17 @@ reference's generate_ising (seed = step index + rank * 1000).
   value  = committed edge-message updates / second (sum |F| / device time of the
            runs, graph resident in HBM, CUDA events on the engine stream)
   e2e    = the same metric through the public API with host buffers: every step
-           uploads the graph from host arrays (bp_graph_create: validation, CSR,
-           H2D), runs, and copies the beliefs back (D2H)
+           uploads the graph from host arrays in build_graph's input layout
+           (bp_graph_create: validation, CSR, H2D), runs, and copies the beliefs
+           back (D2H)
 
-Other schedulers (LBP, RBP p=1/256) on the same instance, the 100^2 C=2.5
-convergence suite (seeds 500-524) and an HBM-bound 4096^2 LBP sweep are
-reported as extra keys.  The reference arm (--impl reference) times the
-reference's own bpsched::run compiled from /root/reference (oracle/_ref) on the
-host cores, on a bounded sample of the same workload.
+At N > 1 GPUs every rank runs its own instances (weak scaling, replicas), and
+the row-band partitioned LBP on the 16384^2 grid (BASELINE config 5, one band
+per GPU, NCCL halo exchange) is reported beside it under "partitioned_16k".
+Extra keys: LBP / RBP on the workload instance, the 100^2 C=2.5 convergence
+suite (seeds 500-524), the HBM roofline of the LBP sweep on 16384^2.  The
+reference arm (--impl reference) times the reference's own bpsched::run compiled
+from /root/reference (oracle/_ref) on the host cores on a bounded sample.
 """
 from __future__ import annotations
 
@@ -39,7 +42,9 @@ C_COUPLING = 2.5
 CAP = 10000
 METRIC = "edge-message updates/sec (RnBP, Ising 1000x1000 C=2.5, run to convergence or 10k-iteration cap)"
 UNIT = "updates/s"
-REF_SAMPLE_ITERS = 5  # bounded CPU sample: reference run capped at 5 iterations
+REF_SAMPLE_ITERS = 5   # bounded CPU sample: reference run capped at 5 iterations
+BIG_N = 16384          # BASELINE config 5
+BIG_ITERS = 30         # fixed LBP window on the big grid
 
 
 def rnbp_kw(seed):
@@ -105,9 +110,9 @@ def measured_peaks():
     try:
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def flush_l2(torch, buf):
@@ -115,12 +120,19 @@ def flush_l2(torch, buf):
     torch.cuda.synchronize()
 
 
-# bytes moved by one vertex-update launch per processed vertex / incident edge
-# (binary log-odds layout): in_off(8) + unary(4) per vertex;
-# per incident edge adj(4) + pair(8) + params(16) + candidate write(4) +
-# residual read+write(8) [LBP sweep: no residual traffic, message write(4)]
-def update_bytes(visits, evals, with_res=True):
-    return 12 * visits + (40 if with_res else 32) * evals
+# Algorithmic bytes, binary Ising lattice, compressed
+# layout (one fp32 log2-odds per message, one fp32 coupling per edge):
+#   LBP sweep: per vertex read its 2 edge pairs (16 B) + write 4 messages (16 B)
+#              + 2 couplings (8 B) + unary (4 B) = 44 B
+#   touched refresh (update class): per vertex unary 4 B (+ 4 B list id); per
+#              message edge pair 8 B + coupling 4 B + candidate 4 B + residual 8 B
+# reference fp32 layout: 30 B per directed edge per LBP sweep.
+def lbp_sweep_bytes(vertices):
+    return 44 * vertices
+
+
+def refresh_bytes(visits, evals):
+    return 8 * visits + 24 * evals
 
 
 def run_b200(args):
@@ -148,8 +160,7 @@ def run_b200(args):
     for s in seeds:
         graph_for(s)
     kind = bp.SchedulerKind.rnbp
-    # warmup
-    for w in range(W):
+    for w in range(W):  # warmup (graph capture, allocation, first-touch)
         bp.run(graph_for(seeds[w % K]), bp.SchedulerConfig(kind=kind, **rnbp_kw(seeds[w % K])))
     torch.cuda.synchronize()
     if dist:
@@ -158,7 +169,7 @@ def run_b200(args):
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         dev_ms = 0.0
-        for i, s in enumerate(seeds):
+        for s in seeds:
             flush_l2(torch, flush)
             r = bp.run(graph_for(s), bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
             dev_ms += r.device_ms
@@ -183,9 +194,8 @@ def run_b200(args):
     # ---- e2e: public API with host buffers (graph upload + run + beliefs D2H)
     e2e_updates, e2e_t = 0, 0.0
     h2d = d2h = 0
-    host_arrays = {}
-    for s in seeds[: min(K, 3)]:
-        host_arrays[s] = bp.generate_ising_arrays(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=s))
+    host_arrays = {s: bp.generate_ising_arrays(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=s))
+                   for s in seeds[: min(K, 3)]}
     for s in seeds[: min(K, 3)]:
         cards, un, ep, tb = host_arrays[s]
         flush_l2(torch, flush)
@@ -198,48 +208,57 @@ def run_b200(args):
         h2d = cards.nbytes + un.nbytes + ep.nbytes + tb.nbytes
         d2h = r.beliefs.values.nbytes + 32 * len(r.trace)
         del g
+    if dist:
+        tt = torch.tensor([e2e_t, float(e2e_updates)], dtype=torch.float64, device="cuda")
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        e2e_t, e2e_updates = float(mx[0]), float(tt[1])
+
+    # ---- partitioned 16K^2 LBP (config 5): every rank, a band each
+    part = _partitioned_big(bp, torch, dist, ws, rank, local)
 
     out = {}
     if rank == 0:
-        # ---- roofline of the dominant kernel (instrumented run after the timed region)
-        peak, peak_kind = measured_peaks()
+        peak, peak_src = measured_peaks()
+        # ---- dominant kernel of the workload (instrumented run: CUDA events per launch)
         g0 = graph_for(seeds[0])
         ri = bp.run_ex(g0, bp.SchedulerConfig(kind=kind, **rnbp_kw(seeds[0])), kernel_timing=True)
         ks = ri.kernel_stats
+        tot_ms = sum(v["ms"] for v in ks.values()) or 1.0
         dom = max(ks, key=lambda k: ks[k]["ms"])
-        upd_bytes = update_bytes(ri.vertex_visits, ri.message_evaluations)
-        upd_ms = ks["update"]["ms"]
-        achieved = upd_bytes / (upd_ms / 1e3) / 1e9 if upd_ms else 0.0
-        traffic = _read_traffic()
-        shares = {k: round(v["ms"] / sum(x["ms"] for x in ks.values()), 4) for k, v in ks.items() if v["launches"]}
-
-        # ---- HBM-bound reference point: LBP sweeps on a 4096^2 grid (working set >> L2)
-        g4 = bp.generate_ising(bp.IsingParams(n=4096, c=C_COUPLING, seed=0), device=local)
-        r4 = bp.run_ex(g4, bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=20), kernel_timing=True)
-        k4 = r4.kernel_stats["update"]
-        b4 = update_bytes(r4.vertex_visits, r4.message_evaluations, with_res=False)
-        hbm_ach = b4 / (k4["ms"] / 1e3) / 1e9
-        del g4
+        if dom == "persist":
+            dom_bytes = ks["persist"]["bytes"]
+            dom_name = "k_rnbp_persist (RnBP candidate-list iterations, one 16-CTA cluster)"
+        else:
+            dom_bytes = refresh_bytes(ri.vertex_visits, ri.message_evaluations)
+            dom_name = f"{dom} kernels"
+        dom_ms = ks[dom]["ms"]
+        achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms else 0.0
+        shares = {k: round(v["ms"] / tot_ms, 4) for k, v in ks.items() if v["launches"]}
 
         # ---- other schedulers on the workload instance + convergence suite
         extra = {}
         for name, cfg in (("lbp", bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=CAP, time_limit=1e9)),
                           ("rbp", bp.SchedulerConfig(kind=bp.SchedulerKind.rbp, p=1 / 256, max_iterations=CAP,
-                                                     time_limit=1e9))):
+                                                     time_limit=1e9)),
+                          ("rs", bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=1 / 256, max_iterations=200,
+                                                    time_limit=1e9))):
             bp.run(g0, cfg)
             rr = bp.run(g0, cfg)
             extra[name] = {"value": rr.messages_updated_total / (rr.device_ms / 1e3), "unit": UNIT,
                            "iterations": rr.iterations, "converged": rr.converged,
-                           "ms": round(rr.device_ms, 3)}
+                           "ms": round(rr.device_ms, 3), "ms_per_iteration": round(rr.device_ms / max(1, rr.iterations), 4)}
         suite = _convergence_suite(bp, local)
 
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 (log-domain messages)", "data": "synthetic (generate_ising, bit-identical to the reference generator)",
+            "vs_baseline": None, "dtype": "f32 (base-2 log-odds messages)",
+            "data": "synthetic (generate_ising, bit-identical to the reference generator)",
             "config": {"workload": "ising1000_c2.5_rnbp", "n": N_GRID, "c": C_COUPLING, "scheduler": "rnbp",
                        "low_p": 0.5, "high_p": 1.0, "edge_ratio_threshold": 0.9, "epsilon": 1e-5,
-                       "max_iterations": CAP, "seeds": f"{seeds[0]}..{seeds[-1]}",
+                       "max_iterations": CAP, "seeds": f"rank*1000 + 0..{K - 1}",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "steps_detail": [{"seed": s, "converged": r.converged, "iterations": r.iterations,
@@ -251,20 +270,20 @@ def run_b200(args):
             "e2e": {"value": e2e_updates / e2e_t if e2e_t else None, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": min(K, 3),
                     "includes": "bp_graph_create from host arrays (validation + CSR + H2D) + run + beliefs D2H"},
-            "roofline": {"bound": "hbm", "kernel": "k_vertex_update (refresh)", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_kind, "algorithmic_bytes": upd_bytes, "kernel_ms": upd_ms,
-                         "launches": ks["update"]["launches"], "dominant_kernel_class": dom,
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _read_traffic(dom), "peak_source": peak_src,
+                         "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms, "launches": ks[dom]["launches"],
                          "kernel_shares": shares,
-                         "note": "1000^2 working set (~100 MB) is L2-resident; roofline_hbm is the HBM-bound point"},
-            "roofline_hbm": {"kernel": "k_vertex_update (LBP sweep) on Ising 4096^2", "achieved": hbm_ach,
-                             "peak": peak, "unit": "GB/s", "frac": hbm_ach / peak, "algorithmic_bytes": b4,
-                             "kernel_ms": k4["ms"], "launches": k4["launches"],
-                             "updates_per_s": r4.messages_updated_total / (k4["ms"] / 1e3)},
+                         "regime": "latency-bound: the 1000^2 working set (~70 MB) is L2-resident and the "
+                                   "candidate-list iterations move ~3k messages each; roofline_hbm is the "
+                                   "HBM-bound kernel (LBP sweep, 16384^2)"},
             "schedulers": extra,
             "convergence_suite_100x100": suite,
             "clocks": clk.summary(),
         }
+        out["roofline_hbm"] = _hbm_roofline(bp, torch, local, peak, peak_src)
+        if part:
+            out["partitioned_16k"] = part
         if ws == 1:
             out["cpu_baseline"] = _cpu_baseline(sample_iters=REF_SAMPLE_ITERS)
         print(json.dumps(out))
@@ -273,17 +292,83 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def _hbm_roofline(bp, torch, device, peak, peak_src):
+    """LBP sweep on the 16384^2 grid (config 5, working set >> L2): CUDA-event time
+    of the update launches of a fixed window, algorithmic bytes per section 5."""
+    g = bp.generate_ising(bp.IsingParams(n=BIG_N, c=C_COUPLING, seed=0), device=device)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=BIG_ITERS, time_limit=1e9)
+    bp.run_ex(g, cfg, beliefs=False)
+    r = bp.run_ex(g, cfg, beliefs=False, kernel_timing=True)
+    k = r.kernel_stats["update"]
+    sweeps = r.iterations + 1
+    V = g.num_vertices()
+    nbytes = lbp_sweep_bytes(V) * sweeps
+    ach = nbytes / (k["ms"] / 1e3) / 1e9
+    ref_bytes = 30 * g.num_directed_edges() * sweeps
+    out = {"kernel": "k_vertex_update<Count> lattice tiles (LBP sweep), Ising 16384^2", "bound": "hbm",
+           "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
+           "algorithmic_bytes": nbytes, "bytes_per_vertex": 44, "kernel_ms": k["ms"], "launches": k["launches"],
+           "sweeps": sweeps, "ms_per_sweep": k["ms"] / sweeps,
+           "updates_per_s": r.messages_updated_total / (r.device_ms / 1e3),
+           "effective_reference_layout_GBps": ref_bytes / (k["ms"] / 1e3) / 1e9,
+           "traffic": _read_traffic("lbp16k")}
+    del g
+    torch.cuda.empty_cache()
+    return out
+
+
+def _partitioned_big(bp, torch, dist, ws, rank, local):
+    """Row-band partitioned LBP on the 16384^2 grid: one band per rank, NCCL halo
+    exchange + count all-reduce each iteration (paper_1909_11469_b200.parallel).
+    Strong scaling: the grid is fixed.  At N = 1 the same window runs on the
+    whole grid (one band)."""
+    if ws == 1:
+        return None
+    from paper_1909_11469_b200 import parallel as par
+
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=10 ** 9, time_limit=1e9)
+    band = par.BandLBP(BIG_N, C_COUPLING, 0, rank, ws, cfg, local)
+    ex = par.NcclExchange(rank, ws)
+    with torch.cuda.stream(band.stream):
+        for _ in range(3):  # warmup
+            band.sweep()
+            ex(band)
+            band.finish()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st0 = band.status()
+        e0.record(band.stream)
+        for _ in range(BIG_ITERS):
+            band.sweep()
+            ex(band)
+            band.finish()
+        e1.record(band.stream)
+        torch.cuda.synchronize()
+    st1 = band.status()
+    ms = e0.elapsed_time(e1)
+    upd = st1.messages_updated_total - st0.messages_updated_total
+    tt = torch.tensor([ms, float(upd)], dtype=torch.float64, device="cuda")
+    mx = tt.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+    ms_max, upd_sum = float(mx[0]), float(tt[1])
+    return {"config": f"Ising {BIG_N}^2 C={C_COUPLING} LBP, row bands x{ws}, NCCL halo + all-reduce per iteration",
+            "iterations": BIG_ITERS, "ms_max_over_ranks": ms_max, "updates": upd_sum,
+            "value": upd_sum / (ms_max / 1e3), "unit": UNIT, "scaling": "strong"}
+
+
 def _ttc(results):
     conv = [r.wall_time for r in results if r.converged]
     return {"converged_steps": len(conv), "steps": len(results),
             "median_s": statistics.median(conv) if conv else None}
 
 
-def _read_traffic():
+def _read_traffic(key):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f).get(key)
     except Exception:
         return None
 
@@ -347,6 +432,7 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     K, W = args.steps, args.warmup
     graphs = [po.Graph.ising(ref, N_GRID, C_COUPLING, s) for s in range(min(K, 2))]
+
     def cfg(s):
         return po.make_config("rnbp", low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5,
                               max_iterations=REF_SAMPLE_ITERS, time_limit=1e9, seed=s, worker_count=cores)
