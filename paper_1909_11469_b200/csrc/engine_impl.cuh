@@ -16,6 +16,7 @@
 #include "kernels.cuh"
 #include "kernels_rs.cuh"
 #include "kernels_persist.cuh"
+#include "kernels_lbp.cuh"
 
 namespace bpb {
 namespace {
@@ -481,6 +482,33 @@ class EngineT final : public EngineBase {
     return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(want, static_cast<size_t>(std::max(per, 1)) * sm_count())));
   }
 
+  // one LBP sweep (ping-pong): the SMEM-staged lattice kernel for binary Ising
+  // lattices, the vertex-centric kernel otherwise
+  unsigned lbp_grid_ = 0;
+  void enqueue_lbp_sweep() {
+    if (QS == 1 && g_.lat_cols && g_.par_mode == 1 && g_.lat_rows >= 2) {
+      if (!lbp_grid_) {
+        cuda_check(cudaFuncSetAttribute(k_lbp_lattice, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(LbpSmem))),
+                   "smem attribute");
+        int per = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lbp_lattice, kBlock, sizeof(LbpSmem)),
+                   "occupancy");
+        lbp_grid_ = static_cast<unsigned>(std::max(1, per) * sm_count());
+      }
+      timed(kKUpdate, [&] {
+        k_lbp_lattice<<<lbp_grid_, kBlock, sizeof(LbpSmem), s_>>>(dg_, live(), cand(), ctl(), eps_);
+      });
+    } else {
+      timed(kKUpdate, [&] {
+        k_vertex_update<QS, kModeCount, false, true, false>
+            <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(
+                dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+      });
+    }
+    launch_check();
+  }
+
   // ---- launch sequences
   void enqueue_finalize(int mode, uint32_t D = 0xFFFFFFFFu, const unsigned long long* ext = nullptr) {
     const uint32_t d = D == 0xFFFFFFFFu ? g_.D : D;
@@ -517,14 +545,12 @@ class EngineT final : public EngineBase {
       ++launches_;
       band_started_ = true;
     }
-    k_vertex_update<QS, kModeCount, false, true, false>
-        <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(
-            dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+    enqueue_lbp_sweep();
     const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
     k_part_pack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
     k_part_count<<<1, kSlots, 0, s_>>>(ctl(), halo_);
     launch_check();
-    launches_ += 3;
+    launches_ += 2;
   }
   void band_finish() override {
     const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
@@ -553,11 +579,7 @@ class EngineT final : public EngineBase {
     launch_check();
     const unsigned gv = grid_cap(g_.V);
     if (lbp) {  // sweep 0 (ResidualTracker ctor, residuals.cpp:9-24)
-      timed(kKUpdate, [&] {
-        k_vertex_update<QS, kModeCount, false, true, false>
-            <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
-      });
-      launch_check();
+      enqueue_lbp_sweep();
       enqueue_finalize(kFinLbp);
     } else {
       timed(kKUpdate, [&] {
@@ -641,16 +663,10 @@ class EngineT final : public EngineBase {
   // one iteration of the loop body (schedulers.cpp:311-346) for the configured scheduler
   void enqueue_iteration() {
     switch (cfg_.kind) {
-      case BP_LBP: {
-        const unsigned gv = grid_cap(g_.V);
-        timed(kKUpdate, [&] {
-          k_vertex_update<QS, kModeCount, false, true, false>
-              <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
-        });
-        launch_check();
+      case BP_LBP:
+        enqueue_lbp_sweep();
         enqueue_finalize(kFinLbp);
         break;
-      }
       case BP_RNBP: {
         timed(kKSelect, [&] {
           if (use_clist_)

@@ -26,7 +26,9 @@ void DevBuf::reset() {
 void DevBuf::alloc(size_t n) {
   reset();
   if (n == 0) n = 16;
-  cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+  // 64 bytes of slack: 16-byte-granular bulk copies (kernels_lbp.cuh) may read
+  // up to one granule past the end of an array
+  cuda_check(cudaMalloc(&p, n + 64), "cudaMalloc");
   bytes = n;
 }
 void DevBuf::upload(const void* src, size_t n) {
