@@ -248,6 +248,35 @@ BP_API int bp_band_lbp_sweep(struct bp_engine* e);
 BP_API int bp_band_lbp_finish(struct bp_engine* e);
 BP_API int bp_band_status(struct bp_engine* e, bp_run_result* result); /* synchronises */
 
+/* RnBP on a band (same row partition; count[] holds 5 values: {delta,
+ * frontier, survivors, time vote, initial count}).  Per iteration, on
+ * bp_band_stream():
+ *   bp_band_rnbp_select(e, 0)  rnbp_frontier attempt 0 over the owned edges
+ *                              (Philox keyed by GLOBAL edge ids) + Jacobi
+ *                              commit; boundary messages -> send_*
+ *   (exchange)                 halos as for LBP
+ *   bp_band_rnbp_refresh       ghost messages <- recv_* (a changed one flags
+ *                              the owned vertex it flows into), touched
+ *                              refresh, sums -> count[0..4]
+ *   (all-reduce count)
+ *   if the global frontier is 0 and survivors exist (schedulers.cpp:204-214):
+ *     select(e, 1) + exchange + refresh + all-reduce; still 0 -> every rank
+ *     lists its survivors (bp_band_survivors), the survivor of global rank
+ *     min(S-1, floor(u S)) in ascending global id (u = bp_philox_u53(seed,
+ *     iteration, 2, 0) * 2^-53) is committed by its owner
+ *     (bp_band_rnbp_fallback; the others pass UINT64_MAX) + exchange +
+ *     refresh + all-reduce
+ *   bp_band_rnbp_finish        loop control on the global sums
+ * before the loop: bp_band_rnbp_begin + all-reduce + bp_band_rnbp_finish_init. */
+BP_API int bp_band_rnbp_begin(struct bp_engine* e);
+BP_API int bp_band_rnbp_finish_init(struct bp_engine* e);
+BP_API int bp_band_rnbp_select(struct bp_engine* e, uint32_t attempt);
+BP_API int bp_band_rnbp_refresh(struct bp_engine* e);
+BP_API int bp_band_rnbp_finish(struct bp_engine* e);
+BP_API int bp_band_survivors(struct bp_engine* e, uint64_t* global_ids, uint64_t cap, uint64_t* n);
+BP_API int bp_band_rnbp_fallback(struct bp_engine* e, uint64_t global_d);
+BP_API uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t d);
+
 #ifdef __cplusplus
 }
 #endif

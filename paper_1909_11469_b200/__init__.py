@@ -170,6 +170,14 @@ def _load():
         "bp_band_lbp_sweep": (C.c_int, [P]),
         "bp_band_lbp_finish": (C.c_int, [P]),
         "bp_band_status": (C.c_int, [P, C.POINTER(_Result)]),
+        "bp_band_rnbp_begin": (C.c_int, [P]),
+        "bp_band_rnbp_finish_init": (C.c_int, [P]),
+        "bp_band_rnbp_select": (C.c_int, [P, C.c_uint32]),
+        "bp_band_rnbp_refresh": (C.c_int, [P]),
+        "bp_band_rnbp_finish": (C.c_int, [P]),
+        "bp_band_survivors": (C.c_int, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
+        "bp_band_rnbp_fallback": (C.c_int, [P, C.c_uint64]),
+        "bp_philox_u53": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -47,6 +47,7 @@ struct DevGraph {
   uint32_t par_mode;
   uint32_t uniform_q;                     // all cardinalities equal (0 = mixed)
   uint32_t cnt_row0, cnt_row1;            // lattice rows whose messages are owned (row-band partition)
+  unsigned long long edge_offset;         // global id of local edge 0 (band: RnBP draws use global ids)
   const float* __restrict__ ising_a;      // E  (binary, par_mode 1): a = e^J of the table {a, 1/a, 1/a, a}
   const float* __restrict__ pw;           // E  (generic, par_mode 1)
 };
@@ -192,7 +193,8 @@ struct PartHalo {
   float* send_down;           // C: down messages of the last owned row (to the band below)
   const float* recv_up;       // C: the band above's send_down
   const float* recv_down;     // C: the band below's send_up
-  unsigned long long* count;  // [0] local unconverged count, [1] local time-limit vote (all-reduced in place)
+  unsigned long long* count;  // LBP: [0] unconverged count, [1] time vote.  RnBP: [0] delta, [1] frontier,
+                              // [2] survivors, [3] time vote, [4] init count.  All-reduced (sum) in place
   uint32_t ghost_up, ghost_down;
 };
 
@@ -345,16 +347,25 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
   return ctr;
 }
 
-// 53-bit uniform integer; u = value * 2^-53 in [0, 1) like uniform_unit (rng.hpp:11-13).
-__device__ __forceinline__ unsigned long long philox_u53(unsigned long long seed,
-                                                         unsigned long long iteration,
-                                                         unsigned attempt, unsigned long long d) {
-  const uint4 ctr = make_uint4(static_cast<uint32_t>(d), static_cast<uint32_t>(d >> 32),
+// One Philox block serves the two directions of undirected edge e = d >> 1:
+// 64 bits each, the top 53 give u = value * 2^-53 in [0, 1) like
+// uniform_unit (rng.hpp:11-13).  Counter = (e, iteration, attempt), key = seed.
+__device__ __forceinline__ uint4 philox_edge(unsigned long long seed, unsigned long long iteration,
+                                             unsigned attempt, unsigned long long e) {
+  const uint4 ctr = make_uint4(static_cast<uint32_t>(e), static_cast<uint32_t>(e >> 32),
                                static_cast<uint32_t>(iteration),
                                (static_cast<uint32_t>(iteration >> 32) & 0x3FFFFFFFu) | (attempt << 30));
   const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
-  const uint4 r = philox4x32_10(ctr, key);
-  return ((static_cast<unsigned long long>(r.x) << 32) | r.y) >> 11;
+  return philox4x32_10(ctr, key);
+}
+__device__ __forceinline__ unsigned long long u53_of(const uint4& r, unsigned long long d) {
+  return (d & 1ull) ? (((static_cast<unsigned long long>(r.z) << 32) | r.w) >> 11)
+                    : (((static_cast<unsigned long long>(r.x) << 32) | r.y) >> 11);
+}
+__device__ __forceinline__ unsigned long long philox_u53(unsigned long long seed,
+                                                         unsigned long long iteration,
+                                                         unsigned attempt, unsigned long long d) {
+  return u53_of(philox_edge(seed, iteration, attempt, d >> 1), d);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/bp_cuda.h): exceptions -> bp_status codes,
 // message kept per thread (errors.hpp:10-38 -> return codes).
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -232,6 +233,7 @@ int bp_graph_generate_ising_band(uint32_t n, double c, uint64_t seed, uint32_t p
     for (uint32_t r = r0; r < r1; ++r)
       owned += static_cast<uint64_t>(n) * ((r > 0) + (r + 1 < n)) + 2ull * (n - 1);
     g->owned_directed = owned;
+    g->edge_offset = static_cast<uint64_t>(r0 - gu) * (2ull * n - 1ull);
     *info = bp_band_info{part, nparts, r0, r1, gu, gd, r1 + gd - (r0 - gu), n, owned};
     wrap_graph(std::move(g), out);
   });
@@ -271,6 +273,68 @@ int bp_band_lbp_finish(bp_engine* e) {
 int bp_band_status(bp_engine* e, bp_run_result* r) {
   if (!e || !r) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] { e->e->band_status(r); });
+}
+
+int bp_band_rnbp_begin(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_rnbp_begin(); });
+}
+int bp_band_rnbp_finish_init(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_rnbp_finish_init(); });
+}
+int bp_band_rnbp_select(bp_engine* e, uint32_t attempt) {
+  if (!e || attempt > 1) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_rnbp_select(attempt); });
+}
+int bp_band_rnbp_refresh(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_rnbp_refresh(); });
+}
+int bp_band_rnbp_finish(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_rnbp_finish(); });
+}
+int bp_band_survivors(bp_engine* e, uint64_t* ids, uint64_t cap, uint64_t* n) {
+  if (!e || !n || (cap && !ids)) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    std::vector<uint64_t> v;
+    e->e->band_survivors(v);
+    *n = v.size();
+    std::memcpy(ids, v.data(), std::min<uint64_t>(cap, v.size()) * 8);
+  });
+}
+int bp_band_rnbp_fallback(bp_engine* e, uint64_t gd) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    e->e->band_commit_global(gd);
+    e->e->band_rnbp_pack();
+  });
+}
+
+// Philox4x32-10 draw of the device (bp_device.cuh philox_u53), for host-side
+// decisions that must match the device stream (the band fallback).
+uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t d) {
+  const uint64_t e = d >> 1;
+  uint32_t c0 = static_cast<uint32_t>(e), c1 = static_cast<uint32_t>(e >> 32), c2 = static_cast<uint32_t>(iteration),
+           c3 = (static_cast<uint32_t>(iteration >> 32) & 0x3FFFFFFFu) | (attempt << 30);
+  uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0, p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
+    const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
+    const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0;
+    c1 = n1;
+    c2 = n2;
+    c3 = n3;
+    if (r < 9) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+  }
+  const uint64_t hi = (d & 1ull) ? c2 : c0, lo = (d & 1ull) ? c3 : c1;
+  return ((hi << 32) | lo) >> 11;
 }
 
 int bp_engine_step(bp_engine* e, uint64_t* frontier_size) {

@@ -32,6 +32,17 @@ class EngineBase {
   virtual uint64_t step() = 0;
   // row-band partition (bp_band_*): LBP on a lattice band with ghost rows
   virtual void band_config(const PartHalo& h, uint64_t owned_directed) = 0;
+  // RnBP on a band: begin = init + first refresh; select (attempt 0/1) =
+  // rnbp_frontier + commit + pack; refresh = unpack (+ flags) + touched refresh
+  // + sums; finish = loop control on the all-reduced sums
+  virtual void band_rnbp_begin() = 0;
+  virtual void band_rnbp_finish_init() = 0;
+  virtual void band_rnbp_select(unsigned attempt) = 0;
+  virtual void band_rnbp_refresh() = 0;
+  virtual void band_rnbp_finish() = 0;
+  virtual void band_survivors(std::vector<uint64_t>& global_ids) = 0;
+  virtual void band_commit_global(uint64_t global_d) = 0;  // UINT64_MAX: nothing to commit here
+  virtual void band_rnbp_pack() = 0;
   virtual void band_sweep() = 0;
   virtual void band_finish() = 0;
   virtual void band_status(bp_run_result* r) = 0;

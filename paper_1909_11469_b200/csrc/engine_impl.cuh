@@ -87,6 +87,7 @@ class EngineT final : public EngineBase {
     prm_.thr = cfg.edge_ratio_threshold;
     prm_.fixed_p = -1.0;
     prm_.commit = 1;
+    prm_.attempt = 0;
   }
 
   ~EngineT() override {
@@ -189,7 +190,7 @@ class EngineT final : public EngineBase {
     std::vector<float> raw(static_cast<size_t>(g_.D) * QS);
     // band engines ping-pong like run()'s LBP: m_t lives in buf[t & 1]
     bool flip = false;
-    if (band_started_) {
+    if (band_started_ && cfg_.kind == BP_LBP) {
       fetch_ctl_header();
       flip = (hctl_->iteration & 1ull) != 0;
     }
@@ -216,7 +217,7 @@ class EngineT final : public EngineBase {
   void beliefs(double* out) override {
     const size_t nb = g_.unary_size();
     ensure_beliefs_buf(nb);
-    enqueue_beliefs(bel_.as<double>(), band_started_);
+    enqueue_beliefs(bel_.as<double>(), band_started_ && cfg_.kind == BP_LBP);
     cuda_check(cudaMemcpyAsync(out, bel_.p, nb * 8, cudaMemcpyDeviceToHost, s_), "d2h");
     sync();
   }
@@ -525,7 +526,8 @@ class EngineT final : public EngineBase {
   void band_config(const PartHalo& h, uint64_t owned_directed) override {
     if (QS != 1 || !g_.lat_cols || g_.par_mode != 1)
       throw Error(BP_ERR_UNSUPPORTED, "row-band partition needs a binary Ising lattice band");
-    if (cfg_.kind != BP_LBP) throw Error(BP_ERR_UNSUPPORTED, "row-band partition: LBP only in this build");
+    if (cfg_.kind != BP_LBP && cfg_.kind != BP_RNBP)
+      throw Error(BP_ERR_UNSUPPORTED, "row-band partition: LBP and RnBP");
     halo_ = h;
     halo_.ghost_up = g_.cnt_row0 > 0 ? 1u : 0u;
     halo_.ghost_down = g_.cnt_row1 < g_.lat_rows ? 1u : 0u;
@@ -533,16 +535,9 @@ class EngineT final : public EngineBase {
     band_started_ = false;
   }
   void band_sweep() override {
+    if (cfg_.kind != BP_LBP) throw_invalid("band_lbp_* on a non-LBP engine");
     if (!band_started_) {
-      reset_ctl(cfg_.max_iterations, 1e300);  // the local clock never stops a band alone
-      const double ns = cfg_.time_limit * 1e9;
-      const unsigned long long lim = ns >= 1.8e19 ? ~0ull : static_cast<unsigned long long>(ns);
-      cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, vote_limit_ns), &lim, 8,
-                                 cudaMemcpyHostToDevice, s_), "ctl h2d");
-      const unsigned gi = grid_cap(static_cast<size_t>(g_.D) * QS);
-      k_init_messages<QS><<<gi, kBlock, 0, s_>>>(dg_, live(), ctl(), 1);
-      launch_check();
-      ++launches_;
+      band_start_common();
       band_started_ = true;
     }
     enqueue_lbp_sweep();
@@ -559,6 +554,80 @@ class EngineT final : public EngineBase {
     ++launches_;
     enqueue_finalize(kFinLbp, static_cast<uint32_t>(band_owned_), halo_.count);
   }
+  void band_start_common() {
+    reset_ctl(cfg_.max_iterations, 1e300);  // the local clock never stops a band alone
+    const double ns = cfg_.time_limit * 1e9;
+    const unsigned long long lim = ns >= 1.8e19 ? ~0ull : static_cast<unsigned long long>(ns);
+    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, vote_limit_ns), &lim, 8,
+                               cudaMemcpyHostToDevice, s_), "ctl h2d");
+    const unsigned gi = grid_cap(static_cast<size_t>(g_.D) * QS);
+    k_init_messages<QS><<<gi, kBlock, 0, s_>>>(dg_, live(), ctl(), 1);
+    launch_check();
+    ++launches_;
+  }
+  unsigned band_cols_grid() const { return static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock); }
+  void band_rnbp_begin() override {
+    if (cfg_.kind != BP_RNBP) throw_invalid("band_rnbp_* on a non-RnBP engine");
+    band_start_common();
+    k_vertex_update<QS, kModeInit, false, false, false>
+        <<<vgrid(k_vertex_update<QS, kModeInit, false, false, false>, g_.V), kBlock, 0, s_>>>(
+            dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
+    k_part_count_rnbp<<<1, kSlots, 0, s_>>>(ctl(), halo_);
+    launch_check();
+    launches_ += 2;
+  }
+  void band_rnbp_finish_init() override { enqueue_finalize(kFinInitExt, g_.D, halo_.count); }
+  void band_rnbp_select(unsigned attempt) override {
+    RnbpParams q = prm_;
+    q.attempt = attempt;
+    k_rnbp_select<QS, false><<<grid_cap(g_.D / 4 + 1), kBlock, 0, s_>>>(
+        dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), nullptr, ctl(), eps_, q,
+        cand_list());
+    k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
+    launch_check();
+    launches_ += 2;
+  }
+  void band_rnbp_refresh() override {
+    k_part_unpack_flag<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), ctl(), vflag_.as<uint32_t>(),
+                                                           vlist_.as<uint32_t>(), halo_);
+    k_vertex_update<QS, kModeDelta, true, false, false>
+        <<<vgrid(k_vertex_update<QS, kModeDelta, true, false, false>, g_.V), kBlock, 0, s_>>>(
+            dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
+            cand_list());
+    k_part_count_rnbp<<<1, kSlots, 0, s_>>>(ctl(), halo_);
+    launch_check();
+    launches_ += 3;
+  }
+  void band_rnbp_finish() override { enqueue_finalize(kFinIterExt, g_.D, halo_.count); }
+  // owned survivors (r >= eps) as GLOBAL directed ids, for the fallback of
+  // rnbp_frontier (schedulers.cpp:212-214) across bands
+  void band_survivors(std::vector<uint64_t>& out) override {
+    std::vector<float> r(g_.D);
+    sync();
+    if (g_.D) cuda_check(cudaMemcpy(r.data(), res_.p, 4ull * g_.D, cudaMemcpyDeviceToHost), "d2h");
+    out.clear();
+    for (uint32_t d = 0; d < g_.D; ++d)
+      if (r[d] >= eps_) out.push_back(d + 2ull * g_.edge_offset);
+  }
+  void band_rnbp_pack() override {
+    k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
+    launch_check();
+    ++launches_;
+  }
+  void band_commit_global(uint64_t gd) override {
+    if (gd == ~0ull) return;
+    const uint64_t d = gd - 2ull * g_.edge_offset;
+    if (gd < 2ull * g_.edge_offset || d >= g_.D) throw_invalid("edge not in this band");
+    const uint32_t d32 = static_cast<uint32_t>(d);
+    DevBuf list;
+    list.upload(&d32, 4);
+    k_commit_list<QS><<<1, kBlock, 0, s_>>>(dg_, list.as<uint32_t>(), 1, live(), cand(), res_.as<float>(),
+                                           vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), eps_, 0);
+    launch_check();
+    ++launches_;
+    sync();
+  }
+
   void band_status(bp_run_result* r) override {
     fetch_ctl_header();
     std::memset(r, 0, sizeof(*r));

@@ -57,6 +57,7 @@ DevGraph GraphImpl::dev() const {
   g.uniform_q = uniform_q;
   g.cnt_row0 = cnt_row0;
   g.cnt_row1 = cnt_row1;
+  g.edge_offset = edge_offset;
   g.ising_a = ising_a.as<float>();
   g.pw = pw.as<float>();
   return g;

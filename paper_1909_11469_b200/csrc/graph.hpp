@@ -50,6 +50,7 @@ struct GraphImpl {
   // [cnt_row0, cnt_row1); other rows are ghosts of the neighbouring bands
   uint32_t cnt_row0 = 0, cnt_row1 = 0xFFFFFFFFu;
   uint64_t owned_directed = 0;          // directed edges whose source is owned
+  uint64_t edge_offset = 0;             // global id of local edge 0
   std::vector<uint32_t> cards_host;  // mixed cardinalities only
 
   DevGraph dev() const;

@@ -24,7 +24,8 @@ enum UpdateMode : int {
   kModeDelta = 2,  // refresh: write candidates + residuals, count (now - was)
 };
 
-enum FinMode : int { kFinNone = 0, kFinLbp = 1, kFinInit = 2, kFinIter = 3, kFinApply = 4 };
+enum FinMode : int { kFinNone = 0, kFinLbp = 1, kFinInit = 2, kFinIter = 3, kFinApply = 4,
+                     kFinInitExt = 5, kFinIterExt = 6 };  // *Ext: RnBP band, all-reduced sums
 
 constexpr int kSinkCap = 4096;
 
@@ -265,6 +266,72 @@ static __global__ void k_part_unpack(DevGraph g, float* buf0, float* buf1, const
   }
 }
 
+// RnBP on a band: halos of the LIVE messages after the commit; a ghost
+// message that changed flags the owned vertex it flows into, whose outgoing
+// messages the refresh then recomputes (collect_touched, schedulers.cpp:31-42)
+static __global__ void k_part_pack_live(DevGraph g, const float* M, PartHalo h) {
+  const uint32_t C = g.lat_cols, L = g.lat_rows;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    if (h.ghost_up) h.send_up[c] = M[2u * lat_edge_down(0u, c, C) + 1u];
+    if (h.ghost_down) h.send_down[c] = M[2u * lat_edge_down(L - 2u, c, C)];
+  }
+}
+
+static __global__ void k_part_unpack_flag(DevGraph g, float* M, Ctl* ctl, uint32_t* vflag, uint32_t* vlist,
+                                          PartHalo h) {
+  if (run_done(ctl)) return;
+  const uint32_t C = g.lat_cols, L = g.lat_rows;
+  const uint32_t stamp = ctl->stamp;
+  const bool dense = ctl->dense != 0u;
+  auto flag = [&](uint32_t v) {
+    if (dense) {
+      vflag[v] = stamp;
+    } else if (atomicMax(&vflag[v], stamp) < stamp) {
+      vlist[atomicAdd(&ctl->nflag, 1u)] = v;
+    }
+  };
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    if (h.ghost_up) {
+      float* m = &M[2u * lat_edge_down(0u, c, C)];
+      if (*m != h.recv_up[c]) {
+        *m = h.recv_up[c];
+        flag(C + c);  // (1, c)
+      }
+    }
+    if (h.ghost_down) {
+      float* m = &M[2u * lat_edge_down(L - 2u, c, C) + 1u];
+      if (*m != h.recv_down[c]) {
+        *m = h.recv_down[c];
+        flag((L - 2u) * C + c);  // (L-2, c)
+      }
+    }
+  }
+}
+
+// the band's contributions of the iteration -> h.count = {delta, frontier,
+// survivors, time vote, count (init)}; slots are left for the finalize
+static __global__ void __launch_bounds__(kSlots) k_part_count_rnbp(Ctl* c, PartHalo h) {
+  __shared__ unsigned long long sh[5][kSlots / 32];
+  const Accum a = c->acc[threadIdx.x];
+  unsigned long long v[4] = {static_cast<unsigned long long>(a.delta), a.frontier, a.survivors, a.count};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = warp_sum(v[k]);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh[k][threadIdx.x >> 5] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 4; ++k)
+      for (int w = 0; w < kSlots / 32; ++w) t[k] += sh[k][w];
+    h.count[0] = t[0];
+    h.count[1] = t[1] + c->frontier;
+    h.count[2] = t[2];
+    h.count[3] = (globaltimer_ns() - c->t0_ns >= c->vote_limit_ns) ? 1ull : 0ull;
+    h.count[4] = t[3];
+  }
+}
+
 // <<<1, kSlots>>>
 // ext (row-band partition): {global unconverged count, time-limit votes},
 // all-reduced over the ranks, replaces the local count and the local clock so
@@ -289,9 +356,11 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
     v[k] = 0;
     for (int w = 0; w < kSlots / 32; ++w) v[k] += sh[k][w];
   }
-  const long long delta = static_cast<long long>(v[0]);
-  const unsigned long long count = ext ? ext[0] : v[1], frontier = v[2] + c->frontier;
-  if (ext && ext[1]) c->time_limit_ns = 0;  // some rank hit the time limit: stop everywhere
+  const bool rnbp_ext = mode == kFinInitExt || mode == kFinIterExt;
+  const long long delta = static_cast<long long>(rnbp_ext ? ext[0] : v[0]);
+  const unsigned long long count = ext ? (rnbp_ext ? ext[4] : ext[0]) : v[1];
+  const unsigned long long frontier = rnbp_ext ? ext[1] : v[2] + c->frontier;
+  if (ext && ext[rnbp_ext ? 3 : 1]) c->time_limit_ns = 0;  // some rank hit the time limit: stop everywhere
   c->evals_total += v[4];
   c->vertex_visits += v[5];
   switch (mode) {
@@ -309,6 +378,7 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
       break;
     }
     case kFinInit:
+    case kFinInitExt:
       c->unconverged = static_cast<unsigned>(count);
       c->iteration = 0;
       if (c->use_clist && 16ull * c->unconverged < D) c->cl_state = 1u;
@@ -316,6 +386,7 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
       fin_check_top(c);
       break;
     case kFinIter:
+    case kFinIterExt:
       fin_iter(c, delta, frontier, D);
       break;
     case kFinApply:
@@ -625,14 +696,16 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       if (hr) B[orr] = lr;
       if (hd) B[od] = ld;
       auto track = [&](bool has, uint32_t out, float r_msg) {
+        // messages of a band's ghost rows belong to the neighbour band: their
+        // residuals stay 0 here, so they are never counted or selected
         const int now = has && owned && r_msg >= eps;
         if (MODE == kModeDelta) {
-          if (has) {
+          if (has && owned) {
             cnt += now - (res[out] >= eps);
             res[out] = r_msg;
           }
         } else {
-          if (MODE == kModeInit && has) res[out] = r_msg;
+          if (MODE == kModeInit && has && owned) res[out] = r_msg;
           cnt += now;
         }
         if (CL && cl_on && now && !inlist[out]) {
@@ -716,6 +789,10 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
         else
           v = vlist[i];
       }
+      if (go && g.lat_cols && (g.cnt_row0 > 0u || g.cnt_row1 < g.lat_rows)) {  // band: owned rows only
+        const uint32_t row = v / g.lat_cols;
+        go = row >= g.cnt_row0 && row < g.cnt_row1;
+      }
       if (go) {
         cnt += vertex_update<QS, MODE, CL>(g, v, A, B, res, eps, &ctl->numeric_error, evals, cand_list.inlist, &cl,
                                            cl_on);
@@ -798,6 +875,7 @@ struct RnbpParams {
   double low_p, high_p, thr;
   double fixed_p;  // >= 0: lockstep override of p_now
   int commit;      // 0: only mark `sel` (lockstep frontier query)
+  unsigned attempt;  // Philox attempt of the select kernel (band retries use 1)
 };
 
 // rnbp_frontier (schedulers.cpp:194-216) attempt 0, fused with the commit of
@@ -842,12 +920,21 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
       if (q < D4) {
         const float4 r4 = res4[q];
         const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
+        // one Philox block per edge pair, only when a survivor needs a draw
+        const bool draw = thresh < (1ull << 53);
+        uint4 ph[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        if (draw) {
+          // keyed by the GLOBAL edge id (edge_offset != 0 for a band of a partition)
+          if (rr[0] >= eps || rr[1] >= eps) ph[0] = philox_edge(prm.seed, it, prm.attempt, 2ull * q + g.edge_offset);
+          if (rr[2] >= eps || rr[3] >= eps)
+            ph[1] = philox_edge(prm.seed, it, prm.attempt, 2ull * q + 1ull + g.edge_offset);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t d = 4 * q + k;
           if (rr[k] >= eps) {  // padding entries are 0
             c.survivors += 1;
-            if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d) < thresh)) {
+            if (!draw || u53_of(ph[k >> 1], d) < thresh) {
               if (prm.commit) {
                 commit_edge<QS>(g, d, rr[k], live, cand, res, eps, vflag, stamp, dense, c, nf[k], tg[k]);
               } else {
@@ -885,7 +972,7 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
         const float r = res[d];
         if (r >= eps) {
           c.survivors += 1;
-          if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d) < thresh)) {
+          if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d + 2ull * g.edge_offset) < thresh)) {
             cl.inlist[d] = 0;
             commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, dense, c, nf, tg);
           } else {
@@ -946,7 +1033,7 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     const uint32_t d = use_list ? list[i] : i;
     const float r = res[d];
-    if (r >= eps && philox_u53(prm.seed, it, 1u, d) < thresh) {
+    if (r >= eps && philox_u53(prm.seed, it, 1u, d + 2ull * g.edge_offset) < thresh) {
       ++fr;
       if (prm.commit) {
         Contrib c;

@@ -32,8 +32,8 @@ from dataclasses import dataclass
 from . import (_Config, _DevOpts, _Result, _check, _lib, GRAPH_TRUSTED, PairwiseMRF, SchedulerConfig,
                SchedulerKind)
 
-__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "NcclExchange", "LocalExchange",
-           "run_band_lbp"]
+__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "BandRnBP", "NcclExchange",
+           "LocalExchange", "NcclComm", "LocalComm", "run_band_lbp", "run_band_rnbp"]
 
 
 def band_rows(n: int, part: int, nparts: int):
@@ -85,12 +85,16 @@ class BandStatus:
 class BandLBP:
     """LBP on one band of the n x n Ising grid, on cuda:`device`."""
 
+    KIND = SchedulerKind.lbp
+    NCOUNT = 2  # {unconverged count, time vote}
+
     def __init__(self, n: int, c: float, seed: int, part: int, nparts: int, config: SchedulerConfig,
                  device: int = 0):
         import torch
 
-        if config.kind != SchedulerKind.lbp:
-            raise ValueError("row-band partition: LBP only")
+        if config.kind != self.KIND:
+            raise ValueError(f"{type(self).__name__} needs kind={self.KIND}")
+        self.seed = int(config.seed)
         info = _BandInfoC()
         h = C.c_void_p()
         _check(_lib.bp_graph_generate_ising_band(n, c, seed, part, nparts, C.byref(_DevOpts(device, GRAPH_TRUSTED)),
@@ -103,7 +107,7 @@ class BandLBP:
         self.send_down = torch.zeros(cols, dtype=torch.float32, device=dev)
         self.recv_up = torch.zeros(cols, dtype=torch.float32, device=dev)
         self.recv_down = torch.zeros(cols, dtype=torch.float32, device=dev)
-        self.count = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.count = torch.zeros(self.NCOUNT, dtype=torch.int64, device=dev)
         halo = _HaloC(self.send_up.data_ptr(), self.send_down.data_ptr(), self.recv_up.data_ptr(),
                       self.recv_down.data_ptr(), self.count.data_ptr())
         self._cfg = config._c()
@@ -145,6 +149,153 @@ class BandLBP:
         _check(_lib.bp_band_status(self._e, C.byref(r)))
         return BandStatus(bool(r.stopped), bool(r.converged), int(r.iterations), int(r.messages_updated_total),
                           int(r.gpu_launches))
+
+
+class BandRnBP(BandLBP):
+    """RnBP on one band (Philox draws keyed by global edge ids, so the run is
+    the same for any number of bands)."""
+
+    KIND = SchedulerKind.rnbp
+    NCOUNT = 5  # {delta, frontier, survivors, time vote, initial count}
+
+    def begin(self):
+        _check(_lib.bp_band_rnbp_begin(self._e))
+
+    def finish_init(self):
+        _check(_lib.bp_band_rnbp_finish_init(self._e))
+
+    def select(self, attempt: int = 0):
+        _check(_lib.bp_band_rnbp_select(self._e, attempt))
+
+    def refresh(self):
+        _check(_lib.bp_band_rnbp_refresh(self._e))
+
+    def finish(self):
+        _check(_lib.bp_band_rnbp_finish(self._e))
+
+    def survivors(self):
+        import numpy as np
+
+        n = C.c_uint64()
+        _check(_lib.bp_band_survivors(self._e, None, 0, C.byref(n)))
+        out = np.zeros(max(int(n.value), 1), np.uint64)
+        _check(_lib.bp_band_survivors(self._e, out.ctypes.data_as(C.c_void_p), out.size, C.byref(n)))
+        return out[: int(n.value)]
+
+    def fallback(self, global_d: int):
+        _check(_lib.bp_band_rnbp_fallback(self._e, global_d))
+
+
+class NcclComm:
+    """Collectives of one band per process (torch.distributed, NCCL between GPUs)."""
+
+    def __init__(self, rank: int, world: int):
+        self.rank, self.world = rank, world
+        self._halo = NcclExchange(rank, world)
+
+    def halo(self, bands):
+        import torch.distributed as dist
+
+        (b,) = bands
+        ops = []
+        if b.info.ghost_up:
+            ops += [dist.P2POp(dist.isend, b.send_up, self.rank - 1), dist.P2POp(dist.irecv, b.recv_up, self.rank - 1)]
+        if b.info.ghost_down:
+            ops += [dist.P2POp(dist.isend, b.send_down, self.rank + 1),
+                    dist.P2POp(dist.irecv, b.recv_down, self.rank + 1)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def reduce(self, bands):
+        import torch.distributed as dist
+
+        dist.all_reduce(bands[0].count)
+
+    def gather_lists(self, lists):
+        import torch.distributed as dist
+
+        out = [None] * self.world
+        dist.all_gather_object(out, [int(x) for x in lists[0]])
+        return out
+
+
+class LocalComm:
+    """All bands in one process on one device (tests): the same data movement."""
+
+    def halo(self, bands):
+        import torch
+
+        torch.cuda.synchronize()
+        for i, b in enumerate(bands):
+            if b.info.ghost_up:
+                b.recv_up.copy_(bands[i - 1].send_down)
+            if b.info.ghost_down:
+                b.recv_down.copy_(bands[i + 1].send_up)
+        torch.cuda.synchronize()
+
+    def reduce(self, bands):
+        import torch
+
+        torch.cuda.synchronize()
+        total = sum(b.count.clone() for b in bands)
+        for b in bands:
+            b.count.copy_(total)
+        torch.cuda.synchronize()
+
+    def gather_lists(self, lists):
+        return [[int(x) for x in l] for l in lists]
+
+
+def run_band_rnbp(bands, comm, max_iterations: int) -> BandStatus:
+    """The run() loop of RnBP over row bands (schedulers.cpp:301-347 with
+    rnbp_frontier, :194-216): `bands` are this process's bands (one per GPU
+    with NcclComm, all of them with LocalComm)."""
+    import torch
+
+    def phase(attempt):
+        for b in bands:
+            with torch.cuda.stream(b.stream):
+                b.select(attempt)
+        comm.halo(bands)
+        for b in bands:
+            with torch.cuda.stream(b.stream):
+                b.refresh()
+        comm.reduce(bands)
+
+    for b in bands:
+        with torch.cuda.stream(b.stream):
+            b.begin()
+    comm.reduce(bands)
+    for b in bands:
+        with torch.cuda.stream(b.stream):
+            b.finish_init()
+    for _ in range(max_iterations + 1):
+        st = bands[0].status()
+        if st.stopped:
+            return st
+        phase(0)
+        delta, frontier, survivors = (int(x) for x in bands[0].count[:3].tolist())
+        if frontier == 0 and survivors > 0:  # retry once, then one survivor (schedulers.cpp:204-214)
+            phase(1)
+            frontier = int(bands[0].count[1].item())
+            if frontier == 0:
+                ids = sorted(x for l in comm.gather_lists([b.survivors() for b in bands]) for x in l)
+                u = _lib.bp_philox_u53(bands[0].seed, st.iterations, 2, 0) * 2.0 ** -53
+                pick = ids[min(len(ids) - 1, int(u * len(ids)))]
+                for b in bands:
+                    owned = pick in set(int(x) for x in b.survivors())
+                    with torch.cuda.stream(b.stream):
+                        b.fallback(pick if owned else (1 << 64) - 1)
+                comm.halo(bands)
+                for b in bands:
+                    with torch.cuda.stream(b.stream):
+                        b.refresh()
+                comm.reduce(bands)
+        for b in bands:
+            with torch.cuda.stream(b.stream):
+                b.finish()
+    return bands[0].status()
 
 
 class NcclExchange:

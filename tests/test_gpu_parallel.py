@@ -57,3 +57,19 @@ def test_band_rows_cover_grid():
             assert all(rows[k][1] == rows[k + 1][0] for k in range(p - 1))
             total = sum(par.owned_directed_edges(n, r0, r1) for r0, r1, _, _ in rows)
             assert total == 4 * n * (n - 1)
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_band_rnbp_equals_unpartitioned(bp, nparts):
+    """RnBP over bands: same iterations, updates and beliefs as the one-GPU
+    run (Philox keyed by global edge ids; retry/fallback across bands)."""
+    n, c, seed = 20, 2.0, 4
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=400, seed=seed)
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)), cfg)
+    bands = [par.BandRnBP(n, c, seed, p, nparts, cfg, 0) for p in range(nparts)]
+    st = par.run_band_rnbp(bands, par.LocalComm(), cfg.max_iterations)
+    assert st.converged == full.converged and st.iterations == full.iterations
+    assert st.messages_updated_total == full.messages_updated_total
+    want = full.beliefs.values.reshape(n, n, 2)
+    for b in bands:
+        assert np.array_equal(b.owned_beliefs(), want[b.info.row0:b.info.row1])
