@@ -390,21 +390,41 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
     // rounds of ready-root resolution
     for (;;) {
       const uint32_t nc = __ldcg(&rc->ncand);
-      // A1: skip claimed candidates, publish priorities over the balls
+      // A1: skip claimed candidates, publish priorities over the balls.
+      // With ball lists a warp takes a candidate and its lanes split the
+      // ball (hubs of random graphs have balls of hundreds of vertices; one
+      // thread per candidate would serialise a load per ball vertex).
       unsigned unres = 0;
-      for (uint32_t i = tid; i < nc; i += stride) {
+      const bool wl = b.boff != nullptr;
+      const uint32_t lane = threadIdx.x & 31u, gw = tid >> 5, nw = stride >> 5;
+      auto warp_ball = [&](uint32_t r, auto&& f) -> bool {  // all lanes; AND of f over the ball
+        const unsigned long long e0 = b.boff[r], e1 = b.boff[r + 1];
+        for (unsigned long long base = e0; base < e1; base += 32) {
+          const unsigned long long i = base + lane;
+          const bool v = i < e1 ? f(__ldg(&b.bl[i])) : true;
+          if (!__all_sync(0xffffffffu, v)) return false;
+        }
+        return true;
+      };
+      for (uint32_t i = wl ? gw : tid; i < nc; i += wl ? nw : stride) {
         const uint32_t r = __ldcg(&b.clist[i]);
         if (__ldcg(&b.state[r]) != kRsCand) continue;
         if (__ldcg(&b.claimed[r]) != kUncl) {
-          b.state[r] = kRsSkip;
+          if (!wl || lane == 0) b.state[r] = kRsSkip;
           continue;
         }
-        ++unres;
+        if (!wl || lane == 0) ++unres;
         const unsigned long long key = rs_key64(__ldcg(&b.vres[r]), r);
-        ball_each(g, b, r, h, [&](uint32_t w) {
-          atomicMax(&b.ballmax[w], key);
-          return true;
-        });
+        if (wl)
+          warp_ball(r, [&](uint32_t w) {
+            atomicMax(&b.ballmax[w], key);
+            return true;
+          });
+        else
+          ball_each(g, b, r, h, [&](uint32_t w) {
+            atomicMax(&b.ballmax[w], key);
+            return true;
+          });
       }
       unres = warp_sum(unres);
       if ((threadIdx.x & 31u) == 0 && unres) atomicAdd(&rc->unres, unres);
@@ -412,12 +432,13 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       grid.sync();
       if (__ldcg(&rc->unres) == 0) break;
       // A2: ready = maximum priority over the whole ball
-      for (uint32_t i = tid; i < nc; i += stride) {
+      for (uint32_t i = wl ? gw : tid; i < nc; i += wl ? nw : stride) {
         const uint32_t r = __ldcg(&b.clist[i]);
         if (__ldcg(&b.state[r]) != kRsCand) continue;
         const unsigned long long key = rs_key64(__ldcg(&b.vres[r]), r);
-        const bool ready = ball_each(g, b, r, h, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; });
-        if (ready) b.rlist[atomicAdd(&rc->nready, 1u)] = r;
+        const bool ready = wl ? warp_ball(r, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; })
+                              : ball_each(g, b, r, h, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; });
+        if (ready && (!wl || lane == 0)) b.rlist[atomicAdd(&rc->nready, 1u)] = r;
       }
       grid.sync();
       // B: build the ready splashes (build_splash, schedulers.cpp:136-167); clear the balls
@@ -454,9 +475,18 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       }
       // unresolved candidates clear their balls (a ready root racing to
       // kRsBuilt may be cleared twice: idempotent)
-      for (uint32_t i = tid; i < nc; i += stride) {
+      for (uint32_t i = wl ? gw : tid; i < nc; i += wl ? nw : stride) {
         const uint32_t r = __ldcg(&b.clist[i]);
-        if (__ldcg(&b.state[r]) == kRsCand)
+        uint32_t st = __ldcg(&b.state[r]);
+        // builders flip states concurrently in this phase: one read per warp
+        if (wl) st = __shfl_sync(0xffffffffu, st, 0);
+        if (st != kRsCand) continue;
+        if (wl)
+          warp_ball(r, [&](uint32_t w) {
+            b.ballmax[w] = 0ull;
+            return true;
+          });
+        else
           ball_each(g, b, r, h, [&](uint32_t w) {
             b.ballmax[w] = 0ull;
             return true;
