@@ -48,7 +48,7 @@ BinaryStreams ising_band_streams(uint32_t n, double c, uint64_t seed, uint32_t a
 BinaryStreams chain_streams(uint32_t length, double c, uint64_t seed);
 
 struct PottsStreams {
-  std::vector<float> unary_log;  // V * q, log(u)
+  std::vector<float> unary_log;  // V * q, log2(u) (device layout: base-2 logs)
   std::vector<float> lambda_c;   // lambda * c per edge
 };
 PottsStreams potts_streams(uint32_t n, uint32_t q, double c, uint64_t seed);

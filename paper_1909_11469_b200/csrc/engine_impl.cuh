@@ -205,7 +205,7 @@ class EngineT final : public EngineBase {
         out[o++] = 1.0 / (1.0 + std::exp2(-l));
       } else {
         const uint32_t q = g_.card_of(ep[d ^ 1u]);
-        for (uint32_t x = 0; x < q; ++x) out[o++] = std::exp(static_cast<double>(raw[static_cast<size_t>(d) * QS + x]));
+        for (uint32_t x = 0; x < q; ++x) out[o++] = std::exp2(static_cast<double>(raw[static_cast<size_t>(d) * QS + x]));
       }
     }
   }

@@ -111,7 +111,7 @@ PottsStreams potts_streams(uint32_t n, uint32_t q, double c, uint64_t seed) {
   for (size_t e = 0; e < E; ++e) s.lambda_c[e] = static_cast<float>((rng.unit() - 0.5) * c);
   s.unary_log.resize(V * q);
   parallel_for(V * q, [&](size_t b, size_t e) {
-    for (size_t k = b; k < e; ++k) s.unary_log[k] = static_cast<float>(std::log(u[k]));
+    for (size_t k = b; k < e; ++k) s.unary_log[k] = static_cast<float>(std::log2(u[k]));  // base-2 (device layout)
   });
   return s;
 }

@@ -294,7 +294,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     for (uint32_t v = 0, o = 0; v < V; o += d->cardinalities[v], ++v) {
       bo[v + 1] = bo[v] + d->cardinalities[v];
       for (uint32_t x = 0; x < d->cardinalities[v]; ++x)
-        ul[static_cast<size_t>(v) * qs + x] = static_cast<float>(std::log(d->unary_values[o + x]));
+        ul[static_cast<size_t>(v) * qs + x] = static_cast<float>(std::log2(d->unary_values[o + x]));  // base 2
     }
     // Potts tables (a on the diagonal, d off it, square): one weight per edge
     bool potts = E > 0;

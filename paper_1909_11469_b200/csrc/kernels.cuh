@@ -539,42 +539,63 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
   for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
   uint32_t deg = 0;
   for_each_in(g, v, [&](uint32_t in) {
-    const float* m = A + static_cast<size_t>(in) * QS;
-#pragma unroll (QS <= 8 ? QS : 2)
-    for (int x = 0; x < QS; ++x) T[x] += ldm<NC>(&m[x]);
+    const float4* m4 = reinterpret_cast<const float4*>(A + static_cast<size_t>(in) * QS);  // QS % 4 == 0
+#pragma unroll (QS <= 8 ? QS / 4 : 1)
+    for (int x4 = 0; x4 < QS / 4; ++x4) {
+      const float4 q4 = ldm<NC>(&m4[x4]);
+      T[4 * x4] += q4.x;
+      T[4 * x4 + 1] += q4.y;
+      T[4 * x4 + 2] += q4.z;
+      T[4 * x4 + 3] += q4.w;
+    }
     ++deg;
   });
   int cnt = 0;
   for_each_in(g, v, [&](uint32_t in) {
     const uint32_t out = in ^ 1u;
     const uint32_t cj = g.uniform_q ? g.uniform_q : g.card[g.ep[in]];  // target of `out` = source of `in`
-    const float* m_in = A + static_cast<size_t>(in) * QS;
+    const float4* mi4 = reinterpret_cast<const float4*>(A + static_cast<size_t>(in) * QS);
+    const float4* mo4 = reinterpret_cast<const float4*>(A + static_cast<size_t>(out) * QS);
     const float r_was = MODE == kModeDelta ? res[out] : 0.f;
+    // the edge pair (incoming and old outgoing q-vectors) with 16-byte loads
+    float mi[QS], mo[QS];
+#pragma unroll (QS <= 8 ? QS / 4 : 1)
+    for (int x4 = 0; x4 < QS / 4; ++x4) {
+      const float4 a4 = ldm<NC>(&mi4[x4]), b4 = ldm<NC>(&mo4[x4]);
+      mi[4 * x4] = a4.x;
+      mi[4 * x4 + 1] = a4.y;
+      mi[4 * x4 + 2] = a4.z;
+      mi[4 * x4 + 3] = a4.w;
+      mo[4 * x4] = b4.x;
+      mo[4 * x4 + 1] = b4.y;
+      mo[4 * x4 + 2] = b4.z;
+      mo[4 * x4 + 3] = b4.w;
+    }
     float p[QS];
     float M = -INFINITY;
 #pragma unroll (QS <= 8 ? QS : 2)
     for (int x = 0; x < QS; ++x) {
-      p[x] = T[x] - ldm<NC>(&m_in[x]);
+      p[x] = T[x] - mi[x];
       if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
     }
 #pragma unroll (QS <= 8 ? QS : 2)
-    for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
+    for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
     float o[QS];
     generic_matvec<QS>(g, out, p, o);
     float s = 0.f;
 #pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
-    const float inv = __frcp_rn(s);
-    const float* m_old = A + static_cast<size_t>(out) * QS;
+    const float inv = frcp(s);
     float* dst = B + static_cast<size_t>(out) * QS;
     float r = 0.f;
+    // the residual compares 2^(stored log) on both sides, so a bitwise fixed
+    // point reports exactly 0 (as for the binary layout)
 #pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) {
       if (xt < static_cast<int>(cj)) {
-        const float pn = o[xt] * inv;
-        const float po = __expf(ldm<NC>(&m_old[xt]));
-        r = fmaxf(r, fabsf(pn - po));
-        dst[xt] = __logf(pn);
+        const float ln = flg2(o[xt] * inv);
+        r = fmaxf(r, fabsf(fex2(ln) - fex2(mo[xt])));
+        dst[xt] = ln;
       }
     }
     if (!(s > 0.f) || !(s < INFINITY)) *numeric_flag = 1u;
@@ -828,7 +849,7 @@ __global__ void k_init_messages(DevGraph g, float* M, Ctl* ctl, int set_t0) {
       const uint32_t d = static_cast<uint32_t>(i / QS);
       const uint32_t x = static_cast<uint32_t>(i % QS);
       const uint32_t q = g.card[g.ep[d ^ 1u]];
-      M[i] = x < q ? -__logf(static_cast<float>(q)) : 0.f;
+      M[i] = x < q ? -log2f(static_cast<float>(q)) : 0.f;  // base-2 log-probabilities
     }
   }
 }
@@ -1404,7 +1425,7 @@ __global__ void k_beliefs(DevGraph g, const float* A0, const float* A1, int ping
       double s = 0.0;
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) {
-        p[x] = x < static_cast<int>(q) ? exp(static_cast<double>(T[x] - M)) : 0.0;
+        p[x] = x < static_cast<int>(q) ? exp2(static_cast<double>(T[x] - M)) : 0.0;
         s += p[x];
       }
       double* o = out + g.bel_off[v];

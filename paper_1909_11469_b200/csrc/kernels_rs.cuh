@@ -298,17 +298,17 @@ __device__ __forceinline__ void splash_vertex_update(const DevGraph& g, uint32_t
         if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
       }
 #pragma unroll (QS <= 8 ? QS : 2)
-      for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
+      for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
       float o[QS], s = 0.f;
       generic_matvec<QS>(g, out, p, o);
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
       if (!(s > 0.f) || !(s < INFINITY)) *nf = 1u;
-      const float inv = __frcp_rn(s);
+      const float inv = frcp(s);
       float* dst = shadow + static_cast<size_t>(out) * QS;
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt)
-        if (xt < static_cast<int>(cj)) dst[xt] = __logf(o[xt] * inv);
+        if (xt < static_cast<int>(cj)) dst[xt] = flg2(o[xt] * inv);
     }
   }
 }
@@ -611,16 +611,16 @@ __global__ void __launch_bounds__(kBlock) k_splash_apply_edges(DevGraph g, const
       for (int x = 0; x < QS; ++x)
         if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
 #pragma unroll (QS <= 8 ? QS : 2)
-      for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? __expf(p[x] - M) : 0.f;
+      for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
       float o[QS], s2 = 0.f;
       generic_matvec<QS>(g, d, p, o);
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt) s2 += xt < static_cast<int>(cj) ? o[xt] : 0.f;
       if (!(s2 > 0.f) || !(s2 < INFINITY)) *nf = 1u;
-      const float inv = __frcp_rn(s2);
+      const float inv = frcp(s2);
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt)
-        if (xt < static_cast<int>(cj)) shadow[static_cast<size_t>(d) * QS + xt] = __logf(o[xt] * inv);
+        if (xt < static_cast<int>(cj)) shadow[static_cast<size_t>(d) * QS + xt] = flg2(o[xt] * inv);
     }
     written[d] = me;
   }
