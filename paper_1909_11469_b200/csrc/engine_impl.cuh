@@ -486,8 +486,15 @@ class EngineT final : public EngineBase {
   // one LBP sweep (ping-pong): the SMEM-staged lattice kernel for binary Ising
   // lattices, the vertex-centric kernel otherwise
   unsigned lbp_grid_ = 0;
+  static constexpr uint64_t kLbpTmaMinVertices = 64ull << 20;
   void enqueue_lbp_sweep() {
-    if (QS == 1 && g_.lat_cols && g_.par_mode == 1 && g_.lat_rows >= 2) {
+    // TMA-staged rows pay off once the grid is far beyond L2; below that the
+    // register-tiled lattice kernel (k_vertex_update) is faster.
+    // BPB_LBP_KERNEL=tma|tiles overrides (measurement).
+    static const char* lk = std::getenv("BPB_LBP_KERNEL");
+    const bool big = static_cast<uint64_t>(g_.V) >= kLbpTmaMinVertices;
+    const bool use_tma = lk ? std::strcmp(lk, "tma") == 0 : big;
+    if (QS == 1 && g_.lat_cols && g_.par_mode == 1 && g_.lat_rows >= 2 && use_tma) {
       if (!lbp_grid_) {
         cuda_check(cudaFuncSetAttribute(k_lbp_lattice, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(LbpSmem))),

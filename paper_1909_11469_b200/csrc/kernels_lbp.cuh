@@ -197,8 +197,9 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
       s_next = 1;
     }
   }
+  // (strip, row) of tile t, advanced incrementally (no 64-bit division per tile)
+  uint32_t strip = static_cast<uint32_t>(t_begin / R), r = static_cast<uint32_t>(t_begin % R);
   for (uint64_t t = t_begin; t < t_end; ++t) {
-    const uint32_t strip = static_cast<uint32_t>(t / R), r = static_cast<uint32_t>(t % R);
     const uint32_t c0 = strip * kSW, w = min(kSW, C - c0);
     const bool lastrow = r + 1u == R, first = r == 0u;
     const bool cont = prev_b && prev_strip == strip && prev_row + 1u == r;
@@ -207,8 +208,8 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
     uint32_t strip1 = 0, r1 = 0;
     bool next_cont = false;
     if (has_t1) {
-      strip1 = static_cast<uint32_t>((t + 1) / R);
-      r1 = static_cast<uint32_t>((t + 1) % R);
+      strip1 = r + 1u == R ? strip + 1u : strip;
+      r1 = r + 1u == R ? 0u : r + 1u;
       next_cont = strip1 == strip && r1 == r + 1u;
       if (leader) issue_row(s_next, strip1, r1);
     }
@@ -335,6 +336,10 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
         s_cur = s_next;
         s_next = old_cur;
       }
+    }
+    if (++r == R) {
+      r = 0;
+      ++strip;
     }
   }
   if (prev_b) write_row(b_cur ^ 1, prev_strip, prev_row, false);  // its D.y: the next block
