@@ -182,6 +182,7 @@ struct Ctl {
   unsigned int pad4_;
   unsigned long long persist_bytes;  // algorithmic bytes moved by the persistent kernel
   unsigned long long vote_limit_ns;  // row-band partition: time limit, decided by an all-reduced vote
+  unsigned long long phase_ns[8];    // persistent kernel phase clock (CTA 0)
   Accum acc[kSlots];
   TraceRec trace[kTraceRing];
 };

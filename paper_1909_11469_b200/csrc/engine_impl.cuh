@@ -917,6 +917,14 @@ class EngineT final : public EngineBase {
       }
       if (!handover()) break;  // not reached: list mode is final
     }
+    if (std::getenv("BPB_DEBUG_PHASES")) {
+      unsigned long long ph[8];
+      cuda_check(cudaMemcpy(ph, reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, phase_ns), sizeof(ph),
+                            cudaMemcpyDeviceToHost), "d2h");
+      std::fprintf(stderr, "persist phases (ms): select %.2f  sync+retry %.2f  refresh-loop %.2f flush %.2f pacc %.2f "
+                   "tail %.2f  sync+finalize %.2f\n",
+                   ph[0] * 1e-6, ph[1] * 1e-6, ph[4] * 1e-6, ph[5] * 1e-6, ph[6] * 1e-6, ph[2] * 1e-6, ph[3] * 1e-6);
+    }
   }
 
   // ---- Residual Splash state (kernels_rs.cuh)

@@ -490,30 +490,37 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
     }
   };
   if (g.lat_cols) {
-    uint32_t ins[4];
+    // fixed neighbour slots (up, left, right, down): statically indexed, so
+    // everything stays in registers (a compacted list would live in local memory)
+    const uint32_t C = g.lat_cols, R = g.lat_rows;
+    const uint32_t r = v / C, c = v - r * C;
+    const uint32_t row = r * (2u * C - 1u);
+    const bool last = r + 1u == R;
+    const bool has[4] = {r > 0u, c > 0u, c + 1u < C, !last};
+    const uint32_t ins[4] = {
+        has[0] ? 2u * ((r - 1u) * (2u * C - 1u) + 2u * c + (c + 1u < C ? 1u : 0u)) : 0u,
+        has[1] ? 2u * (last ? row + c - 1u : row + 2u * (c - 1u)) : 0u,
+        has[2] ? 2u * (last ? row + c : row + 2u * c) + 1u : 0u,
+        has[3] ? 2u * (row + 2u * c + (c + 1u < C ? 1u : 0u)) + 1u : 0u};
     float2 prs[4];
     float rw[4];
-    uint8_t il[4];
-    for_each_in(g, v, [&](uint32_t in) {
-      ins[deg] = in;
-      prs[deg] = ldm<NC>(&A2[in >> 1]);
-      T += (in & 1u) ? prs[deg].y : prs[deg].x;
-      ++deg;
-    });
-    // prefetch the per-message state so the four updates do not serialise
-    // on (possibly aliasing) loads between their stores
+    bool il[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      rw[k] = 0.f;
-      il[k] = 1;
-      if (k < static_cast<int>(deg)) {
-        if (MODE == kModeDelta) rw[k] = res[ins[k] ^ 1u];
-        if (CL && cl_on) il[k] = inlist[ins[k] ^ 1u];
-      }
+      prs[k] = has[k] ? ldm<NC>(&A2[ins[k] >> 1]) : make_float2(0.f, 0.f);
+      // prefetch the per-message state so the four updates do not serialise
+      // on (possibly aliasing) loads between their stores
+      rw[k] = (MODE == kModeDelta && has[k]) ? res[ins[k] ^ 1u] : 0.f;
+      il[k] = (CL && cl_on && has[k]) ? inlist[ins[k] ^ 1u] != 0 : true;
     }
 #pragma unroll
+    for (int k = 0; k < 4; ++k) T += has[k] ? ((ins[k] & 1u) ? prs[k].y : prs[k].x) : 0.f;
+#pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (k < static_cast<int>(deg)) emit_pre(ins[k], prs[k], rw[k], il[k] != 0);
+      if (has[k]) {
+        emit_pre(ins[k], prs[k], rw[k], il[k]);
+        ++deg;
+      }
   } else {
     for_each_in(g, v, [&](uint32_t in) {
       const float2 pr = ldm<NC>(&A2[in >> 1]);

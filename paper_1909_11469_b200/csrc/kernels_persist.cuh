@@ -95,6 +95,14 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     ctl->time_stop = 0u;
   }
   sync_all();
+  unsigned long long tclk = lead ? globaltimer_ns() : 0ull;
+  auto mark = [&](int k) {  // phase clock of CTA 0 (profiling aid, one timer read per phase)
+    if (lead) {
+      const unsigned long long t = globaltimer_ns();
+      ctl->phase_ns[k] += t - tclk;
+      tclk = t;
+    }
+  };
   for (;;) {
     const unsigned pb = static_cast<unsigned>(it % 3ull), fb = static_cast<unsigned>(it & 1ull);
     unsigned long long* acc = pacc3 + 6 * pb;
@@ -150,6 +158,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       fl.flush(0);
       block_add_pacc(acc, c);
     }
+    mark(0);
     sync_all();
     // ---- retry / fallback (schedulers.cpp:204-214): uniform decision, one block
     unsigned long long retry_front = 0;
@@ -175,6 +184,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       sync_all();
       retry_front = ctl->frontier;
     }
+    mark(1);
     // ---- refresh over the touched vertices; new unconverged edges join the list
     {
       const uint32_t nv = *nfl;
@@ -192,7 +202,9 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         }
         st.flush(1024);
       }
+      mark(4);
       st.flush(0);
+      mark(5);
       Contrib c;
       c.delta = cnt;
       c.evals = evals;
@@ -201,8 +213,10 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       // coupling, candidate write, residual read + write
       c.count = 8ull * visits + static_cast<unsigned long long>(8 * QS + 4 + 4 * QS + 8) * evals;
       block_add_pacc(acc, c);
+      mark(6);
       if (lead && globaltimer_ns() - ctl->t0_ns >= ctl->time_limit_ns) ctl->time_stop = 1u;
     }
+    mark(2);
     sync_all();
     // ---- finalize (fin_iter), replicated: converged check before the caps
     const long long delta = static_cast<long long>(acc[0]);
@@ -239,6 +253,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       done = true;
       reason = kStopTime;
     }
+    mark(3);
     if (done) {
       if (lead) {  // mirror the final state for the host
         ctl->iteration = it;

@@ -225,3 +225,41 @@ def test_rnbp_persistent_tail_matches_graph_loop(bp, orc, n, c, seed):
     assert a.trace_signature() == b.trace_signature()
     assert np.max(np.abs(a.beliefs.values - b.beliefs.values)) <= 1e-6
     assert a.gpu_launches <= b.gpu_launches
+
+
+def _lattice_arrays(orc, rows, cols, seed, c=2.0):
+    """rows x cols Ising lattice in generate_ising's edge order, as build_graph input."""
+    rng = Stream(orc, seed)
+    V = rows * cols
+    unary = []
+    for _ in range(V):
+        a, b = rng.unit(), rng.unit()
+        unary += [a or 0.5, b or 0.5]
+    ep, tb = [], []
+    for r in range(rows):
+        for col in range(cols):
+            v = r * cols + col
+            for w in ([v + 1] if col + 1 < cols else []) + ([v + cols] if r + 1 < rows else []):
+                lam = rng.unit() - 0.5
+                a, d = np.exp(lam * c), np.exp(-lam * c)
+                ep.append((v, w))
+                tb += [a, d, d, a]
+    return (np.full(V, 2, np.uint32), np.asarray(unary), np.asarray(ep, np.uint32).reshape(-1, 2),
+            np.asarray(tb))
+
+
+@pytest.mark.parametrize("rows,cols", [(7, 11), (13, 4), (1, 9), (9, 1)])
+def test_nonsquare_lattice_detected_and_exact(bp, orc, rows, cols):
+    """Descriptor lattices (any rows x cols) take the arithmetic-neighbour path;
+    LBP stays in lockstep with the oracle and converged runs agree."""
+    cards, un, ep, tb = _lattice_arrays(orc, rows, cols, 17 + rows)
+    dg = bp.PairwiseMRF.from_arrays(cards, un, ep, tb)
+    og = po.Graph.from_arrays(orc, cards, un, ep, tb)
+    _lockstep_lbp(bp, orc, dg, og, ep, 30)
+    for kind in ("lbp", "rnbp", "rbp", "rs"):
+        cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.from_string(kind), low_p=0.5, p=0.25, max_iterations=20000)
+        r = bp.run(dg, cfg)
+        o = po.run(og, oracle_config(cfg))
+        assert r.converged == o.converged, kind
+        if r.converged:
+            assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL, kind
