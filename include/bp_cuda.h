@@ -272,6 +272,11 @@ BP_API int bp_band_rnbp_begin(struct bp_engine* e);
 BP_API int bp_band_rnbp_finish_init(struct bp_engine* e);
 BP_API int bp_band_rnbp_select(struct bp_engine* e, uint32_t attempt);
 BP_API int bp_band_rnbp_refresh(struct bp_engine* e);
+/* RBP on a band: the band's local top-k (k = max(1, llround(p * owned directed
+ * edges)), ties to the lower id) + commit + pack; then refresh / all-reduce /
+ * finish exactly as RnBP (no retry).  Per-partition local frontiers (SURVEY
+ * 8(e)): differs from the global select_top_k when P > 1, by design. */
+BP_API int bp_band_rbp_select(struct bp_engine* e);
 BP_API int bp_band_rnbp_finish(struct bp_engine* e);
 BP_API int bp_band_survivors(struct bp_engine* e, uint64_t* global_ids, uint64_t cap, uint64_t* n);
 BP_API int bp_band_rnbp_fallback(struct bp_engine* e, uint64_t global_d);

@@ -86,6 +86,15 @@ __device__ __forceinline__ bool ball_walk(const DevGraph& g, uint32_t r, uint32_
   return true;
 }
 
+// Row-band partition: does the band own directed edge d (its source row)?
+__device__ __forceinline__ bool band_graph(const DevGraph& g) {
+  return g.lat_cols != 0u && (g.cnt_row0 > 0u || g.cnt_row1 < g.lat_rows);
+}
+__device__ __forceinline__ bool edge_owned(const DevGraph& g, uint32_t d) {
+  const uint32_t r = g.ep[d] / g.lat_cols;
+  return r >= g.cnt_row0 && r < g.cnt_row1;
+}
+
 // Incoming directed edges of v in CSR order (mrf.cpp:93-104).  Lattice: up,
 // left, right, down, from the edge numbering of generate_ising
 // (generators.cpp:37-43): per row the right edge then the down edge of each

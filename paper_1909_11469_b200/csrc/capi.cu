@@ -287,6 +287,10 @@ int bp_band_rnbp_select(bp_engine* e, uint32_t attempt) {
   if (!e || attempt > 1) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] { e->e->band_rnbp_select(attempt); });
 }
+int bp_band_rbp_select(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_rbp_select(); });
+}
 int bp_band_rnbp_refresh(bp_engine* e) {
   if (!e) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] { e->e->band_rnbp_refresh(); });

@@ -533,8 +533,8 @@ class EngineT final : public EngineBase {
   void band_config(const PartHalo& h, uint64_t owned_directed) override {
     if (QS != 1 || !g_.lat_cols || g_.par_mode != 1)
       throw Error(BP_ERR_UNSUPPORTED, "row-band partition needs a binary Ising lattice band");
-    if (cfg_.kind != BP_LBP && cfg_.kind != BP_RNBP)
-      throw Error(BP_ERR_UNSUPPORTED, "row-band partition: LBP and RnBP");
+    if (cfg_.kind != BP_LBP && cfg_.kind != BP_RNBP && cfg_.kind != BP_RBP)
+      throw Error(BP_ERR_UNSUPPORTED, "row-band partition: LBP, RnBP and RBP");
     halo_ = h;
     halo_.ghost_up = g_.cnt_row0 > 0 ? 1u : 0u;
     halo_.ghost_down = g_.cnt_row1 < g_.lat_rows ? 1u : 0u;
@@ -574,7 +574,7 @@ class EngineT final : public EngineBase {
   }
   unsigned band_cols_grid() const { return static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock); }
   void band_rnbp_begin() override {
-    if (cfg_.kind != BP_RNBP) throw_invalid("band_rnbp_* on a non-RnBP engine");
+    if (cfg_.kind != BP_RNBP && cfg_.kind != BP_RBP) throw_invalid("band frontier API on an LBP engine");
     band_start_common();
     k_vertex_update<QS, kModeInit, false, false, false>
         <<<vgrid(k_vertex_update<QS, kModeInit, false, false, false>, g_.V), kBlock, 0, s_>>>(
@@ -593,6 +593,16 @@ class EngineT final : public EngineBase {
     k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
     launch_check();
     launches_ += 2;
+  }
+  // RBP on a band: local top-k over the band's own edges, k = max(1, llround(p owned))
+  // (per-partition local frontier, a deviation from the global select_top_k by design)
+  void band_rbp_select() override {
+    ensure_rbp_scratch();
+    const long long kr = std::llround(cfg_.p * static_cast<double>(band_owned_));
+    enqueue_topk(kr < 1 ? 1ull : static_cast<uint64_t>(kr), 1);
+    k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
+    launch_check();
+    ++launches_;
   }
   void band_rnbp_refresh() override {
     k_part_unpack_flag<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), ctl(), vflag_.as<uint32_t>(),
@@ -710,7 +720,7 @@ class EngineT final : public EngineBase {
 
   void enqueue_topk(uint64_t k, int commit) {
     const int dense = k > g_.V / 16 ? 1 : 0;
-    if (k >= g_.D) {
+    if (k >= (band_owned_ ? band_owned_ : g_.D)) {
       timed(kKSelect, [&] {
         k_rbp_commit<QS><<<nchunks_, kBlock, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
                                                       vlist_.as<uint32_t>(), sel_.as<uint8_t>(), chunk_.as<unsigned>(),
@@ -722,11 +732,11 @@ class EngineT final : public EngineBase {
     const unsigned gh = grid_cap(g_.D / 4 + 1, 4);
     for (int pass = 0; pass < 3; ++pass) {
       timed(kKTopk, [&] {
-        k_radix_hist<<<gh, kBlock, 0, s_>>>(res_.as<float>(), g_.D, pass, hist_.as<unsigned>(), ctl());
+        k_radix_hist<<<gh, kBlock, 0, s_>>>(dg_, res_.as<float>(), g_.D, pass, hist_.as<unsigned>(), ctl());
       });
       timed(kKTopk, [&] { k_radix_scan<<<1, 1024, 0, s_>>>(hist_.as<unsigned>(), pass, k, ctl()); });
     }
-    timed(kKTopk, [&] { k_tie_count<<<nchunks_, kBlock, 0, s_>>>(res_.as<float>(), g_.D, chunk_.as<unsigned>(), ctl()); });
+    timed(kKTopk, [&] { k_tie_count<<<nchunks_, kBlock, 0, s_>>>(dg_, res_.as<float>(), g_.D, chunk_.as<unsigned>(), ctl()); });
     timed(kKTopk, [&] { k_tie_scan<<<1, 1024, 0, s_>>>(chunk_.as<unsigned>(), nchunks_, ctl()); });
     timed(kKSelect, [&] {
       k_rbp_commit<QS><<<nchunks_, kBlock, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),

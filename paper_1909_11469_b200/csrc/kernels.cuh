@@ -1193,9 +1193,11 @@ __device__ __forceinline__ uint32_t float_key(float r) { return __float_as_uint(
 
 // pass 0: bins key>>20; pass 1: (key>>8)&0xfff for key>>20 == prefix;
 // pass 2: key&0xff for key>>8 == prefix
-static __global__ void __launch_bounds__(kBlock) k_radix_hist(const float* res, uint32_t D, int pass,
+// band graphs: only the band's own edges compete (per-partition local top-k)
+static __global__ void __launch_bounds__(kBlock) k_radix_hist(DevGraph g, const float* res, uint32_t D, int pass,
                                                        unsigned* hist, Ctl* ctl) {
   if (run_done(ctl)) return;
+  const bool band = band_graph(g);
   __shared__ unsigned sh[kRadixBins];
   const int nb = pass == 2 ? 256 : kRadixBins;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
@@ -1209,6 +1211,7 @@ static __global__ void __launch_bounds__(kBlock) k_radix_hist(const float* res, 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (4 * q + k >= D) break;
+      if (band && !edge_owned(g, 4 * q + k)) continue;
       const uint32_t key = float_key(rr[k]);
       if (pass == 0) {
         atomicAdd(&sh[key >> 20], 1u);
@@ -1284,14 +1287,15 @@ static __global__ void __launch_bounds__(1024) k_radix_scan(unsigned* hist, int 
 constexpr uint32_t kTieChunk = 8192;
 
 // per-chunk count of keys equal to the threshold (only when not all ties are taken)
-static __global__ void __launch_bounds__(kBlock) k_tie_count(const float* res, uint32_t D, unsigned* chunk_cnt,
-                                                      Ctl* ctl) {
+static __global__ void __launch_bounds__(kBlock) k_tie_count(DevGraph g, const float* res, uint32_t D,
+                                                      unsigned* chunk_cnt, Ctl* ctl) {
+  const bool band = band_graph(g);
   if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
   const uint32_t key = ctl->rx_prefix;
   const size_t c0 = static_cast<size_t>(blockIdx.x) * kTieChunk;
   unsigned n = 0;
   for (size_t d = c0 + threadIdx.x; d < c0 + kTieChunk && d < D; d += blockDim.x)
-    n += float_key(res[d]) == key;
+    n += float_key(res[d]) == key && (!band || edge_owned(g, static_cast<uint32_t>(d)));
   __shared__ unsigned sh[kBlock / 32];
   const unsigned tot = block_sum(n, sh);
   if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = tot;
@@ -1347,6 +1351,7 @@ __global__ void __launch_bounds__(kBlock) k_rbp_commit(DevGraph g, float* live, 
   if (blockIdx.x == 0 && threadIdx.x == 0 && commit) ctl->dense = dense;
   fl.init();
   const uint32_t key = ctl->rx_prefix;
+  const bool band = band_graph(g);
   const bool rank_ties = !select_all && ctl->rx_need != ctl->rx_ties;
   const unsigned need = ctl->rx_need;
   const uint32_t stamp = ctl->stamp;
@@ -1359,7 +1364,7 @@ __global__ void __launch_bounds__(kBlock) k_rbp_commit(DevGraph g, float* live, 
   const size_t c0 = static_cast<size_t>(blockIdx.x) * kTieChunk;
   for (size_t base = c0; base < c0 + kTieChunk && base < g.D; base += blockDim.x) {
     const size_t di = base + threadIdx.x;
-    const bool valid = di < g.D && di < c0 + kTieChunk;
+    const bool valid = di < g.D && di < c0 + kTieChunk && (!band || edge_owned(g, static_cast<uint32_t>(di)));
     const float r = valid ? res[di] : 0.f;
     const uint32_t k = float_key(r);
     bool take = valid && (select_all || k > key);

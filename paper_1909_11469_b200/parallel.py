@@ -32,7 +32,7 @@ from dataclasses import dataclass
 from . import (_Config, _DevOpts, _Result, _check, _lib, GRAPH_TRUSTED, PairwiseMRF, SchedulerConfig,
                SchedulerKind)
 
-__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "BandRnBP", "NcclExchange",
+__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "BandRnBP", "BandRBP", "NcclExchange",
            "LocalExchange", "NcclComm", "LocalComm", "run_band_lbp", "run_band_rnbp"]
 
 
@@ -186,6 +186,16 @@ class BandRnBP(BandLBP):
         _check(_lib.bp_band_rnbp_fallback(self._e, global_d))
 
 
+class BandRBP(BandRnBP):
+    """RBP on one band with a per-partition local frontier: the band's top
+    k = max(1, llround(p * owned directed edges)) residuals."""
+
+    KIND = SchedulerKind.rbp
+
+    def select(self, attempt: int = 0):
+        _check(_lib.bp_band_rbp_select(self._e))
+
+
 class NcclComm:
     """Collectives of one band per process (torch.distributed, NCCL between GPUs)."""
 
@@ -248,9 +258,10 @@ class LocalComm:
 
 
 def run_band_rnbp(bands, comm, max_iterations: int) -> BandStatus:
-    """The run() loop of RnBP over row bands (schedulers.cpp:301-347 with
-    rnbp_frontier, :194-216): `bands` are this process's bands (one per GPU
-    with NcclComm, all of them with LocalComm)."""
+    """The run() loop of RnBP (or RBP, BandRBP) over row bands
+    (schedulers.cpp:301-347 with rnbp_frontier :194-216 / rbp_frontier
+    :122-126): `bands` are this process's bands (one per GPU with NcclComm, all
+    of them with LocalComm)."""
     import torch
 
     def phase(attempt):
@@ -276,7 +287,8 @@ def run_band_rnbp(bands, comm, max_iterations: int) -> BandStatus:
             return st
         phase(0)
         delta, frontier, survivors = (int(x) for x in bands[0].count[:3].tolist())
-        if frontier == 0 and survivors > 0:  # retry once, then one survivor (schedulers.cpp:204-214)
+        rnbp = bands[0].KIND == SchedulerKind.rnbp
+        if rnbp and frontier == 0 and survivors > 0:  # retry once, then one survivor (schedulers.cpp:204-214)
             phase(1)
             frontier = int(bands[0].count[1].item())
             if frontier == 0:
