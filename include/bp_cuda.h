@@ -277,6 +277,10 @@ BP_API int bp_band_rnbp_refresh(struct bp_engine* e);
  * finish exactly as RnBP (no retry).  Per-partition local frontiers (SURVEY
  * 8(e)): differs from the global select_top_k when P > 1, by design. */
 BP_API int bp_band_rbp_select(struct bp_engine* e);
+/* Residual Splash on a band: local splashes (roots and claims on owned
+ * vertices, k = max(1, llround(p * owned vertices))) + commit + pack; then as
+ * RnBP.  Per-partition local frontiers, by design. */
+BP_API int bp_band_rs_select(struct bp_engine* e);
 BP_API int bp_band_rnbp_finish(struct bp_engine* e);
 BP_API int bp_band_survivors(struct bp_engine* e, uint64_t* global_ids, uint64_t cap, uint64_t* n);
 BP_API int bp_band_rnbp_fallback(struct bp_engine* e, uint64_t global_d);

@@ -175,6 +175,7 @@ def _load():
         "bp_band_rnbp_select": (C.c_int, [P, C.c_uint32]),
         "bp_band_rnbp_refresh": (C.c_int, [P]),
         "bp_band_rbp_select": (C.c_int, [P]),
+        "bp_band_rs_select": (C.c_int, [P]),
         "bp_band_rnbp_finish": (C.c_int, [P]),
         "bp_band_survivors": (C.c_int, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
         "bp_band_rnbp_fallback": (C.c_int, [P, C.c_uint64]),

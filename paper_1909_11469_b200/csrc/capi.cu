@@ -291,6 +291,10 @@ int bp_band_rbp_select(bp_engine* e) {
   if (!e) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] { e->e->band_rbp_select(); });
 }
+int bp_band_rs_select(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->band_rs_select(); });
+}
 int bp_band_rnbp_refresh(bp_engine* e) {
   if (!e) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] { e->e->band_rnbp_refresh(); });

@@ -44,6 +44,7 @@ class EngineBase {
   virtual void band_commit_global(uint64_t global_d) = 0;  // UINT64_MAX: nothing to commit here
   virtual void band_rnbp_pack() = 0;
   virtual void band_rbp_select() = 0;
+  virtual void band_rs_select() = 0;
   virtual void band_sweep() = 0;
   virtual void band_finish() = 0;
   virtual void band_status(bp_run_result* r) = 0;

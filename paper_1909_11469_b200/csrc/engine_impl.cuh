@@ -533,8 +533,7 @@ class EngineT final : public EngineBase {
   void band_config(const PartHalo& h, uint64_t owned_directed) override {
     if (QS != 1 || !g_.lat_cols || g_.par_mode != 1)
       throw Error(BP_ERR_UNSUPPORTED, "row-band partition needs a binary Ising lattice band");
-    if (cfg_.kind != BP_LBP && cfg_.kind != BP_RNBP && cfg_.kind != BP_RBP)
-      throw Error(BP_ERR_UNSUPPORTED, "row-band partition: LBP, RnBP and RBP");
+    if (cfg_.kind == BP_SERIAL_RBP) throw Error(BP_ERR_UNSUPPORTED, "row-band partition: not for serial RBP");
     halo_ = h;
     halo_.ghost_up = g_.cnt_row0 > 0 ? 1u : 0u;
     halo_.ghost_down = g_.cnt_row1 < g_.lat_rows ? 1u : 0u;
@@ -574,7 +573,7 @@ class EngineT final : public EngineBase {
   }
   unsigned band_cols_grid() const { return static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock); }
   void band_rnbp_begin() override {
-    if (cfg_.kind != BP_RNBP && cfg_.kind != BP_RBP) throw_invalid("band frontier API on an LBP engine");
+    if (cfg_.kind == BP_LBP) throw_invalid("band frontier API on an LBP engine");
     band_start_common();
     k_vertex_update<QS, kModeInit, false, false, false>
         <<<vgrid(k_vertex_update<QS, kModeInit, false, false, false>, g_.V), kBlock, 0, s_>>>(
@@ -603,6 +602,16 @@ class EngineT final : public EngineBase {
     k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
     launch_check();
     ++launches_;
+  }
+  // RS on a band: local splashes, k = max(1, llround(p owned vertices))
+  void band_rs_select() override {
+    const uint64_t vown = static_cast<uint64_t>(g_.cnt_row1 - g_.cnt_row0) * g_.lat_cols;
+    const long long kr = std::llround(cfg_.p * static_cast<double>(vown));
+    ensure_rs(cfg_.splash_depth);
+    launch_rs(kr < 1 ? 1ull : static_cast<unsigned long long>(kr), cfg_.splash_depth, 1);
+    k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
+    launch_check();
+    launches_ += 2;
   }
   void band_rnbp_refresh() override {
     k_part_unpack_flag<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), ctl(), vflag_.as<uint32_t>(),

@@ -346,6 +346,15 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
   const unsigned long long k = prm.k;
   const uint32_t h = prm.h;
   const uint32_t stamp = __ldcg(&ctl->stamp);
+  // row-band partition: splashes are local to the band (roots and claims on
+  // owned vertices only; SURVEY 8(e) per-partition local frontiers)
+  const bool band = band_graph(g);
+  auto vown = [&](uint32_t v) {
+    if (!band) return true;
+    const uint32_t row = v / g.lat_cols;
+    return row >= g.cnt_row0 && row < g.cnt_row1;
+  };
+  const uint32_t Vown = band ? (min(g.cnt_row1, g.lat_rows) - g.cnt_row0) * g.lat_cols : V;
 
   // P0: vertex residuals (vertex_residual, schedulers.cpp:128-134) + reset
   for (uint32_t v = tid; v < V; v += stride) {
@@ -359,7 +368,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
   if (tid == 0) {
     const unsigned long long m0 = k * 4ull < 1024ull ? 1024ull : k * 4ull;
     rc->k = k;
-    rc->M = static_cast<unsigned>(m0 < V ? m0 : V);
+    rc->M = static_cast<unsigned>(m0 < Vown ? m0 : Vown);
     rc->ncand = rc->nbuilt = rc->nready = rc->nkept = rc->unres = 0;
     rc->rounds = rc->passes = 0;
     rc->edges = 0;
@@ -376,7 +385,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
         grid, V, M,
         [&](uint32_t v, uint32_t& key) {
           key = __float_as_uint(__ldcg(&b.vres[v]));
-          return true;
+          return vown(v);
         },
         [&](uint32_t v) {
           if (__ldcg(&b.state[v]) == kRsNone) {
@@ -455,7 +464,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
           if (dv < h) {
             for (uint32_t a = g.in_off[v]; a < g.in_off[v + 1]; ++a) {
               const uint32_t w = g.ep[g.in_adj[a]];
-              if (__ldcg(&b.claimed[w]) == kUncl) {
+              if (__ldcg(&b.claimed[w]) == kUncl && vown(w)) {
                 b.claimed[w] = r;
                 b.depth[w] = dv + 1;
                 b.spos[w] = n++;
@@ -499,9 +508,9 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       grid.sync();
     }
     const unsigned nbuilt = __ldcg(&rc->nbuilt), Mc = __ldcg(&rc->M);
-    if (nbuilt >= k || Mc >= V) break;
+    if (nbuilt >= k || Mc >= Vown) break;
     grid.sync();
-    if (tid == 0) rc->M = static_cast<unsigned>(min(static_cast<unsigned long long>(V), 4ull * Mc));
+    if (tid == 0) rc->M = static_cast<unsigned>(min(static_cast<unsigned long long>(Vown), 4ull * Mc));
     grid.sync();
   }
 

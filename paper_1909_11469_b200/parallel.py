@@ -32,7 +32,7 @@ from dataclasses import dataclass
 from . import (_Config, _DevOpts, _Result, _check, _lib, GRAPH_TRUSTED, PairwiseMRF, SchedulerConfig,
                SchedulerKind)
 
-__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "BandRnBP", "BandRBP", "NcclExchange",
+__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "BandRnBP", "BandRBP", "BandRS", "NcclExchange",
            "LocalExchange", "NcclComm", "LocalComm", "run_band_lbp", "run_band_rnbp"]
 
 
@@ -194,6 +194,16 @@ class BandRBP(BandRnBP):
 
     def select(self, attempt: int = 0):
         _check(_lib.bp_band_rbp_select(self._e))
+
+
+class BandRS(BandRnBP):
+    """Residual Splash on one band with per-partition local splashes (roots and
+    claims on owned vertices, k = max(1, llround(p * owned vertices)))."""
+
+    KIND = SchedulerKind.rs
+
+    def select(self, attempt: int = 0):
+        _check(_lib.bp_band_rs_select(self._e))
 
 
 class NcclComm:

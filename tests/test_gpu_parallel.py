@@ -102,3 +102,29 @@ def test_band_rbp_local_frontiers_converge_to_the_fixed_point(bp, orc, nparts):
     want = np.asarray(o.beliefs).reshape(n, n, 2)
     for b in bands:
         assert np.max(np.abs(b.owned_beliefs() - want[b.info.row0:b.info.row1])) <= 1e-4
+
+
+def test_band_rs_single_band_equals_unpartitioned(bp):
+    n, c, seed = 14, 2.0, 3
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=1 / 16, splash_depth=2, max_iterations=3000)
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)), cfg)
+    (b,) = bands = [par.BandRS(n, c, seed, 0, 1, cfg, 0)]
+    st = par.run_band_rnbp(bands, par.LocalComm(), cfg.max_iterations)
+    assert st.converged == full.converged and st.iterations == full.iterations
+    assert st.messages_updated_total == full.messages_updated_total
+    assert np.array_equal(b.owned_beliefs(), full.beliefs.values.reshape(n, n, 2))
+
+
+@pytest.mark.parametrize("nparts", [2, 4])
+def test_band_rs_local_splashes_converge_to_the_fixed_point(bp, orc, nparts):
+    from oracle import pyoracle as po
+    from tests.helpers import oracle_config
+    n, c, seed = 16, 1.5, 5
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=1 / 16, splash_depth=2, max_iterations=20000)
+    o = po.run(po.Graph.ising(orc, n, c, seed), oracle_config(cfg))
+    bands = [par.BandRS(n, c, seed, p, nparts, cfg, 0) for p in range(nparts)]
+    st = par.run_band_rnbp(bands, par.LocalComm(), cfg.max_iterations)
+    assert st.converged and o.converged
+    want = np.asarray(o.beliefs).reshape(n, n, 2)
+    for b in bands:
+        assert np.max(np.abs(b.owned_beliefs() - want[b.info.row0:b.info.row1])) <= 1e-4
