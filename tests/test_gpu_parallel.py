@@ -128,3 +128,20 @@ def test_band_rs_local_splashes_converge_to_the_fixed_point(bp, orc, nparts):
     want = np.asarray(o.beliefs).reshape(n, n, 2)
     for b in bands:
         assert np.max(np.abs(b.owned_beliefs() - want[b.info.row0:b.info.row1])) <= 1e-4
+
+
+def test_band_loops_through_nccl_torchrun():
+    """The NCCL transport path (NcclExchange / NcclComm on the band's external
+    stream) under torchrun; world size = the GPUs present (1 here)."""
+    import os
+    import subprocess
+    import sys
+
+    import torch
+    ngpu = torch.cuda.device_count()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ngpu}",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(root, "tools", "band_nccl_check.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert "OK" in p.stdout, p.stdout + p.stderr[-2000:]
