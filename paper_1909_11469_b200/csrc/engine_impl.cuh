@@ -672,7 +672,6 @@ class EngineT final : public EngineBase {
     const unsigned gi = grid_cap(static_cast<size_t>(g_.D) * QS);
     timed(kKInit, [&] { k_init_messages<QS><<<gi, kBlock, 0, s_>>>(dg_, live(), ctl(), 1); });
     launch_check();
-    const unsigned gv = grid_cap(g_.V);
     if (lbp) {  // sweep 0 (ResidualTracker ctor, residuals.cpp:9-24)
       enqueue_lbp_sweep();
       enqueue_finalize(kFinLbp);
@@ -691,7 +690,6 @@ class EngineT final : public EngineBase {
   }
 
   void enqueue_refresh(int fin) {
-    const unsigned gv = grid_cap(g_.V);
     timed(kKUpdate, [&] {
       if (use_clist_)
         k_vertex_update<QS, kModeDelta, true, false, true><<<vgrid(k_vertex_update<QS, kModeDelta, true, false, true>, g_.V), kBlock, 0, s_>>>(
