@@ -452,7 +452,63 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       grid.sync();
       // B: build the ready splashes (build_splash, schedulers.cpp:136-167); clear the balls
       const uint32_t nr = __ldcg(&rc->nready);
-      for (uint32_t i = tid; i < nr; i += stride) {
+      if (wl) {
+        // one warp per ready root: the lanes scan a vertex's CSR neighbours and
+        // claim in lane (= CSR) order, so the visit order is build_splash's
+        for (uint32_t i = gw; i < nr; i += nw) {
+          const uint32_t r = __ldcg(&b.rlist[i]);
+          if (lane == 0) {
+            b.claimed[r] = r;
+            b.spos[r] = 0;
+            b.depth[r] = 0;
+            b.qnext[r] = kUncl;
+          }
+          __syncwarp();
+          uint32_t tail = r, n = 1;
+          for (uint32_t v = r; v != kUncl;) {
+            const uint32_t dv = b.depth[v];
+            if (dv < h) {
+              const uint32_t a0 = g.in_off[v], a1 = g.in_off[v + 1];
+              for (uint32_t base = a0; base < a1; base += 32) {
+                const uint32_t a = base + lane;
+                uint32_t w = kUncl;
+                bool cand = false;
+                if (a < a1) {
+                  w = g.ep[g.in_adj[a]];
+                  cand = __ldcg(&b.claimed[w]) == kUncl && vown(w);
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, cand);
+                if (m) {
+                  const unsigned below = m & ((1u << lane) - 1u);
+                  const int prev_lane = below ? 31 - __clz(below) : 0;
+                  const uint32_t wp = __shfl_sync(0xffffffffu, w, prev_lane);
+                  if (cand) {
+                    b.claimed[w] = r;
+                    b.depth[w] = dv + 1;
+                    b.spos[w] = n + __popc(below);
+                    b.qnext[w] = kUncl;
+                    b.qnext[below ? wp : tail] = w;
+                  }
+                  tail = __shfl_sync(0xffffffffu, w, 31 - __clz(m));
+                  n += __popc(m);
+                }
+                __syncwarp();
+              }
+            }
+            __syncwarp();
+            v = b.qnext[v];
+          }
+          if (lane == 0) {
+            b.state[r] = kRsBuilt;
+            b.blist[atomicAdd(&rc->nbuilt, 1u)] = r;
+          }
+          warp_ball(r, [&](uint32_t w) {
+            b.ballmax[w] = 0ull;
+            return true;
+          });
+        }
+      }
+      for (uint32_t i = tid; i < (wl ? 0u : nr); i += stride) {
         const uint32_t r = __ldcg(&b.rlist[i]);
         b.claimed[r] = r;
         b.spos[r] = 0;
@@ -539,11 +595,51 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
   // live buffer stays the pre-step snapshot for every other splash.
   const unsigned nk = __ldcg(&rc->nkept);
   unsigned long long edges = 0;
-  for (uint32_t i = tid; i < nk; i += stride) {
-    const uint32_t r = __ldcg(&b.klist[i]);
-    for (uint32_t v = r; v != kUncl; v = __ldcg(&b.qnext[v])) {
-      splash_vertex_update<QS>(g, v, r, live, b.shadow, b.claimed, b.spos, &ctl->numeric_error);
-      edges += g.in_off[v + 1] - g.in_off[v];
+  // binary graphs: a warp per splash, lanes over the incoming edges of each
+  // visited vertex (cavity sums by warp reduction); otherwise a thread per splash
+  const bool wsplash = QS == 1;
+  const uint32_t wlane = threadIdx.x & 31u, wgw = tid >> 5, wnw = stride >> 5;
+  if (wsplash) {
+    for (uint32_t i = wgw; i < nk; i += wnw) {
+      const uint32_t r = __ldcg(&b.klist[i]);
+      for (uint32_t v = r; v != kUncl; v = __ldcg(&b.qnext[v])) {
+        const uint32_t a0 = g.in_off[v], a1 = g.in_off[v + 1];
+        const uint32_t pv = __ldcg(&b.spos[v]);
+        auto msg_in = [&](uint32_t in) {
+          const uint32_t k = g.ep[in];
+          const bool ov = __ldcg(&b.claimed[k]) == r && __ldcg(&b.spos[k]) < pv;
+          return ov ? b.shadow[in] : live[in];
+        };
+        // cavity total in CSR order (unary first), exactly as the refresh
+        // kernels sum it, so a fixed point stays bitwise stable: the lanes load
+        // in parallel, the accumulation walks the lanes in order
+        float T = g.unary_lo[v];
+        for (uint32_t base = a0; base < a1; base += 32) {
+          const float m = base + wlane < a1 ? msg_in(g.in_adj[base + wlane]) : 0.f;
+          const uint32_t cnt = min(32u, a1 - base);
+          for (uint32_t j = 0; j < cnt; ++j) T += __shfl_sync(0xffffffffu, m, j);
+        }
+        bool bad = false;
+        for (uint32_t base = a0; base < a1; base += 32) {
+          if (base + wlane < a1) {
+            const uint32_t in = g.in_adj[base + wlane], out = in ^ 1u;
+            const float lnew = binary_msg(g, T - msg_in(in), out);
+            bad |= !(fabsf(lnew) < INFINITY);
+            b.shadow[out] = lnew;
+          }
+        }
+        if (bad) ctl->numeric_error = 1u;
+        if (wlane == 0) edges += a1 - a0;
+        __syncwarp();
+      }
+    }
+  } else {
+    for (uint32_t i = tid; i < nk; i += stride) {
+      const uint32_t r = __ldcg(&b.klist[i]);
+      for (uint32_t v = r; v != kUncl; v = __ldcg(&b.qnext[v])) {
+        splash_vertex_update<QS>(g, v, r, live, b.shadow, b.claimed, b.spos, &ctl->numeric_error);
+        edges += g.in_off[v + 1] - g.in_off[v];
+      }
     }
   }
   edges = warp_sum(edges);
@@ -554,7 +650,21 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
   grid.sync();
   // P6: commit_shadow + touched flags (every vertex of a splash and its neighbours)
   const bool dense = __ldcg(&rc->dense) != 0u;
-  for (uint32_t i = tid; i < nk; i += stride) {
+  if (wsplash) {  // same splash -> warp mapping as P5: the shadow writes are this warp's own
+    for (uint32_t i = wgw; i < nk; i += wnw) {
+      const uint32_t r = __ldcg(&b.klist[i]);
+      for (uint32_t v = r; v != kUncl; v = __ldcg(&b.qnext[v])) {
+        if (wlane == 0) rs_flag(v, vflag, vlist, &ctl->nflag, stamp, dense);
+        const uint32_t a0 = g.in_off[v], a1 = g.in_off[v + 1];
+        for (uint32_t a = a0 + wlane; a < a1; a += 32) {
+          const uint32_t in = g.in_adj[a], out = in ^ 1u;
+          live[out] = b.shadow[out];
+          rs_flag(g.ep[in], vflag, vlist, &ctl->nflag, stamp, dense);
+        }
+      }
+    }
+  }
+  for (uint32_t i = tid; i < (wsplash ? 0u : nk); i += stride) {
     const uint32_t r = __ldcg(&b.klist[i]);
     for (uint32_t v = r; v != kUncl; v = __ldcg(&b.qnext[v])) {
       rs_flag(v, vflag, vlist, &ctl->nflag, stamp, dense);
