@@ -74,7 +74,10 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       cgp::this_grid().sync();
   };
   const uint32_t stride = gridDim.x * blockDim.x;
-  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  // the bookkeeping thread lives in the LAST CTA, which rarely holds list work
+  // (lists are short and start at CTA 0), so its global writes stay off the
+  // critical path of the iteration
+  const bool lead = blockIdx.x == gridDim.x - 1 && threadIdx.x == 0;
   // replicated loop state (identical in every thread of every CTA)
   if (ctl->done || ctl->cl_state != 2u) return;
   unsigned long long it = ctl->iteration;
@@ -154,8 +157,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         kp.flush(kPersistBlock);
         fl.flush(kPersistBlock);
       }
-      kp.flush(0);
-      fl.flush(0);
+      flush2(kp, fl);
       block_add_pacc(acc, c);
     }
     mark(0);
