@@ -30,7 +30,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libbp_b200.so")
+_LIB_PATH = os.environ.get("BPB_LIB") or os.path.join(_HERE, "libbp_b200.so")  # BPB_LIB: A/B builds
 
 
 def library_path() -> str:

@@ -27,27 +27,40 @@ namespace bpb {
 namespace cgp = cooperative_groups;
 
 constexpr int kPersistBlock = 512;
+// candidate-list length below which the tail runs on one 16-CTA cluster
+// (cluster barrier ~0.35 us vs grid barrier ~1.3 us, but 16 SMs instead of
+// 148 share the list: measured at 115 entries cluster 8.9 vs grid 11.5
+// us/iteration, at 6443 entries 12.0 vs 10.8)
+constexpr uint32_t kPersistClusterList = 2048;
 
-// block reduction of the per-iteration contributions into acc[0..5]
-__device__ __forceinline__ void block_add_pacc(unsigned long long* accum, const Contrib& c) {
-  __shared__ unsigned long long sh[6][kPersistBlock / 32];
-  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  unsigned long long v[6] = {static_cast<unsigned long long>(c.delta), c.count, c.frontier, c.survivors,
-                             c.evals, c.visits};
+// Per-iteration contributions: one redux.sync per value and warp, summed in
+// shared memory (s_pacc), pushed to acc[0..5] by threads 0..5 after the next
+// block barrier (pacc_push).  The warp sums fit 32 bits (a warp touches at
+// most a few thousand entries per iteration, a CTA a few hundred thousand).
+__device__ __forceinline__ void warp_contrib(unsigned* s_pacc, const Contrib& c) {
+  const int d = __reduce_add_sync(0xffffffffu, static_cast<int>(c.delta));
+  const unsigned v[5] = {__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c.count)),
+                         __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c.frontier)),
+                         __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c.survivors)),
+                         __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c.evals)),
+                         __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c.visits))};
+  if ((threadIdx.x & 31u) == 0) {
+    if (d) atomicAdd(reinterpret_cast<int*>(&s_pacc[0]), d);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) v[k] = warp_sum(v[k]);
-  __syncthreads();
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < 6; ++k) sh[k][wid] = v[k];
-  __syncthreads();
-  if (wid == 0) {
-    const unsigned nw = blockDim.x >> 5;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      unsigned long long x = lane < nw ? sh[k][lane] : 0ull;
-      x = warp_sum(x);
-      if (lane == 0 && x) atomicAdd(&accum[k], x);
+    for (int k = 0; k < 5; ++k)
+      if (v[k]) atomicAdd(&s_pacc[k + 1], v[k]);
+  }
+}
+// after a block barrier that follows every warp_contrib of the phase
+__device__ __forceinline__ void pacc_push(unsigned* s_pacc, unsigned long long* accum) {
+  if (threadIdx.x < 6) {
+    const unsigned x = s_pacc[threadIdx.x];
+    if (x) {  // slot 0 (unconverged delta) is signed: sign-extend
+      const unsigned long long w = threadIdx.x == 0 ? static_cast<unsigned long long>(static_cast<long long>(
+                                                          static_cast<int>(x)))
+                                                    : static_cast<unsigned long long>(x);
+      atomicAdd(&accum[threadIdx.x], w);
+      s_pacc[threadIdx.x] = 0u;
     }
   }
 }
@@ -74,12 +87,20 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       cgp::this_grid().sync();
   };
   const uint32_t stride = gridDim.x * blockDim.x;
+  // Entry slot of this thread within a stride: consecutive 32-entry chunks go
+  // to the same warp slot of consecutive CTAs, so a short list spreads over
+  // every SM (latency, not one SM's L1/L2 request rate, bounds the phase)
+  // while each warp still reads a contiguous chunk.  The trip count stays
+  // block-uniform (the stagers flush at block barriers).
+  const uint32_t spread = (((threadIdx.x >> 5) * gridDim.x + blockIdx.x) << 5) + (threadIdx.x & 31u);
   // the bookkeeping thread lives in the LAST CTA, which rarely holds list work
   // (lists are short and start at CTA 0), so its global writes stay off the
   // critical path of the iteration
   const bool lead = blockIdx.x == gridDim.x - 1 && threadIdx.x == 0;
   // replicated loop state (identical in every thread of every CTA)
   if (ctl->done || ctl->cl_state != 2u) return;
+  __shared__ unsigned s_pacc[6];  // per-CTA sums of one phase (32 bits suffice)
+  if (threadIdx.x < 6) s_pacc[threadIdx.x] = 0u;
   unsigned long long it = ctl->iteration;
   unsigned unc = ctl->unconverged, prev = ctl->prev_unconverged, has_prev = ctl->has_prev;
   uint32_t stamp = ctl->stamp;
@@ -98,9 +119,13 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     ctl->time_stop = 0u;
   }
   sync_all();
-  unsigned long long tclk = lead ? globaltimer_ns() : 0ull;
-  auto mark = [&](int k) {  // phase clock of CTA 0 (profiling aid, one timer read per phase)
-    if (lead) {
+  uint32_t list_n = ctl->cl_n[cur];
+  // phase clock of CTA 0, the CTA that holds the most list work (profiling
+  // aid, one timer read per phase)
+  const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long tclk = clk ? globaltimer_ns() : 0ull;
+  auto mark = [&](int k) {
+    if (clk) {
       const unsigned long long t = globaltimer_ns();
       ctl->phase_ns[k] += t - tclk;
       tclk = t;
@@ -112,7 +137,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     unsigned* nfl = &ctl->nfl2[fb];
     // ---- select + commit over the candidate list (rnbp_frontier attempt 0)
     {
-      const uint32_t n = ctl->cl_n[cur];
+      const uint32_t n = list_n;
       const uint32_t* list = cur ? cl.list[1] : cl.list[0];
       uint32_t* keep = cur ? cl.list[0] : cl.list[1];
       unsigned long long thresh = th_high;  // select_parallelism (schedulers.cpp:218-224)
@@ -130,8 +155,8 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       kp.init();
       fl.init();
       Contrib c;
-      for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
-        const uint32_t i = base + threadIdx.x;
+      for (uint32_t base = 0; base < n; base += stride) {
+        const uint32_t i = base + spread;
         bool nf = false, kept = false;
         uint32_t tg = 0, d = 0;
         if (i < n) {
@@ -157,8 +182,10 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         kp.flush(kPersistBlock);
         fl.flush(kPersistBlock);
       }
-      flush2(kp, fl);
-      block_add_pacc(acc, c);
+      mark(7);
+      warp_contrib(s_pacc, c);
+      flush2(kp, fl);  // its first barrier orders the warp sums
+      pacc_push(s_pacc, acc);
     }
     mark(0);
     sync_all();
@@ -195,8 +222,8 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       st.init();
       int cnt = 0;
       unsigned long long evals = 0, visits = 0;
-      for (uint32_t base = blockIdx.x * blockDim.x; base < nv; base += stride) {
-        const uint32_t i = base + threadIdx.x;
+      for (uint32_t base = 0; base < nv; base += stride) {
+        const uint32_t i = base + spread;
         if (i < nv) {
           cnt += vertex_update<QS, kModeDelta, true, false>(g, vlist[i], live, cand, res, eps, &ctl->numeric_error,
                                                             evals, cl.inlist, &st, true);
@@ -205,8 +232,6 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         st.flush(1024);
       }
       mark(4);
-      st.flush(0);
-      mark(5);
       Contrib c;
       c.delta = cnt;
       c.evals = evals;
@@ -214,7 +239,10 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       // per vertex: list id + unary; per message: edge pair (in + old out),
       // coupling, candidate write, residual read + write
       c.count = 8ull * visits + static_cast<unsigned long long>(8 * QS + 4 + 4 * QS + 8) * evals;
-      block_add_pacc(acc, c);
+      warp_contrib(s_pacc, c);
+      st.flush(0);  // its first barrier orders the warp sums
+      mark(5);
+      pacc_push(s_pacc, acc);
       mark(6);
       if (lead && globaltimer_ns() - ctl->t0_ns >= ctl->time_limit_ns) ctl->time_stop = 1u;
     }
@@ -228,6 +256,9 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     prev = start;  // set_prev_unconverged (schedulers.cpp:327)
     has_prev = 1u;
     msgs += frontier;
+    // the list refilled this iteration: loaded with the other finalize reads,
+    // reused by the next select
+    const uint32_t next_n = ctl->cl_n[cur ^ 1u];
     const bool numeric = ctl->numeric_error != 0u;
     const bool tstop = ctl->time_stop != 0u;
     if (lead) {
@@ -256,8 +287,13 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       reason = kStopTime;
     }
     mark(3);
-    if (done) {
-      if (lead) {  // mirror the final state for the host
+    // barrier flavour no longer fits the list length: hand back to the host,
+    // which relaunches with the other one (hysteresis around the host's
+    // kPersistClusterList choice)
+    list_n = next_n;
+    const bool switch_mode = CLUSTER ? next_n > 2u * kPersistClusterList : next_n < kPersistClusterList / 2u;
+    if (done || switch_mode) {
+      if (lead) {  // mirror the loop state for the host
         ctl->iteration = it;
         ctl->unconverged = unc;
         ctl->prev_unconverged = prev;
@@ -267,9 +303,11 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         ctl->msgs_total = msgs;
         ctl->frontier = 0;
         ctl->nflag = 0;
-        ctl->done = 1u;
-        ctl->converged = reason == kStopConverged ? 1u : 0u;
-        ctl->stop_reason = reason;
+        if (done) {
+          ctl->done = 1u;
+          ctl->converged = reason == kStopConverged ? 1u : 0u;
+          ctl->stop_reason = reason;
+        }
       }
       return;
     }
