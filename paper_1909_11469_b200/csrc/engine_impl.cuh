@@ -880,7 +880,9 @@ class EngineT final : public EngineBase {
   // while the candidate list is short, else on a cooperative grid of one CTA
   // per SM.
   // BPB_PERSIST_GRID / BPB_PERSIST_CLUSTER override the choice (tuning).
+  DevBuf vslot_;  // refresh slots of the persistent tail (one per candidate-list entry)
   void run_persist_loop(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
+    if (!vslot_.p) vslot_.alloc(static_cast<size_t>(dg_.D) * 4);
     if (!persist_grid_) {
       int per_sm = 0;
       cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rnbp_persist<QS, false>, kPersistBlock, 0),
@@ -919,11 +921,11 @@ class EngineT final : public EngineBase {
       timed(kKPersist, [&] {
         if (cluster)
           cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, true>, dg_, live(), cand(), res_.as<float>(),
-                                        vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
+                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
                      "persistent cluster launch");
         else
           cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, false>, dg_, live(), cand(), res_.as<float>(),
-                                        vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
+                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
                      "persistent launch");
       });
       fetch_ctl_header();

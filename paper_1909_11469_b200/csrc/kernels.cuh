@@ -482,13 +482,13 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
     }
   };
   // emit with prefetched residual / in-list flag
-  auto emit_pre = [&](uint32_t in, float2 pr, float r_was, bool in_list) {
+  auto emit_pre = [&](uint32_t in, float2 pr, float r_was, bool in_list, float a) {
     const uint32_t out = in ^ 1u;
     const float m_in = (in & 1u) ? pr.y : pr.x;
     const float m_old = (in & 1u) ? pr.x : pr.y;
     float lnew, r;
     if (g.par_mode) {
-      r = ising_update(T - m_in, __ldg(&g.ising_a[out >> 1]), m_old, lnew);
+      r = ising_update(T - m_in, a, m_old, lnew);
     } else {
       lnew = binary_msg(g, T - m_in, out);
       r = binary_residual(lnew, m_old);
@@ -522,11 +522,12 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
         has[2] ? 2u * (last ? row + c : row + 2u * c) + 1u : 0u,
         has[3] ? 2u * (row + 2u * c + (c + 1u < C ? 1u : 0u)) + 1u : 0u};
     float2 prs[4];
-    float rw[4];
+    float rw[4], ia[4];
     bool il[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       prs[k] = has[k] ? ldm<NC>(&A2[ins[k] >> 1]) : make_float2(0.f, 0.f);
+      ia[k] = (g.par_mode && has[k]) ? __ldg(&g.ising_a[ins[k] >> 1]) : 0.f;  // with the pair loads
       // prefetch the per-message state so the four updates do not serialise
       // on (possibly aliasing) loads between their stores
       rw[k] = (MODE == kModeDelta && has[k]) ? res[ins[k] ^ 1u] : 0.f;
@@ -537,7 +538,7 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if (has[k]) {
-        emit_pre(ins[k], prs[k], rw[k], il[k]);
+        emit_pre(ins[k], prs[k], rw[k], il[k], ia[k]);
         ++deg;
       }
   } else {
@@ -791,6 +792,8 @@ __device__ __forceinline__ int vertex_update(const DevGraph& g, uint32_t v, cons
 // index held on the device (A = buf[s & 1], B = buf[(s + 1) & 1]).
 // CL: maintain the RnBP candidate list (init appends to list cl_cur, the
 // refresh to list cl_cur ^ 1, which the select of this iteration is filling).
+constexpr uint32_t kSlotEmpty = 0xffffffffu;  // hole of a slot list (persistent tail)
+
 struct CandList {
   uint32_t* list[2];
   uint8_t* inlist;
@@ -1055,7 +1058,13 @@ template <int QS, bool CL>
 __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live, const float* cand, float* res,
                                                  uint32_t* vflag, uint32_t* vlist, uint8_t* sel, Ctl* ctl,
                                                  float eps, const RnbpParams& prm, const CandList& cl,
-                                                 unsigned long long surv, long long* delta_out) {
+                                                 unsigned long long surv, long long* delta_out,
+                                                 const uint32_t* slots = nullptr, uint32_t slot_n = 0,
+                                                 uint32_t* vslot = nullptr) {
+  // slots != nullptr (persistent tail): the survivors are the kept entries of
+  // the slot list (kSlotEmpty holes), and a committed edge's target goes to
+  // the refresh slot of the same index (the fallback's to slot 0, which is
+  // empty whenever the fallback runs)
   __shared__ unsigned long long s_front, s_surv;
   __shared__ unsigned warp_tot[32];
   __shared__ unsigned long long running_s;
@@ -1075,10 +1084,11 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
   unsigned long long fr = 0;
   long long delta = 0;
   const bool use_list = CL && ctl->cl_state == 2u;  // survivors = the kept list
-  const uint32_t n = use_list ? ctl->cl_n[ctl->cl_cur ^ 1u] : g.D;
-  const uint32_t* list = use_list ? (ctl->cl_cur ? cl.list[0] : cl.list[1]) : nullptr;
+  const uint32_t n = slots ? slot_n : use_list ? ctl->cl_n[ctl->cl_cur ^ 1u] : g.D;
+  const uint32_t* list = slots ? slots : use_list ? (ctl->cl_cur ? cl.list[0] : cl.list[1]) : nullptr;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t d = use_list ? list[i] : i;
+    const uint32_t d = (use_list || slots) ? list[i] : i;
+    if (d == kSlotEmpty) continue;
     const float r = res[d];
     if (r >= eps && philox_u53(prm.seed, it, 1u, d + 2ull * g.edge_offset) < thresh) {
       ++fr;
@@ -1088,7 +1098,10 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
         uint32_t tg = 0;
         commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, false, c, nf, tg);
         delta += c.delta;
-        if (nf) vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
+        if (vslot)
+          vslot[i] = nf ? tg : kSlotEmpty;
+        else if (nf)
+          vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
       } else {
         sel[d] = 1;
       }
@@ -1130,7 +1143,10 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
         bool nf = false;
         uint32_t tg = 0;
         commit_edge<QS>(g, d, res[d], live, cand, res, eps, vflag, stamp, false, c, nf, tg);
-        if (nf) vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
+        if (vslot)
+          vslot[0] = nf ? tg : kSlotEmpty;
+        else if (nf)
+          vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
         atomicAdd(reinterpret_cast<unsigned long long*>(delta_out), static_cast<unsigned long long>(c.delta));
       } else {
         sel[d] = 1;

@@ -78,7 +78,7 @@ __device__ __forceinline__ void pacc_push(unsigned* s_pacc, unsigned long long* 
 // mirrors the state into Ctl and writes the trace record for the host.
 template <int QS, bool CLUSTER>
 __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, float* live, float* cand, float* res,
-                                                                uint32_t* vflag, uint32_t* vlist, Ctl* ctl,
+                                                                uint32_t* vflag, uint32_t* vslot, Ctl* ctl,
                                                                 float eps, RnbpParams prm, CandList cl) {
   auto sync_all = [] {
     if constexpr (CLUSTER)
@@ -110,12 +110,11 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
   const unsigned long long th_low = static_cast<unsigned long long>(ceil(ldexp(prm.low_p, 53)));
   const unsigned long long th_high = static_cast<unsigned long long>(ceil(ldexp(prm.high_p, 53)));
   unsigned long long msgs = ctl->msgs_total;
-  // buffers indexed by iteration: pacc3[it % 3], nfl2[it & 1]
+  // reduction buffers indexed by iteration: pacc3[it % 3]
   unsigned long long* pacc3 = ctl->pacc3[0];
   if (lead) {
     for (int b = 0; b < 3; ++b)
       for (int k = 0; k < 6; ++k) ctl->pacc3[b][k] = 0ull;
-    ctl->nfl2[0] = ctl->nfl2[1] = 0u;
     ctl->time_stop = 0u;
   }
   sync_all();
@@ -132,14 +131,16 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     }
   };
   for (;;) {
-    const unsigned pb = static_cast<unsigned>(it % 3ull), fb = static_cast<unsigned>(it & 1ull);
+    const unsigned pb = static_cast<unsigned>(it % 3ull);
     unsigned long long* acc = pacc3 + 6 * pb;
-    unsigned* nfl = &ctl->nfl2[fb];
-    // ---- select + commit over the candidate list (rnbp_frontier attempt 0)
+    // ---- select + commit over the candidate list (rnbp_frontier attempt 0).
+    // Slot form: entry i's outcome stays at index i -- list[i] keeps the edge
+    // if it stays a candidate (else kSlotEmpty), vslot[i] names the target to
+    // refresh if this commit flagged it first (else kSlotEmpty) -- so the
+    // phase needs no compaction; the refresh compacts both in one flush.
+    uint32_t* list = cur ? cl.list[1] : cl.list[0];
+    const uint32_t n = list_n;
     {
-      const uint32_t n = list_n;
-      const uint32_t* list = cur ? cl.list[1] : cl.list[0];
-      uint32_t* keep = cur ? cl.list[0] : cl.list[1];
       unsigned long long thresh = th_high;  // select_parallelism (schedulers.cpp:218-224)
       if (has_prev && prev != 0u) {
         const double ratio = static_cast<double>(unc) / static_cast<double>(prev);
@@ -148,21 +149,16 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       if (lead) {  // buffers of the NEXT iteration: last read two barriers ago
         unsigned long long* nx = pacc3 + 6 * static_cast<unsigned>((it + 1) % 3ull);
         for (int k = 0; k < 6; ++k) nx[k] = 0ull;
-        ctl->nfl2[fb ^ 1u] = 0u;
       }
-      BPB_STAGER(kp, 2048, keep, &ctl->cl_n[cur ^ 1u]);
-      BPB_STAGER(fl, 2048, vlist, nfl);
-      kp.init();
-      fl.init();
       Contrib c;
       for (uint32_t base = 0; base < n; base += stride) {
         const uint32_t i = base + spread;
-        bool nf = false, kept = false;
-        uint32_t tg = 0, d = 0;
         if (i < n) {
-          d = list[i];
+          bool nf = false, kept = false;
+          uint32_t tg = 0;
+          const uint32_t d = list[i];
           const float r = res[d];
-          c.count += 8;  // algorithmic bytes: list entry + residual
+          c.count += 16;  // algorithmic bytes: list entry + residual, both slots written
           if (r >= eps) {
             c.survivors += 1;
             if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d) < thresh)) {
@@ -171,20 +167,17 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
               c.count += 8 * QS + 12;  // candidate -> live, residual, target id, flag
             } else {
               kept = true;
-              c.count += 4;  // kept list entry
             }
           } else {
             cl.inlist[d] = 0;
           }
+          if (!kept) list[i] = kSlotEmpty;
+          vslot[i] = nf ? tg : kSlotEmpty;
         }
-        kp.push_warp(kept, d);
-        fl.push_warp(nf, tg);
-        kp.flush(kPersistBlock);
-        fl.flush(kPersistBlock);
       }
       mark(7);
       warp_contrib(s_pacc, c);
-      flush2(kp, fl);  // its first barrier orders the warp sums
+      __syncthreads();
       pacc_push(s_pacc, acc);
     }
     mark(0);
@@ -201,33 +194,39 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
           ctl->has_prev = has_prev;
           ctl->stamp = stamp;
           ctl->cl_cur = cur;
-          ctl->nflag = *nfl;
+          ctl->nflag = 0;
           ctl->frontier = 0;
         }
         __syncthreads();
-        rnbp_retry_block<QS, true>(g, live, cand, res, vflag, vlist, nullptr, ctl, eps, prm, cl, acc[3],
-                                   reinterpret_cast<long long*>(&acc[0]));
-        __syncthreads();
-        if (threadIdx.x == 0) *nfl = ctl->nflag;  // fallback / attempt-1 targets appended there
+        rnbp_retry_block<QS, true>(g, live, cand, res, vflag, nullptr, nullptr, ctl, eps, prm, cl, acc[3],
+                                   reinterpret_cast<long long*>(&acc[0]), list, n, vslot);
       }
       sync_all();
       retry_front = ctl->frontier;
     }
     mark(1);
-    // ---- refresh over the touched vertices; new unconverged edges join the list
+    // ---- refresh: per slot, carry the kept entry over and refresh the
+    // flagged target; new unconverged edges join the list
     {
-      const uint32_t nv = *nfl;
       if (lead) ctl->cl_n[cur] = 0u;  // the list just read is refilled next iteration
       BPB_STAGER(st, 2048, cur ? cl.list[0] : cl.list[1], &ctl->cl_n[cur ^ 1u]);
       st.init();
       int cnt = 0;
-      unsigned long long evals = 0, visits = 0;
-      for (uint32_t base = 0; base < nv; base += stride) {
+      unsigned long long evals = 0, visits = 0, kept = 0, slots = 0;
+      for (uint32_t base = 0; base < n; base += stride) {
         const uint32_t i = base + spread;
-        if (i < nv) {
-          cnt += vertex_update<QS, kModeDelta, true, false>(g, vlist[i], live, cand, res, eps, &ctl->numeric_error,
-                                                            evals, cl.inlist, &st, true);
-          ++visits;
+        if (i < n) {
+          ++slots;
+          const uint32_t d = list[i], v = vslot[i];
+          if (d != kSlotEmpty) {
+            st.push(d);
+            ++kept;
+          }
+          if (v != kSlotEmpty) {
+            cnt += vertex_update<QS, kModeDelta, true, false>(g, v, live, cand, res, eps, &ctl->numeric_error,
+                                                              evals, cl.inlist, &st, true);
+            ++visits;
+          }
         }
         st.flush(1024);
       }
@@ -236,9 +235,11 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       c.delta = cnt;
       c.evals = evals;
       c.visits = visits;
-      // per vertex: list id + unary; per message: edge pair (in + old out),
-      // coupling, candidate write, residual read + write
-      c.count = 8ull * visits + static_cast<unsigned long long>(8 * QS + 4 + 4 * QS + 8) * evals;
+      // per slot: two slot words; per kept entry: list write; per vertex:
+      // unary; per message: edge pair (in + old out), coupling, candidate
+      // write, residual read + write
+      c.count = 8ull * slots + 4ull * kept + 4ull * visits +
+                static_cast<unsigned long long>(8 * QS + 4 + 4 * QS + 8) * evals;
       warp_contrib(s_pacc, c);
       st.flush(0);  // its first barrier orders the warp sums
       mark(5);

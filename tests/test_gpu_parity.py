@@ -214,12 +214,16 @@ def test_zero_edge_graph(bp, orc):
         assert abs(r.beliefs.at(1)[2] - 0.5) < 1e-6
 
 
-@pytest.mark.parametrize("n,c,seed", [(100, 2.5, 500), (60, 3.0, 7)])
-def test_rnbp_persistent_tail_matches_graph_loop(bp, orc, n, c, seed):
+@pytest.mark.parametrize("n,c,seed,p", [(100, 2.5, 500, 0.5), (60, 3.0, 7, 0.5), (20, 2.0, 3, 0.05)])
+def test_rnbp_persistent_tail_matches_graph_loop(bp, orc, n, c, seed, p):
     """The persistent list-mode kernel runs the same iterations as the
-    per-kernel graph loop: identical traces (frontier sizes, counts)."""
+    per-kernel graph loop: identical traces (frontier sizes, counts).  p = 0.05
+    on short lists makes empty attempt-0 draws common, so the in-kernel retry
+    (attempt 1) and the single-survivor fallback run too (50 single-edge
+    frontiers in the 20x20 run)."""
     g = bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed))
-    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=3000, seed=seed)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=p, high_p=p if p < 0.5 else 1.0,
+                             max_iterations=3000, seed=seed)
     a = bp.run(g, cfg)
     b = bp.run_ex(g, cfg, flags=bp.RUN_NO_PERSIST)
     assert a.trace_signature() == b.trace_signature()
