@@ -682,6 +682,10 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
     bool act[kLatVPT];
     float2 pU[kLatVPT], pL[kLatVPT], pR[kLatVPT], pD[kLatVPT];
     float aU[kLatVPT], aL[kLatVPT], aR[kLatVPT], aD[kLatVPT], un[kLatVPT];
+    // per vertex, prefetched with the messages: bit j = old residual of out
+    // message j (up, left, right, down) >= eps, bit 4 + j = it is in the
+    // candidate list; the bookkeeping below then needs no dependent loads
+    uint32_t pre[kLatVPT];
 #pragma unroll
     for (int k = 0; k < kLatVPT; ++k) {
       const uint32_t c = c0 + k * kBlock;
@@ -720,6 +724,22 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
     }
 #pragma unroll
     for (int k = 0; k < kLatVPT; ++k) {
+      pre[k] = 0u;
+      if (MODE != kModeDelta && !(CL && cl_on)) continue;
+      const uint32_t c = c0 + k * kBlock;
+      const uint32_t dn = c + 1u < C ? 1u : 0u;
+      const bool has[4] = {act[k] && !first, act[k] && c > 0u, act[k] && dn, act[k] && !last};
+      const uint32_t outs[4] = {2u * (prow + 2u * c + dn) + 1u, 2u * (last ? row + c - 1u : row + 2u * c - 2u) + 1u,
+                                2u * (last ? row + c : row + 2u * c), 2u * (row + 2u * c + dn)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!has[j]) continue;
+        if (MODE == kModeDelta && res[outs[j]] >= eps) pre[k] |= 1u << j;
+        if (CL && cl_on && inlist[outs[j]]) pre[k] |= 16u << j;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kLatVPT; ++k) {
       if (CL) cl->flush(1024);  // <= 4 kBlock pushes per k
       const uint32_t c = c0 + k * kBlock;
       const uint32_t dn = c + 1u < C ? 1u : 0u;
@@ -743,28 +763,28 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       if (hl) B[ol] = ll;
       if (hr) B[orr] = lr;
       if (hd) B[od] = ld;
-      auto track = [&](bool has, uint32_t out, float r_msg) {
+      auto track = [&](int j, bool has, uint32_t out, float r_msg) {
         // messages of a band's ghost rows belong to the neighbour band: their
         // residuals stay 0 here, so they are never counted or selected
         const int now = has && owned && r_msg >= eps;
         if (MODE == kModeDelta) {
           if (has && owned) {
-            cnt += now - (res[out] >= eps);
+            cnt += now - static_cast<int>((pre[k] >> j) & 1u);
             res[out] = r_msg;
           }
         } else {
           if (MODE == kModeInit && has && owned) res[out] = r_msg;
           cnt += now;
         }
-        if (CL && cl_on && now && !inlist[out]) {
+        if (CL && cl_on && now && !((pre[k] >> (4 + j)) & 1u)) {
           inlist[out] = 1;
           cl->push(out);
         }
       };
-      track(hu, ou, ru);
-      track(hl, ol, rl);
-      track(hr, orr, rr);
-      track(hd, od, rd);
+      track(0, hu, ou, ru);
+      track(1, hl, ol, rl);
+      track(2, hr, orr, rr);
+      track(3, hd, od, rd);
       const uint32_t deg = (hu ? 1u : 0u) + (hl ? 1u : 0u) + (hr ? 1u : 0u) + (hd ? 1u : 0u);
       evals += owned ? deg : 0u;
       visits += act[k] && owned ? 1u : 0u;
