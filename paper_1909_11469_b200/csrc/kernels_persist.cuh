@@ -158,12 +158,25 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
           uint32_t tg = 0;
           const uint32_t d = list[i];
           const float r = res[d];
+          // binary: the commit's loads (candidate, target) are issued with the
+          // residual's, speculatively, saving a dependent round trip
+          const float cv = QS == 1 ? cand[d] : 0.f;
+          const uint32_t tgp = QS == 1 ? __ldg(&g.ep[d ^ 1u]) : 0u;
           c.count += 16;  // algorithmic bytes: list entry + residual, both slots written
           if (r >= eps) {
             c.survivors += 1;
             if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d) < thresh)) {
               cl.inlist[d] = 0;
-              commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, false, c, nf, tg);
+              if (QS == 1) {  // commit_edge with the prefetched operands
+                c.delta -= 1;
+                c.frontier += 1;
+                res[d] = 0.f;
+                live[d] = cv;
+                tg = tgp;
+                nf = atomicMax(&vflag[tg], stamp) < stamp;
+              } else {
+                commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, false, c, nf, tg);
+              }
               c.count += 8 * QS + 12;  // candidate -> live, residual, target id, flag
             } else {
               kept = true;
