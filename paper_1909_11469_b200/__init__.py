@@ -259,6 +259,36 @@ class IterationRecord:
     elapsed_seconds: float
 
 
+_TRACE_DTYPE = np.dtype([("iteration", np.uint64), ("frontier_size", np.uint64), ("unconverged", np.uint32),
+                         ("_pad", np.uint32), ("elapsed_seconds", np.float64)])
+
+
+class Trace(Sequence):
+    """RunResult::trace (schedulers.hpp:40-52): a read-only sequence of
+    IterationRecord over the records the run copied out (numpy-backed, so a
+    10^4-iteration run does not build 10^4 Python objects up front)."""
+
+    def __init__(self, recs: np.ndarray):
+        self._r = recs
+
+    def __len__(self):
+        return int(self._r.shape[0])
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        x = self._r[k]
+        return IterationRecord(int(x["iteration"]), int(x["frontier_size"]), int(x["unconverged"]),
+                               float(x["elapsed_seconds"]))
+
+    def column(self, name: str) -> np.ndarray:
+        """one field of every record as an array (iteration, frontier_size, ...)"""
+        return self._r[name]
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+
 class BeliefTable:
     """BeliefTable (messages.hpp:83-107): per-vertex probability vectors."""
 
@@ -376,7 +406,11 @@ class PairwiseMRF:
         if un.size != expected_unary:
             raise ModelError(f"expected {expected_unary} unary entries, got {un.size}")
         E = ep.size // 2
-        if E:
+        if E and cards.size and cards.min() == cards.max():  # uniform cardinality: q^2 entries per table
+            q = int(cards[0])
+            if tb.size != E * q * q:
+                raise ModelError(f"pairwise tables hold {tb.size} entries, expected {E * q * q}")
+        elif E:
             i, j = ep[0::2], ep[1::2]
             ok = (i < cards.size) & (j < cards.size)
             sizes = np.where(ok, cards[np.minimum(i, max(cards.size - 1, 0))].astype(np.int64) *
@@ -464,7 +498,7 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
            trace_cap: Optional[int] = None, kernel_timing: bool = False, beliefs_device_ptr: int = 0) -> RunResult:
     c = config._c()
     nb = int(graph.belief_offsets[-1])
-    bel = np.zeros(max(nb, 1)) if beliefs and not beliefs_device_ptr else None
+    bel = np.empty(max(nb, 1)) if beliefs and not beliefs_device_ptr else None  # filled by bp_run_ex
     if trace_cap is None:
         trace_cap = int(min(config.max_iterations, 1 << 20)) + 1
     tr = (_Record * max(trace_cap, 1))()
@@ -475,8 +509,7 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
     _check(_lib.bp_run_ex(graph._h, C.byref(c), C.byref(opts), C.byref(res), _ptr(bel), C.cast(tr, C.c_void_p),
                           trace_cap))
     n = min(int(res.trace_len), trace_cap)
-    trace = [IterationRecord(int(tr[k].iteration), int(tr[k].frontier_size), int(tr[k].unconverged),
-                             float(tr[k].elapsed_seconds)) for k in range(n)]
+    trace = Trace(np.frombuffer(tr, dtype=_TRACE_DTYPE, count=n).copy())
     bt = BeliefTable(bel[:nb], graph.belief_offsets) if bel is not None else None
     return RunResult(bool(res.converged), int(res.iterations), float(res.wall_time),
                      int(res.messages_updated_total), bt, trace, float(res.device_ms),

@@ -126,7 +126,7 @@ struct TraceRec {
   double elapsed_seconds;
 };
 
-constexpr unsigned kTraceRing = 4096;
+constexpr unsigned kTraceRing = 16384;  // 512 KB: a 10^4-iteration run drains twice
 
 enum StopReason : unsigned { kStopNone = 0, kStopConverged = 1, kStopMaxIter = 2, kStopTime = 3, kStopNumeric = 4 };
 

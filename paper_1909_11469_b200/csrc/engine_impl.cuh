@@ -67,6 +67,7 @@ class EngineT final : public EngineBase {
       clist_[0].alloc(static_cast<size_t>(g.D) * 4);
       clist_[1].alloc(static_cast<size_t>(g.D) * 4);
       inlist_.alloc(g.D ? g.D : 1);
+      vslot_.alloc(static_cast<size_t>(g.D ? g.D : 1) * 4);  // here, not mid-run: cudaMalloc can stall the device
     }
     vlist_.alloc(static_cast<size_t>(g.V) * 4);
     ctl_.alloc(sizeof(Ctl));
@@ -405,10 +406,17 @@ class EngineT final : public EngineBase {
       return;
     }
     if (n - copied > kTraceRing) throw Error(BP_ERR_CUDA, "trace ring overrun");
+    // only the new records: at most two contiguous pieces of the ring
     std::vector<TraceRec> tmp(kTraceRing);
-    cuda_check(cudaMemcpy(tmp.data(), reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, trace),
-                          sizeof(TraceRec) * kTraceRing, cudaMemcpyDeviceToHost),
-               "trace d2h");
+    const uint64_t last = std::min(n, cap);
+    for (uint64_t it = copied; it < last;) {
+      const uint64_t slot = it % kTraceRing, len = std::min<uint64_t>(last - it, kTraceRing - slot);
+      cuda_check(cudaMemcpy(tmp.data() + slot,
+                            reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, trace) + sizeof(TraceRec) * slot,
+                            sizeof(TraceRec) * len, cudaMemcpyDeviceToHost),
+                 "trace d2h");
+      it += len;
+    }
     for (uint64_t it = copied; it < n && it < cap; ++it) {
       const TraceRec& r = tmp[it % kTraceRing];
       trace[it].iteration = r.iteration;
@@ -882,16 +890,20 @@ class EngineT final : public EngineBase {
   // BPB_PERSIST_GRID / BPB_PERSIST_CLUSTER override the choice (tuning).
   DevBuf vslot_;  // refresh slots of the persistent tail (one per candidate-list entry)
   void run_persist_loop(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
-    if (!vslot_.p) vslot_.alloc(static_cast<size_t>(dg_.D) * 4);
     if (!persist_grid_) {
-      int per_sm = 0;
-      cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rnbp_persist<QS, false>, kPersistBlock, 0),
-                 "occupancy");
-      // one CTA per SM: the tail is latency-bound, a second CTA per SM only
-      // adds barrier participants (measured: 296 CTAs 3% slower than 148)
-      persist_grid_ = static_cast<unsigned>(std::min(std::max(1, per_sm), 1) * sm_count());
-      cuda_check(cudaFuncSetAttribute(k_rnbp_persist<QS, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                 "cluster attribute");
+      // once per process: one CTA per SM (the tail is latency-bound, a second
+      // CTA per SM only adds barrier participants: 296 CTAs measured 3%
+      // slower than 148)
+      static const unsigned grid = [this] {
+        int per_sm = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rnbp_persist<QS, false>, kPersistBlock, 0),
+                   "occupancy");
+        if (per_sm < 1) throw Error(BP_ERR_CUDA, "persistent RnBP kernel does not fit on an SM");
+        cuda_check(cudaFuncSetAttribute(k_rnbp_persist<QS, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                   "cluster attribute");
+        return static_cast<unsigned>(sm_count());
+      }();
+      persist_grid_ = grid;
     }
     const char* eg = std::getenv("BPB_PERSIST_GRID");
     const char* ec = std::getenv("BPB_PERSIST_CLUSTER");

@@ -1,6 +1,10 @@
 // Graph construction and upload: the device counterpart of build_graph
 // (mrf.cpp:25-106) and of the generators (generators.cpp:24-71).
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -149,6 +153,38 @@ __global__ void k_iota_mul(uint32_t* p, size_t n, uint32_t mul) {
     p[i] = static_cast<uint32_t>(i * mul);
 }
 
+// Host loops over vertices / edges, split over the host's cores (graph
+// construction from host arrays is on the end-to-end path).
+template <class F>
+void parallel_for(uint64_t n, F&& f) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const unsigned nt = n < (1u << 16) ? 1u : hw;
+  if (nt == 1) {
+    f(uint64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  for (unsigned t = 0; t < nt; ++t)
+    ts.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt); });
+  for (auto& th : ts) th.join();
+}
+
+// smallest index in [0, n) with bad(i), or n
+template <class F>
+uint64_t first_bad(uint64_t n, F&& bad) {
+  std::atomic<uint64_t> first{n};
+  parallel_for(n, [&](uint64_t a, uint64_t b) {
+    for (uint64_t i = a; i < b && i < first.load(std::memory_order_relaxed); ++i)
+      if (bad(i)) {
+        uint64_t cur = first.load();
+        while (i < cur && !first.compare_exchange_weak(cur, i)) {
+        }
+        return;
+      }
+  });
+  return first.load();
+}
+
 unsigned grid_for(size_t n) {
   return static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148ull * 32));
 }
@@ -190,6 +226,15 @@ void upload_ising_weights(GraphImpl& g, const std::vector<float>& J) {
 }  // namespace
 
 std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_device_opts* opts) {
+  // BPB_DEBUG_BUILD: stage times on stderr (tuning aid)
+  static const bool dbg = std::getenv("BPB_DEBUG_BUILD") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!dbg) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "build %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - tprev).count());
+    tprev = t;
+  };
   if (!d) throw_invalid("null graph descriptor");
   const uint32_t V = d->num_vertices, E = d->num_edges;
   if (E > (1u << 31) - 1) throw_model("too many edges for 32-bit directed edge ids");
@@ -202,32 +247,64 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     maxq = std::max(maxq, d->cardinalities[v]);
     usz += d->cardinalities[v];
   }
+  stage("cards");
   if (usz && !d->unary_values) throw_invalid("null unary values");
-  for (uint32_t v = 0, o = 0; v < V; o += d->cardinalities[v], ++v)
-    for (uint32_t x = 0; x < d->cardinalities[v]; ++x) {
-      const double u = d->unary_values[o + x];
-      if (!(u > 0.0) || !std::isfinite(u))
-        throw_model("unary(" + std::to_string(v) + ") entries must be strictly positive and finite");
-    }
-  if (E && (!d->edge_endpoints || !d->pairwise_values)) throw_invalid("null edge arrays");
-  std::vector<size_t> poff(static_cast<size_t>(E) + 1, 0);
-  for (uint32_t e = 0; e < E; ++e) {
-    const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
-    if (i >= V || j >= V) throw_model("edge " + std::to_string(e) + " references a vertex out of range");
-    if (i == j) throw_model("edge " + std::to_string(e) + " is a self-loop on vertex " + std::to_string(i));
-    if (i > j) throw_model("edge " + std::to_string(e) + " endpoints must satisfy i < j");
-    poff[e + 1] = poff[e] + static_cast<size_t>(d->cardinalities[i]) * d->cardinalities[j];
+  const bool all_binary = V > 0 && maxq == 2 && usz == 2ull * V;
+  auto bad_entry = [](double u) { return !(u > 0.0) || !std::isfinite(u); };
+  if (all_binary) {  // offsets 2v: checked in parallel, first offender reported
+    const uint64_t bv = first_bad(V, [&](uint64_t v) {
+      return bad_entry(d->unary_values[2 * v]) || bad_entry(d->unary_values[2 * v + 1]);
+    });
+    if (bv < V) throw_model("unary(" + std::to_string(bv) + ") entries must be strictly positive and finite");
+  } else {
+    for (uint32_t v = 0, o = 0; v < V; o += d->cardinalities[v], ++v)
+      for (uint32_t x = 0; x < d->cardinalities[v]; ++x)
+        if (bad_entry(d->unary_values[o + x]))
+          throw_model("unary(" + std::to_string(v) + ") entries must be strictly positive and finite");
   }
-  for (uint32_t e = 0; e < E; ++e)
-    for (size_t k = poff[e]; k < poff[e + 1]; ++k) {
-      const double t = d->pairwise_values[k];
-      if (!(t > 0.0) || !std::isfinite(t))
-        throw_model("pairwise(" + std::to_string(d->edge_endpoints[2 * e]) + "," +
-                    std::to_string(d->edge_endpoints[2 * e + 1]) + ") entries must be strictly positive and finite");
-    }
+  stage("unary check");
+  if (E && (!d->edge_endpoints || !d->pairwise_values)) throw_invalid("null edge arrays");
+  // endpoint checks in parallel; the first offending edge gets the
+  // reference's message for its first failing test
+  const uint64_t bep = first_bad(E, [&](uint64_t e) {
+    const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
+    return i >= V || j >= V || i >= j;
+  });
+  if (bep < E) {
+    const uint32_t i = d->edge_endpoints[2 * bep], j = d->edge_endpoints[2 * bep + 1];
+    if (i >= V || j >= V) throw_model("edge " + std::to_string(bep) + " references a vertex out of range");
+    if (i == j) throw_model("edge " + std::to_string(bep) + " is a self-loop on vertex " + std::to_string(i));
+    throw_model("edge " + std::to_string(bep) + " endpoints must satisfy i < j");
+  }
+  // table offsets: e q^2 for a uniform cardinality q, else a prefix sum
+  const bool uniform_cards = V == 0 || (maxq * static_cast<uint64_t>(V) == usz);
+  std::vector<size_t> poff;
+  if (!uniform_cards) {
+    poff.assign(static_cast<size_t>(E) + 1, 0);
+    for (uint32_t e = 0; e < E; ++e)
+      poff[e + 1] = poff[e] + static_cast<size_t>(d->cardinalities[d->edge_endpoints[2 * e]]) *
+                                  d->cardinalities[d->edge_endpoints[2 * e + 1]];
+  }
+  auto table_at = [&](uint64_t e) -> size_t { return uniform_cards ? e * maxq * maxq : poff[e]; };
+  auto table_size = [&](uint64_t e) -> size_t { return uniform_cards ? size_t{maxq} * maxq : poff[e + 1] - poff[e]; };
+  stage("edge check");
+  const uint64_t be = first_bad(E, [&](uint64_t e) {
+    const size_t k0 = table_at(e), k1 = k0 + table_size(e);
+    for (size_t k = k0; k < k1; ++k)
+      if (bad_entry(d->pairwise_values[k])) return true;
+    return false;
+  });
+  if (be < E)
+    throw_model("pairwise(" + std::to_string(d->edge_endpoints[2 * be]) + "," +
+                std::to_string(d->edge_endpoints[2 * be + 1]) + ") entries must be strictly positive and finite");
+  // generate_ising's lattice numbering: the topology is generated on the
+  // device (no host CSR; the numbering has no duplicate edges by construction)
+  stage("pair check");
+  const uint32_t lat_cols = detect_lattice(V, E, d->edge_endpoints);
+  stage("lattice");
   std::vector<uint32_t> off, adj;
-  build_csr(V, E, d->edge_endpoints, off, adj);
-  if (!(opts && (opts->flags & BP_GRAPH_TRUSTED))) {
+  if (!lat_cols) build_csr(V, E, d->edge_endpoints, off, adj);
+  if (!lat_cols && !(opts && (opts->flags & BP_GRAPH_TRUSTED))) {
     // duplicate edges: two incoming edges of one vertex from the same source
     std::vector<uint32_t> mark(V, std::numeric_limits<uint32_t>::max());
     for (uint32_t v = 0; v < V; ++v)
@@ -240,6 +317,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
         mark[s] = v;
       }
   }
+  stage("csr");
   auto g = std::make_unique<GraphImpl>();
   g->device = select_device(opts);
   g->V = V;
@@ -251,39 +329,54 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   for (uint32_t v = 1; v < V; ++v) uniform = uniform && d->cardinalities[v] == d->cardinalities[0];
   if (uniform && V) g->uniform_q = d->cardinalities[0];
   else g->cards_host.assign(d->cardinalities, d->cardinalities + V);
-  g->in_off.upload(off.data(), off.size() * 4);
-  g->in_adj.upload(adj.data(), adj.size() * 4);
-  g->ep.upload(d->edge_endpoints, static_cast<size_t>(E) * 8);
+  if (lat_cols) {
+    g->in_off.alloc((static_cast<size_t>(V) + 1) * 4);
+    g->in_adj.alloc(static_cast<size_t>(E) * 8);
+    g->ep.alloc(static_cast<size_t>(E) * 8);
+    k_lattice_topology<<<grid_for(V), 256>>>(V / lat_cols, lat_cols, g->in_off.as<uint32_t>(),
+                                             g->in_adj.as<uint32_t>(), g->ep.as<uint32_t>());
+    cuda_check(cudaGetLastError(), "lattice topology");
+  } else {
+    g->in_off.upload(off.data(), off.size() * 4);
+    g->in_adj.upload(adj.data(), adj.size() * 4);
+    g->ep.upload(d->edge_endpoints, static_cast<size_t>(E) * 8);
+  }
+  stage("topology");
   if (g->binary || V == 0) {
     g->binary = true;
     g->qs = 1;
     std::vector<float> ulo(V);
-    for (uint32_t v = 0; v < V; ++v)
-      ulo[v] = static_cast<float>(std::log2(d->unary_values[2 * v + 1]) - std::log2(d->unary_values[2 * v]));
-    std::vector<float4> par(E);
-    for (uint32_t e = 0; e < E; ++e) {
-      const double* t = d->pairwise_values + 4ull * e;
-      const double l00 = std::log2(t[0]), l01 = std::log2(t[1]), l10 = std::log2(t[2]), l11 = std::log2(t[3]);
-      const double alpha = l01 - l00, beta = l10 - l00, gg = l11 - l00;
-      par[e] = make_float4(static_cast<float>(alpha), static_cast<float>(beta), static_cast<float>(gg - alpha),
-                           static_cast<float>(gg - beta));
-    }
+    parallel_for(V, [&](uint64_t a, uint64_t b) {
+      for (uint64_t v = a; v < b; ++v)
+        ulo[v] = static_cast<float>(std::log2(d->unary_values[2 * v + 1]) - std::log2(d->unary_values[2 * v]));
+    });
     g->unary_lo.upload(ulo.data(), ulo.size() * 4);
     // Ising tables {a, d, d, a} (generators.cpp:18-22): one coupling per edge
-    bool ising = E > 0;
-    for (uint32_t e = 0; e < E && ising; ++e) {
-      const double* t = d->pairwise_values + 4ull * e;
-      ising = t[0] == t[3] && t[1] == t[2];
-    }
+    const bool ising = E > 0 && first_bad(E, [&](uint64_t e) {
+                                  const double* t = d->pairwise_values + 4ull * e;
+                                  return !(t[0] == t[3] && t[1] == t[2]);
+                                }) == E;
     if (ising) {
       std::vector<float> a(E);
-      for (uint32_t e = 0; e < E; ++e) {
-        const double* t = d->pairwise_values + 4ull * e;
-        a[e] = ising_weight(std::log(t[0]) - std::log(t[1]));
-      }
+      parallel_for(E, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t e = lo; e < hi; ++e) {
+          const double* t = d->pairwise_values + 4ull * e;
+          a[e] = ising_weight(std::log(t[0]) - std::log(t[1]));
+        }
+      });
       g->ising_a.upload(a.data(), a.size() * 4);
       g->par_mode = 1;
     } else {
+      std::vector<float4> par(E);
+      parallel_for(E, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t e = lo; e < hi; ++e) {
+          const double* t = d->pairwise_values + 4ull * e;
+          const double l00 = std::log2(t[0]), l01 = std::log2(t[1]), l10 = std::log2(t[2]), l11 = std::log2(t[3]);
+          const double alpha = l01 - l00, beta = l10 - l00, gg = l11 - l00;
+          par[e] = make_float4(static_cast<float>(alpha), static_cast<float>(beta), static_cast<float>(gg - alpha),
+                               static_cast<float>(gg - beta));
+        }
+      });
       g->epar.upload(par.data(), par.size() * 16);
     }
   } else {
@@ -302,7 +395,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     for (uint32_t e = 0; e < E && potts; ++e) {
       const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
       const uint32_t ci = d->cardinalities[i], cj = d->cardinalities[j];
-      const double* t = d->pairwise_values + poff[e];
+      const double* t = d->pairwise_values + table_at(e);
       if (ci != cj || ci < 2) {
         potts = false;
         break;
@@ -320,7 +413,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     for (uint32_t e = 0; e < E && !potts; ++e) {
       const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
       const uint32_t ci = d->cardinalities[i], cj = d->cardinalities[j];
-      const double* t = d->pairwise_values + poff[e];
+      const double* t = d->pairwise_values + table_at(e);
       double mx = 0.0;
       for (size_t k = 0; k < static_cast<size_t>(ci) * cj; ++k) mx = std::max(mx, t[k]);
       for (uint32_t a = 0; a < ci; ++a)
@@ -336,9 +429,10 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     if (!potts) g->table.upload(tb.data(), tb.size() * 4);
     g->bel_off.upload(bo.data(), bo.size() * 4);
   }
-  g->lat_cols = detect_lattice(V, E, d->edge_endpoints);
-  g->lat_rows = g->lat_cols ? V / g->lat_cols : 0;
+  g->lat_cols = lat_cols;
+  g->lat_rows = lat_cols ? V / lat_cols : 0;
   cuda_check(cudaDeviceSynchronize(), "graph upload");
+  stage("potentials");
   return g;
 }
 

@@ -451,36 +451,10 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
   float T = g.unary_lo[v];
   const float2* __restrict__ A2 = reinterpret_cast<const float2*>(A);
   // incoming messages and (same edge pair) the old outgoing ones, kept in
-  // registers between the two passes (lattice: exactly 4; CSR: re-read)
+  // registers between the two passes (lattice: exactly 4; CSR: re-read in
+  // groups of 4)
   int cnt = 0;
   uint32_t deg = 0;
-  auto emit = [&](uint32_t in, float2 pr) {
-    const uint32_t out = in ^ 1u;
-    const float r_was = MODE == kModeDelta ? res[out] : 0.f;
-    const float m_in = (in & 1u) ? pr.y : pr.x;
-    const float m_old = (in & 1u) ? pr.x : pr.y;
-    float lnew, r;
-    if (g.par_mode) {
-      r = ising_update(T - m_in, __ldg(&g.ising_a[out >> 1]), m_old, lnew);
-    } else {
-      lnew = binary_msg(g, T - m_in, out);
-      r = binary_residual(lnew, m_old);
-    }
-    if (!(fabsf(lnew) < INFINITY)) *numeric_flag = 1u;
-    B[out] = lnew;
-    const int now = r >= eps;
-    if (MODE == kModeDelta) {
-      cnt += now - (r_was >= eps);
-      res[out] = r;
-    } else {
-      if (MODE == kModeInit) res[out] = r;
-      cnt += now;
-    }
-    if (CL && cl_on && now && !inlist[out]) {
-      inlist[out] = 1;
-      cl->push(out);
-    }
-  };
   // emit with prefetched residual / in-list flag
   auto emit_pre = [&](uint32_t in, float2 pr, float r_was, bool in_list, float a) {
     const uint32_t out = in ^ 1u;
@@ -542,12 +516,33 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
         ++deg;
       }
   } else {
-    for_each_in(g, v, [&](uint32_t in) {
+    const uint32_t b = g.in_off[v], e = g.in_off[v + 1];
+    for (uint32_t a = b; a < e; ++a) {
+      const uint32_t in = g.in_adj[a];
       const float2 pr = ldm<NC>(&A2[in >> 1]);
       T += (in & 1u) ? pr.y : pr.x;
-      ++deg;
-    });
-    for_each_in(g, v, [&](uint32_t in) { emit(in, ldm<NC>(&A2[in >> 1])); });
+    }
+    deg = e - b;
+    // emit in groups of 4 with the per-message state prefetched, so the
+    // updates do not serialise on loads behind the previous group's stores
+    for (uint32_t a0 = b; a0 < e; a0 += 4) {
+      uint32_t ins[4];
+      float2 prs[4];
+      float rw[4], ia[4];
+      bool il[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool has = a0 + k < e;
+        ins[k] = has ? g.in_adj[a0 + k] : 0u;
+        prs[k] = has ? ldm<NC>(&A2[ins[k] >> 1]) : make_float2(0.f, 0.f);
+        rw[k] = (MODE == kModeDelta && has) ? res[ins[k] ^ 1u] : 0.f;
+        il[k] = (CL && cl_on && has) ? inlist[ins[k] ^ 1u] != 0 : true;
+        ia[k] = (g.par_mode && has) ? __ldg(&g.ising_a[ins[k] >> 1]) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (a0 + k < e) emit_pre(ins[k], prs[k], rw[k], il[k], ia[k]);
+    }
   }
   evals += deg;
   return cnt;

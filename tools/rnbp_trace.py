@@ -8,8 +8,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1909_11469_b200 as bp  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
-g = bp.generate_ising(bp.IsingParams(n=n, c=2.5, seed=0))
-cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=10000, time_limit=1e9)
+seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+g = bp.generate_ising(bp.IsingParams(n=n, c=2.5, seed=seed))
+cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=10000, time_limit=1e9, seed=seed)
 bp.run(g, cfg)
 r = bp.run(g, cfg)
 t = np.array([x.elapsed_seconds for x in r.trace])
