@@ -235,7 +235,7 @@ def run_b200(args):
         dom = max(ks, key=lambda k: ks[k]["ms"])
         if dom == "persist":
             dom_bytes = ks["persist"]["bytes"]
-            dom_name = "k_rnbp_persist (RnBP candidate-list iterations, one 16-CTA cluster)"
+            dom_name = "k_rnbp_persist (RnBP candidate-list iterations, cooperative grid of one CTA per SM, one 16-CTA cluster for lists under 2048 entries)"
         else:
             dom_bytes = refresh_bytes(ri.vertex_visits, ri.message_evaluations)
             dom_name = f"{dom} kernels"
