@@ -119,6 +119,9 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
   }
   sync_all();
   uint32_t list_n = ctl->cl_n[cur];
+  // first-pass list entry of this thread, loaded ahead (with the loads after
+  // the previous barrier) so the select does not start with a round trip
+  uint32_t pre_d = spread < g.D ? (cur ? cl.list[1] : cl.list[0])[spread] : 0u;
   // phase clock of CTA 0, the CTA that holds the most list work (profiling
   // aid, one timer read per phase)
   const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         if (i < n) {
           bool nf = false, kept = false;
           uint32_t tg = 0;
-          const uint32_t d = list[i];
+          const uint32_t d = base == 0 ? pre_d : list[i];
           const float r = res[d];
           // binary: the commit's loads (candidate, target) are issued with the
           // residual's, speculatively, saving a dependent round trip
@@ -197,6 +200,9 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     sync_all();
     // ---- retry / fallback (schedulers.cpp:204-214): uniform decision, one block
     unsigned long long retry_front = 0;
+    // the refresh's first-pass slots, loaded with the retry test's sums
+    const uint32_t pre_k = spread < n ? list[spread] : kSlotEmpty;
+    uint32_t pre_v = spread < n ? vslot[spread] : kSlotEmpty;
     if (acc[2] == 0ull && acc[3] > 0ull) {
       if (blockIdx.x == 0) {
         // rnbp_retry_block reads the loop state from Ctl: mirror it first
@@ -216,6 +222,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       }
       sync_all();
       retry_front = ctl->frontier;
+      pre_v = spread < n ? vslot[spread] : kSlotEmpty;  // the retry wrote refresh targets
     }
     mark(1);
     // ---- refresh: per slot, carry the kept entry over and refresh the
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         const uint32_t i = base + spread;
         if (i < n) {
           ++slots;
-          const uint32_t d = list[i], v = vslot[i];
+          const uint32_t d = base == 0 ? pre_k : list[i], v = base == 0 ? pre_v : vslot[i];
           if (d != kSlotEmpty) {
             st.push(d);
             ++kept;
@@ -273,6 +280,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     // the list refilled this iteration: loaded with the other finalize reads,
     // reused by the next select
     const uint32_t next_n = ctl->cl_n[cur ^ 1u];
+    pre_d = spread < g.D ? (cur ? cl.list[0] : cl.list[1])[spread] : 0u;  // the next iteration's list
     const bool numeric = ctl->numeric_error != 0u;
     const bool tstop = ctl->time_stop != 0u;
     if (lead) {

@@ -7,6 +7,51 @@
 namespace cg = cooperative_groups;
 
 __device__ unsigned long long g_ctr[64];
+__device__ unsigned g_bar[32 * 32];  // sub-counters, one 128-byte line each; [31*32] = root
+__device__ unsigned g_gen;
+
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned x) {
+  unsigned v;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "r"(x) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(unsigned* p, unsigned x) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+// flat (GROUP = 0) or two-level (GROUP CTAs per sub-counter) generation barrier
+template <int GROUP>
+__device__ __forceinline__ void grid_bar() {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned G = gridDim.x;
+    const unsigned gen = ld_acq(&g_gen);
+    bool last;
+    if (GROUP == 0) {
+      last = atom_add_acqrel(&g_bar[31 * 32], 1u) == G - 1;
+    } else {
+      const unsigned grp = blockIdx.x / GROUP, ng = (G + GROUP - 1) / GROUP;
+      const unsigned gsz = min(GROUP, G - grp * GROUP);
+      last = atom_add_acqrel(&g_bar[grp * 32], 1u) == gsz - 1;
+      if (last) {
+        g_bar[grp * 32] = 0;
+        last = atom_add_acqrel(&g_bar[31 * 32], 1u) == ng - 1;
+      }
+    }
+    if (last) {
+      g_bar[31 * 32] = 0;
+      st_rel(&g_gen, gen + 1);
+    } else {
+      while (ld_acq(&g_gen) == gen) {
+      }
+    }
+  }
+  __syncthreads();
+}
 __device__ unsigned g_chain[1 << 20];
 
 template <int MODE>
@@ -29,6 +74,9 @@ __global__ void bench(int iters, unsigned long long* out) {
       cg::this_cluster().sync();
     }
     if (MODE == 5) __syncthreads();
+    if (MODE == 8) grid_bar<0>();
+    if (MODE == 9) grid_bar<16>();
+    if (MODE == 10) grid_bar<8>();
     if (MODE == 6) {  // %globaltimer read by one thread + cluster barrier
       if (threadIdx.x == 0) {
         unsigned long long t;
@@ -54,14 +102,15 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   const int iters = 20000;
-  for (int mode = 0; mode < 8; ++mode) {
+  for (int mode = 0; mode < 11; ++mode) {
     for (int blocks : {16, 32, 148}) {
-      if (mode != 1 && mode != 5 && blocks > 16) continue;
+      const bool gridmode = mode == 1 || mode >= 8;
+      if (!gridmode && mode != 5 && blocks > 16) continue;
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(blocks);
       lc.blockDim = dim3(512);
       cudaLaunchAttribute at[1];
-      if (mode == 1) {
+      if (gridmode) {
         at[0].id = cudaLaunchAttributeCooperative;
         at[0].val.cooperative = 1;
       } else {
@@ -91,6 +140,9 @@ int main() {
                 e = cudaLaunchKernelEx(&lc, bench<6>, iters, d); break;
         case 7: cudaFuncSetAttribute(bench<7>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                 e = cudaLaunchKernelEx(&lc, bench<7>, iters, d); break;
+        case 8: e = cudaLaunchKernelEx(&lc, bench<8>, iters, d); break;
+        case 9: e = cudaLaunchKernelEx(&lc, bench<9>, iters, d); break;
+        case 10: e = cudaLaunchKernelEx(&lc, bench<10>, iters, d); break;
         default: e = cudaLaunchKernelEx(&lc, bench<5>, iters, d); break;
       }
       cudaEventRecord(b);
