@@ -99,6 +99,26 @@ __device__ __forceinline__ bool edge_owned(const DevGraph& g, uint32_t d) {
 // left, right, down, from the edge numbering of generate_ising
 // (generators.cpp:37-43): per row the right edge then the down edge of each
 // vertex; the last row has right edges only.
+// target vertex of directed edge d in generate_ising's lattice numbering
+// (generators.cpp:37-43): rows r < R-1 hold (right, down) per column and a
+// last down edge, the last row only right edges; d = 2e runs lo -> hi.
+__device__ __forceinline__ uint32_t lattice_edge_target(const DevGraph& g, uint32_t d) {
+  const uint32_t C = g.lat_cols, R = g.lat_rows, W = 2u * C - 1u, e = d >> 1;
+  uint32_t r, c, down;
+  if (e < (R - 1u) * W) {
+    r = e / W;
+    const uint32_t o = e - r * W;
+    c = o < 2u * (C - 1u) ? o >> 1 : C - 1u;
+    down = o < 2u * (C - 1u) ? (o & 1u) : 1u;
+  } else {
+    r = R - 1u;
+    c = e - (R - 1u) * W;
+    down = 0u;
+  }
+  const uint32_t lo = r * C + c, hi = down ? lo + C : lo + 1u;
+  return (d & 1u) ? lo : hi;
+}
+
 template <class F>
 __device__ __forceinline__ void for_each_in(const DevGraph& g, uint32_t v, F&& f) {
   if (g.lat_cols) {

@@ -68,6 +68,7 @@ class EngineT final : public EngineBase {
       clist_[1].alloc(static_cast<size_t>(g.D) * 4);
       inlist_.alloc(g.D ? g.D : 1);
       vslot_.alloc(static_cast<size_t>(g.D ? g.D : 1) * 4);  // here, not mid-run: cudaMalloc can stall the device
+      cstamp_.alloc(static_cast<size_t>(g.D ? g.D : 1) * 4);
     }
     vlist_.alloc(static_cast<size_t>(g.V) * 4);
     ctl_.alloc(sizeof(Ctl));
@@ -375,6 +376,7 @@ class EngineT final : public EngineBase {
     hctl_->use_clist = use_clist_ ? 1u : 0u;
     hctl_->persist_ok = use_clist_ && persist ? 1u : 0u;
     if (use_clist_) cuda_check(cudaMemsetAsync(inlist_.p, 0, inlist_.bytes, s_), "memset inlist");
+    if (use_clist_ && persist) cuda_check(cudaMemsetAsync(cstamp_.p, 0, cstamp_.bytes, s_), "memset cstamp");
     hctl_->max_iterations = max_iter;
     const double ns = time_limit * 1e9;
     hctl_->time_limit_ns = ns >= 1.8e19 ? std::numeric_limits<unsigned long long>::max()
@@ -888,7 +890,8 @@ class EngineT final : public EngineBase {
   // while the candidate list is short, else on a cooperative grid of one CTA
   // per SM.
   // BPB_PERSIST_GRID / BPB_PERSIST_CLUSTER override the choice (tuning).
-  DevBuf vslot_;  // refresh slots of the persistent tail (one per candidate-list entry)
+  DevBuf vslot_;   // refresh slots of the persistent tail (one per candidate-list entry)
+  DevBuf cstamp_;  // per-edge commit stamps of the persistent tail (owner test, lattices)
   void run_persist_loop(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
     if (!persist_grid_) {
       // once per process: one CTA per SM (the tail is latency-bound, a second
@@ -933,11 +936,13 @@ class EngineT final : public EngineBase {
       timed(kKPersist, [&] {
         if (cluster)
           cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, true>, dg_, live(), cand(), res_.as<float>(),
-                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
+                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), cstamp_.as<uint32_t>(), ctl(), eps_, prm_,
+                                        cand_list()),
                      "persistent cluster launch");
         else
           cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, false>, dg_, live(), cand(), res_.as<float>(),
-                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), ctl(), eps_, prm_, cand_list()),
+                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), cstamp_.as<uint32_t>(), ctl(), eps_, prm_,
+                                        cand_list()),
                      "persistent launch");
       });
       fetch_ctl_header();

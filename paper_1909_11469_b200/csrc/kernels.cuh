@@ -447,7 +447,13 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
                                                     float* __restrict__ B, float* __restrict__ res,
                                                     float eps, unsigned* numeric_flag,
                                                     unsigned long long& evals, uint8_t* inlist,
-                                                    Stager* cl, bool cl_on) {
+                                                    Stager* cl, bool cl_on, const uint32_t* cstamp = nullptr,
+                                                    uint32_t stamp = 0u, uint32_t via = 0u,
+                                                    bool* skipped = nullptr) {
+  // cstamp (persistent tail, lattice): v was reached through committed edge
+  // `via`; the vertex is refreshed by the thread of its LOWEST committed
+  // incoming edge (cstamp == stamp) only, so duplicate targets need no
+  // atomic dedupe -- the stamps are loaded with the messages
   float T = g.unary_lo[v];
   const float2* __restrict__ A2 = reinterpret_cast<const float2*>(A);
   // incoming messages and (same edge pair) the old outgoing ones, kept in
@@ -498,14 +504,26 @@ __device__ __forceinline__ int vertex_update_binary(const DevGraph& g, uint32_t 
     float2 prs[4];
     float rw[4], ia[4];
     bool il[4];
+    uint32_t cs[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      cs[k] = (cstamp && has[k]) ? cstamp[ins[k]] : 0u;
       prs[k] = has[k] ? ldm<NC>(&A2[ins[k] >> 1]) : make_float2(0.f, 0.f);
       ia[k] = (g.par_mode && has[k]) ? __ldg(&g.ising_a[ins[k] >> 1]) : 0.f;  // with the pair loads
       // prefetch the per-message state so the four updates do not serialise
       // on (possibly aliasing) loads between their stores
       rw[k] = (MODE == kModeDelta && has[k]) ? res[ins[k] ^ 1u] : 0.f;
       il[k] = (CL && cl_on && has[k]) ? inlist[ins[k] ^ 1u] != 0 : true;
+    }
+    if (cstamp) {
+      uint32_t owner = 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (has[k] && cs[k] == stamp) owner = min(owner, ins[k]);
+      if (owner != via) {
+        *skipped = true;
+        return 0;
+      }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) T += has[k] ? ((ins[k] & 1u) ? prs[k].y : prs[k].x) : 0.f;
@@ -793,9 +811,11 @@ template <int QS, int MODE, bool CL, bool NC = true>
 __device__ __forceinline__ int vertex_update(const DevGraph& g, uint32_t v, const float* A, float* B,
                                              float* res, float eps, unsigned* nf,
                                              unsigned long long& evals, uint8_t* inlist, Stager* cl,
-                                             bool cl_on) {
+                                             bool cl_on, const uint32_t* cstamp = nullptr, uint32_t stamp = 0u,
+                                             uint32_t via = 0u, bool* skipped = nullptr) {
   if constexpr (QS == 1)
-    return vertex_update_binary<MODE, CL, NC>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
+    return vertex_update_binary<MODE, CL, NC>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on, cstamp, stamp, via,
+                                              skipped);
   else
     return vertex_update_generic<QS, MODE, CL, NC>(g, v, A, B, res, eps, nf, evals, inlist, cl, cl_on);
 }
@@ -1075,7 +1095,9 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
                                                  float eps, const RnbpParams& prm, const CandList& cl,
                                                  unsigned long long surv, long long* delta_out,
                                                  const uint32_t* slots = nullptr, uint32_t slot_n = 0,
-                                                 uint32_t* vslot = nullptr) {
+                                                 uint32_t* vslot = nullptr, uint32_t* cstamp = nullptr) {
+  // cstamp != nullptr (persistent tail, lattice): a committed edge is stamped
+  // and its slot names the EDGE (the refresh's owner test dedupes targets)
   // slots != nullptr (persistent tail): the survivors are the kept entries of
   // the slot list (kSlotEmpty holes), and a committed edge's target goes to
   // the refresh slot of the same index (the fallback's to slot 0, which is
@@ -1113,7 +1135,10 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
         uint32_t tg = 0;
         commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, false, c, nf, tg);
         delta += c.delta;
-        if (vslot)
+        if (cstamp) {
+          cstamp[d] = stamp;
+          vslot[i] = d;
+        } else if (vslot)
           vslot[i] = nf ? tg : kSlotEmpty;
         else if (nf)
           vlist[atomicAdd(&ctl->nflag, 1u)] = tg;
@@ -1158,7 +1183,10 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
         bool nf = false;
         uint32_t tg = 0;
         commit_edge<QS>(g, d, res[d], live, cand, res, eps, vflag, stamp, false, c, nf, tg);
-        if (vslot)
+        if (cstamp) {
+          cstamp[d] = stamp;
+          vslot[0] = d;
+        } else if (vslot)
           vslot[0] = nf ? tg : kSlotEmpty;
         else if (nf)
           vlist[atomicAdd(&ctl->nflag, 1u)] = tg;

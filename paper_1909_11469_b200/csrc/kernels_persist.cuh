@@ -78,7 +78,8 @@ __device__ __forceinline__ void pacc_push(unsigned* s_pacc, unsigned long long* 
 // mirrors the state into Ctl and writes the trace record for the host.
 template <int QS, bool CLUSTER>
 __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, float* live, float* cand, float* res,
-                                                                uint32_t* vflag, uint32_t* vslot, Ctl* ctl,
+                                                                uint32_t* vflag, uint32_t* vslot, uint32_t* cstamp,
+                                                                Ctl* ctl,
                                                                 float eps, RnbpParams prm, CandList cl) {
   auto sync_all = [] {
     if constexpr (CLUSTER)
@@ -87,6 +88,9 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       cgp::this_grid().sync();
   };
   const uint32_t stride = gridDim.x * blockDim.x;
+  // binary lattice: refresh targets are deduplicated by the owner test on
+  // per-edge commit stamps instead of an atomic on the target's flag
+  const bool own = QS == 1 && g.lat_cols != 0u;
   // Entry slot of this thread within a stride: consecutive 32-entry chunks go
   // to the same warp slot of consecutive CTAs, so a short list spreads over
   // every SM (latency, not one SM's L1/L2 request rate, bounds the phase)
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
           // binary: the commit's loads (candidate, target) are issued with the
           // residual's, speculatively, saving a dependent round trip
           const float cv = QS == 1 ? cand[d] : 0.f;
-          const uint32_t tgp = QS == 1 ? __ldg(&g.ep[d ^ 1u]) : 0u;
+          const uint32_t tgp = (QS == 1 && !own) ? __ldg(&g.ep[d ^ 1u]) : 0u;
           c.count += 16;  // algorithmic bytes: list entry + residual, both slots written
           if (r >= eps) {
             c.survivors += 1;
@@ -175,8 +179,14 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
                 c.frontier += 1;
                 res[d] = 0.f;
                 live[d] = cv;
-                tg = tgp;
-                nf = atomicMax(&vflag[tg], stamp) < stamp;
+                if (own) {  // the slot names the edge; the refresh's owner test dedupes targets
+                  cstamp[d] = stamp;
+                  tg = d;
+                  nf = true;
+                } else {
+                  tg = tgp;
+                  nf = atomicMax(&vflag[tg], stamp) < stamp;
+                }
               } else {
                 commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, false, c, nf, tg);
               }
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
         }
         __syncthreads();
         rnbp_retry_block<QS, true>(g, live, cand, res, vflag, nullptr, nullptr, ctl, eps, prm, cl, acc[3],
-                                   reinterpret_cast<long long*>(&acc[0]), list, n, vslot);
+                                   reinterpret_cast<long long*>(&acc[0]), list, n, vslot, own ? cstamp : nullptr);
       }
       sync_all();
       retry_front = ctl->frontier;
@@ -242,7 +252,13 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
             st.push(d);
             ++kept;
           }
-          if (v != kSlotEmpty) {
+          if (v != kSlotEmpty && own) {  // v = the committed edge
+            bool skipped = false;
+            cnt += vertex_update<QS, kModeDelta, true, false>(g, lattice_edge_target(g, v), live, cand, res, eps,
+                                                              &ctl->numeric_error, evals, cl.inlist, &st, true,
+                                                              cstamp, stamp, v, &skipped);
+            visits += skipped ? 0u : 1u;
+          } else if (v != kSlotEmpty) {
             cnt += vertex_update<QS, kModeDelta, true, false>(g, v, live, cand, res, eps, &ctl->numeric_error,
                                                               evals, cl.inlist, &st, true);
             ++visits;
