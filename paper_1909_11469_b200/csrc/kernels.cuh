@@ -92,6 +92,18 @@ struct Stager {
   }
 };
 
+// Last flush of a phase: one barrier before the reservation, one after; the
+// buffer is not reset (the next phase's init() does that behind its barrier).
+__device__ __forceinline__ void flush_final(Stager& st) {
+  __syncthreads();
+  const unsigned n = min(*st.scount, st.cap);
+  if (n == 0) return;
+  if (threadIdx.x == 0) *st.sbase = atomicAdd(st.gcount, n);
+  __syncthreads();
+  const unsigned gb = *st.sbase;
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) st.gdst[gb + i] = st.sbuf[i];
+}
+
 // Flush two stagers with their global reservations issued concurrently
 // (threads 0 and 32), one round trip instead of two.
 __device__ __forceinline__ void flush2(Stager& a, Stager& b) {

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       c.count = 8ull * slots + 4ull * kept + 4ull * visits +
                 static_cast<unsigned long long>(8 * QS + 4 + 4 * QS + 8) * evals;
       warp_contrib(s_pacc, c);
-      st.flush(0);  // its first barrier orders the warp sums
+      flush_final(st);  // its first barrier orders the warp sums
       mark(5);
       pacc_push(s_pacc, acc);
       mark(6);
