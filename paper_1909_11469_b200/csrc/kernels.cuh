@@ -1026,13 +1026,35 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
           if (rr[2] >= eps || rr[3] >= eps)
             ph[1] = philox_edge(prm.seed, it, prm.attempt, 2ull * q + 1ull + g.edge_offset);
         }
+        // binary: the four commits' operands (candidates, targets) in two
+        // 16-byte loads, one round trip instead of one per commit
+        float4 cv4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint4 ep4 = make_uint4(0u, 0u, 0u, 0u);
+        if (QS == 1 && prm.commit && 4 * q + 3 < g.D &&
+            (rr[0] >= eps || rr[1] >= eps || rr[2] >= eps || rr[3] >= eps)) {
+          cv4 = reinterpret_cast<const float4*>(cand)[q];
+          ep4 = __ldg(reinterpret_cast<const uint4*>(g.ep) + q);
+        }
+        const float cvs[4] = {cv4.x, cv4.y, cv4.z, cv4.w};
+        const uint32_t tgs[4] = {ep4.y, ep4.x, ep4.w, ep4.z};  // target of d = ep[d ^ 1]
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t d = 4 * q + k;
           if (rr[k] >= eps) {  // padding entries are 0
             c.survivors += 1;
             if (!draw || u53_of(ph[k >> 1], d) < thresh) {
-              if (prm.commit) {
+              if (QS == 1 && prm.commit && 4 * q + 3 < g.D) {  // commit_edge with the prefetched operands
+                c.delta -= 1;
+                c.frontier += 1;
+                res[d] = 0.f;
+                live[d] = cvs[k];
+                tg[k] = tgs[k];
+                if (dense) {
+                  vflag[tg[k]] = stamp;
+                } else {
+                  nf[k] = atomicMax(&vflag[tg[k]], stamp) < stamp;
+                }
+              } else if (prm.commit) {
                 commit_edge<QS>(g, d, rr[k], live, cand, res, eps, vflag, stamp, dense, c, nf[k], tg[k]);
               } else {
                 sel[d] = 1;
