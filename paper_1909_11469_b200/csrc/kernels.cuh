@@ -679,7 +679,7 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
 constexpr int kLatVPT = 4;
 constexpr uint32_t kLatTile = kBlock * kLatVPT;
 
-template <int MODE, bool CL>
+template <int MODE, bool CL, int VPT = kLatVPT>
 __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const float* __restrict__ A,
                                                      float* __restrict__ B, float* __restrict__ res,
                                                      const uint32_t* __restrict__ vflag, uint32_t stamp,
@@ -687,13 +687,13 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
                                                      unsigned long long& evals, unsigned long long& visits,
                                                      uint8_t* inlist, Stager* cl, bool cl_on) {
   const uint32_t C = g.lat_cols, R = g.lat_rows;
-  const uint32_t tpr = (C + kLatTile - 1) / kLatTile;
+  const uint32_t tpr = (C + (kBlock * VPT) - 1) / (kBlock * VPT);
   const uint64_t ntiles = static_cast<uint64_t>(R) * tpr;
   const float2* __restrict__ A2 = reinterpret_cast<const float2*>(A);
   const float* __restrict__ ea = g.ising_a;
   bool bad = false;
   // Each block walks a contiguous run of tiles in (column strip, row) order:
-  // down the rows of one kLatTile-wide strip, so the upper neighbour's edge
+  // down the rows of one (kBlock * VPT)-wide strip, so the upper neighbour's edge
   // pairs were read by this block one tile ago and the message sectors it
   // half-writes are completed by its next tile -- the live working set is
   // ~2 rows x strip x blocks (L2-resident even at 16384^2).
@@ -701,24 +701,24 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
   for (uint64_t t = t_begin; t < t_end; ++t) {
     const uint32_t strip = static_cast<uint32_t>(t / R);
     const uint32_t r = static_cast<uint32_t>(t - static_cast<uint64_t>(strip) * R);
-    const uint32_t c0 = strip * kLatTile + threadIdx.x;
+    const uint32_t c0 = strip * (kBlock * VPT) + threadIdx.x;
     const bool last = r + 1u == R, first = r == 0u;
     const uint32_t row = r * (2u * C - 1u), prow = first ? 0u : (r - 1u) * (2u * C - 1u);
-    bool act[kLatVPT];
-    float2 pU[kLatVPT], pL[kLatVPT], pR[kLatVPT], pD[kLatVPT];
-    float aU[kLatVPT], aL[kLatVPT], aR[kLatVPT], aD[kLatVPT], un[kLatVPT];
+    bool act[VPT];
+    float2 pU[VPT], pL[VPT], pR[VPT], pD[VPT];
+    float aU[VPT], aL[VPT], aR[VPT], aD[VPT], un[VPT];
     // per vertex, prefetched with the messages: bit j = old residual of out
     // message j (up, left, right, down) >= eps, bit 4 + j = it is in the
     // candidate list; the bookkeeping below then needs no dependent loads
-    uint32_t pre[kLatVPT];
+    uint32_t pre[VPT];
 #pragma unroll
-    for (int k = 0; k < kLatVPT; ++k) {
+    for (int k = 0; k < VPT; ++k) {
       const uint32_t c = c0 + k * kBlock;
       act[k] = c < C;
       if (check_flag && act[k]) act[k] = vflag[r * C + c] == stamp;
     }
 #pragma unroll
-    for (int k = 0; k < kLatVPT; ++k) {
+    for (int k = 0; k < VPT; ++k) {
       const uint32_t c = c0 + k * kBlock;
       pU[k] = pL[k] = pR[k] = pD[k] = make_float2(0.f, 0.f);
       aU[k] = aL[k] = aR[k] = aD[k] = 1.f;
@@ -748,7 +748,7 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       un[k] = __ldg(&g.unary_lo[r * C + c]);
     }
 #pragma unroll
-    for (int k = 0; k < kLatVPT; ++k) {
+    for (int k = 0; k < VPT; ++k) {
       pre[k] = 0u;
       if (MODE != kModeDelta && !(CL && cl_on)) continue;
       const uint32_t c = c0 + k * kBlock;
@@ -764,7 +764,7 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       }
     }
 #pragma unroll
-    for (int k = 0; k < kLatVPT; ++k) {
+    for (int k = 0; k < VPT; ++k) {
       if (CL) cl->flush(1024);  // <= 4 kBlock pushes per k
       const uint32_t c = c0 + k * kBlock;
       const uint32_t dn = c + 1u < C ? 1u : 0u;
@@ -873,7 +873,9 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
   const bool cl_on = CL && ctl->cl_state >= 1u;
   const bool lattice = QS == 1 && g.lat_cols != 0u && g.par_mode != 0u && dense;
   if (lattice)
-    lattice_binary_tiles<MODE, CL>(g, A, B, res, vflag, stamp, LIST, eps, &ctl->numeric_error, cnt, evals, visits,
+    // the refresh keeps more state per vertex (old-residual / in-list bits):
+    // 2 vertices per thread keep it within 128 registers
+    lattice_binary_tiles<MODE, CL, MODE == kModeDelta ? 2 : kLatVPT>(g, A, B, res, vflag, stamp, LIST, eps, &ctl->numeric_error, cnt, evals, visits,
                                    cand_list.inlist, &cl, cl_on);
   for (uint32_t base = lattice ? n : blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint32_t i = base + threadIdx.x;
