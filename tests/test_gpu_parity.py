@@ -267,3 +267,19 @@ def test_nonsquare_lattice_detected_and_exact(bp, orc, rows, cols):
         assert r.converged == o.converged, kind
         if r.converged:
             assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL, kind
+
+
+@pytest.mark.parametrize("name", ["er", "potts4", "potts8"])
+def test_rnbp_persistent_tail_generic_graphs(bp, name):
+    """The persistent tail on CSR (non-lattice) binary graphs and on generic
+    q-state graphs (atomic target dedupe, generic vertex update) runs the same
+    iterations as the per-kernel graph loop."""
+    g = {"er": lambda: bp.generate_er(20000, 40000, 2.5, 1),
+         "potts4": lambda: bp.generate_potts(64, 4, 1.5, 2),
+         "potts8": lambda: bp.generate_potts(48, 8, 1.0, 5)}[name]()
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=3000, seed=3)
+    a = bp.run(g, cfg)
+    b = bp.run_ex(g, cfg, flags=bp.RUN_NO_PERSIST)
+    assert a.trace_signature() == b.trace_signature()
+    assert np.max(np.abs(a.beliefs.values - b.beliefs.values)) == 0.0
+    assert a.gpu_launches < b.gpu_launches  # the persistent kernel took over
