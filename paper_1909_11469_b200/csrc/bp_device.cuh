@@ -206,6 +206,7 @@ struct Ctl {
   // evals, visits), triple-buffered by iteration; touched-list counters,
   // double-buffered; the time-limit verdict of CTA 0
   unsigned long long pacc3[3][6];
+  unsigned long long handover_it;  // iteration at which the graph loop handed over to the persistent kernel
   unsigned int nfl2[2];
   unsigned int time_stop;
   unsigned int pad4_;

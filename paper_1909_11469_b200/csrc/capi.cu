@@ -4,6 +4,9 @@
 #include <cstring>
 #include <string>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "engine.hpp"
 #include "graph.hpp"
 
@@ -129,8 +132,19 @@ int bp_run_ex(const bp_graph* g, const bp_sched_config* cfg, const bp_run_opts* 
     if (cfg->kind == BP_SERIAL_RBP)
       throw bpb::Error(BP_ERR_UNSUPPORTED,
                        "serial RBP is strictly sequential and is not offloaded (use the reference run_serial_rbp)");
+    static const bool dbg = std::getenv("BPB_DEBUG_BUILD") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     auto e = bpb::make_engine(*g->impl, *cfg);
+    const auto t1 = std::chrono::steady_clock::now();
     e->run(opts, result, beliefs_out, trace_out, trace_cap);
+    const auto t2 = std::chrono::steady_clock::now();
+    e.reset();
+    if (dbg) {
+      const auto t3 = std::chrono::steady_clock::now();
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "bp_run: engine %.2f ms, run %.2f ms (device %.2f), teardown %.2f ms\n", ms(t0, t1),
+                   ms(t1, t2), result->device_ms, ms(t2, t3));
+    }
   });
 }
 

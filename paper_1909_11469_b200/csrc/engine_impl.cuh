@@ -120,9 +120,12 @@ class EngineT final : public EngineBase {
     enqueue_init(cfg_.kind == BP_LBP);
 
     uint64_t copied = 0;
-    // first look: did the initial sweep already converge / hit a cap?
-    fetch_ctl_header();
-    drain_trace(trace, trace_cap, copied);
+    // first look: did the initial sweep already converge / hit a cap?  (The
+    // device loop checks that itself, so the graph path skips the round trip.)
+    if (!use_graph) {
+      fetch_ctl_header();
+      drain_trace(trace, trace_cap, copied);
+    }
     if (!hctl_->done) {
       if (use_graph) {
         run_graph_loop(trace, trace_cap, copied);
@@ -841,6 +844,10 @@ class EngineT final : public EngineBase {
       const uint64_t start_it = hctl_->iteration;
       set_iteration_budget(start_it + kTraceRing / 2);
       cuda_check(cudaGraphLaunch(gexec_, s_), "graph launch");
+      // RnBP: the persistent tail is enqueued right behind the graph (it
+      // returns at once unless the graph handed list mode over), so the
+      // handover costs no host round trip
+      if (persist_) launch_persist(false);
       fetch_ctl_header();
       drain_trace(trace, cap, copied);
       if (!hctl_->done && handover()) break;  // RnBP list mode -> persistent kernel
@@ -848,38 +855,38 @@ class EngineT final : public EngineBase {
         if (hctl_->stop_reason == kStopMaxIter && hctl_->iteration < cfg_.max_iterations && budget_stop_) {
           // stopped by the chunk budget, not by the run: continue
           clear_budget_stop();
+          if (handover()) break;
           continue;
         }
         break;
       }
     }
-    launches_ += (hctl_->iteration - it0) * body_launches_;
+    // iterations run by the graph body (the chained persistent kernel counts its own launches)
+    const uint64_t graph_end = hctl_->handover_it >= it0 && hctl_->handover_it ? std::min(hctl_->iteration, hctl_->handover_it)
+                                                                               : hctl_->iteration;
+    launches_ += (graph_end - it0) * body_launches_;
     set_cond_handle(0);
   }
 
   // Chunking of the device loop: temporarily lower max_iterations so the ring
   // never overruns; a stop caused by it is undone before continuing.
   bool budget_stop_ = false;
+  // (stream-ordered: no host synchronisation, so the device never idles on
+  // these between a loop launch and the next)
   void set_iteration_budget(uint64_t limit) {
     const uint64_t eff = std::min<uint64_t>(limit, cfg_.max_iterations);
     budget_stop_ = eff < cfg_.max_iterations;
-    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, max_iterations), &eff, 8,
-                               cudaMemcpyHostToDevice, s_),
-               "ctl h2d");
-    sync();
+    k_set_u64<<<1, 1, 0, s_>>>(&ctl()->max_iterations, eff);
+    launch_check();
   }
   void clear_budget_stop() {
-    const unsigned zero = 0;
-    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, done), &zero, 4,
-                               cudaMemcpyHostToDevice, s_),
-               "ctl h2d");
-    sync();
+    k_set_u32<<<1, 1, 0, s_>>>(&ctl()->done, 0u);
+    launch_check();
+    hctl_->done = 0u;  // host mirror
   }
   void set_cond_handle(unsigned long long h) {
-    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + offsetof(Ctl, cond_handle), &h, 8,
-                               cudaMemcpyHostToDevice, s_),
-               "ctl h2d");
-    sync();
+    k_set_u64<<<1, 1, 0, s_>>>(&ctl()->cond_handle, h);
+    launch_check();
   }
 
   // ---- persistent RnBP tail (kernels_persist.cuh)
@@ -892,59 +899,66 @@ class EngineT final : public EngineBase {
   // BPB_PERSIST_GRID / BPB_PERSIST_CLUSTER override the choice (tuning).
   DevBuf vslot_;   // refresh slots of the persistent tail (one per candidate-list entry)
   DevBuf cstamp_;  // per-edge commit stamps of the persistent tail (owner test, lattices)
-  void run_persist_loop(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
-    if (!persist_grid_) {
-      // once per process: one CTA per SM (the tail is latency-bound, a second
-      // CTA per SM only adds barrier participants: 296 CTAs measured 3%
-      // slower than 148)
-      static const unsigned grid = [this] {
-        int per_sm = 0;
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rnbp_persist<QS, false>, kPersistBlock, 0),
-                   "occupancy");
-        if (per_sm < 1) throw Error(BP_ERR_CUDA, "persistent RnBP kernel does not fit on an SM");
-        cuda_check(cudaFuncSetAttribute(k_rnbp_persist<QS, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                   "cluster attribute");
-        return static_cast<unsigned>(sm_count());
-      }();
-      persist_grid_ = grid;
+  void ensure_persist_setup() {
+    if (persist_grid_) return;
+    // once per process: one CTA per SM (the tail is latency-bound, a second
+    // CTA per SM only adds barrier participants: 296 CTAs measured 3% slower
+    // than 148)
+    static const unsigned grid = [] {
+      int per_sm = 0;
+      cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rnbp_persist<QS, false>, kPersistBlock, 0),
+                 "occupancy");
+      if (per_sm < 1) throw Error(BP_ERR_CUDA, "persistent RnBP kernel does not fit on an SM");
+      cuda_check(cudaFuncSetAttribute(k_rnbp_persist<QS, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                 "cluster attribute");
+      return static_cast<unsigned>(sm_count());
+    }();
+    persist_grid_ = grid;
+  }
+
+  // one launch of the persistent tail: a 16-CTA cluster or a cooperative grid
+  // of one CTA per SM (BPB_PERSIST_GRID / BPB_PERSIST_CLUSTER: tuning overrides)
+  void launch_persist(bool cluster) {
+    ensure_persist_setup();
+    static const char* eg = std::getenv("BPB_PERSIST_GRID");
+    static const char* ec = std::getenv("BPB_PERSIST_CLUSTER");
+    if (ec) cluster = std::atoi(ec) != 0;
+    unsigned grid = cluster ? 16u : persist_grid_;
+    if (eg && !cluster) grid = std::min<unsigned>(persist_grid_, std::max(1, std::atoi(eg)));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kPersistBlock);
+    lc.stream = s_;
+    cudaLaunchAttribute at[1];
+    if (cluster) {
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = grid;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+    } else {
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
     }
-    const char* eg = std::getenv("BPB_PERSIST_GRID");
-    const char* ec = std::getenv("BPB_PERSIST_CLUSTER");
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    timed(kKPersist, [&] {
+      if (cluster)
+        cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, true>, dg_, live(), cand(), res_.as<float>(),
+                                      vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), cstamp_.as<uint32_t>(), ctl(),
+                                      eps_, prm_, cand_list()),
+                   "persistent cluster launch");
+      else
+        cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, false>, dg_, live(), cand(), res_.as<float>(),
+                                      vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), cstamp_.as<uint32_t>(), ctl(),
+                                      eps_, prm_, cand_list()),
+                   "persistent launch");
+    });
+  }
+
+  void run_persist_loop(bp_iter_record* trace, uint64_t cap, uint64_t& copied) {
     for (;;) {
       set_iteration_budget(hctl_->iteration + kTraceRing / 2);
-      const uint32_t list_n = hctl_->cl_n[hctl_->cl_cur];
-      bool cluster = list_n < kPersistClusterList;
-      if (ec) cluster = std::atoi(ec) != 0;
-      unsigned grid = cluster ? 16u : persist_grid_;
-      if (eg && !cluster) grid = std::min<unsigned>(persist_grid_, std::max(1, std::atoi(eg)));
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(grid);
-      lc.blockDim = dim3(kPersistBlock);
-      lc.stream = s_;
-      cudaLaunchAttribute at[1];
-      if (cluster) {
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = grid;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-      } else {
-        at[0].id = cudaLaunchAttributeCooperative;
-        at[0].val.cooperative = 1;
-      }
-      lc.attrs = at;
-      lc.numAttrs = 1;
-      timed(kKPersist, [&] {
-        if (cluster)
-          cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, true>, dg_, live(), cand(), res_.as<float>(),
-                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), cstamp_.as<uint32_t>(), ctl(), eps_, prm_,
-                                        cand_list()),
-                     "persistent cluster launch");
-        else
-          cuda_check(cudaLaunchKernelEx(&lc, k_rnbp_persist<QS, false>, dg_, live(), cand(), res_.as<float>(),
-                                        vflag_.as<uint32_t>(), vslot_.as<uint32_t>(), cstamp_.as<uint32_t>(), ctl(), eps_, prm_,
-                                        cand_list()),
-                     "persistent launch");
-      });
+      launch_persist(hctl_->cl_n[hctl_->cl_cur] < kPersistClusterList);
       fetch_ctl_header();
       drain_trace(trace, cap, copied);
       if (hctl_->done) {

@@ -2,6 +2,8 @@
 // (mrf.cpp:25-106) and of the generators (generators.cpp:24-71).
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -21,19 +23,88 @@ void cuda_check(cudaError_t e, const char* what) {
   throw Error(BP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+namespace {
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free;  // (device, capacity) -> block
+  size_t held = 0;
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache;  // process lifetime (no teardown-order issues)
+  return *c;
+}
+constexpr size_t kCacheMaxBlock = size_t{1} << 31;  // larger blocks are freed, not cached
+constexpr size_t kCacheMaxHeld = size_t{16} << 30;
+}  // namespace
+
+void DevBuf::trim_cache() {
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (auto& kv : c.free) {
+    cudaSetDevice(kv.first.first);
+    cudaFree(kv.second);
+  }
+  cudaSetDevice(dev);
+  c.free.clear();
+  c.held = 0;
+}
+
 DevBuf::~DevBuf() { reset(); }
 void DevBuf::reset() {
-  if (p) cudaFree(p);
+  if (p) {
+    BlockCache& c = block_cache();
+    // the block may still be read by queued work: settle the device first
+    // (cudaFree would synchronise too)
+    cudaDeviceSynchronize();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (cap <= kCacheMaxBlock && c.held + cap <= kCacheMaxHeld) {
+      c.free.emplace(std::make_pair(dev, cap), p);
+      c.held += cap;
+    } else {
+      cudaFree(p);
+    }
+  }
   p = nullptr;
   bytes = 0;
+  cap = 0;
 }
 void DevBuf::alloc(size_t n) {
   reset();
   if (n == 0) n = 16;
   // 64 bytes of slack: 16-byte-granular bulk copies (kernels_lbp.cuh) may read
   // up to one granule past the end of an array
-  cuda_check(cudaMalloc(&p, n + 64), "cudaMalloc");
+  const size_t want = n + 64;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    BlockCache& c = block_cache();
+    std::unique_lock<std::mutex> lk(c.mu);
+    auto it = c.free.lower_bound(std::make_pair(dev, want));
+    if (it != c.free.end() && it->first.first == dev && it->first.second <= want + want / 4) {  // close fit only
+      p = it->second;
+      cap = it->first.second;
+      c.held -= cap;
+      c.free.erase(it);
+      lk.unlock();
+      bytes = n;
+      // zero-filled like a fresh allocation in practice is
+      cuda_check(cudaMemset(p, 0, cap), "memset (cached block)");
+      return;
+    }
+  }
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e == cudaErrorMemoryAllocation) {  // cached blocks first
+    cudaGetLastError();
+    trim_cache();
+    e = cudaMalloc(&p, want);
+  }
+  cuda_check(e, "cudaMalloc");
   bytes = n;
+  cap = want;
 }
 void DevBuf::upload(const void* src, size_t n) {
   alloc(n);

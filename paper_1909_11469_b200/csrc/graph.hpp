@@ -15,9 +15,14 @@ namespace bpb {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Device buffer.  Freed blocks go back to a process-wide cache (keyed by
+// size) instead of cudaFree: a run allocates ~10 arrays of O(D) and graph
+// construction as many again, and cudaMalloc/cudaFree of such blocks costs
+// milliseconds each (and stalls the device) on the end-to-end path.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  size_t cap = 0;  // allocated bytes (>= bytes + 64)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -25,6 +30,7 @@ struct DevBuf {
   void alloc(size_t n);
   void upload(const void* src, size_t n);
   void reset();
+  static void trim_cache();  // cudaFree every cached block
   template <class T>
   T* as() const {
     return static_cast<T*>(p);

@@ -171,6 +171,11 @@ __device__ __forceinline__ void block_accumulate(Ctl* ctl, const Contrib& c) {
   }
 }
 
+// Stream-ordered scalar stores into the control block (the value travels as a
+// kernel argument: no pinned staging, no host synchronisation)
+static __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+static __global__ void k_set_u32(unsigned* p, unsigned v) { *p = v; }
+
 // Early exit of every loop kernel once the run is over; inside the device-side
 // WHILE loop it also clears the loop condition.
 __device__ __forceinline__ bool run_done(Ctl* c) {
@@ -429,6 +434,7 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
   }
   // the graph loop also hands RnBP list mode over to the persistent kernel
   const bool handover = c->persist_ok && c->cl_state == 2u;
+  if (handover && !c->handover_it) c->handover_it = c->iteration;
   if (c->cond_handle && mode != kFinApply)
     cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(c->cond_handle), c->done || handover ? 0u : 1u);
 }

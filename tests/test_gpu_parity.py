@@ -228,7 +228,7 @@ def test_rnbp_persistent_tail_matches_graph_loop(bp, orc, n, c, seed, p):
     b = bp.run_ex(g, cfg, flags=bp.RUN_NO_PERSIST)
     assert a.trace_signature() == b.trace_signature()
     assert np.max(np.abs(a.beliefs.values - b.beliefs.values)) <= 1e-6
-    assert a.gpu_launches <= b.gpu_launches
+    assert a.gpu_launches <= b.gpu_launches + 2  # + the persistent launch chained behind each graph chunk
 
 
 def _lattice_arrays(orc, rows, cols, seed, c=2.0):
