@@ -23,13 +23,17 @@ constexpr int kSVPT = 2;                  // vertices per thread per tile
 constexpr uint32_t kSW = kBlock * kSVPT;  // strip width (columns)
 constexpr int kSEdges = 2 * kSW;          // edges of a strip row
 
+// ring of row slots: the row above, the tile row, and kLbpAhead rows in flight
+constexpr int kLbpAhead = 2;
+constexpr int kRing = 2 + kLbpAhead;
+
 struct LbpSmem {
-  float2 A[3][kSEdges + 2];  // ring: message pairs (+ alignment slack)
-  float E[3][kSEdges + 8];   // ring: couplings
-  float U[3][kSW + 8];       // ring: unaries
+  float2 A[kRing][kSEdges + 2];  // ring: message pairs (+ alignment slack)
+  float E[kRing][kSEdges + 8];   // ring: couplings
+  float U[kRing][kSW + 8];       // ring: unaries
   float2 B[2][kSEdges + 2];  // new message pairs being assembled (row above / tile row)
-  unsigned long long bar[3];  // mbarriers of the ring slots
-  uint32_t aoff[3], eoff[3], uoff[3];  // alignment offsets of the ring slots
+  unsigned long long bar[kRing];  // mbarriers of the ring slots
+  uint32_t aoff[kRing], eoff[kRing], uoff[kRing];  // alignment offsets of the ring slots
   // S.B[b] holds the pair of global edge e0 + k at index k + boff[b]: same
   // 16-byte phase as global memory, so completed rows leave by bulk store
 };
@@ -100,7 +104,7 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
   if (t_begin >= t_end) return;
   const bool leader = threadIdx.x == 0;
   if (leader) {
-    for (int k = 0; k < 3; ++k) mbar_init(&S.bar[k], 1);
+    for (int k = 0; k < kRing; ++k) mbar_init(&S.bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -178,41 +182,55 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
   int cnt = 0;
   unsigned long long evals = 0, visits = 0;
   bool bad = false;
-  // ring bookkeeping: slot of the tile row, slot of the row above (-1 = none)
-  int s_cur = 0, s_up = -1, s_next = 1;
+  // ring bookkeeping: slot of the tile row, of the row above (-1 = none), and
+  // of the next kLbpAhead tiles' rows (in flight; -1 = no such tile)
+  int s_cur = 0, s_up = -1;
+  int q[kLbpAhead];
   int b_cur = 0;           // S.B[b_cur] receives the tile row; S.B[b_cur ^ 1] the row above
   bool prev_b = false;     // S.B[b_cur ^ 1] holds the row above's messages (to write out)
   uint32_t prev_strip = 0xFFFFFFFFu, prev_row = 0;
-
-  // prologue: the first tile's row above (if any) and its row
+  auto step = [&](uint32_t& st, uint32_t& rr) {  // (strip, row) of the next tile
+    if (++rr == R) {
+      rr = 0;
+      ++st;
+    }
+  };
+  // a ring slot not holding the row above, the tile row or a row in flight
+  auto free_slot = [&](int up, int cur) {
+    for (int k = 0; k < kRing; ++k) {
+      bool used = k == up || k == cur;
+      for (int j = 0; j < kLbpAhead; ++j) used = used || q[j] == k;
+      if (!used) return k;
+    }
+    return 0;  // not reached: kRing = 2 + kLbpAhead slots, at most kRing - 1 in use here
+  };
+  // prologue: the first tile's row above (if any), its row, and the rows of
+  // the next kLbpAhead tiles
+  uint32_t strip = static_cast<uint32_t>(t_begin / R), r = static_cast<uint32_t>(t_begin % R);
   {
-    const uint32_t strip = static_cast<uint32_t>(t_begin / R), r = static_cast<uint32_t>(t_begin % R);
-    if (leader) {
-      if (r > 0) issue_row(2, strip, r - 1u);
-      issue_row(0, strip, r);
-    }
+    int used = 0;
     if (r > 0) {
-      wait_slot(2);
-      s_up = 2;
-      s_next = 1;
+      s_up = used++;
+      if (leader) issue_row(s_up, strip, r - 1u);
     }
+    s_cur = used++;
+    if (leader) issue_row(s_cur, strip, r);
+    uint32_t st = strip, rr = r;
+    for (int k = 0; k < kLbpAhead; ++k) {
+      step(st, rr);
+      q[k] = t_begin + 1 + k < t_end ? used++ : -1;
+      if (q[k] >= 0 && leader) issue_row(q[k], st, rr);
+    }
+    if (s_up >= 0) wait_slot(s_up);
   }
   // (strip, row) of tile t, advanced incrementally (no 64-bit division per tile)
-  uint32_t strip = static_cast<uint32_t>(t_begin / R), r = static_cast<uint32_t>(t_begin % R);
   for (uint64_t t = t_begin; t < t_end; ++t) {
     const uint32_t c0 = strip * kSW, w = min(kSW, C - c0);
     const bool lastrow = r + 1u == R, first = r == 0u;
     const bool cont = prev_b && prev_strip == strip && prev_row + 1u == r;
-    // prefetch the next tile's row (and, across a strip change, its row above)
     const bool has_t1 = t + 1 < t_end;
-    uint32_t strip1 = 0, r1 = 0;
-    bool next_cont = false;
-    if (has_t1) {
-      strip1 = r + 1u == R ? strip + 1u : strip;
-      r1 = r + 1u == R ? 0u : r + 1u;
-      next_cont = strip1 == strip && r1 == r + 1u;
-      if (leader) issue_row(s_next, strip1, r1);
-    }
+    // the next tile continues this strip (a strip change always restarts at row 0)
+    const bool next_cont = has_t1 && r + 1u < R;
     wait_slot(s_cur);
     if (!cont && prev_b) {  // strip changed: flush the previous row without its D.y
       write_row(b_cur ^ 1, prev_strip, prev_row, false);
@@ -315,32 +333,23 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
     prev_strip = strip;
     prev_row = r;
     b_cur ^= 1;
-    // ring rotation: the next tile's row above is this row when continuing
+    // ring rotation: this row becomes the row above when the next tile
+    // continues the strip; the freed slot takes the row kLbpAhead + 1 tiles ahead
     if (has_t1) {
-      if (next_cont) {
-        const int freed = s_up;
-        s_up = s_cur;
-        s_cur = s_next;
-        s_next = freed >= 0 ? freed : 3 - s_up - s_cur;
-      } else {
-        // strip change: load the next tile's row above into the free slot
-        const int free_slot = 3 - s_cur - s_next;  // {0,1,2} minus the two in use
-        if (leader && r1 > 0) issue_row(free_slot, strip1, r1 - 1u);
-        if (r1 > 0) {
-          wait_slot(free_slot);
-          s_up = free_slot;
-        } else {
-          s_up = -1;
-        }
-        const int old_cur = s_cur;
-        s_cur = s_next;
-        s_next = old_cur;
+      const int new_up = next_cont ? s_cur : -1;
+      s_cur = q[0];
+      for (int k = 0; k + 1 < kLbpAhead; ++k) q[k] = q[k + 1];
+      q[kLbpAhead - 1] = -1;
+      if (t + 1 + kLbpAhead < t_end) {
+        uint32_t st = strip, rr = r;
+        for (int k = 0; k <= kLbpAhead; ++k) step(st, rr);
+        const int f = free_slot(new_up, s_cur);
+        q[kLbpAhead - 1] = f;
+        if (leader) issue_row(f, st, rr);
       }
+      s_up = new_up;
     }
-    if (++r == R) {
-      r = 0;
-      ++strip;
-    }
+    step(strip, r);
   }
   if (prev_b) write_row(b_cur ^ 1, prev_strip, prev_row, false);  // its D.y: the next block
   if (leader) bulk_wait_all();
