@@ -182,10 +182,12 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
   int cnt = 0;
   unsigned long long evals = 0, visits = 0;
   bool bad = false;
-  // ring bookkeeping: slot of the tile row, of the row above (-1 = none), and
-  // of the next kLbpAhead tiles' rows (in flight; -1 = no such tile)
-  int s_cur = 0, s_up = -1;
-  int q[kLbpAhead];
+  // Ring bookkeeping is modular: rows enter the ring in consumption order, so
+  // tile i of this block (i = t - t_begin) holds slot (base + i) % kRing, its
+  // row above (the previous tile's row, or the prologue's row) the slot
+  // before, and the row kLbpAhead + 1 tiles ahead goes into that slot once
+  // the tile is done.  (A strip change restarts at row 0: no row above.)
+  static_assert((kRing & (kRing - 1)) == 0, "power-of-two ring");
   int b_cur = 0;           // S.B[b_cur] receives the tile row; S.B[b_cur ^ 1] the row above
   bool prev_b = false;     // S.B[b_cur ^ 1] holds the row above's messages (to write out)
   uint32_t prev_strip = 0xFFFFFFFFu, prev_row = 0;
@@ -195,42 +197,24 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
       ++st;
     }
   };
-  // a ring slot not holding the row above, the tile row or a row in flight
-  auto free_slot = [&](int up, int cur) {
-    for (int k = 0; k < kRing; ++k) {
-      bool used = k == up || k == cur;
-      for (int j = 0; j < kLbpAhead; ++j) used = used || q[j] == k;
-      if (!used) return k;
-    }
-    return 0;  // not reached: kRing = 2 + kLbpAhead slots, at most kRing - 1 in use here
-  };
-  // prologue: the first tile's row above (if any), its row, and the rows of
-  // the next kLbpAhead tiles
   uint32_t strip = static_cast<uint32_t>(t_begin / R), r = static_cast<uint32_t>(t_begin % R);
-  {
-    int used = 0;
-    if (r > 0) {
-      s_up = used++;
-      if (leader) issue_row(s_up, strip, r - 1u);
+  const int base = r > 0u ? 1 : 0;
+  // (strip, row) of the tile whose row is issued next (leader only)
+  uint32_t st_i = strip, r_i = r;
+  if (leader) {  // prologue: the first tile's row above, its row and kLbpAhead more rows
+    if (r > 0u) issue_row(0, strip, r - 1u);
+    for (int k = 0; k <= kLbpAhead && t_begin + k < t_end; ++k) {
+      issue_row((base + k) & (kRing - 1), st_i, r_i);
+      step(st_i, r_i);
     }
-    s_cur = used++;
-    if (leader) issue_row(s_cur, strip, r);
-    uint32_t st = strip, rr = r;
-    for (int k = 0; k < kLbpAhead; ++k) {
-      step(st, rr);
-      q[k] = t_begin + 1 + k < t_end ? used++ : -1;
-      if (q[k] >= 0 && leader) issue_row(q[k], st, rr);
-    }
-    if (s_up >= 0) wait_slot(s_up);
   }
-  // (strip, row) of tile t, advanced incrementally (no 64-bit division per tile)
-  for (uint64_t t = t_begin; t < t_end; ++t) {
+  if (r > 0u) wait_slot(0);
+  int s_cur = base;
+  for (uint64_t t = t_begin; t < t_end; ++t, s_cur = (s_cur + 1) & (kRing - 1)) {
+    const int s_up = r > 0u ? (s_cur + kRing - 1) & (kRing - 1) : -1;
     const uint32_t c0 = strip * kSW, w = min(kSW, C - c0);
     const bool lastrow = r + 1u == R, first = r == 0u;
     const bool cont = prev_b && prev_strip == strip && prev_row + 1u == r;
-    const bool has_t1 = t + 1 < t_end;
-    // the next tile continues this strip (a strip change always restarts at row 0)
-    const bool next_cont = has_t1 && r + 1u < R;
     wait_slot(s_cur);
     if (!cont && prev_b) {  // strip changed: flush the previous row without its D.y
       write_row(b_cur ^ 1, prev_strip, prev_row, false);
@@ -333,21 +317,10 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
     prev_strip = strip;
     prev_row = r;
     b_cur ^= 1;
-    // ring rotation: this row becomes the row above when the next tile
-    // continues the strip; the freed slot takes the row kLbpAhead + 1 tiles ahead
-    if (has_t1) {
-      const int new_up = next_cont ? s_cur : -1;
-      s_cur = q[0];
-      for (int k = 0; k + 1 < kLbpAhead; ++k) q[k] = q[k + 1];
-      q[kLbpAhead - 1] = -1;
-      if (t + 1 + kLbpAhead < t_end) {
-        uint32_t st = strip, rr = r;
-        for (int k = 0; k <= kLbpAhead; ++k) step(st, rr);
-        const int f = free_slot(new_up, s_cur);
-        q[kLbpAhead - 1] = f;
-        if (leader) issue_row(f, st, rr);
-      }
-      s_up = new_up;
+    // the row above's slot is free now: it takes the row kLbpAhead + 1 tiles ahead
+    if (leader && t + 1 + kLbpAhead < t_end) {
+      issue_row((s_cur + kRing - 1) & (kRing - 1), st_i, r_i);
+      step(st_i, r_i);
     }
     step(strip, r);
   }
