@@ -28,8 +28,8 @@ constexpr int kLbpAhead = 2;
 constexpr int kRing = 2 + kLbpAhead;
 
 struct LbpSmem {
-  float2 A[kRing][kSEdges + 2];  // ring: message pairs (+ alignment slack)
-  float E[kRing][kSEdges + 8];   // ring: couplings
+  float2 A[kRing][kSEdges + 6];  // ring: message pairs (+ left neighbour pair + alignment slack)
+  float E[kRing][kSEdges + 12];  // ring: couplings (+ left neighbour + alignment slack)
   float U[kRing][kSW + 8];       // ring: unaries
   float2 B[2][kSEdges + 2];  // new message pairs being assembled (row above / tile row)
   unsigned long long bar[kRing];  // mbarriers of the ring slots
@@ -102,7 +102,9 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
   const uint64_t ntiles = static_cast<uint64_t>(R) * nstrip;
   const uint64_t t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
   if (t_begin >= t_end) return;
-  const bool leader = threadIdx.x == 0;
+  // the bulk-copy issuer sits in the last warp: warp 0 already carries the
+  // strip's first column (general path), so the two costs land on different warps
+  const bool leader = threadIdx.x == kBlock - 32;
   if (leader) {
     for (int k = 0; k < kRing; ++k) mbar_init(&S.bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -115,8 +117,11 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
     const uint32_t c0 = strip * kSW, w = min(kSW, C - c0);
     const bool lastrow = r + 1u == R;
     const uint32_t e0 = strip_e0(r, c0, C, lastrow), ne = strip_ne(c0, w, C, lastrow);
-    const uint32_t a0 = e0 & ~1u, a1 = (e0 + ne + 1u) & ~1u;      // pairs, 16-byte granules
-    const uint32_t f0 = e0 & ~3u, f1 = (e0 + ne + 3u) & ~3u;      // floats
+    // one more edge on the left: the strip-boundary left edge of column c0
+    // (it belongs to the previous strip), so column 0 reads it from SMEM too
+    const uint32_t ext = c0 > 0u ? (lastrow ? 1u : 2u) : 0u;
+    const uint32_t a0 = (e0 - ext) & ~1u, a1 = (e0 + ne + 1u) & ~1u;  // pairs, 16-byte granules
+    const uint32_t f0 = (e0 - ext) & ~3u, f1 = (e0 + ne + 3u) & ~3u;  // floats
     const uint32_t v0 = r * C + c0, u0 = v0 & ~3u, u1 = (v0 + w + 3u) & ~3u;
     S.aoff[s] = e0 - a0;
     S.eoff[s] = e0 - f0;
@@ -275,8 +280,8 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
           pL = Ac[ko_r(j - 1u, lastrow)];
           aL = Ec[ko_r(j - 1u, lastrow)];
         } else {  // strip boundary: the left edge belongs to the previous strip
-          pL = __ldg(&A2[e0 - (lastrow ? 1u : 2u)]);
-          aL = __ldg(&ea[e0 - (lastrow ? 1u : 2u)]);
+          pL = Ac[-static_cast<int>(lastrow ? 1u : 2u)];  // staged with the row
+          aL = Ec[-static_cast<int>(lastrow ? 1u : 2u)];
         }
       }
       const float T = Uc[j] + pU.x + pL.x + pR.y + pD.y;
