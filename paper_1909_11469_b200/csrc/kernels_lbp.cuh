@@ -243,9 +243,12 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
       const uint32_t j = threadIdx.x + q * kBlock;
       if (j >= w) continue;
       const uint32_t c = c0 + j;
-      if (fast_tile && j > 0u && c + 1u < C) {
-        const float2 pR = Ac[2u * j], pD = Ac[2u * j + 1u], pL = Ac[2u * j - 2u], pU = Au[2u * j + 1u];
-        const float aR = Ec[2u * j], aD = Ec[2u * j + 1u], aL = Ec[2u * j - 2u], aU = Eu[2u * j + 1u];
+      // (column 0 of a strip takes this path too: its left pair is staged with
+      // the row; only its left message goes to the previous strip's pair in HBM)
+      if (fast_tile && c > 0u && c + 1u < C) {
+        const int jl = 2 * static_cast<int>(j) - 2;  // left pair: index -2 (staged) for column 0
+        const float2 pR = Ac[2u * j], pD = Ac[2u * j + 1u], pL = Ac[jl], pU = Au[2u * j + 1u];
+        const float aR = Ec[2u * j], aD = Ec[2u * j + 1u], aL = Ec[jl], aU = Eu[2u * j + 1u];
         const float T = Uc[j] + pU.x + pL.x + pR.y + pD.y;
         float lu, ll, lr, ld;
         const float ru = ising_update(T - pU.x, aU, pU.y, lu);
@@ -254,7 +257,10 @@ static __global__ void __launch_bounds__(kBlock) k_lbp_lattice(DevGraph g, const
         const float rd = ising_update(T - pD.y, aD, pD.x, ld);
         Bc[2u * j].x = lr;
         Bc[2u * j + 1u].x = ld;
-        Bc[2u * j - 2u].y = ll;
+        if (j > 0u)
+          Bc[2u * j - 2u].y = ll;
+        else
+          B[2u * (e0 - 2u) + 1u] = ll;
         Bu[2u * j + 1u].y = lu;
         bad |= !(fabsf(lu + ll + lr + ld) < INFINITY);
         if (owned) {
