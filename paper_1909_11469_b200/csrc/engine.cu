@@ -5,10 +5,46 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 
 #include "engine.hpp"
 
 namespace bpb {
+
+namespace {
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* p = new PinnedPool;  // process lifetime
+  return *p;
+}
+}  // namespace
+
+void* pinned_acquire(size_t bytes) {
+  {
+    PinnedPool& pp = pinned_pool();
+    std::lock_guard<std::mutex> lk(pp.mu);
+    auto it = pp.free.find(bytes);
+    if (it != pp.free.end()) {
+      void* p = it->second;
+      pp.free.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cuda_check(cudaMallocHost(&p, bytes), "cudaMallocHost");
+  return p;
+}
+
+void pinned_release(void* p, size_t bytes) {
+  PinnedPool& pp = pinned_pool();
+  std::lock_guard<std::mutex> lk(pp.mu);
+  pp.free.emplace(bytes, p);
+}
+
 
 void validate_config(const bp_sched_config& c) {  // schedulers.cpp:78-90
   if (!(c.epsilon > 0.0) || !std::isfinite(c.epsilon)) throw_invalid("epsilon must be positive");

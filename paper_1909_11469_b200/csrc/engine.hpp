@@ -9,6 +9,11 @@
 
 namespace bpb {
 
+// Process-wide pool of pinned host blocks (one size class per size):
+// cudaMallocHost / cudaFreeHost cost milliseconds to hundreds of ms per call.
+void* pinned_acquire(size_t bytes);
+void pinned_release(void* p, size_t bytes);
+
 class EngineBase {
  public:
   virtual ~EngineBase() = default;

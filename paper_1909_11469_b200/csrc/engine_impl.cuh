@@ -72,7 +72,7 @@ class EngineT final : public EngineBase {
     }
     vlist_.alloc(static_cast<size_t>(g.V) * 4);
     ctl_.alloc(sizeof(Ctl));
-    cuda_check(cudaMallocHost(&hctl_, sizeof(Ctl)), "cudaMallocHost");
+    hctl_ = static_cast<Ctl*>(pinned_acquire(sizeof(Ctl)));
     std::memset(hctl_, 0, sizeof(Ctl));
     if (cfg.kind == BP_RBP) {
       hist_.alloc(kRadixBins * 4);
@@ -96,7 +96,10 @@ class EngineT final : public EngineBase {
     if (gexec_) cudaGraphExecDestroy(gexec_);
     if (graph_) cudaGraphDestroy(graph_);
     for (auto& ev : evs_) cudaEventDestroy(ev);
-    if (hctl_) cudaFreeHost(hctl_);
+    // back to the process-wide pool: cudaFreeHost was measured at 75-750 ms
+    // on some calls (page unpinning), on the end-to-end path of every run
+    if (s_) cudaStreamSynchronize(s_);  // no copy into / out of the mirror may be in flight
+    if (hctl_) pinned_release(hctl_, sizeof(Ctl));
     if (s_) cudaStreamDestroy(s_);
   }
 
