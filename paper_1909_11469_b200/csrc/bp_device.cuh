@@ -203,11 +203,10 @@ struct Ctl {
   unsigned int persist_ok;    // RnBP: hand list mode over to the persistent kernel (graph loop exits)
   unsigned int pad3_;
   // persistent kernel: per-iteration sums (delta, count, frontier, survivors,
-  // evals, visits), triple-buffered by iteration; touched-list counters,
-  // double-buffered; the time-limit verdict of CTA 0
+  // evals, visits), triple-buffered by iteration; the time-limit verdict of
+  // the bookkeeping thread
   unsigned long long pacc3[3][6];
   unsigned long long handover_it;  // iteration at which the graph loop handed over to the persistent kernel
-  unsigned int nfl2[2];
   unsigned int time_stop;
   unsigned int pad4_;
   unsigned long long persist_bytes;  // algorithmic bytes moved by the persistent kernel

@@ -1,17 +1,23 @@
-// Persistent RnBP tail (sm_100a, cooperative launch).
+// Persistent RnBP tail (sm_100a; cooperative grid of one CTA per SM, or one
+// 16-CTA thread-block cluster for short lists).
 //
 // Once the RnBP run walks its candidate list (cl_state 2: fewer than 1/16 of
 // the directed edges unconverged) an iteration is a few thousand message
 // updates, and four kernel launches per iteration would cost more than the
 // work.  k_rnbp_persist runs the iterations of run() (schedulers.cpp:301-347)
-// back to back inside one launch, with grid-wide barriers between the phases
-// of an iteration:
+// back to back inside one launch, with two grid-wide barriers per iteration:
 //
 //   select   rnbp_frontier attempt 0 over the candidate list + the Jacobi
-//            commit of apply_frontier (schedulers.cpp:194-216, 231-241)
-//   retry    block 0: attempt 1 + single-survivor fallback (:204-214)
+//            commit of apply_frontier (schedulers.cpp:194-216, 231-241), in
+//            slot form (outcomes stay at the entry's index)
+//   --- barrier
+//   retry    CTA 0, when nothing was drawn: attempt 1 + single-survivor
+//            fallback (:204-214)
 //   refresh  refresh_residuals over the touched vertices (residuals.cpp:26-59)
-//   finalize block 0 / thread 0: the loop control of run() (fin_iter)
+//            + compaction of the next candidate list
+//   --- barrier
+//   finalize replicated in every CTA: the loop control of run() (fin_iter);
+//            the bookkeeping thread writes the trace record
 //
 // It stops when the run is done (converged / max_iterations / time limit /
 // the host's trace-ring budget).  All data written inside the launch is read
@@ -27,7 +33,7 @@ namespace bpb {
 namespace cgp = cooperative_groups;
 
 constexpr int kPersistBlock = 512;
-// candidate-list length below which the tail runs on one 16-CTA cluster
+// candidate-list length below which the tail runs on one 16-CTA cluster (above it: a grid of one CTA per SM)
 // (cluster barrier ~0.35 us vs grid barrier ~1.3 us, but 16 SMs instead of
 // 148 share the list: measured at 115 entries cluster 8.9 vs grid 11.5
 // us/iteration, at 6443 entries 12.0 vs 10.8)
@@ -74,7 +80,7 @@ __device__ __forceinline__ void pacc_push(unsigned* s_pacc, unsigned long long* 
 // barrier each CTA applies the finalize step itself from the reduced sums,
 // so an iteration needs two barriers and no global read-modify-write of the
 // control block.  Reductions and list counters are multi-buffered by
-// iteration so no CTA resets a value another CTA may still read.  CTA 0 / thread 0
+// iteration so no CTA resets a value another CTA may still read.  The bookkeeping thread (last CTA)
 // mirrors the state into Ctl and writes the trace record for the host.
 template <int QS, bool CLUSTER>
 __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, float* live, float* cand, float* res,
