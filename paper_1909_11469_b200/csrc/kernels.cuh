@@ -644,18 +644,24 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
 #pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
     const float inv = frcp(s);
-    float* dst = B + static_cast<size_t>(out) * QS;
     float r = 0.f;
     // the residual compares 2^(stored log) on both sides, so a bitwise fixed
-    // point reports exactly 0 (as for the binary layout)
+    // point reports exactly 0 (as for the binary layout); states >= cj keep
+    // their stored value, so the q-vector leaves with 16-byte stores
 #pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) {
       if (xt < static_cast<int>(cj)) {
         const float ln = flg2(o[xt] * inv);
         r = fmaxf(r, fabsf(fex2(ln) - fex2(mo[xt])));
-        dst[xt] = ln;
+        o[xt] = ln;
+      } else {
+        o[xt] = mo[xt];
       }
     }
+    float4* dst4 = reinterpret_cast<float4*>(B + static_cast<size_t>(out) * QS);
+#pragma unroll (QS <= 8 ? QS / 4 : 1)
+    for (int x4 = 0; x4 < QS / 4; ++x4)
+      dst4[x4] = make_float4(o[4 * x4], o[4 * x4 + 1], o[4 * x4 + 2], o[4 * x4 + 3]);
     if (!(s > 0.f) || !(s < INFINITY)) *numeric_flag = 1u;
     const int now = r >= eps;
     if (MODE == kModeDelta) {
