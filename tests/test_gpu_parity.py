@@ -283,3 +283,16 @@ def test_rnbp_persistent_tail_generic_graphs(bp, name):
     assert a.trace_signature() == b.trace_signature()
     assert np.max(np.abs(a.beliefs.values - b.beliefs.values)) == 0.0
     assert a.gpu_launches < b.gpu_launches  # the persistent kernel took over
+
+
+@pytest.mark.timeout(300)
+def test_rnbp_persistent_tail_potts_multipass(bp):
+    """Potts 1024^2, q = 8: the candidate list at the handover (~10^5 entries)
+    takes several passes of the persistent grid per phase; the run must match
+    the graph loop iteration for iteration."""
+    g = bp.generate_potts(1024, 8, 2.5, 0)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=200, seed=1)
+    a = bp.run(g, cfg)
+    b = bp.run_ex(g, cfg, flags=bp.RUN_NO_PERSIST)
+    assert a.trace_signature() == b.trace_signature()
+    assert np.max(np.abs(a.beliefs.values - b.beliefs.values)) == 0.0
