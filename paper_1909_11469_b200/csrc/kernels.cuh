@@ -688,7 +688,7 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
 // down pair (L1 / L2 hits), the four a = e^J and its unary: all kLatVPT x 9
 // loads are issued before any arithmetic.  check_flag: dense touched-set
 // refresh (only vertices with vflag == stamp).
-constexpr int kLatVPT = 4;
+constexpr int kLatVPT = 1;  // measured at 1000^2: 4 -> 2 -> 1 vertices per thread, 23.0 -> 22.5 -> 22.4 us per LBP iteration
 constexpr uint32_t kLatTile = kBlock * kLatVPT;
 
 template <int MODE, bool CL, int VPT = kLatVPT>
@@ -885,9 +885,9 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
   const bool cl_on = CL && ctl->cl_state >= 1u;
   const bool lattice = QS == 1 && g.lat_cols != 0u && g.par_mode != 0u && dense;
   if (lattice)
-    // the refresh keeps more state per vertex (old-residual / in-list bits):
-    // one vertex per thread: more warps in flight (measured 2 -> 1: 63 -> 56 us per early RnBP iteration)
-    lattice_binary_tiles<MODE, CL, MODE == kModeDelta ? 1 : kLatVPT>(g, A, B, res, vflag, stamp, LIST, eps, &ctl->numeric_error, cnt, evals, visits,
+    // one vertex per thread: more warps in flight (the delta-mode refresh
+    // measured 63 -> 56 us per early RnBP iteration going from 2 to 1)
+    lattice_binary_tiles<MODE, CL, kLatVPT>(g, A, B, res, vflag, stamp, LIST, eps, &ctl->numeric_error, cnt, evals, visits,
                                    cand_list.inlist, &cl, cl_on);
   for (uint32_t base = lattice ? n : blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint32_t i = base + threadIdx.x;
