@@ -90,6 +90,9 @@ class EngineT final : public EngineBase {
     prm_.fixed_p = -1.0;
     prm_.commit = 1;
     prm_.attempt = 0;
+    // the set-up memsets above ran on the legacy stream, which the engine's
+    // non-blocking stream does not wait for
+    cuda_check(cudaDeviceSynchronize(), "engine set-up");
   }
 
   ~EngineT() override {
@@ -322,6 +325,7 @@ class EngineT final : public EngineBase {
     if (!rs_written_.p) {
       rs_written_.alloc(static_cast<size_t>(g_.D) * 4);
       cuda_check(cudaMemset(rs_written_.p, 0, rs_written_.bytes), "memset");
+      cuda_check(cudaDeviceSynchronize(), "memset");  // legacy stream: not ordered before s_
     }
     std::vector<unsigned long long> off(ns + 1);
     for (uint64_t i = 0; i <= ns; ++i) off[i] = eoff[i] - eoff[0];
@@ -724,6 +728,7 @@ class EngineT final : public EngineBase {
     if (!hist_.p) {
       hist_.alloc(kRadixBins * 4);
       cuda_check(cudaMemset(hist_.p, 0, kRadixBins * 4), "memset");
+      cuda_check(cudaDeviceSynchronize(), "memset");  // legacy stream: not ordered before s_
     }
     if (!chunk_.p) {
       nchunks_ = std::max<uint32_t>(1, (g_.D + kTieChunk - 1) / kTieChunk);
@@ -1010,6 +1015,7 @@ class EngineT final : public EngineBase {
     rs_blk_.alloc(static_cast<size_t>(rs_grid_) * 4);
     rs_ctl_.alloc(sizeof(RsCtl));
     cuda_check(cudaMemset(rs_ctl_.p, 0, sizeof(RsCtl)), "memset");
+      cuda_check(cudaDeviceSynchronize(), "memset");  // legacy stream: not ordered before s_
     rs_shadow_.alloc(std::max<size_t>(static_cast<size_t>(g_.D) * QS * 4, 16));
   }
   RsBufs rs_bufs() {

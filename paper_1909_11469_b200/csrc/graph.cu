@@ -91,8 +91,11 @@ void DevBuf::alloc(size_t n) {
       c.free.erase(it);
       lk.unlock();
       bytes = n;
-      // zero-filled like a fresh allocation in practice is
+      // zero-filled like a fresh allocation in practice is; completed before
+      // returning (the engines' streams are non-blocking: a legacy-stream
+      // memset is not ordered before their kernels)
       cuda_check(cudaMemset(p, 0, cap), "memset (cached block)");
+      cuda_check(cudaDeviceSynchronize(), "memset (cached block)");
       return;
     }
   }
@@ -103,6 +106,11 @@ void DevBuf::alloc(size_t n) {
     e = cudaMalloc(&p, want);
   }
   cuda_check(e, "cudaMalloc");
+  // zero-filled like the recycled blocks (memory freed earlier in this
+  // process comes back from cudaMalloc with its old contents), completed
+  // before returning
+  cuda_check(cudaMemset(p, 0, want), "memset (new block)");
+  cuda_check(cudaDeviceSynchronize(), "memset (new block)");
   bytes = n;
   cap = want;
 }

@@ -296,3 +296,16 @@ def test_rnbp_persistent_tail_potts_multipass(bp):
     b = bp.run_ex(g, cfg, flags=bp.RUN_NO_PERSIST)
     assert a.trace_signature() == b.trace_signature()
     assert np.max(np.abs(a.beliefs.values - b.beliefs.values)) == 0.0
+
+
+@pytest.mark.timeout(180)
+def test_rnbp_persistent_tail_potts_4096(bp):
+    """Potts 4096^2, q = 8, first 20 RnBP iterations (the persistent grid on a
+    list of ~10^6 entries): identical to the graph loop.  Guards the set-up
+    race fixed this round (legacy-stream memsets of recycled device blocks were
+    not ordered before the engine's non-blocking stream)."""
+    g = bp.generate_potts(4096, 8, 2.5, 0)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=20, time_limit=60)
+    a = bp.run_ex(g, cfg, beliefs=False)
+    b = bp.run_ex(g, cfg, beliefs=False, flags=bp.RUN_NO_PERSIST)
+    assert a.trace_signature() == b.trace_signature()
