@@ -595,40 +595,23 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
   float T[QS];
 #pragma unroll (QS <= 8 ? QS : 2)
   for (int x = 0; x < QS; ++x) T[x] = g.unary_log[static_cast<size_t>(v) * QS + x];
-  uint32_t deg = 0;
-  for_each_in(g, v, [&](uint32_t in) {
-    const float4* m4 = reinterpret_cast<const float4*>(A + static_cast<size_t>(in) * QS);  // QS % 4 == 0
+  auto load_q = [&](uint32_t d, float* m) {  // a q-vector with 16-byte loads (QS % 4 == 0)
+    const float4* m4 = reinterpret_cast<const float4*>(A + static_cast<size_t>(d) * QS);
 #pragma unroll (QS <= 8 ? QS / 4 : 1)
     for (int x4 = 0; x4 < QS / 4; ++x4) {
       const float4 q4 = ldm<NC>(&m4[x4]);
-      T[4 * x4] += q4.x;
-      T[4 * x4 + 1] += q4.y;
-      T[4 * x4 + 2] += q4.z;
-      T[4 * x4 + 3] += q4.w;
+      m[4 * x4] = q4.x;
+      m[4 * x4 + 1] = q4.y;
+      m[4 * x4 + 2] = q4.z;
+      m[4 * x4 + 3] = q4.w;
     }
-    ++deg;
-  });
+  };
   int cnt = 0;
-  for_each_in(g, v, [&](uint32_t in) {
+  // one outgoing message from the incoming q-vector mi (same edge pair) and
+  // the old outgoing one mo
+  auto emit = [&](uint32_t in, const float* mi, const float* mo, float r_was) {
     const uint32_t out = in ^ 1u;
     const uint32_t cj = g.uniform_q ? g.uniform_q : g.card[g.ep[in]];  // target of `out` = source of `in`
-    const float4* mi4 = reinterpret_cast<const float4*>(A + static_cast<size_t>(in) * QS);
-    const float4* mo4 = reinterpret_cast<const float4*>(A + static_cast<size_t>(out) * QS);
-    const float r_was = MODE == kModeDelta ? res[out] : 0.f;
-    // the edge pair (incoming and old outgoing q-vectors) with 16-byte loads
-    float mi[QS], mo[QS];
-#pragma unroll (QS <= 8 ? QS / 4 : 1)
-    for (int x4 = 0; x4 < QS / 4; ++x4) {
-      const float4 a4 = ldm<NC>(&mi4[x4]), b4 = ldm<NC>(&mo4[x4]);
-      mi[4 * x4] = a4.x;
-      mi[4 * x4 + 1] = a4.y;
-      mi[4 * x4 + 2] = a4.z;
-      mi[4 * x4 + 3] = a4.w;
-      mo[4 * x4] = b4.x;
-      mo[4 * x4 + 1] = b4.y;
-      mo[4 * x4 + 2] = b4.z;
-      mo[4 * x4 + 3] = b4.w;
-    }
     float p[QS];
     float M = -INFINITY;
 #pragma unroll (QS <= 8 ? QS : 2)
@@ -675,7 +658,54 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
       inlist[out] = 1;
       cl->push(out);
     }
-  });
+  };
+  uint32_t deg = 0;
+  if (MODE == kModeCount && QS <= 8 && g.lat_cols) {
+    // LBP sweep on a lattice, q <= 8: the (at most 4) incoming and old outgoing
+    // q-vectors are loaded at once and kept in registers for both passes
+    const uint32_t C = g.lat_cols, R = g.lat_rows;
+    const uint32_t r = v / C, c = v - r * C;
+    const uint32_t row = r * (2u * C - 1u);
+    const bool last = r + 1u == R;
+    const bool has[4] = {r > 0u, c > 0u, c + 1u < C, !last};
+    const uint32_t ins[4] = {
+        has[0] ? 2u * ((r - 1u) * (2u * C - 1u) + 2u * c + (c + 1u < C ? 1u : 0u)) : 0u,
+        has[1] ? 2u * (last ? row + c - 1u : row + 2u * (c - 1u)) : 0u,
+        has[2] ? 2u * (last ? row + c : row + 2u * c) + 1u : 0u,
+        has[3] ? 2u * (row + 2u * c + (c + 1u < C ? 1u : 0u)) + 1u : 0u};
+    float mi[4][QS], mo[4][QS];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (has[k]) {
+        load_q(ins[k], mi[k]);
+        load_q(ins[k] ^ 1u, mo[k]);
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (has[k]) {
+#pragma unroll
+        for (int x = 0; x < QS; ++x) T[x] += mi[k][x];
+        ++deg;
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (has[k]) emit(ins[k], mi[k], mo[k], 0.f);
+  } else {
+    for_each_in(g, v, [&](uint32_t in) {
+      float mi[QS];
+      load_q(in, mi);
+#pragma unroll (QS <= 8 ? QS : 2)
+      for (int x = 0; x < QS; ++x) T[x] += mi[x];
+      ++deg;
+    });
+    for_each_in(g, v, [&](uint32_t in) {
+      const float r_was = MODE == kModeDelta ? res[in ^ 1u] : 0.f;
+      float mi[QS], mo[QS];
+      load_q(in, mi);
+      load_q(in ^ 1u, mo);
+      emit(in, mi, mo, r_was);
+    });
+  }
   evals += deg;
   return cnt;
 }
