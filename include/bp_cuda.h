@@ -139,6 +139,13 @@ typedef struct {
 #define BP_RUN_NO_GRAPHS 2u     /* launch kernels directly instead of CUDA-graph batches */
 #define BP_RUN_NO_BELIEFS 4u    /* skip beliefs */
 #define BP_RUN_NO_PERSIST 8u    /* RnBP: keep the per-kernel graph loop in candidate-list mode */
+#define BP_RUN_LBP_TMA 16u      /* LBP: force the TMA-staged lattice sweep (binary Ising lattices, >= 2 rows) */
+#define BP_RUN_LBP_TILES 32u    /* LBP: force the register-tiled lattice sweep (default below 2^21 vertices) */
+
+/* LBP sweep kernels (bp_engine_lbp_sweep's *kernel_out) */
+#define BP_LBP_KERNEL_VERTEX 0u /* k_vertex_update: vertex-centric (CSR / generic q-state / Potts lattice) */
+#define BP_LBP_KERNEL_TILES 1u  /* k_vertex_update lattice tiles (binary Ising lattice) */
+#define BP_LBP_KERNEL_TMA 2u    /* k_lbp_lattice: TMA-staged rows (binary Ising lattice) */
 
 BP_API const char* bp_last_error(void);
 BP_API int bp_abi_version(void);
@@ -210,6 +217,15 @@ BP_API int bp_engine_rs_frontier(struct bp_engine* e, double p, uint32_t h, uint
 /* One full iteration of the configured scheduler (frontier + apply), exactly
  * as one pass of the run loop; *frontier_size receives |F|. */
 BP_API int bp_engine_step(struct bp_engine* e, uint64_t* frontier_size);
+/* One fused LBP sweep, the kernel bp_run executes per LBP iteration (flags:
+ * BP_RUN_LBP_TMA / BP_RUN_LBP_TILES force a lattice kernel).  Sweep t reads
+ * m_t and writes m_{t+1} = f(m_t); afterwards bp_engine_messages = m_t,
+ * bp_engine_candidates = m_{t+1}, bp_engine_unconverged = #{r(m_t) >= eps},
+ * bp_engine_iteration = t: the reference's EngineState after t
+ * apply_frontier(frontier_lbp()) calls (schedulers.cpp:99-103, 226-251).
+ * The first call re-initialises the messages (init_messages, messages.cpp:23-39).
+ * kernel_out (optional): BP_LBP_KERNEL_* that ran.  Residuals are not stored. */
+BP_API int bp_engine_lbp_sweep(struct bp_engine* e, uint32_t flags, uint32_t* kernel_out);
 BP_API int bp_engine_iteration(const struct bp_engine* e, uint64_t* out);
 
 /* ---- Row-band partition of a lattice across GPUs ----------
@@ -285,6 +301,17 @@ BP_API int bp_band_rnbp_finish(struct bp_engine* e);
 BP_API int bp_band_survivors(struct bp_engine* e, uint64_t* global_ids, uint64_t cap, uint64_t* n);
 BP_API int bp_band_rnbp_fallback(struct bp_engine* e, uint64_t global_d);
 BP_API uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t d);
+
+/* ---- Diagnostics: the DEVICE random stream, for known-answer tests ---------
+ * bp_philox4x32_10_device: the device's Philox4x32-10 (Salmon et al., SC'11;
+ * Random123 philox4x32_R with R = 10) on n (counter[4], key[2]) pairs.
+ * bp_philox_u53_device: the 53-bit RnBP draw of directed edge d[i] in
+ * (seed, iteration, attempt), as k_rnbp_select draws it (u = value * 2^-53,
+ * the device analogue of uniform_unit, rng.hpp:11-13).  device: -1 = current. */
+BP_API int bp_philox4x32_10_device(int32_t device, uint64_t n, const uint32_t* ctr, const uint32_t* key,
+                                   uint32_t* out);
+BP_API int bp_philox_u53_device(int32_t device, uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t n,
+                                const uint64_t* d, uint64_t* out);
 
 #ifdef __cplusplus
 }

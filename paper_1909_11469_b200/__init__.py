@@ -123,6 +123,9 @@ RUN_KERNEL_TIMING = 1
 RUN_NO_GRAPHS = 2
 RUN_NO_BELIEFS = 4
 RUN_NO_PERSIST = 8
+RUN_LBP_TMA = 16
+RUN_LBP_TILES = 32
+LBP_KERNELS = {0: "vertex", 1: "tiles", 2: "tma"}  # BP_LBP_KERNEL_*
 GRAPH_TRUSTED = 1
 
 
@@ -163,6 +166,7 @@ def _load():
         "bp_engine_rbp_frontier": (C.c_int, [P, C.c_double, P, C.POINTER(C.c_uint64)]),
         "bp_engine_rs_frontier": (C.c_int, [P, C.c_double, C.c_uint32, P, P, P, C.POINTER(C.c_uint64)]),
         "bp_engine_step": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+        "bp_engine_lbp_sweep": (C.c_int, [P, C.c_uint32, C.POINTER(C.c_uint32)]),
         "bp_graph_generate_ising_band": (C.c_int, [C.c_uint32, C.c_double, C.c_uint64, C.c_uint32, C.c_uint32,
                                                    C.POINTER(_DevOpts), C.POINTER(P), C.c_void_p]),
         "bp_band_engine_create": (C.c_int, [P, C.POINTER(_Config), C.c_void_p, C.c_void_p, C.POINTER(P)]),
@@ -180,6 +184,8 @@ def _load():
         "bp_band_survivors": (C.c_int, [P, P, C.c_uint64, C.POINTER(C.c_uint64)]),
         "bp_band_rnbp_fallback": (C.c_int, [P, C.c_uint64]),
         "bp_philox_u53": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64]),
+        "bp_philox4x32_10_device": (C.c_int, [C.c_int32, C.c_uint64, P, P, P]),
+        "bp_philox_u53_device": (C.c_int, [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -523,6 +529,30 @@ def run(graph: PairwiseMRF, config: SchedulerConfig) -> RunResult:
 
 
 # --------------------------------------------------------------------------
+# the device random stream (diagnostics for known-answer tests)
+
+def philox4x32_10_device(ctr, key, device: int = -1) -> np.ndarray:
+    """The device's Philox4x32-10 on counters (n, 4) / keys (n, 2) -> (n, 4) uint32."""
+    ctr = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
+    key = np.ascontiguousarray(key, np.uint32).reshape(-1, 2)
+    out = np.zeros_like(ctr)
+    _check(_lib.bp_philox4x32_10_device(device, ctr.shape[0], _ptr(ctr), _ptr(key), _ptr(out)))
+    return out
+
+
+def philox_u53_device(seed: int, iteration: int, attempt: int, d, device: int = -1) -> np.ndarray:
+    """53-bit RnBP draws of directed edges d in (seed, iteration, attempt), on the device."""
+    d = np.ascontiguousarray(d, np.uint64)
+    out = np.zeros_like(d)
+    _check(_lib.bp_philox_u53_device(device, seed, iteration, attempt, d.size, _ptr(d), _ptr(out)))
+    return out
+
+
+def philox_u53(seed: int, iteration: int, attempt: int, d: int) -> int:
+    """Host restatement of the same draw (bp_philox_u53; the band fallback)."""
+    return int(_lib.bp_philox_u53(seed, iteration, attempt, d))
+
+
 # EngineState + per-phase API (schedulers.hpp:61-151), for lockstep parity
 
 class EngineState:
@@ -626,3 +656,13 @@ class EngineState:
         n = C.c_uint64()
         _check(_lib.bp_engine_step(self._h, C.byref(n)))
         return int(n.value)
+
+    def lbp_sweep(self, kernel: str = "auto") -> str:
+        """One fused LBP sweep with the production kernel (bp_engine_lbp_sweep):
+        afterwards messages() = m_t, candidates() = f(m_t), unconverged_count()
+        = #{r(m_t) >= eps}.  kernel: "auto" | "tma" | "tiles"; returns the
+        kernel that ran ("vertex", "tiles" or "tma")."""
+        flags = {"auto": 0, "tma": RUN_LBP_TMA, "tiles": RUN_LBP_TILES}[kernel]
+        k = C.c_uint32()
+        _check(_lib.bp_engine_lbp_sweep(self._h, flags, C.byref(k)))
+        return LBP_KERNELS[int(k.value)]

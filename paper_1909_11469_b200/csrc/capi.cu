@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include "bp_device.cuh"
 #include "engine.hpp"
 #include "graph.hpp"
 
@@ -38,6 +39,23 @@ int guarded(F&& f) {
     g_last_error = e.what();
     return BP_ERR_INVALID_ARGUMENT;
   }
+}
+
+// the device's Philox4x32-10 (bp_device.cuh), evaluated for known-answer tests
+__global__ void k_philox_kat(uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint4 r = bpb::philox4x32_10(make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]),
+                                     make_uint2(key[2 * i], key[2 * i + 1]));
+  out[4 * i] = r.x;
+  out[4 * i + 1] = r.y;
+  out[4 * i + 2] = r.z;
+  out[4 * i + 3] = r.w;
+}
+__global__ void k_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t n, const uint64_t* d,
+                             uint64_t* out) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = bpb::philox_u53(seed, iteration, attempt, d[i]);
 }
 
 int wrap_graph(std::unique_ptr<bpb::GraphImpl> g, bp_graph** out) {
@@ -357,6 +375,46 @@ uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint
   }
   const uint64_t hi = (d & 1ull) ? c2 : c0, lo = (d & 1ull) ? c3 : c1;
   return ((hi << 32) | lo) >> 11;
+}
+
+int bp_philox4x32_10_device(int32_t device, uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  if (n && (!ctr || !key || !out)) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (device >= 0) bpb::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (!n) return;
+    bpb::DevBuf dc, dk, dout;
+    dc.upload(ctr, n * 16);
+    dk.upload(key, n * 8);
+    dout.alloc(n * 16);
+    k_philox_kat<<<static_cast<unsigned>((n + 127) / 128), 128>>>(n, dc.as<uint32_t>(), dk.as<uint32_t>(),
+                                                                  dout.as<uint32_t>());
+    bpb::cuda_check(cudaGetLastError(), "philox launch");
+    bpb::cuda_check(cudaMemcpy(out, dout.p, n * 16, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int bp_philox_u53_device(int32_t device, uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t n,
+                         const uint64_t* d, uint64_t* out) {
+  if (n && (!d || !out)) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (device >= 0) bpb::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (!n) return;
+    bpb::DevBuf dd, dout;
+    dd.upload(d, n * 8);
+    dout.alloc(n * 8);
+    k_philox_u53<<<static_cast<unsigned>((n + 127) / 128), 128>>>(seed, iteration, attempt, n, dd.as<uint64_t>(),
+                                                                  dout.as<uint64_t>());
+    bpb::cuda_check(cudaGetLastError(), "philox launch");
+    bpb::cuda_check(cudaMemcpy(out, dout.p, n * 8, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int bp_engine_lbp_sweep(bp_engine* e, uint32_t flags, uint32_t* kernel_out) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    const uint32_t k = e->e->lbp_sweep(flags);
+    if (kernel_out) *kernel_out = k;
+  });
 }
 
 int bp_engine_step(bp_engine* e, uint64_t* frontier_size) {

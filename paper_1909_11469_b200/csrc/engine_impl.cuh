@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 
 #include "engine.hpp"
 #include "kernels.cuh"
@@ -30,14 +31,18 @@ float eps_ceil(double eps) {
   return f;
 }
 
+// SM count of the current device (cached per ordinal)
 int sm_count() {
-  static int n = [] {
-    int dev = 0, c = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
-    return c > 0 ? c : 148;
-  }();
-  return n;
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int c = 148;
+  cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev] = c > 0 ? c : 148;
 }
 
 unsigned grid_cap(size_t n, int per_sm = 8) {
@@ -116,6 +121,14 @@ class EngineT final : public EngineBase {
     launches_ = 0;
     const bool use_graph = !(flags & BP_RUN_NO_GRAPHS) && !timing_;
     persist_ = cfg_.kind == BP_RNBP && !(flags & BP_RUN_NO_PERSIST);
+    lbp_force_ = flags & (BP_RUN_LBP_TMA | BP_RUN_LBP_TILES);
+    if (gexec_ && lbp_force_ != graph_force_) {  // the captured loop body embeds the sweep choice
+      cudaGraphExecDestroy(gexec_);
+      cudaGraphDestroy(graph_);
+      gexec_ = nullptr;
+      graph_ = nullptr;
+    }
+    graph_force_ = lbp_force_;
     const Clock::time_point t0 = Clock::now();  // schedulers.cpp:297
 
     cudaEvent_t e0, e1;
@@ -201,12 +214,13 @@ class EngineT final : public EngineBase {
     std::vector<float> raw(static_cast<size_t>(g_.D) * QS);
     // band engines ping-pong like run()'s LBP: m_t lives in buf[t & 1]
     bool flip = false;
-    if (band_started_ && cfg_.kind == BP_LBP) {
+    if (pingpong_ && cfg_.kind == BP_LBP) {
       fetch_ctl_header();
       flip = (hctl_->iteration & 1ull) != 0;
     }
     const DevBuf& src = (candidates != flip) ? bufB_ : bufA_;
-    if (!raw.empty()) cuda_check(cudaMemcpy(raw.data(), src.p, raw.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+    if (!raw.empty()) cuda_check(cudaMemcpyAsync(raw.data(), src.p, raw.size() * 4, cudaMemcpyDeviceToHost, s_), "d2h");
+    sync();
     const auto& ep = g_.host_ep();
     size_t o = 0;
     for (uint32_t d = 0; d < g_.D; ++d) {
@@ -222,13 +236,14 @@ class EngineT final : public EngineBase {
   }
   void residuals(double* out) override {
     std::vector<float> raw(g_.D);
-    if (g_.D) cuda_check(cudaMemcpy(raw.data(), res_.p, raw.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+    if (g_.D) cuda_check(cudaMemcpyAsync(raw.data(), res_.p, raw.size() * 4, cudaMemcpyDeviceToHost, s_), "d2h");
+    sync();
     for (uint32_t d = 0; d < g_.D; ++d) out[d] = raw[d];
   }
   void beliefs(double* out) override {
     const size_t nb = g_.unary_size();
     ensure_beliefs_buf(nb);
-    enqueue_beliefs(bel_.as<double>(), band_started_ && cfg_.kind == BP_LBP);
+    enqueue_beliefs(bel_.as<double>(), pingpong_ && cfg_.kind == BP_LBP);
     cuda_check(cudaMemcpyAsync(out, bel_.p, nb * 8, cudaMemcpyDeviceToHost, s_), "d2h");
     sync();
   }
@@ -347,6 +362,31 @@ class EngineT final : public EngineBase {
     fetch_ctl_header();
     if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
   }
+  // One fused LBP sweep exactly as run() executes it (the production kernel
+  // for this graph, or the one the flags force): sweep t reads m_t, writes
+  // m_{t+1} = f(m_t) and counts r(m_t) >= eps.  Afterwards messages() = m_t,
+  // candidates() = m_{t+1}, unconverged() = #{r(m_t) >= eps}, iteration() = t
+  // -- the reference's EngineState after t apply_frontier(frontier_lbp())
+  // calls (schedulers.cpp:99-103, 226-251).
+  uint32_t lbp_sweep(uint32_t flags) override {
+    if (cfg_.kind != BP_LBP) throw_invalid("lbp_sweep on a non-LBP engine");
+    if (band_owned_) throw_invalid("lbp_sweep on a band engine (use bp_band_lbp_sweep)");
+    lbp_force_ = flags & (BP_RUN_LBP_TMA | BP_RUN_LBP_TILES);
+    if (!pingpong_) {
+      reset_ctl(std::numeric_limits<uint64_t>::max(), 1e300);
+      const unsigned gi = grid_cap(static_cast<size_t>(g_.D) * QS);
+      k_init_messages<QS><<<gi, kBlock, 0, s_>>>(dg_, live(), ctl(), 1);
+      launch_check();
+      pingpong_ = true;
+    }
+    enqueue_lbp_sweep();
+    enqueue_finalize(kFinLbp);
+    sync();
+    fetch_ctl_header();
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
+    return lbp_kernel_;
+  }
+
   uint64_t step() override {
     force_not_done();
     fetch_ctl_header();
@@ -507,14 +547,17 @@ class EngineT final : public EngineBase {
   // lattices, the vertex-centric kernel otherwise
   unsigned lbp_grid_ = 0;
   static constexpr uint64_t kLbpTmaMinVertices = uint64_t{1} << 21;  // TMA = tiles at 1000^2, 7% faster at 2048^2, 22% at 8192^2
+  uint32_t lbp_force_ = 0;   // BP_RUN_LBP_TMA / BP_RUN_LBP_TILES of the current call
+  uint32_t lbp_kernel_ = 0;  // BP_LBP_KERNEL_* of the last sweep
   void enqueue_lbp_sweep() {
     // TMA-staged rows pay off once the grid is far beyond L2; below that the
-    // register-tiled lattice kernel (k_vertex_update) is faster.
-    // BPB_LBP_KERNEL=tma|tiles overrides (measurement).
-    static const char* lk = std::getenv("BPB_LBP_KERNEL");
+    // register-tiled lattice kernel (k_vertex_update) is faster.  The per-call
+    // flags BP_RUN_LBP_TMA / BP_RUN_LBP_TILES override the size rule.
+    const bool tma_ok = QS == 1 && g_.lat_cols && g_.par_mode == 1 && g_.lat_rows >= 2;
     const bool big = static_cast<uint64_t>(g_.V) >= kLbpTmaMinVertices;
-    const bool use_tma = lk ? std::strcmp(lk, "tma") == 0 : big;
-    if (QS == 1 && g_.lat_cols && g_.par_mode == 1 && g_.lat_rows >= 2 && use_tma) {
+    const bool use_tma = tma_ok && ((lbp_force_ & BP_RUN_LBP_TMA) || (!(lbp_force_ & BP_RUN_LBP_TILES) && big));
+    if (use_tma) {
+      lbp_kernel_ = BP_LBP_KERNEL_TMA;
       if (!lbp_grid_) {
         cuda_check(cudaFuncSetAttribute(k_lbp_lattice, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(LbpSmem))),
@@ -528,6 +571,7 @@ class EngineT final : public EngineBase {
         k_lbp_lattice<<<lbp_grid_, kBlock, sizeof(LbpSmem), s_>>>(dg_, live(), cand(), ctl(), eps_);
       });
     } else {
+      lbp_kernel_ = (QS == 1 && g_.lat_cols && g_.par_mode) ? BP_LBP_KERNEL_TILES : BP_LBP_KERNEL_VERTEX;
       timed(kKUpdate, [&] {
         k_vertex_update<QS, kModeCount, false, true, false>
             <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(
@@ -548,7 +592,7 @@ class EngineT final : public EngineBase {
   // collectives on stream()] -> unpack ghosts -> finalize with the global count
   PartHalo halo_{};
   uint64_t band_owned_ = 0;
-  bool band_started_ = false;
+  bool pingpong_ = false;
   cudaStream_t stream() const override { return s_; }
   void band_config(const PartHalo& h, uint64_t owned_directed) override {
     if (QS != 1 || !g_.lat_cols || g_.par_mode != 1)
@@ -558,13 +602,13 @@ class EngineT final : public EngineBase {
     halo_.ghost_up = g_.cnt_row0 > 0 ? 1u : 0u;
     halo_.ghost_down = g_.cnt_row1 < g_.lat_rows ? 1u : 0u;
     band_owned_ = owned_directed;
-    band_started_ = false;
+    pingpong_ = false;
   }
   void band_sweep() override {
     if (cfg_.kind != BP_LBP) throw_invalid("band_lbp_* on a non-LBP engine");
-    if (!band_started_) {
+    if (!pingpong_) {
       band_start_common();
-      band_started_ = true;
+      pingpong_ = true;
     }
     enqueue_lbp_sweep();
     const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
@@ -912,16 +956,21 @@ class EngineT final : public EngineBase {
     // once per process: one CTA per SM (the tail is latency-bound, a second
     // CTA per SM only adds barrier participants: 296 CTAs measured 3% slower
     // than 148)
-    static const unsigned grid = [] {
+    // function attributes are per device: set them once per device ordinal
+    static std::mutex mu;
+    static std::map<int, unsigned> grids;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = grids.find(g_.device);
+    if (it == grids.end()) {
       int per_sm = 0;
       cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rnbp_persist<QS, false>, kPersistBlock, 0),
                  "occupancy");
       if (per_sm < 1) throw Error(BP_ERR_CUDA, "persistent RnBP kernel does not fit on an SM");
       cuda_check(cudaFuncSetAttribute(k_rnbp_persist<QS, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                  "cluster attribute");
-      return static_cast<unsigned>(sm_count());
-    }();
-    persist_grid_ = grid;
+      it = grids.emplace(g_.device, static_cast<unsigned>(sm_count())).first;
+    }
+    persist_grid_ = it->second;
   }
 
   // one launch of the persistent tail: a 16-CTA cluster or a cooperative grid
@@ -1112,6 +1161,7 @@ class EngineT final : public EngineBase {
   uint64_t body_launches_ = 0;
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t gexec_ = nullptr;
+  uint32_t graph_force_ = 0;
   cudaGraphConditionalHandle cond_{};
 };
 

@@ -116,7 +116,13 @@ void DevBuf::alloc(size_t n) {
 }
 void DevBuf::upload(const void* src, size_t n) {
   alloc(n);
-  if (src && n) cuda_check(cudaMemcpy(p, src, n, cudaMemcpyHostToDevice), "upload");
+  if (src && n) {
+    cuda_check(cudaMemcpy(p, src, n, cudaMemcpyHostToDevice), "upload");
+    // a pageable-source cudaMemcpy may return before the DMA has landed, and
+    // the engines' non-blocking streams are not ordered after the legacy
+    // stream: complete it before any kernel can read the buffer
+    cuda_check(cudaDeviceSynchronize(), "upload");
+  }
 }
 
 DevGraph GraphImpl::dev() const {

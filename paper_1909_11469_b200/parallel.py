@@ -216,6 +216,8 @@ class NcclComm:
     def halo(self, bands):
         import torch.distributed as dist
 
+        import torch
+
         (b,) = bands
         ops = []
         if b.info.ghost_up:
@@ -223,14 +225,19 @@ class NcclComm:
         if b.info.ghost_down:
             ops += [dist.P2POp(dist.isend, b.send_down, self.rank + 1),
                     dist.P2POp(dist.irecv, b.recv_down, self.rank + 1)]
+        # on the band's (non-blocking) stream: ordered after the select / pack
+        # kernels that fill send_*, and before the refresh that reads recv_*
         if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+            with torch.cuda.stream(b.stream):
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
 
     def reduce(self, bands):
+        import torch
         import torch.distributed as dist
 
-        dist.all_reduce(bands[0].count)
+        with torch.cuda.stream(bands[0].stream):  # after k_part_count_rnbp wrote count
+            dist.all_reduce(bands[0].count)
 
     def gather_lists(self, lists):
         import torch.distributed as dist
@@ -296,11 +303,13 @@ def run_band_rnbp(bands, comm, max_iterations: int) -> BandStatus:
         if st.stopped:
             return st
         phase(0)
-        delta, frontier, survivors = (int(x) for x in bands[0].count[:3].tolist())
+        with torch.cuda.stream(bands[0].stream):  # the D2H read is ordered after the all-reduce
+            delta, frontier, survivors = (int(x) for x in bands[0].count[:3].tolist())
         rnbp = bands[0].KIND == SchedulerKind.rnbp
         if rnbp and frontier == 0 and survivors > 0:  # retry once, then one survivor (schedulers.cpp:204-214)
             phase(1)
-            frontier = int(bands[0].count[1].item())
+            with torch.cuda.stream(bands[0].stream):
+                frontier = int(bands[0].count[1].item())
             if frontier == 0:
                 ids = sorted(x for l in comm.gather_lists([b.survivors() for b in bands]) for x in l)
                 u = _lib.bp_philox_u53(bands[0].seed, st.iterations, 2, 0) * 2.0 ** -53

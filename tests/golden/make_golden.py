@@ -3,7 +3,7 @@
 oracle/Makefile).  Run in the build container:
 
     python tests/golden/make_golden.py            # small fixtures (seconds)
-    python tests/golden/make_golden.py --suite    # + 100x100 convergence suite (minutes)
+    python tests/golden/make_golden.py --suite    # + the convergence suites (minutes)
 
 The fixtures are committed so the oracle and the GPU tests are pinned to the
 reference's outputs even where /root/reference is absent (the GPU box)."""
@@ -68,24 +68,37 @@ def instance_hashes(ref):
     return out
 
 
-def suite(ref, workers):
-    """BASELINE config 1: 100x100 Ising C=2.5 seeds 500-524, eps 1e-5, cap 10k."""
-    rows = []
-    for s in range(500, 525):
-        g = po.Graph.ising(ref, 100, 2.5, s)
+SUITES = {
+    # BASELINE config 1 / acceptance criteria 5-6 (acceptance.cpp:282-351): 100x100
+    # Ising C=2.5 seeds 500-524, eps 1e-5; an iteration cap instead of the 60 s limit
+    "ising100": dict(n=100, c=2.5, seeds=range(500, 525), cap=10000,
+                     runs=(("lbp", dict()), ("rnbp_low0.5", dict(low_p=0.5)), ("rnbp_low0.7", dict(low_p=0.7)))),
+    # acceptance criterion 7 (acceptance.cpp:353-378): 30x30 C=3 seeds 700-709, LBP vs RnBP low_p 0.1
+    "hard30": dict(n=30, c=3.0, seeds=range(700, 710), cap=20000,
+                   runs=(("lbp", dict()), ("rnbp_low0.1", dict(low_p=0.1)))),
+}
+
+
+def suite(ref, workers, name):
+    """Converged flags, iterations, reference wall times and (converged runs)
+    the full marginals P(x = 1) per vertex as float32 (for the 1e-4 check)."""
+    sp = SUITES[name]
+    rows, marg = [], {}
+    for s in sp["seeds"]:
+        g = po.Graph.ising(ref, sp["n"], sp["c"], s)
         row = {"seed": s}
-        for name, kw in (("lbp", dict()), ("rnbp_low0.5", dict(low_p=0.5, high_p=1.0, seed=s - 500)),
-                         ("rnbp_low0.7", dict(low_p=0.7, high_p=1.0, seed=s - 500))):
-            kind = "lbp" if name == "lbp" else "rnbp"
-            r = po.run(g, po.make_config(kind, max_iterations=10000, time_limit=1e9, worker_count=workers, **kw),
-                       trace_cap=1)
-            row[name] = {"converged": r.converged, "iterations": r.iterations, "wall_time": r.wall_time,
-                         "beliefs_sha": h(r.beliefs)}
+        for run_name, kw in sp["runs"]:
+            kind = "lbp" if run_name == "lbp" else "rnbp"
+            extra = dict(high_p=1.0, edge_ratio_threshold=0.9, seed=s - sp["seeds"][0]) if kind == "rnbp" else {}
+            r = po.run(g, po.make_config(kind, max_iterations=sp["cap"], time_limit=1e9, worker_count=workers,
+                                         **kw, **extra), trace_cap=1)
+            row[run_name] = {"converged": r.converged, "iterations": r.iterations, "wall_time": r.wall_time,
+                             "messages_updated_total": r.messages_updated_total, "beliefs_sha": h(r.beliefs)}
             if r.converged:
-                row[name]["beliefs_head"] = r.beliefs[:20].tolist()
-        print(s, {k: (v["converged"], v["iterations"]) for k, v in row.items() if k != "seed"}, flush=True)
+                marg[f"{run_name}_{s}"] = r.beliefs[1::2].astype(np.float32)
+        print(name, s, {k: (v["converged"], v["iterations"]) for k, v in row.items() if k != "seed"}, flush=True)
         rows.append(row)
-    return rows
+    return rows, marg
 
 
 def main():
@@ -103,12 +116,19 @@ def main():
         json.dump(fx, f, indent=1)
     print("wrote reference_small.json")
     if a.suite:
-        rows = suite(ref, a.workers)
-        with open(os.path.join(HERE, "reference_suite_100x100.json"), "w") as f:
-            json.dump({"generated_by": "tests/golden/make_golden.py --suite (reference, oracle/_ref)",
-                       "config": "Ising 100x100 C=2.5, eps 1e-5, cap 10000, RnBP high_p 1.0 thr 0.9 seed = s-500",
-                       "workers": a.workers, "rows": rows}, f, indent=1)
-        print("wrote reference_suite_100x100.json")
+        out, marg = {}, {}
+        for name in SUITES:
+            rows, m = suite(ref, a.workers, name)
+            sp = SUITES[name]
+            out[name] = {"n": sp["n"], "c": sp["c"], "seeds": list(sp["seeds"]), "max_iterations": sp["cap"],
+                         "epsilon": 1e-5, "rows": rows}
+            marg.update({f"{name}/{k}": v for k, v in m.items()})
+        with open(os.path.join(HERE, "reference_suites.json"), "w") as f:
+            json.dump({"generated_by": "tests/golden/make_golden.py --suite (the reference, oracle/_ref)",
+                       "rnbp": "high_p 1.0, edge_ratio_threshold 0.9, seed = instance index (acceptance.cpp:50-61)",
+                       "workers": a.workers, "suites": out}, f, indent=1)
+        np.savez_compressed(os.path.join(HERE, "reference_suites_marginals.npz"), **marg)
+        print("wrote reference_suites.json, reference_suites_marginals.npz")
 
 
 if __name__ == "__main__":

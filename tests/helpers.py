@@ -96,3 +96,27 @@ def oracle_config(cfg):
     return po.make_config(int(cfg.kind), epsilon=cfg.epsilon, p=cfg.p, splash_depth=cfg.splash_depth,
                           low_p=cfg.low_p, high_p=cfg.high_p, edge_ratio_threshold=cfg.edge_ratio_threshold,
                           max_iterations=cfg.max_iterations, time_limit=cfg.time_limit, seed=cfg.seed)
+
+
+def lattice_arrays(orc, rows, cols, seed, c=2.0):
+    """rows x cols Ising lattice in generate_ising's edge order (per vertex the
+    right edge, then the down edge, generators.cpp:37-43) as build_graph input:
+    unaries (u, u') per vertex, then one lambda = u - 0.5 per edge, table
+    {e^{lambda c}, e^{-lambda c}, e^{-lambda c}, e^{lambda c}}; a zero draw in a
+    unary becomes 0.5.  Vectorised: any shape, including C > 512 strips."""
+    V = rows * cols
+    v = np.arange(V, dtype=np.int64)
+    col = v % cols
+    right = np.stack([v, v + 1], 1)
+    down = np.stack([v, v + cols], 1)
+    pairs = np.stack([right, down], 1).reshape(-1, 2)
+    mask = np.stack([col + 1 < cols, v + cols < V], 1).reshape(-1)
+    ep = pairs[mask].astype(np.uint32)
+    E = ep.shape[0]
+    _, u = po.mt_draws(orc, seed, 2 * V + E)
+    unary = u[: 2 * V].copy()
+    unary[unary == 0.0] = 0.5
+    lam = u[2 * V:] - 0.5
+    a, d = np.exp(lam * c), np.exp(-lam * c)
+    tb = np.stack([a, d, d, a], 1).reshape(-1)
+    return np.full(V, 2, np.uint32), unary, ep, tb

@@ -106,3 +106,12 @@ def test_import_fails_loudly_without_extension(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_1909_11469_b200"], cwd=tmp_path,
                        capture_output=True, text=True)
     assert r.returncode != 0 and "build the CUDA extension" in r.stderr
+
+
+def test_host_philox_known_answer(bp):
+    """The host restatement of the device draw (bp_philox_u53, used by the
+    band fallback) on Random123's first philox4x32-10 known-answer vector
+    (counter 0, key 0 -> 6627e8d5 e169c58d bc57ac4c 9b00dbd8): edge pair 0,
+    iteration 0, attempt 0, seed 0; d = 0 takes words 0-1, d = 1 words 2-3."""
+    assert bp.philox_u53(0, 0, 0, 0) == ((0x6627E8D5 << 32) | 0xE169C58D) >> 11
+    assert bp.philox_u53(0, 0, 0, 1) == ((0xBC57AC4C << 32) | 0x9B00DBD8) >> 11

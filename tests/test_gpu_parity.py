@@ -1,6 +1,6 @@
 """GPU parity tests: the CUDA engine (through the C ABI) against the fp64
 oracle (oracle/bp_oracle.c, pinned bitwise to the reference in
-tests/test_oracle_vs_ref.py).
+tests/test_oracle.py).
 
 Tolerances (north_star): LBP per-iteration messages within 1e-5 abs (fp32
 device vs fp64 reference); converged marginals within 1e-4."""
@@ -77,11 +77,10 @@ def test_lbp_run_matches_oracle(bp, orc, n, c, seed):
     cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=3000)
     r = bp.run(g, cfg)
     o = po.run(og, oracle_config(cfg))
-    assert r.converged == o.converged
+    assert o.converged and r.converged  # instances chosen to converge
     assert abs(r.iterations - o.iterations) <= 1
     assert len(r.trace) == r.iterations
-    if r.converged:
-        assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL
+    assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL
     assert r.messages_updated_total == r.iterations * 2 * g.num_edges()
 
 
@@ -264,9 +263,8 @@ def test_nonsquare_lattice_detected_and_exact(bp, orc, rows, cols):
         cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.from_string(kind), low_p=0.5, p=0.25, max_iterations=20000)
         r = bp.run(dg, cfg)
         o = po.run(og, oracle_config(cfg))
-        assert r.converged == o.converged, kind
-        if r.converged:
-            assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL, kind
+        assert o.converged and r.converged, kind
+        assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL, kind
 
 
 @pytest.mark.parametrize("name", ["er", "potts4", "potts8"])

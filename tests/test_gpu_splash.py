@@ -174,9 +174,8 @@ def test_rs_run_matches_reference(bp, orc, n, c, seed, p, h):
     cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=p, splash_depth=h, max_iterations=200000)
     r = bp.run(g, cfg)
     o = po.run(og, oracle_config(cfg))
-    assert r.converged == o.converged
-    if r.converged:
-        assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL
+    assert o.converged and r.converged  # instances chosen to converge
+    assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL
     # frontier_size = splash edges; messages_updated_total = its sum (schedulers.cpp:335,343)
     assert sum(t.frontier_size for t in r.trace) == r.messages_updated_total
     assert len(r.trace) == r.iterations
@@ -201,6 +200,5 @@ def test_rs_run_er_graph(bp, orc):
     cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=1 / 128, splash_depth=2, max_iterations=100000)
     r = bp.run(g, cfg)
     o = po.run(og, oracle_config(cfg))
-    assert r.converged == o.converged
-    if r.converged:
-        assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL
+    assert o.converged and r.converged
+    assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL

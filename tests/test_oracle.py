@@ -264,3 +264,24 @@ def test_new_generators_are_deterministic(orc):
     assert e.num_edges == 400 and np.all(ep[:, 0] < ep[:, 1])
     keys = ep[:, 0] * 1000 + ep[:, 1]
     assert np.all(np.diff(keys) > 0)  # sorted, unique
+
+
+def test_oracle_reproduces_reference_suite_fixtures(orc):
+    """The C restatement reproduces the reference's suite fixtures bitwise
+    (tests/golden/reference_suites.json, generated from oracle/_ref)."""
+    import json
+    import os
+    from tests.golden.make_golden import h
+    with open(os.path.join(os.path.dirname(__file__), "golden", "reference_suites.json")) as f:
+        suites = json.load(f)["suites"]
+    for suite, seed, name in (("ising100", 513, "lbp"), ("hard30", 700, "rnbp_low0.1"), ("hard30", 709, "lbp")):
+        sp = suites[suite]
+        row = next(r for r in sp["rows"] if r["seed"] == seed)[name]
+        g = po.Graph.ising(orc, sp["n"], sp["c"], seed)
+        kw = dict(low_p=float(name.split("low")[1]), high_p=1.0, edge_ratio_threshold=0.9,
+                  seed=seed - sp["seeds"][0]) if name != "lbp" else {}
+        r = po.run(g, po.make_config("lbp" if name == "lbp" else "rnbp", max_iterations=sp["max_iterations"],
+                                     time_limit=1e9, **kw), trace_cap=1)
+        assert (r.converged, r.iterations, r.messages_updated_total) == \
+            (row["converged"], row["iterations"], row["messages_updated_total"])
+        assert h(r.beliefs) == row["beliefs_sha"]
