@@ -1,25 +1,33 @@
 #!/usr/bin/env python
 """Benchmark of the BP message-scheduling hot path (BASELINE.json configs[1]).
 
-Workload ("step"): one complete bpsched::run (schedulers.cpp:293-353) of RnBP
-(low_p 0.5, high_p 1.0, EdgeRatio threshold 0.9, epsilon 1e-5, 10,000-iteration
-cap) on the 1000 x 1000 Ising grid, C = 2.5, generated bit-identically to the
-reference's generate_ising (seed = step index + rank * 1000).
+Headline workload ("step"), IDENTICAL on both arms (`--impl b200` and
+`--impl reference`): one bpsched::run (schedulers.cpp:293-353) of RnBP
+(low_p 0.5, high_p 1.0, EdgeRatio threshold 0.9, epsilon 1e-5) capped at a
+fixed window of HEAD_ITERS iterations, on the 1000 x 1000 Ising grid, C = 2.5,
+generated bit-identically to the reference's generate_ising; seed = step index
+(warm-up steps: the first W indices; rank r of N adds r * 1000).
 
-  value  = committed edge-message updates / second (sum |F| / device time of the
-           runs, graph resident in HBM, CUDA events on the engine stream)
-  e2e    = the same metric through the public API with host buffers: every step
-           uploads the graph from host arrays in build_graph's input layout
+  value  = committed edge-message updates / second = sum |F| / time
+           (messages_updated_total / wall_time in the reference, :343,350);
+           B200: graph resident in HBM, CUDA-event time of each run on the
+           engine stream, L2 flushed between steps
+  e2e    = the same metric through the public API with host buffers: every
+           step uploads the graph from host arrays in build_graph's input layout
            (bp_graph_create: validation, CSR, H2D), runs, and copies the beliefs
            back (D2H)
+  reference arm: the unmodified reference core (oracle/_ref, compiled from
+           /root/reference) on the host cores, worker_count = nproc, same
+           seeds, same window, same warm-up
 
-At N > 1 GPUs every rank runs its own instances (weak scaling, replicas), and
-the row-band partitioned LBP on the 16384^2 grid (BASELINE config 5, one band
-per GPU, NCCL halo exchange) is reported beside it under "partitioned_16k".
-Extra keys: LBP / RBP on the workload instance, the 100^2 C=2.5 convergence
-suite (seeds 500-524), the HBM roofline of the LBP sweep on 16384^2.  The
-reference arm (--impl reference) times the reference's own bpsched::run compiled
-from /root/reference (oracle/_ref) on the host cores on a bounded sample.
+Extra keys (rank 0, N = 1), each with the reference's CPU figure beside it:
+time_to_convergence (BASELINE config 1 suite, both arms), full_run_10k (the
+10k-cap run of the headline instance, persistent-tail latency roofline),
+config3_er1m (Residual Splash), config4_potts4096 (LBP roofline + RnBP low_p
+sweep 0.1-1.0), config5_16k (LBP and RnBP windows on one GPU, HBM rooflines).
+At N > 1 every rank runs its own instances (weak scaling, replicas), and the
+row-band partitioned 16384^2 grid (config 5) is reported under
+"partitioned_16k".
 """
 from __future__ import annotations
 
@@ -38,17 +46,20 @@ sys.path.insert(0, ROOT)
 
 N_GRID = 1000
 C_COUPLING = 2.5
-CAP = 10000
-METRIC = "edge-message updates/sec (RnBP, Ising 1000x1000 C=2.5, run to convergence or 10k-iteration cap)"
+HEAD_ITERS = 20        # the headline window (both arms)
+CAP = 10000            # BASELINE config 1/2 iteration cap (full runs, suites)
+METRIC = ("edge-message updates/sec (RnBP low_p 0.5, Ising 1000x1000 C=2.5, "
+          f"run() capped at a fixed {HEAD_ITERS}-iteration window)")
 UNIT = "updates/s"
-REF_SAMPLE_ITERS = 5   # bounded CPU sample: reference run capped at 5 iterations
 BIG_N = 16384          # BASELINE config 5
 BIG_ITERS = 30         # fixed LBP window on the big grid
-BIG_RNBP_ITERS = 10    # fixed RnBP window on the big grid (N > 1)
+BIG_RNBP_ITERS = 20    # fixed RnBP window on the big grid
+POTTS_N, POTTS_Q = 4096, 8
+SUITE_SEEDS = range(500, 525)
 
 
-def rnbp_kw(seed):
-    return dict(low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5, max_iterations=CAP,
+def rnbp_kw(seed, iters=HEAD_ITERS):
+    return dict(low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5, max_iterations=iters,
                 time_limit=1e9, seed=seed)
 
 
@@ -63,8 +74,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region:
     ONE `nvidia-smi --query-gpu=... -lms 200` process (the profiling recipe's
     clocks line), started before the region and stopped after it by its own
-    handle.  (Spawning nvidia-smi per sample initialises NVML each time and
-    can stall the run's host round trips.)"""
+    handle."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -126,12 +136,17 @@ def flush_l2(torch, buf):
     torch.cuda.synchronize()
 
 
-# Algorithmic bytes, binary Ising lattice, compressed
-# layout (one fp32 log2-odds per message, one fp32 coupling per edge):
-#   LBP sweep: per vertex read its 2 edge pairs (16 B) + write 4 messages (16 B)
-#              + 2 couplings (8 B) + unary (4 B) = 44 B
-#   touched refresh (update class): per vertex unary 4 B (+ 4 B list id); per
-#              message edge pair 8 B + coupling 4 B + candidate 4 B + residual 8 B
+# Algorithmic bytes, compressed device layouts:
+#   binary LBP sweep (one fp32 log2-odds per message, one fp32 coupling per
+#     edge): per vertex read its 2 edge pairs (16 B) + write 4 messages (16 B)
+#     + 2 couplings (8 B) + unary (4 B) = 44 B
+#   refresh (update class, Init / Delta modes): per vertex unary 4 B (+ 4 B list
+#     id); per message: edge pair 8 B + coupling 4 B + candidate 4 B + residual 8 B
+#   q-state LBP sweep (QS floats per message, one Potts weight per edge): per
+#     directed edge read its q-vector once (4 QS; it serves as the incoming
+#     message at its target and as the old outgoing one at its source) and
+#     write the new one (4 QS), weight 4 B / 2 (shared by the edge pair); per
+#     vertex the unary (4 QS)
 # reference fp32 layout: 30 B per directed edge per LBP sweep.
 def lbp_sweep_bytes(vertices):
     return 44 * vertices
@@ -140,6 +155,90 @@ def lbp_sweep_bytes(vertices):
 def refresh_bytes(visits, evals):
     return 8 * visits + 24 * evals
 
+
+def qstate_sweep_bytes(V, D, qs):
+    return D * (8 * qs + 2) + V * 4 * qs
+
+
+def _roofline(name, nbytes, ms, peak, peak_src, **extra):
+    ach = nbytes / (ms / 1e3) / 1e9 if ms else 0.0
+    out = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+           "peak_source": peak_src, "algorithmic_bytes": nbytes, "kernel_ms": ms}
+    out.update(extra)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the reference on the host cores (oracle/_ref = the reference compiled from
+# its own sources; oracle/liboracle.so = the C restatement if it is absent)
+
+def _ref_lib():
+    from oracle import pyoracle as po
+    try:
+        return po, po.load("ref"), "reference"
+    except FileNotFoundError:
+        return po, po.load("orc"), "port"
+
+
+def _ref_headline(K, W, rank=0):
+    """The headline workload on the reference: K timed steps after W warm-up
+    steps, seeds as the B200 arm."""
+    po, ref, kind = _ref_lib()
+    cores = os.cpu_count() or 1
+    upd, t, steps = 0, 0.0, []
+    for i in range(W + K):
+        s = rank * 1000 + (i if i < W else i - W)
+        g = po.Graph.ising(ref, N_GRID, C_COUPLING, s)  # outside the timed span (like bp_graph_create)
+        r = po.run(g, po.make_config("rnbp", worker_count=cores, **rnbp_kw(s)), trace_cap=1)
+        del g
+        if i >= W:
+            upd += r.messages_updated_total
+            t += r.wall_time
+            steps.append({"seed": s, "iterations": r.iterations, "updates": r.messages_updated_total,
+                          "wall_s": round(r.wall_time, 4)})
+    return {"value": upd / t, "unit": UNIT, "cores": cores, "kind": kind, "seconds": t, "steps": steps,
+            "sample": f"the headline workload itself: {K} steps x RnBP run() capped at {HEAD_ITERS} iterations on "
+                      f"Ising {N_GRID}^2 C={C_COUPLING}, seeds as the B200 arm (EngineState ctor + loop, "
+                      f"schedulers.cpp:297-350), after {W} warm-up steps"}
+
+
+def _ref_suite(names=("rnbp_low0.5", "rnbp_low0.7")):
+    """Time to convergence on BASELINE config 1 (100^2 C=2.5, seeds 500-524,
+    cap 10k) on the reference: fraction converged + median wall time."""
+    po, ref, kind = _ref_lib()
+    cores = os.cpu_count() or 1
+    out = {}
+    for name in names:
+        conv, times, iters = 0, [], []
+        t0 = time.perf_counter()
+        for s in SUITE_SEEDS:
+            g = po.Graph.ising(ref, 100, 2.5, s)
+            kw = dict(low_p=float(name.split("low")[1]), high_p=1.0, edge_ratio_threshold=0.9, seed=s - 500) \
+                if name != "lbp" else {}
+            r = po.run(g, po.make_config("lbp" if name == "lbp" else "rnbp", max_iterations=CAP, time_limit=1e9,
+                                         worker_count=cores, **kw), trace_cap=1)
+            conv += r.converged
+            if r.converged:
+                times.append(r.wall_time)
+                iters.append(r.iterations)
+        out[name] = {"converged": conv, "of": len(SUITE_SEEDS), "median_time_s": statistics.median(times) if times else None,
+                     "median_iterations": statistics.median(iters) if iters else None,
+                     "suite_wall_s": round(time.perf_counter() - t0, 3), "cores": cores, "kind": kind}
+    return out
+
+
+def _ref_window(graph_fn, cfg_kw, kind_name, sample):
+    """One bounded run of the reference on a prepared instance."""
+    po, ref, kind = _ref_lib()
+    cores = os.cpu_count() or 1
+    g = graph_fn(po, ref)
+    r = po.run(g, po.make_config(kind_name, worker_count=cores, time_limit=1e9, **cfg_kw), trace_cap=1)
+    return {"value": r.messages_updated_total / r.wall_time, "unit": UNIT, "cores": cores, "kind": kind,
+            "iterations": r.iterations, "wall_s": round(r.wall_time, 4),
+            "ms_per_iteration": round(r.wall_time * 1e3 / max(1, r.iterations), 3), "sample": sample}
+
+
+# ---------------------------------------------------------------------------
 
 def run_b200(args):
     import torch
@@ -154,20 +253,14 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     K, W = args.steps, args.warmup
-
-    graphs = {}
-
-    def graph_for(seed):
-        if seed not in graphs:
-            graphs[seed] = bp.generate_ising(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=seed), device=local)
-        return graphs[seed]
-
-    seeds = [rank * 1000 + s for s in range(K)]
-    for s in seeds:
-        graph_for(s)
     kind = bp.SchedulerKind.rnbp
-    for w in range(W):  # warmup (graph capture, allocation, first-touch)
-        bp.run(graph_for(seeds[w % K]), bp.SchedulerConfig(kind=kind, **rnbp_kw(seeds[w % K])))
+
+    warm_seeds = [rank * 1000 + s for s in range(W)]
+    seeds = [rank * 1000 + s for s in range(K)]
+    graphs = {s: bp.generate_ising(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=s), device=local)
+              for s in sorted(set(seeds + warm_seeds))}
+    for s in warm_seeds:  # warm-up (graph capture, allocation, first-touch)
+        bp.run(graphs[s], bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -177,7 +270,7 @@ def run_b200(args):
         dev_ms = 0.0
         for s in seeds:
             flush_l2(torch, flush)
-            r = bp.run(graph_for(s), bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
+            r = bp.run(graphs[s], bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
             dev_ms += r.device_ms
             results.append(r)
         torch.cuda.synchronize()
@@ -200,15 +293,13 @@ def run_b200(args):
     # ---- e2e: public API with host buffers (graph upload + run + beliefs D2H)
     e2e_updates, e2e_t = 0, 0.0
     h2d = d2h = 0
-    host_arrays = {s: bp.generate_ising_arrays(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=s))
-                   for s in seeds[: min(K, 5)]}
+    host_arrays = {s: bp.generate_ising_arrays(bp.IsingParams(n=N_GRID, c=C_COUPLING, seed=s)) for s in seeds}
     e2e_steps = []
     # one untimed call first: process-level first use of the host-array path
-    # (module loading of its kernels, host thread pool start-up)
     cards, un, ep, tb = host_arrays[seeds[0]]
     bp.run(bp.PairwiseMRF.from_arrays(cards, un, ep, tb, device=local),
-           bp.SchedulerConfig(kind=kind, **dict(rnbp_kw(seeds[0]), max_iterations=10)))
-    for s in seeds[: min(K, 5)]:
+           bp.SchedulerConfig(kind=kind, **rnbp_kw(seeds[0], 2)))
+    for s in seeds:
         cards, un, ep, tb = host_arrays[s]
         flush_l2(torch, flush)
         t1 = time.perf_counter()
@@ -222,6 +313,7 @@ def run_b200(args):
         h2d = cards.nbytes + un.nbytes + ep.nbytes + tb.nbytes
         d2h = r.beliefs.values.nbytes + 32 * len(r.trace)
         del g
+    del host_arrays
     if dist:
         tt = torch.tensor([e2e_t, float(e2e_updates)], dtype=torch.float64, device="cuda")
         mx = tt.clone()
@@ -229,113 +321,273 @@ def run_b200(args):
         dist.all_reduce(tt, op=dist.ReduceOp.SUM)
         e2e_t, e2e_updates = float(mx[0]), float(tt[1])
 
-    # ---- partitioned 16K^2 LBP (config 5): every rank, a band each
+    # ---- partitioned 16K^2 (config 5): every rank, a band each
     part = _partitioned_big(bp, torch, dist, ws, rank, local)
 
-    out = {}
     if rank == 0:
         peak, peak_src = measured_peaks()
-        # ---- dominant kernel of the workload (instrumented run: CUDA events per launch)
-        g0 = graph_for(seeds[0])
+        # ---- dominant kernel class of the workload (instrumented run: CUDA events per launch)
+        g0 = graphs[seeds[0]]
         ri = bp.run_ex(g0, bp.SchedulerConfig(kind=kind, **rnbp_kw(seeds[0])), kernel_timing=True)
         ks = ri.kernel_stats
         tot_ms = sum(v["ms"] for v in ks.values()) or 1.0
-        dom = max(ks, key=lambda k: ks[k]["ms"])
-        if dom == "persist":
-            dom_bytes = ks["persist"]["bytes"]
-            dom_name = "k_rnbp_persist (RnBP candidate-list iterations, cooperative grid of one CTA per SM, one 16-CTA cluster for lists under 2048 entries)"
-        else:
-            dom_bytes = refresh_bytes(ri.vertex_visits, ri.message_evaluations)
-            dom_name = f"{dom} kernels"
-        dom_ms = ks[dom]["ms"]
-        achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms else 0.0
         shares = {k: round(v["ms"] / tot_ms, 4) for k, v in ks.items() if v["launches"]}
+        D = g0.num_directed_edges()
+        V = g0.num_vertices()
+        # update class = init sweep + touched refreshes (k_vertex_update Init/Delta)
+        upd_bytes = refresh_bytes(ri.vertex_visits, ri.message_evaluations)
+        # select class = residual scan 4 B per directed edge per iteration + commit
+        # of every selected edge (read candidate 4 B, write message 4 B, zero residual 4 B)
+        sel_bytes = 4 * D * ri.iterations + 12 * ri.messages_updated_total
+        dom = "update" if ks["update"]["ms"] >= ks["select"]["ms"] else "select"
+        roof = _roofline(
+            "k_vertex_update<Init/Delta> (dense touched refresh)" if dom == "update" else
+            "k_rnbp_select (filter + Bernoulli + commit)", upd_bytes if dom == "update" else sel_bytes,
+            ks[dom]["ms"], peak, peak_src, launches=ks[dom]["launches"], kernel_shares=shares,
+            traffic=_read_traffic("rnbp_refresh" if dom == "update" else "rnbp_select"),
+            select={"bytes": sel_bytes, "ms": ks["select"]["ms"],
+                    "GBps": sel_bytes / (ks["select"]["ms"] / 1e3) / 1e9 if ks["select"]["ms"] else None},
+            regime="1000^2: the 70 MB working set is L2-resident within a window (L2 flushed between steps); "
+                   "the HBM-bound configs are config4_potts4096 and config5_16k below")
 
-        # ---- other schedulers on the workload instance + convergence suite
-        extra = {}
-        for name, cfg in (("lbp", bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=CAP, time_limit=1e9)),
-                          ("rbp", bp.SchedulerConfig(kind=bp.SchedulerKind.rbp, p=1 / 256, max_iterations=CAP,
-                                                     time_limit=1e9)),
-                          ("rs", bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=1 / 256, max_iterations=200,
-                                                    time_limit=1e9))):
-            bp.run(g0, cfg)
-            rr = bp.run(g0, cfg)
-            extra[name] = {"value": rr.messages_updated_total / (rr.device_ms / 1e3), "unit": UNIT,
-                           "iterations": rr.iterations, "converged": rr.converged,
-                           "ms": round(rr.device_ms, 3), "ms_per_iteration": round(rr.device_ms / max(1, rr.iterations), 4)}
-        suite = _convergence_suite(bp, local)
-
+        cpu_head = _ref_headline(min(K, 3), 1) if ws == 1 else None
+        extra = {
+            "full_run_10k": _full_run(bp, g0, seeds[0], peak, peak_src),
+            "schedulers_1000": _schedulers(bp, g0),
+            "time_to_convergence": _ttc_suite(bp, local),
+        }
+        if ws == 1:
+            extra["time_to_convergence"]["reference"] = _ref_suite()
+            extra["config3_er1m"] = _config3(bp, torch, local)
+            extra["config4_potts4096"] = _config4(bp, torch, local, peak, peak_src)
+            extra["config5_16k"] = _config5(bp, torch, local, peak, peak_src, cpu_head)
+        del graphs
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 (base-2 log-odds messages)",
             "data": "synthetic (generate_ising, bit-identical to the reference generator)",
-            "config": {"workload": "ising1000_c2.5_rnbp", "n": N_GRID, "c": C_COUPLING, "scheduler": "rnbp",
-                       "low_p": 0.5, "high_p": 1.0, "edge_ratio_threshold": 0.9, "epsilon": 1e-5,
-                       "max_iterations": CAP, "seeds": f"rank*1000 + 0..{K - 1}",
+            "config": {"workload": f"ising1000_c2.5_rnbp_window{HEAD_ITERS}", "n": N_GRID, "c": C_COUPLING,
+                       "scheduler": "rnbp", "low_p": 0.5, "high_p": 1.0, "edge_ratio_threshold": 0.9,
+                       "epsilon": 1e-5, "max_iterations": HEAD_ITERS, "seeds": f"rank*1000 + 0..{K - 1}",
+                       "warmup_seeds": f"rank*1000 + 0..{W - 1}", "same_config_as_reference_arm": True,
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                        "l2": "flushed between timed steps (256 MiB write)"},
-            "steps_detail": [{"seed": s, "converged": r.converged, "iterations": r.iterations,
-                              "updates": r.messages_updated_total, "ms": round(r.device_ms, 3)}
-                             for s, r in zip(seeds, results)],
-            "time_to_convergence_s": _ttc(results),
+            "steps_detail": [{"seed": s, "iterations": r.iterations, "updates": r.messages_updated_total,
+                              "ms": round(r.device_ms, 4)} for s, r in zip(seeds, results)],
             "wall_s": wall,
             "gpu_launches": launches,
             "e2e": {"value": e2e_updates / e2e_t if e2e_t else None, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps": min(K, 5), "steps_ms": e2e_steps,
+                    "d2h_bytes_per_step": d2h, "steps": K, "steps_ms": e2e_steps,
                     "includes": "bp_graph_create from host arrays (validation + CSR + H2D) + run + beliefs D2H"},
-            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _read_traffic(dom), "peak_source": peak_src,
-                         "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms, "launches": ks[dom]["launches"],
-                         "kernel_shares": shares,
-                         "regime": "latency-bound: the 1000^2 working set (~70 MB) is L2-resident and the "
-                                   "candidate-list iterations move ~3k messages each; roofline_hbm is the "
-                                   "HBM-bound kernel (LBP sweep, 16384^2)"},
-            "schedulers": extra,
-            "convergence_suite_100x100": suite,
+            "roofline": roof,
             "clocks": clk.summary(),
         }
-        out["roofline_hbm"] = _hbm_roofline(bp, torch, local, peak, peak_src)
+        out.update(extra)
         if part:
             out["partitioned_16k"] = part
         if ws == 1:
-            out["cpu_baseline"] = _cpu_baseline(sample_iters=REF_SAMPLE_ITERS)
+            out["cpu_baseline"] = cpu_head
         print(json.dumps(out))
     if dist:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def _hbm_roofline(bp, torch, device, peak, peak_src):
-    """LBP sweep on the 16384^2 grid (config 5, working set >> L2): CUDA-event time
-    of the update launches of a fixed window, algorithmic bytes per section 5."""
+def _full_run(bp, g0, seed, peak, peak_src):
+    """The 10k-cap run of the headline instance (config 2 as the reference
+    runs it to convergence or the cap): RnBP's dense phase, then the
+    candidate-list tail in the persistent kernel.  Latency roofline of the
+    tail: per-iteration time against two grid barriers (measured 1.27 us each,
+    tools/microbench)."""
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, **rnbp_kw(seed, CAP))
+    bp.run(g0, cfg)
+    r = bp.run(g0, cfg)
+    ri = bp.run_ex(g0, cfg, kernel_timing=True)
+    ks = ri.kernel_stats
+    tot = sum(v["ms"] for v in ks.values()) or 1.0
+    pers = ks.get("persist", {"ms": 0.0, "launches": 0, "bytes": 0})
+    tail_its = max(1, ri.persist_iterations)  # iterations run inside the persistent kernel
+    us_it = pers["ms"] * 1e3 / tail_its if pers["ms"] else None
+    return {"value": r.messages_updated_total / (r.device_ms / 1e3), "unit": UNIT, "iterations": r.iterations,
+            "converged": r.converged, "device_ms": round(r.device_ms, 3), "updates": r.messages_updated_total,
+            "kernel_shares": {k: round(v["ms"] / tot, 4) for k, v in ks.items() if v["launches"]},
+            "persist": {"ms": pers["ms"], "bytes": pers["bytes"], "iterations": ri.persist_iterations,
+                        "GBps": pers["bytes"] / (pers["ms"] / 1e3) / 1e9 if pers["ms"] else None,
+                        "hbm_frac": pers["bytes"] / (pers["ms"] / 1e3) / 1e9 / peak if pers["ms"] else None,
+                        "peak_source": peak_src,
+                        "latency_roofline": {"us_per_iteration": us_it, "floor_us": 2 * 1.27,
+                                             "floor": "two cooperative grid barriers per iteration "
+                                                      "(1.27 us each, tools/microbench/sync_bench.cu)",
+                                             "frac": (2 * 1.27) / us_it if us_it else None}}}
+
+
+def _schedulers(bp, g0):
+    out = {}
+    for name, cfg in (("lbp", bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=CAP, time_limit=1e9)),
+                      ("rbp", bp.SchedulerConfig(kind=bp.SchedulerKind.rbp, p=1 / 256, max_iterations=2000,
+                                                 time_limit=1e9)),
+                      ("rs", bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=1 / 256, max_iterations=200,
+                                                time_limit=1e9))):
+        bp.run(g0, cfg)
+        rr = bp.run(g0, cfg)
+        out[name] = {"value": rr.messages_updated_total / (rr.device_ms / 1e3), "unit": UNIT,
+                     "iterations": rr.iterations, "converged": rr.converged, "ms": round(rr.device_ms, 3),
+                     "ms_per_iteration": round(rr.device_ms / max(1, rr.iterations), 4)}
+    return out
+
+
+def _ttc_suite(bp, device):
+    """Time to convergence on BASELINE config 1: Ising 100^2 C=2.5, seeds
+    500-524, eps 1e-5, cap 10k (wall_time spans schedulers.cpp:297-350)."""
+    out = {}
+    for name, cfg_kw in (("lbp", dict(kind=bp.SchedulerKind.lbp)),
+                         ("rnbp_low0.5", dict(kind=bp.SchedulerKind.rnbp, low_p=0.5, high_p=1.0)),
+                         ("rnbp_low0.7", dict(kind=bp.SchedulerKind.rnbp, low_p=0.7, high_p=1.0))):
+        conv, times, iters = 0, [], []
+        t0 = time.perf_counter()
+        for s in SUITE_SEEDS:
+            g = bp.generate_ising(bp.IsingParams(n=100, c=2.5, seed=s), device=device)
+            kw = dict(cfg_kw)
+            if kw["kind"] == bp.SchedulerKind.rnbp:
+                kw["seed"] = s - 500
+            r = bp.run(g, bp.SchedulerConfig(max_iterations=CAP, time_limit=1e9, **kw))
+            conv += r.converged
+            if r.converged:
+                times.append(r.wall_time)
+                iters.append(r.iterations)
+        out[name] = {"converged": conv, "of": len(SUITE_SEEDS),
+                     "median_time_s": statistics.median(times) if times else None,
+                     "median_iterations": statistics.median(iters) if iters else None,
+                     "suite_wall_s": round(time.perf_counter() - t0, 3)}
+    return {"b200": out, "config": "Ising 100^2 C=2.5, seeds 500-524, eps 1e-5, cap 10k; RnBP seed = s - 500"}
+
+
+def _config3(bp, torch, device):
+    """Config 3: Erdos-Renyi G(1M, 2M), binary, Residual Splash h = 2, fixed
+    20-iteration windows, p = 1/128 and 1/256; the reference on the same
+    instance (built through its own build_graph) for a 3-iteration sample."""
+    out = {}
+    g = bp.generate_er(1_000_000, 2_000_000, 2.5, 0, device=device)
+    for p in (1 / 128, 1 / 256):
+        cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rs, p=p, splash_depth=2, max_iterations=20, time_limit=1e9)
+        bp.run_ex(g, cfg, beliefs=False)
+        r = bp.run_ex(g, cfg, beliefs=False)
+        out[f"rs_p1/{round(1 / p)}"] = {"value": r.messages_updated_total / (r.device_ms / 1e3), "unit": UNIT,
+                                        "iterations": r.iterations, "device_ms": round(r.device_ms, 3),
+                                        "ms_per_iteration": round(r.device_ms / max(1, r.iterations), 4),
+                                        "splashes": r.splashes, "splash_rounds": r.splash_rounds}
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=20, time_limit=1e9)
+    bp.run_ex(g, cfg, beliefs=False)
+    r = bp.run_ex(g, cfg, beliefs=False)
+    out["lbp"] = {"value": r.messages_updated_total / (r.device_ms / 1e3), "unit": UNIT,
+                  "ms_per_iteration": round(r.device_ms / max(1, r.iterations + 1), 4)}
+    del g
+    torch.cuda.empty_cache()
+
+    def er(po, ref):
+        a = po.Graph.er(po.load("orc"), 1_000_000, 2_000_000, 2.5, 0).arrays()
+        return po.Graph.from_arrays(ref, a.cardinalities, a.unary, a.endpoints, a.tables)
+    out["reference"] = _ref_window(er, dict(p=1 / 128, splash_depth=2, max_iterations=3), "rs",
+                                   "RS p=1/128 h=2 on the same ER-1M instance (reference build_graph), "
+                                   "first 3 iterations incl. EngineState ctor")
+    out["config"] = "Erdos-Renyi G(n=1e6, m=2e6), binary Ising-style potentials, C=2.5, seed 0 (DESIGN.md 3)"
+    return out
+
+
+def _config4(bp, torch, device, peak, peak_src):
+    """Config 4: Potts 4096^2, q = 8: the LBP sweep with its HBM roofline and
+    the RnBP parallelism sweep low_p = 0.1 ... 1.0 (high_p 1), fixed
+    20-iteration windows.  The reference cannot hold this instance in a
+    bounded sample (17 GB of fp64 tables); its rate on Potts 512^2 q = 8 is
+    reported beside it, per directed edge, labelled as such."""
+    out = {}
+    g = bp.generate_potts(POTTS_N, POTTS_Q, 2.5, 0, device=device)
+    V, D = g.num_vertices(), g.num_directed_edges()
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=10, time_limit=1e9)
+    bp.run_ex(g, cfg, beliefs=False)
+    r = bp.run_ex(g, cfg, beliefs=False, kernel_timing=True)
+    k = r.kernel_stats["update"]
+    sweeps = r.iterations + 1
+    nbytes = qstate_sweep_bytes(V, D, 8) * sweeps
+    out["lbp"] = _roofline("k_vertex_update<Count> q-state lattice sweep (LBP), Potts 4096^2 q=8", nbytes, k["ms"],
+                           peak, peak_src, launches=k["launches"], sweeps=sweeps, ms_per_sweep=k["ms"] / sweeps,
+                           updates_per_s=r.messages_updated_total / (r.device_ms / 1e3),
+                           bytes_per_directed_edge=round(qstate_sweep_bytes(V, D, 8) / D, 2),
+                           reference_layout_bytes_per_directed_edge=204,
+                           traffic=_read_traffic("potts_lbp"))
+    sweep = {}
+    for lp in (0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0):
+        cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=lp, high_p=1.0, max_iterations=20,
+                                 time_limit=1e9, seed=1)
+        r = bp.run_ex(g, cfg, beliefs=False)
+        sweep[str(lp)] = {"value": r.messages_updated_total / (r.device_ms / 1e3), "iterations": r.iterations,
+                          "ms_per_iteration": round(r.device_ms / max(1, r.iterations), 4),
+                          "unconverged_end": r.trace[-1].unconverged if len(r.trace) else None}
+    out["rnbp_low_p_sweep"] = sweep
+    del g
+    torch.cuda.empty_cache()
+
+    def potts(po, ref):
+        a = po.Graph.potts(po.load("orc"), 512, 8, 2.5, 0).arrays()
+        return po.Graph.from_arrays(ref, a.cardinalities, a.unary, a.endpoints, a.tables)
+    out["reference"] = _ref_window(potts, dict(max_iterations=3), "lbp",
+                                   "LBP on Potts 512^2 q=8 (same generator, reference build_graph), 3 iterations "
+                                   "incl. EngineState ctor; per-edge rate, not the 4096^2 instance (host RAM)")
+    out["reference"]["extrapolated_4096_ms_per_iteration"] = out["reference"]["ms_per_iteration"] * 64
+    out["config"] = "Potts 4096^2 q=8 C=2.5 seed 0 (DESIGN.md 3)"
+    return out
+
+
+def _config5(bp, torch, device, peak, peak_src, cpu_head):
+    """Config 5 at N = 1: the 16384^2 grid (working set >> L2): fixed LBP and
+    RnBP windows with HBM rooflines.  The reference needs ~126 GB of host RAM
+    for this instance; its per-edge rate from the headline sample is
+    extrapolated and labelled."""
     g = bp.generate_ising(bp.IsingParams(n=BIG_N, c=C_COUPLING, seed=0), device=device)
+    V, D = g.num_vertices(), g.num_directed_edges()
     cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=BIG_ITERS, time_limit=1e9)
     bp.run_ex(g, cfg, beliefs=False)
     r = bp.run_ex(g, cfg, beliefs=False, kernel_timing=True)
     k = r.kernel_stats["update"]
     sweeps = r.iterations + 1
-    V = g.num_vertices()
     nbytes = lbp_sweep_bytes(V) * sweeps
-    ach = nbytes / (k["ms"] / 1e3) / 1e9
-    ref_bytes = 30 * g.num_directed_edges() * sweeps
-    out = {"kernel": "k_vertex_update<Count> lattice tiles (LBP sweep), Ising 16384^2", "bound": "hbm",
-           "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
-           "algorithmic_bytes": nbytes, "bytes_per_vertex": 44, "kernel_ms": k["ms"], "launches": k["launches"],
-           "sweeps": sweeps, "ms_per_sweep": k["ms"] / sweeps,
-           "updates_per_s": r.messages_updated_total / (r.device_ms / 1e3),
-           "effective_reference_layout_GBps": ref_bytes / (k["ms"] / 1e3) / 1e9,
-           "traffic": _read_traffic("lbp16k")}
+    out = {"lbp": _roofline("k_lbp_lattice (TMA-staged LBP sweep), Ising 16384^2", nbytes, k["ms"], peak, peak_src,
+                            bytes_per_vertex=44, launches=k["launches"], sweeps=sweeps, ms_per_sweep=k["ms"] / sweeps,
+                            updates_per_s=r.messages_updated_total / (r.device_ms / 1e3),
+                            effective_reference_layout_GBps=30 * D * sweeps / (k["ms"] / 1e3) / 1e9,
+                            traffic=_read_traffic("lbp16k"))}
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, **rnbp_kw(0, BIG_RNBP_ITERS))
+    bp.run_ex(g, cfg, beliefs=False)
+    r = bp.run_ex(g, cfg, beliefs=False)
+    ri = bp.run_ex(g, cfg, beliefs=False, kernel_timing=True)
+    ks = ri.kernel_stats
+    ub = refresh_bytes(ri.vertex_visits, ri.message_evaluations)
+    sb = 4 * D * ri.iterations + 12 * ri.messages_updated_total
+    out["rnbp"] = {"value": r.messages_updated_total / (r.device_ms / 1e3), "unit": UNIT, "iterations": r.iterations,
+                   "device_ms": round(r.device_ms, 3), "ms_per_iteration": round(r.device_ms / max(1, r.iterations), 4),
+                   "refresh": _roofline("k_vertex_update<Init/Delta> (dense touched refresh)", ub, ks["update"]["ms"],
+                                        peak, peak_src, launches=ks["update"]["launches"]),
+                   "select": _roofline("k_rnbp_select (filter + Bernoulli + commit)", sb, ks["select"]["ms"], peak,
+                                       peak_src, launches=ks["select"]["launches"])}
     del g
     torch.cuda.empty_cache()
+    if cpu_head:
+        per_update_s = 1.0 / cpu_head["value"]
+        out["reference"] = {"kind": "extrapolated", "cores": cpu_head["cores"],
+                            "value": cpu_head["value"], "unit": UNIT,
+                            "extrapolated_rnbp_window_s": per_update_s * r.messages_updated_total,
+                            "sample": "not runnable on the host in a bounded sample (~126 GB of host RAM for the "
+                                      "reference's fp64 16384^2 instance): the headline sample's per-update rate "
+                                      "on 1000^2 applied to this window's update count"}
+    out["config"] = f"Ising {BIG_N}^2 C={C_COUPLING} seed 0"
     return out
 
 
 def _partitioned_big(bp, torch, dist, ws, rank, local):
     """Row-band partitioned LBP on the 16384^2 grid: one band per rank, NCCL halo
     exchange + count all-reduce each iteration (paper_1909_11469_b200.parallel).
-    Strong scaling: the grid is fixed.  At N = 1 the same window runs on the
-    whole grid (one band)."""
+    Strong scaling: the grid is fixed."""
     if ws == 1:
         return None
     from paper_1909_11469_b200 import parallel as par
@@ -363,8 +615,6 @@ def _partitioned_big(bp, torch, dist, ws, rank, local):
     ms = e0.elapsed_time(e1)
     upd = st1.messages_updated_total - st0.messages_updated_total
     del band
-    # RnBP on the same bands: a fixed window of the run loop (host polls the
-    # all-reduced sums every iteration; Philox keyed by global edge ids)
     rcfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=BIG_RNBP_ITERS, time_limit=1e9)
     rb = [par.BandRnBP(BIG_N, C_COUPLING, 0, rank, ws, rcfg, local)]
     torch.cuda.synchronize()
@@ -388,12 +638,6 @@ def _partitioned_big(bp, torch, dist, ws, rank, local):
             "scaling": "strong"}
 
 
-def _ttc(results):
-    conv = [r.wall_time for r in results if r.converged]
-    return {"converged_steps": len(conv), "steps": len(results),
-            "median_s": statistics.median(conv) if conv else None}
-
-
 def _read_traffic(key):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -403,85 +647,27 @@ def _read_traffic(key):
         return None
 
 
-def _convergence_suite(bp, device):
-    """BASELINE config 1: Ising 100^2 C=2.5, seeds 500-524, eps 1e-5, cap 10k."""
-    out = {}
-    for name, cfg_kw in (("lbp", dict(kind=bp.SchedulerKind.lbp)),
-                         ("rnbp_low0.5", dict(kind=bp.SchedulerKind.rnbp, low_p=0.5, high_p=1.0)),
-                         ("rnbp_low0.7", dict(kind=bp.SchedulerKind.rnbp, low_p=0.7, high_p=1.0))):
-        conv, times, iters = 0, [], []
-        t0 = time.perf_counter()
-        for s in range(500, 525):
-            g = bp.generate_ising(bp.IsingParams(n=100, c=2.5, seed=s), device=device)
-            kw = dict(cfg_kw)
-            if kw["kind"] == bp.SchedulerKind.rnbp:
-                kw["seed"] = s - 500
-            r = bp.run(g, bp.SchedulerConfig(max_iterations=CAP, time_limit=1e9, **kw))
-            conv += r.converged
-            if r.converged:
-                times.append(r.wall_time)
-                iters.append(r.iterations)
-        out[name] = {"converged": conv, "of": 25, "median_time_s": statistics.median(times) if times else None,
-                     "median_iterations": statistics.median(iters) if iters else None,
-                     "suite_wall_s": round(time.perf_counter() - t0, 3)}
-    return out
-
-
-def _cpu_baseline(sample_iters):
-    """The reference's bpsched::run (oracle/_ref, compiled from /root/reference)
-    on this host, bounded sample of the workload."""
-    from oracle import pyoracle as po
-    try:
-        ref = po.load("ref")
-        kind = "reference"
-    except FileNotFoundError:
-        ref = po.load("orc")
-        kind = "port"
-    cores = os.cpu_count() or 1
-    g = po.Graph.ising(ref, N_GRID, C_COUPLING, 0)
-    cfg = po.make_config("rnbp", low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5,
-                         max_iterations=sample_iters, time_limit=1e9, seed=0, worker_count=cores)
-    r = po.run(g, cfg)
-    return {"value": r.messages_updated_total / r.wall_time, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"RnBP Ising {N_GRID}^2 C={C_COUPLING} seed 0, first {sample_iters} iterations "
-                      f"(EngineState ctor + loop, {r.wall_time:.2f} s, {r.messages_updated_total} updates)",
-            "wall_s": r.wall_time}
-
-
 def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    from oracle import pyoracle as po
-    try:
-        ref = po.load("ref")
-        kind = "reference"
-    except FileNotFoundError:
-        ref = po.load("orc")
-        kind = "port"
-    cores = os.cpu_count() or 1
     K, W = args.steps, args.warmup
-    graphs = [po.Graph.ising(ref, N_GRID, C_COUPLING, s) for s in range(min(K, 2))]
-
-    def cfg(s):
-        return po.make_config("rnbp", low_p=0.5, high_p=1.0, edge_ratio_threshold=0.9, epsilon=1e-5,
-                              max_iterations=REF_SAMPLE_ITERS, time_limit=1e9, seed=s, worker_count=cores)
-    for w in range(W):
-        po.run(graphs[w % len(graphs)], cfg(w))
-    upd, t = 0, 0.0
-    for k in range(K):
-        r = po.run(graphs[k % len(graphs)], cfg(k))
-        upd += r.messages_updated_total
-        t += r.wall_time
-    v = upd / t
+    head = _ref_headline(K, W)
+    v = head["value"]
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
-           "ms_per_step": t / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f64", "data": "synthetic (generate_ising)",
-           "config": {"workload": "ising1000_c2.5_rnbp", "n": N_GRID, "c": C_COUPLING, "scheduler": "rnbp",
-                      "low_p": 0.5, "sample_iterations": REF_SAMPLE_ITERS},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                            "sample": f"first {REF_SAMPLE_ITERS} RnBP iterations per step (incl. EngineState ctor)"},
-           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "ms_per_step": head["seconds"] / K * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (generate_ising)",
+           "config": {"workload": f"ising1000_c2.5_rnbp_window{HEAD_ITERS}", "n": N_GRID, "c": C_COUPLING,
+                      "scheduler": "rnbp", "low_p": 0.5, "high_p": 1.0, "edge_ratio_threshold": 0.9,
+                      "epsilon": 1e-5, "max_iterations": HEAD_ITERS, "seeds": f"0..{K - 1}",
+                      "warmup_seeds": f"0..{W - 1}", "same_config_as_reference_arm": True},
+           "steps_detail": head["steps"],
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": head["cores"], "kind": head["kind"],
+                            "sample": head["sample"]},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "time_to_convergence": {"reference": _ref_suite(),
+                                   "config": "Ising 100^2 C=2.5, seeds 500-524, eps 1e-5, cap 10k; "
+                                             "RnBP seed = s - 500"}}
     print(json.dumps(out))
 
 

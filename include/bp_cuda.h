@@ -109,6 +109,7 @@ typedef struct {
   uint64_t vertex_visits;          /* vertices processed by update kernels                  */
   uint64_t splashes;               /* residual splash: splashes applied (all iterations)    */
   uint64_t splash_rounds;          /* residual splash: parallel claiming rounds             */
+  uint64_t persist_iterations;     /* RnBP: iterations run inside the persistent tail kernel */
 } bp_run_result;
 
 typedef struct {

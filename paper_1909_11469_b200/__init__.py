@@ -95,7 +95,8 @@ class _Result(C.Structure):
                 ("wall_time", C.c_double), ("messages_updated_total", C.c_uint64),
                 ("trace_len", C.c_uint64), ("device_ms", C.c_double),
                 ("message_evaluations", C.c_uint64), ("gpu_launches", C.c_uint64),
-                ("vertex_visits", C.c_uint64), ("splashes", C.c_uint64), ("splash_rounds", C.c_uint64)]
+                ("vertex_visits", C.c_uint64), ("splashes", C.c_uint64), ("splash_rounds", C.c_uint64),
+                ("persist_iterations", C.c_uint64)]
 
 
 class _Info(C.Structure):
@@ -324,6 +325,7 @@ class RunResult:
     kernel_stats: Optional[dict] = None
     splashes: int = 0
     splash_rounds: int = 0
+    persist_iterations: int = 0
 
     def trace_signature(self) -> str:
         """tests/support/test_helpers.hpp:158-166"""
@@ -520,7 +522,8 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
     return RunResult(bool(res.converged), int(res.iterations), float(res.wall_time),
                      int(res.messages_updated_total), bt, trace, float(res.device_ms),
                      int(res.message_evaluations), int(res.gpu_launches), int(res.vertex_visits),
-                     stats.as_dict() if kernel_timing else None, int(res.splashes), int(res.splash_rounds))
+                     stats.as_dict() if kernel_timing else None, int(res.splashes), int(res.splash_rounds),
+                     int(res.persist_iterations))
 
 
 def run(graph: PairwiseMRF, config: SchedulerConfig) -> RunResult:

@@ -192,6 +192,8 @@ class EngineT final : public EngineBase {
     res->vertex_visits = hctl_->vertex_visits;
     res->splashes = hctl_->splashes;
     res->splash_rounds = hctl_->rs_rounds;
+    res->persist_iterations =
+        persist_ && hctl_->handover_it && hctl_->iteration > hctl_->handover_it ? hctl_->iteration - hctl_->handover_it : 0;
     res->gpu_launches = launches_;
     res->wall_time = std::chrono::duration<double>(Clock::now() - t0).count();
   }

@@ -79,9 +79,15 @@ SUITES = {
 }
 
 
+RNBP_REPLICATES = 4  # RnBP is randomized: replicate k uses seed = instance index + 1000 k
+
+
 def suite(ref, workers, name):
     """Converged flags, iterations, reference wall times and (converged runs)
-    the full marginals P(x = 1) per vertex as float32 (for the 1e-4 check)."""
+    the full marginals P(x = 1) per vertex as float32 (for the 1e-4 check).
+    RnBP runs are repeated with RNBP_REPLICATES seeds (the convergence
+    fraction of a randomized scheduler at a cap is a random variable);
+    replicate 0 is the acceptance suite's own seed (acceptance.cpp:50-61)."""
     sp = SUITES[name]
     rows, marg = [], {}
     for s in sp["seeds"]:
@@ -89,14 +95,22 @@ def suite(ref, workers, name):
         row = {"seed": s}
         for run_name, kw in sp["runs"]:
             kind = "lbp" if run_name == "lbp" else "rnbp"
-            extra = dict(high_p=1.0, edge_ratio_threshold=0.9, seed=s - sp["seeds"][0]) if kind == "rnbp" else {}
-            r = po.run(g, po.make_config(kind, max_iterations=sp["cap"], time_limit=1e9, worker_count=workers,
-                                         **kw, **extra), trace_cap=1)
-            row[run_name] = {"converged": r.converged, "iterations": r.iterations, "wall_time": r.wall_time,
-                             "messages_updated_total": r.messages_updated_total, "beliefs_sha": h(r.beliefs)}
-            if r.converged:
-                marg[f"{run_name}_{s}"] = r.beliefs[1::2].astype(np.float32)
-        print(name, s, {k: (v["converged"], v["iterations"]) for k, v in row.items() if k != "seed"}, flush=True)
+            reps = []
+            for k in range(RNBP_REPLICATES if kind == "rnbp" else 1):
+                extra = dict(high_p=1.0, edge_ratio_threshold=0.9, seed=s - sp["seeds"][0] + 1000 * k) \
+                    if kind == "rnbp" else {}
+                r = po.run(g, po.make_config(kind, max_iterations=sp["cap"], time_limit=1e9, worker_count=workers,
+                                             **kw, **extra), trace_cap=1)
+                reps.append({"converged": r.converged, "iterations": r.iterations, "wall_time": r.wall_time,
+                             "messages_updated_total": r.messages_updated_total, "beliefs_sha": h(r.beliefs)})
+                if r.converged and k == 0:
+                    marg[f"{run_name}_{s}"] = r.beliefs[1::2].astype(np.float32)
+            row[run_name] = dict(reps[0])
+            if len(reps) > 1:
+                row[run_name]["replicates"] = [{"converged": x["converged"], "iterations": x["iterations"]}
+                                               for x in reps]
+        print(name, s, {k: [x["iterations"] if x["converged"] else -1 for x in v.get("replicates", [v])]
+                        for k, v in row.items() if k != "seed"}, flush=True)
         rows.append(row)
     return rows, marg
 
@@ -125,7 +139,8 @@ def main():
             marg.update({f"{name}/{k}": v for k, v in m.items()})
         with open(os.path.join(HERE, "reference_suites.json"), "w") as f:
             json.dump({"generated_by": "tests/golden/make_golden.py --suite (the reference, oracle/_ref)",
-                       "rnbp": "high_p 1.0, edge_ratio_threshold 0.9, seed = instance index (acceptance.cpp:50-61)",
+                       "rnbp": "high_p 1.0, edge_ratio_threshold 0.9, seed = instance index (acceptance.cpp:50-61) "
+                               "+ 1000 k for replicate k",
                        "workers": a.workers, "suites": out}, f, indent=1)
         np.savez_compressed(os.path.join(HERE, "reference_suites_marginals.npz"), **marg)
         print("wrote reference_suites.json, reference_suites_marginals.npz")
