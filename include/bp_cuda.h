@@ -120,13 +120,17 @@ typedef struct {
   uint64_t device_bytes;  /* graph bytes resident in HBM */
   int32_t device;
   uint32_t layout;        /* 0 = binary log-odds, 1 = generic log-domain */
+  uint64_t message_values;/* sum over directed edges d of card(target(d)): MessageStore size (messages.cpp:23-39) */
 } bp_graph_info;
 
 /* Per-kernel-class device time, filled when BP_RUN_KERNEL_TIMING is set. */
+#define BP_KERNEL_CLASSES 8
 typedef struct {
-  double ms[8];          /* 0 sweep/refresh, 1 select, 2 radix/top-k, 3 splash, 4 init, 5 beliefs, 6 other */
-  uint64_t launches[8];
-  uint64_t bytes[8];     /* algorithmic bytes moved by the timed launches */
+  /* 0 sweep/refresh, 1 select, 2 radix/top-k, 3 splash, 4 init, 5 beliefs, 6 other,
+   * 7 persistent RnBP list-mode tail */
+  double ms[BP_KERNEL_CLASSES];
+  uint64_t launches[BP_KERNEL_CLASSES];
+  uint64_t bytes[BP_KERNEL_CLASSES]; /* algorithmic bytes moved by the timed launches */
 } bp_kernel_stats;
 
 typedef struct {
@@ -134,6 +138,9 @@ typedef struct {
   uint32_t batch;        /* iterations per device batch (0 = adaptive) */
   bp_kernel_stats* stats;/* optional */
   double* beliefs_device;/* optional: write beliefs (fp64) to this DEVICE pointer instead */
+  double* messages_host; /* optional: the live messages at the end of the run as fp64 probabilities,
+                            message_values doubles in directed-edge order (MessageStore::view,
+                            messages.hpp:24-26; EngineState::messages(), schedulers.hpp:71) */
 } bp_run_opts;
 
 #define BP_RUN_KERNEL_TIMING 1u /* CUDA events around every kernel (adds overhead) */

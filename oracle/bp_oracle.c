@@ -595,6 +595,24 @@ void orc_engine_residuals(const orc_engine* e, double* out) {
   memcpy(out, e->res, sizeof(double) * e->g->D);
 }
 
+/* Load a message state into the engine (test aid, no reference counterpart):
+ * live messages <- msgs (MessageStore layout), then the ResidualTracker is
+ * rebuilt from scratch as in its ctor (residuals.cpp:9-24) -- candidates
+ * f(m), residuals r(m) and the unconverged count of that state, in fp64 with
+ * the reference's arithmetic.  Used to check that a device run's converged
+ * state is a converged state of the reference's update rule. */
+int orc_engine_set_messages(orc_engine* e, const double* msgs) {
+  const uint32_t D = e->g->D;
+  memcpy(e->msg, msgs, sizeof(double) * e->moff[D]);
+  memcpy(e->shadow, e->msg, sizeof(double) * e->moff[D]);
+  for (uint32_t d = 0; d < D; ++d) {
+    e->res[d] = 0.0;
+    e->touched[d] = d;
+  }
+  e->unconverged = 0;
+  return refresh(e, e->touched, D);
+}
+
 int orc_engine_update_message(const orc_engine* e, uint32_t d, double* out) {
   if (d >= e->g->D) return fail(ORC_INVALID_ARGUMENT, "directed edge out of range");
   double* scratch = (double*)malloc(sizeof(double) * (e->g->maxq ? e->g->maxq : 1));

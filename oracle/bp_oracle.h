@@ -126,6 +126,8 @@ int orc_engine_build_splash(const orc_engine* e, uint32_t root, uint32_t h, uint
                             uint32_t* edges, uint64_t* n);
 /* One-off update of message d against the live store (messages.cpp:67-73). */
 int orc_engine_update_message(const orc_engine* e, uint32_t d, double* out);
+/* test aid: load a message state, rebuild candidates / residuals / count (fp64) */
+int orc_engine_set_messages(orc_engine* e, const double* msgs);
 /* select_top_k (schedulers.cpp:105-116) over an arbitrary residual array. */
 void orc_select_top_k(const double* residuals, uint64_t m, uint64_t k, uint32_t* out, uint64_t* n);
 

@@ -109,6 +109,7 @@ class Lib:
         if which == "orc":
             f("generate_potts", C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(_P)])
             f("generate_er", C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(_P)])
+            f("engine_set_messages", C.c_int, [_P, _f64p])
         f("mt_draws", None, [C.c_uint64, C.c_uint64, _u64p, _f64p])
         f("validate_config", C.c_int, [C.POINTER(OrcConfig)])
         f("select_parallelism", C.c_double, [C.c_uint32, C.c_uint32, C.POINTER(OrcConfig)])
@@ -390,6 +391,11 @@ class Engine:
         out = np.zeros(max(n, 1))
         self.lib.check(self.lib.engine_beliefs(self.h, out))
         return out[:n]
+
+    def set_messages(self, msgs):
+        """Load a message state (C restatement only): candidates, residuals and
+        the unconverged count are recomputed from it in fp64."""
+        self.lib.check(self.lib.engine_set_messages(self.h, np.ascontiguousarray(msgs, np.float64)))
 
     def update_message(self, d):
         out = np.zeros(max(int(self.moff[d + 1] - self.moff[d]), 1))

@@ -102,7 +102,7 @@ class _Result(C.Structure):
 class _Info(C.Structure):
     _fields_ = [("num_vertices", C.c_uint32), ("num_edges", C.c_uint32), ("max_cardinality", C.c_uint32),
                 ("state_stride", C.c_uint32), ("device_bytes", C.c_uint64), ("device", C.c_int32),
-                ("layout", C.c_uint32)]
+                ("layout", C.c_uint32), ("message_values", C.c_uint64)]
 
 
 class KernelStats(C.Structure):
@@ -117,7 +117,7 @@ class KernelStats(C.Structure):
 
 class _RunOpts(C.Structure):
     _fields_ = [("flags", C.c_uint32), ("batch", C.c_uint32), ("stats", C.POINTER(KernelStats)),
-                ("beliefs_device", C.c_void_p)]
+                ("beliefs_device", C.c_void_p), ("messages_host", C.c_void_p)]
 
 
 RUN_KERNEL_TIMING = 1
@@ -326,6 +326,7 @@ class RunResult:
     splashes: int = 0
     splash_rounds: int = 0
     persist_iterations: int = 0
+    messages: Optional[np.ndarray] = field(default=None, repr=False)
 
     def trace_signature(self) -> str:
         """tests/support/test_helpers.hpp:158-166"""
@@ -374,7 +375,7 @@ class PairwiseMRF:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # the module may be torn down first at interpreter exit
             _lib.bp_graph_destroy(h)
             self._h = None
 
@@ -503,8 +504,12 @@ def generate_er(n: int, m: int, c: float, seed: int, device: int = -1) -> Pairwi
 # run (schedulers.cpp:293-353)
 
 def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: int = 0, beliefs: bool = True,
-           trace_cap: Optional[int] = None, kernel_timing: bool = False, beliefs_device_ptr: int = 0) -> RunResult:
+           trace_cap: Optional[int] = None, kernel_timing: bool = False, beliefs_device_ptr: int = 0,
+           messages: bool = False) -> RunResult:
+    """bp_run_ex.  messages=True also returns the live messages at the end of
+    the run (RunResult.messages, fp64 probabilities in MessageStore order)."""
     c = config._c()
+    msgs = np.empty(max(int(graph.info.message_values), 1)) if messages else None
     nb = int(graph.belief_offsets[-1])
     bel = np.empty(max(nb, 1)) if beliefs and not beliefs_device_ptr else None  # filled by bp_run_ex
     if trace_cap is None:
@@ -513,7 +518,7 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
     res = _Result()
     stats = KernelStats()
     fl = flags | (RUN_KERNEL_TIMING if kernel_timing else 0) | (0 if beliefs else RUN_NO_BELIEFS)
-    opts = _RunOpts(fl, batch, C.pointer(stats), beliefs_device_ptr or None)
+    opts = _RunOpts(fl, batch, C.pointer(stats), beliefs_device_ptr or None, _ptr(msgs))
     _check(_lib.bp_run_ex(graph._h, C.byref(c), C.byref(opts), C.byref(res), _ptr(bel), C.cast(tr, C.c_void_p),
                           trace_cap))
     n = min(int(res.trace_len), trace_cap)
@@ -523,7 +528,8 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
                      int(res.messages_updated_total), bt, trace, float(res.device_ms),
                      int(res.message_evaluations), int(res.gpu_launches), int(res.vertex_visits),
                      stats.as_dict() if kernel_timing else None, int(res.splashes), int(res.splash_rounds),
-                     int(res.persist_iterations))
+                     int(res.persist_iterations),
+                     msgs[: int(graph.info.message_values)] if msgs is not None else None)
 
 
 def run(graph: PairwiseMRF, config: SchedulerConfig) -> RunResult:
@@ -572,7 +578,7 @@ class EngineState:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.bp_engine_destroy(h)
             self._h = None
 

@@ -208,7 +208,7 @@ struct Ctl {
   unsigned long long pacc3[3][6];
   unsigned long long handover_it;  // iteration at which the graph loop handed over to the persistent kernel
   unsigned int time_stop;
-  unsigned int pad4_;
+  unsigned int blocks_done;  // last-block-done counter of the kernel-fused finalize / retry (reset by the last block)
   unsigned long long persist_bytes;  // algorithmic bytes moved by the persistent kernel
   unsigned long long vote_limit_ns;  // row-band partition: time limit, decided by an all-reduced vote
   unsigned long long phase_ns[8];    // persistent kernel phase clock (CTA 0)

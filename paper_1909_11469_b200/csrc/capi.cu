@@ -130,6 +130,14 @@ int bp_graph_info_get(const bp_graph* g, bp_graph_info* info) {
   info->device_bytes = G.device_bytes();
   info->device = G.device;
   info->layout = G.binary ? 0u : 1u;
+  if (G.binary) {
+    info->message_values = 4ull * G.E;
+  } else {
+    uint64_t n = 0;
+    const auto& ep = G.host_ep();
+    for (uint64_t d = 0; d < 2ull * G.E; ++d) n += G.card_of(ep[d ^ 1ull]);
+    info->message_values = n;
+  }
   return BP_OK;
 }
 

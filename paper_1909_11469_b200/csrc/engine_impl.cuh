@@ -163,6 +163,8 @@ class EngineT final : public EngineBase {
     drain_trace(trace, trace_cap, copied);
     if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
 
+    if (opts && opts->messages_host)  // LBP reports m_t, which lives in buf[t & 1]
+      read_messages(opts->messages_host, cfg_.kind == BP_LBP && (hctl_->iteration & 1ull));
     const size_t nb = g_.unary_size();
     if (!(flags & BP_RUN_NO_BELIEFS) && (beliefs_host || (opts && opts->beliefs_device))) {
       double* dst = opts && opts->beliefs_device ? opts->beliefs_device : nullptr;
@@ -213,14 +215,19 @@ class EngineT final : public EngineBase {
     return hctl_->iteration;
   }
   void messages(double* out, bool candidates) override {
-    std::vector<float> raw(static_cast<size_t>(g_.D) * QS);
-    // band engines ping-pong like run()'s LBP: m_t lives in buf[t & 1]
+    // fused LBP sweeps (lockstep, bands) ping-pong like run()'s LBP: m_t lives in buf[t & 1]
     bool flip = false;
     if (pingpong_ && cfg_.kind == BP_LBP) {
       fetch_ctl_header();
       flip = (hctl_->iteration & 1ull) != 0;
     }
-    const DevBuf& src = (candidates != flip) ? bufB_ : bufA_;
+    read_messages(out, candidates != flip);
+  }
+  // the messages of one buffer (A = live, B = candidates / the other ping-pong
+  // buffer) as fp64 probabilities in MessageStore order
+  void read_messages(double* out, bool buf_b) {
+    std::vector<float> raw(static_cast<size_t>(g_.D) * QS);
+    const DevBuf& src = buf_b ? bufB_ : bufA_;
     if (!raw.empty()) cuda_check(cudaMemcpyAsync(raw.data(), src.p, raw.size() * 4, cudaMemcpyDeviceToHost, s_), "d2h");
     sync();
     const auto& ep = g_.host_ep();
@@ -275,10 +282,7 @@ class EngineT final : public EngineBase {
     q.commit = 0;
     k_rnbp_select<QS, false><<<grid_cap(g_.D / 4 + 1), kBlock, 0, s_>>>(
         dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), sel_.as<uint8_t>(),
-        ctl(), eps_, q, cand_list());
-    k_rnbp_retry<QS, false><<<1, 1024, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
-                                                vlist_.as<uint32_t>(), sel_.as<uint8_t>(), ctl(), eps_, q,
-                                                cand_list());
+        ctl(), eps_, q, cand_list(), 1);
     launch_check();
     collect_sel(out);
   }
@@ -381,8 +385,7 @@ class EngineT final : public EngineBase {
       launch_check();
       pingpong_ = true;
     }
-    enqueue_lbp_sweep();
-    enqueue_finalize(kFinLbp);
+    enqueue_lbp_sweep(kFinLbp);
     sync();
     fetch_ctl_header();
     if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
@@ -551,14 +554,18 @@ class EngineT final : public EngineBase {
   static constexpr uint64_t kLbpTmaMinVertices = uint64_t{1} << 21;  // TMA = tiles at 1000^2, 7% faster at 2048^2, 22% at 8192^2
   uint32_t lbp_force_ = 0;   // BP_RUN_LBP_TMA / BP_RUN_LBP_TILES of the current call
   uint32_t lbp_kernel_ = 0;  // BP_LBP_KERNEL_* of the last sweep
-  void enqueue_lbp_sweep() {
-    // TMA-staged rows pay off once the grid is far beyond L2; below that the
-    // register-tiled lattice kernel (k_vertex_update) is faster.  The per-call
-    // flags BP_RUN_LBP_TMA / BP_RUN_LBP_TILES override the size rule.
+  // TMA-staged rows pay off once the grid is far beyond L2; below that the
+  // register-tiled lattice kernel (k_vertex_update) is faster.  The per-call
+  // flags BP_RUN_LBP_TMA / BP_RUN_LBP_TILES override the size rule.
+  bool lbp_uses_tma() const {
     const bool tma_ok = QS == 1 && g_.lat_cols && g_.par_mode == 1 && g_.lat_rows >= 2;
     const bool big = static_cast<uint64_t>(g_.V) >= kLbpTmaMinVertices;
-    const bool use_tma = tma_ok && ((lbp_force_ & BP_RUN_LBP_TMA) || (!(lbp_force_ & BP_RUN_LBP_TILES) && big));
-    if (use_tma) {
+    return tma_ok && ((lbp_force_ & BP_RUN_LBP_TMA) || (!(lbp_force_ & BP_RUN_LBP_TILES) && big));
+  }
+  // fin: the loop control fused into the sweep's last block (kFinNone: none)
+  void enqueue_lbp_sweep(int fin) {
+    const FinArgs fa{fin, g_.D};
+    if (lbp_uses_tma()) {
       lbp_kernel_ = BP_LBP_KERNEL_TMA;
       if (!lbp_grid_) {
         cuda_check(cudaFuncSetAttribute(k_lbp_lattice, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -572,12 +579,15 @@ class EngineT final : public EngineBase {
       timed(kKUpdate, [&] {
         k_lbp_lattice<<<lbp_grid_, kBlock, sizeof(LbpSmem), s_>>>(dg_, live(), cand(), ctl(), eps_);
       });
+      // separate finalize: the fused one's static shared memory would cost the
+      // TMA sweep its third resident block per SM (2.66 -> 3.10 ms at 16384^2)
+      if (fin != kFinNone) enqueue_finalize(fin);
     } else {
       lbp_kernel_ = (QS == 1 && g_.lat_cols && g_.par_mode) ? BP_LBP_KERNEL_TILES : BP_LBP_KERNEL_VERTEX;
       timed(kKUpdate, [&] {
         k_vertex_update<QS, kModeCount, false, true, false>
             <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(
-                dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list());
+                dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list(), fa);
       });
     }
     launch_check();
@@ -612,7 +622,7 @@ class EngineT final : public EngineBase {
       band_start_common();
       pingpong_ = true;
     }
-    enqueue_lbp_sweep();
+    enqueue_lbp_sweep(kFinNone);
     const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
     k_part_pack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
     k_part_count<<<1, kSlots, 0, s_>>>(ctl(), halo_);
@@ -643,7 +653,7 @@ class EngineT final : public EngineBase {
     band_start_common();
     k_vertex_update<QS, kModeInit, false, false, false>
         <<<vgrid(k_vertex_update<QS, kModeInit, false, false, false>, g_.V), kBlock, 0, s_>>>(
-            dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
+            dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list(), FinArgs{kFinNone, 0});
     k_part_count_rnbp<<<1, kSlots, 0, s_>>>(ctl(), halo_);
     launch_check();
     launches_ += 2;
@@ -654,7 +664,7 @@ class EngineT final : public EngineBase {
     q.attempt = attempt;
     k_rnbp_select<QS, false><<<grid_cap(g_.D / 4 + 1), kBlock, 0, s_>>>(
         dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), nullptr, ctl(), eps_, q,
-        cand_list());
+        cand_list(), 0);
     k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
     launch_check();
     launches_ += 2;
@@ -685,7 +695,7 @@ class EngineT final : public EngineBase {
     k_vertex_update<QS, kModeDelta, true, false, false>
         <<<vgrid(k_vertex_update<QS, kModeDelta, true, false, false>, g_.V), kBlock, 0, s_>>>(
             dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
-            cand_list());
+            cand_list(), FinArgs{kFinNone, 0});
     k_part_count_rnbp<<<1, kSlots, 0, s_>>>(ctl(), halo_);
     launch_check();
     launches_ += 3;
@@ -739,35 +749,35 @@ class EngineT final : public EngineBase {
     timed(kKInit, [&] { k_init_messages<QS><<<gi, kBlock, 0, s_>>>(dg_, live(), ctl(), 1); });
     launch_check();
     if (lbp) {  // sweep 0 (ResidualTracker ctor, residuals.cpp:9-24)
-      enqueue_lbp_sweep();
-      enqueue_finalize(kFinLbp);
+      enqueue_lbp_sweep(kFinLbp);
     } else {
+      const FinArgs fa{kFinInit, g_.D};
       timed(kKUpdate, [&] {
         if (use_clist_)
           k_vertex_update<QS, kModeInit, false, false, true><<<vgrid(k_vertex_update<QS, kModeInit, false, false, true>, g_.V), kBlock, 0, s_>>>(
-              dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
+              dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list(), fa);
         else
           k_vertex_update<QS, kModeInit, false, false, false><<<vgrid(k_vertex_update<QS, kModeInit, false, false, false>, g_.V), kBlock, 0, s_>>>(
-              dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list());
+              dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, cand_list(), fa);
       });
       launch_check();
-      enqueue_finalize(kFinInit);
     }
   }
 
+  // touched refresh; the iteration's loop control (fin) runs in its last block
   void enqueue_refresh(int fin) {
+    const FinArgs fa{fin, g_.D};
     timed(kKUpdate, [&] {
       if (use_clist_)
         k_vertex_update<QS, kModeDelta, true, false, true><<<vgrid(k_vertex_update<QS, kModeDelta, true, false, true>, g_.V), kBlock, 0, s_>>>(
             dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
-            cand_list());
+            cand_list(), fa);
       else
         k_vertex_update<QS, kModeDelta, true, false, false><<<vgrid(k_vertex_update<QS, kModeDelta, true, false, false>, g_.V), kBlock, 0, s_>>>(
             dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
-            cand_list());
+            cand_list(), fa);
     });
     launch_check();
-    enqueue_finalize(fin);
   }
 
   void ensure_rbp_scratch() {
@@ -824,19 +834,22 @@ class EngineT final : public EngineBase {
   void enqueue_iteration() {
     switch (cfg_.kind) {
       case BP_LBP:
-        enqueue_lbp_sweep();
-        enqueue_finalize(kFinLbp);
+        enqueue_lbp_sweep(kFinLbp);
         break;
       case BP_RNBP: {
+        // select + commit; its last block runs the retry / fallback
+        // select + commit, then the retry / fallback as its own one-block
+        // launch (a last-block-done retry in the select measured 5% slower:
+        // ~1000 blocks serialise on the done counter)
         timed(kKSelect, [&] {
           if (use_clist_)
             k_rnbp_select<QS, true><<<grid_cap(g_.D), kBlock, 0, s_>>>(
                 dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), nullptr, ctl(),
-                eps_, prm_, cand_list());
+                eps_, prm_, cand_list(), 0);
           else
             k_rnbp_select<QS, false><<<grid_cap(g_.D / 4 + 1), kBlock, 0, s_>>>(
                 dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), nullptr, ctl(),
-                eps_, prm_, cand_list());
+                eps_, prm_, cand_list(), 0);
         });
         timed(kKSelect, [&] {
           if (use_clist_)

@@ -199,57 +199,142 @@ __device__ __forceinline__ void fin_record(Ctl* c, unsigned long long it, unsign
   c->trace_len = it + 1;
 }
 
+// The loop-control fields of Ctl the finalize touches, loaded into registers
+// as one batch of independent loads and stored back as one batch: the
+// finalize is the serial tail of every iteration, and a chain of dependent
+// control-block round trips would cost microseconds.
+struct FinRegs {
+  unsigned done, converged, numeric_error, has_prev, unconverged, prev_unconverged, nflag, dense;
+  unsigned stamp, stop_reason, cl_cur, use_clist, cl_state, persist_ok, rx_prefix;
+  unsigned cl_n[2];
+  unsigned long long iteration, sweeps, max_iterations, msgs_total, evals_total, vertex_visits, t0_ns,
+      time_limit_ns, frontier, survivors, rx_above, trace_len, cond_handle, handover_it;
+
+  __device__ __forceinline__ void load(const Ctl* c) {
+    done = c->done;
+    converged = c->converged;
+    numeric_error = c->numeric_error;
+    has_prev = c->has_prev;
+    unconverged = c->unconverged;
+    prev_unconverged = c->prev_unconverged;
+    nflag = c->nflag;
+    dense = c->dense;
+    stamp = c->stamp;
+    stop_reason = c->stop_reason;
+    cl_cur = c->cl_cur;
+    use_clist = c->use_clist;
+    cl_state = c->cl_state;
+    persist_ok = c->persist_ok;
+    rx_prefix = c->rx_prefix;
+    cl_n[0] = c->cl_n[0];
+    cl_n[1] = c->cl_n[1];
+    iteration = c->iteration;
+    sweeps = c->sweeps;
+    max_iterations = c->max_iterations;
+    msgs_total = c->msgs_total;
+    evals_total = c->evals_total;
+    vertex_visits = c->vertex_visits;
+    t0_ns = c->t0_ns;
+    time_limit_ns = c->time_limit_ns;
+    frontier = c->frontier;
+    survivors = c->survivors;
+    rx_above = c->rx_above;
+    trace_len = c->trace_len;
+    cond_handle = c->cond_handle;
+    handover_it = c->handover_it;
+  }
+  // numeric_error is never stored back: any thread may raise it concurrently
+  __device__ __forceinline__ void store(Ctl* c) const {
+    c->done = done;
+    c->converged = converged;
+    c->has_prev = has_prev;
+    c->unconverged = unconverged;
+    c->prev_unconverged = prev_unconverged;
+    c->nflag = nflag;
+    c->dense = dense;
+    c->stamp = stamp;
+    c->stop_reason = stop_reason;
+    c->cl_cur = cl_cur;
+    c->cl_state = cl_state;
+    c->rx_prefix = rx_prefix;
+    c->cl_n[0] = cl_n[0];
+    c->cl_n[1] = cl_n[1];
+    c->iteration = iteration;
+    c->sweeps = sweeps;
+    c->msgs_total = msgs_total;
+    c->evals_total = evals_total;
+    c->vertex_visits = vertex_visits;
+    c->time_limit_ns = time_limit_ns;
+    c->frontier = frontier;
+    c->survivors = survivors;
+    c->rx_above = rx_above;
+    c->trace_len = trace_len;
+    c->handover_it = handover_it;
+  }
+};
+
+__device__ __forceinline__ void fin_record(FinRegs& f, TraceRec* trace, unsigned long long it, unsigned long long fs,
+                                           unsigned un) {
+  TraceRec& r = trace[it % kTraceRing];
+  r.iteration = it;
+  r.frontier_size = fs;
+  r.unconverged = un;
+  r.elapsed_seconds = 1e-9 * static_cast<double>(globaltimer_ns() - f.t0_ns);
+  f.trace_len = it + 1;
+}
+
 // top of the loop: converged check BEFORE the cap check (schedulers.cpp:302-309)
-__device__ __forceinline__ void fin_check_top(Ctl* c) {
-  if (c->numeric_error) {
-    c->done = 1;
-    c->stop_reason = kStopNumeric;
+__device__ __forceinline__ void fin_check_top(FinRegs& c) {
+  if (c.numeric_error) {
+    c.done = 1;
+    c.stop_reason = kStopNumeric;
     return;
   }
-  if (c->unconverged == 0) {
-    c->converged = 1;
-    c->done = 1;
-    c->stop_reason = kStopConverged;
+  if (c.unconverged == 0) {
+    c.converged = 1;
+    c.done = 1;
+    c.stop_reason = kStopConverged;
     return;
   }
-  if (c->iteration >= c->max_iterations) {
-    c->done = 1;
-    c->stop_reason = kStopMaxIter;
-  } else if (globaltimer_ns() - c->t0_ns >= c->time_limit_ns) {
-    c->done = 1;
-    c->stop_reason = kStopTime;
+  if (c.iteration >= c.max_iterations) {
+    c.done = 1;
+    c.stop_reason = kStopMaxIter;
+  } else if (globaltimer_ns() - c.t0_ns >= c.time_limit_ns) {
+    c.done = 1;
+    c.stop_reason = kStopTime;
   }
 }
 
-__device__ __forceinline__ void fin_reset_scratch(Ctl* c) {
-  c->frontier = 0;
-  c->survivors = 0;
-  c->nflag = 0;
-  c->dense = 0;
-  c->stamp += 1;
-  c->rx_prefix = 0;
-  c->rx_above = 0;
+__device__ __forceinline__ void fin_reset_scratch(FinRegs& c) {
+  c.frontier = 0;
+  c.survivors = 0;
+  c.nflag = 0;
+  c.dense = 0;
+  c.stamp += 1;
+  c.rx_prefix = 0;
+  c.rx_above = 0;
 }
 
 // end of one iteration of the run loop (schedulers.cpp:326-346)
-__device__ __forceinline__ void fin_iter(Ctl* c, long long delta, unsigned long long frontier, uint32_t D) {
-  const unsigned start = c->unconverged;
-  c->unconverged = static_cast<unsigned>(static_cast<long long>(start) + delta);
-  fin_record(c, c->iteration, frontier, c->unconverged);
-  c->msgs_total += frontier;
-  c->prev_unconverged = start;  // set_prev_unconverged (schedulers.cpp:327)
-  c->has_prev = 1;
-  c->iteration += 1;
-  if (c->use_clist) {
+__device__ __forceinline__ void fin_iter(FinRegs& c, TraceRec* trace, long long delta, unsigned long long frontier,
+                                         uint32_t D) {
+  const unsigned start = c.unconverged;
+  c.unconverged = static_cast<unsigned>(static_cast<long long>(start) + delta);
+  fin_record(c, trace, c.iteration, frontier, c.unconverged);
+  c.msgs_total += frontier;
+  c.prev_unconverged = start;  // set_prev_unconverged (schedulers.cpp:327)
+  c.has_prev = 1;
+  c.iteration += 1;
+  if (c.use_clist) {
     // RnBP candidate list: scan residuals while most edges are unconverged;
     // once fewer than 1/16 are, the next select builds the list (state 1) and
     // from then on iterations walk it (state 2)
-    if (c->cl_state >= 1u) {
-      c->cl_cur ^= 1u;
-      c->cl_n[c->cl_cur ^ 1u] = 0;
-      c->cl_state = 2u;
-    } else if (16ull * c->unconverged < D) {
-      c->cl_state = 1u;
+    if (c.cl_state >= 1u) {
+      c.cl_cur ^= 1u;
+      c.cl_n[c.cl_cur ^ 1u] = 0;
+      c.cl_state = 2u;
+    } else if (16ull * c.unconverged < D) {
+      c.cl_state = 1u;
     }
   }
   fin_reset_scratch(c);
@@ -372,13 +457,17 @@ static __global__ void __launch_bounds__(kSlots) k_part_count_rnbp(Ctl* c, PartH
 // ext (row-band partition): {global unconverged count, time-limit votes},
 // all-reduced over the ranks, replaces the local count and the local clock so
 // every rank takes the same stop decision.
-static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D,
-                                                          const unsigned long long* ext = nullptr) {
+// finalize_block: the same by one whole block of any size >= kSlots (a
+// multiple of 32), inside the persistent loop kernels.
+__device__ __forceinline__ void finalize_block(Ctl* c, int mode, uint32_t D, const unsigned long long* ext = nullptr) {
   if (run_done(c)) return;
   const int t = threadIdx.x;
-  const Accum a = c->acc[t];
-  c->acc[t] = Accum{};
-  __shared__ unsigned long long sh[6][kSlots / 32];
+  // thread 0's control-block loads are issued with the slot loads
+  FinRegs f;
+  if (t == 0) f.load(c);
+  const Accum a = t < kSlots ? c->acc[t] : Accum{};
+  if (t < kSlots) c->acc[t] = Accum{};
+  __shared__ unsigned long long sh[6][32];
   unsigned long long v[6] = {static_cast<unsigned long long>(a.delta), a.count, a.frontier, a.survivors,
                              a.evals, a.visits};
 #pragma unroll
@@ -390,53 +479,86 @@ static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, ui
   if (t != 0) return;
   for (int k = 0; k < 6; ++k) {
     v[k] = 0;
-    for (int w = 0; w < kSlots / 32; ++w) v[k] += sh[k][w];
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) v[k] += sh[k][w];
   }
   const bool rnbp_ext = mode == kFinInitExt || mode == kFinIterExt;
   const long long delta = static_cast<long long>(rnbp_ext ? ext[0] : v[0]);
   const unsigned long long count = ext ? (rnbp_ext ? ext[4] : ext[0]) : v[1];
-  const unsigned long long frontier = rnbp_ext ? ext[1] : v[2] + c->frontier;
-  if (ext && ext[rnbp_ext ? 3 : 1]) c->time_limit_ns = 0;  // some rank hit the time limit: stop everywhere
-  c->evals_total += v[4];
-  c->vertex_visits += v[5];
+  const unsigned long long frontier = rnbp_ext ? ext[1] : v[2] + f.frontier;
+  if (ext && ext[rnbp_ext ? 3 : 1]) f.time_limit_ns = 0;  // some rank hit the time limit: stop everywhere
+  f.evals_total += v[4];
+  f.vertex_visits += v[5];
   switch (mode) {
     case kFinLbp: {  // sweep s computed r(m_s): it closes iteration s-1
-      const unsigned long long s = c->sweeps;
+      const unsigned long long s = f.sweeps;
       if (s > 0) {
-        fin_record(c, s - 1, D, static_cast<unsigned>(count));
-        c->msgs_total += D;
+        fin_record(f, c->trace, s - 1, D, static_cast<unsigned>(count));
+        f.msgs_total += D;
       }
-      c->iteration = s;
-      c->unconverged = static_cast<unsigned>(count);
-      c->sweeps = s + 1;
-      fin_reset_scratch(c);
-      fin_check_top(c);
+      f.iteration = s;
+      f.unconverged = static_cast<unsigned>(count);
+      f.sweeps = s + 1;
+      fin_reset_scratch(f);
+      fin_check_top(f);
       break;
     }
     case kFinInit:
     case kFinInitExt:
-      c->unconverged = static_cast<unsigned>(count);
-      c->iteration = 0;
-      if (c->use_clist && 16ull * c->unconverged < D) c->cl_state = 1u;
-      fin_reset_scratch(c);
-      fin_check_top(c);
+      f.unconverged = static_cast<unsigned>(count);
+      f.iteration = 0;
+      if (f.use_clist && 16ull * f.unconverged < D) f.cl_state = 1u;
+      fin_reset_scratch(f);
+      fin_check_top(f);
       break;
     case kFinIter:
     case kFinIterExt:
-      fin_iter(c, delta, frontier, D);
+      fin_iter(f, c->trace, delta, frontier, D);
       break;
     case kFinApply:
-      c->unconverged = static_cast<unsigned>(static_cast<long long>(c->unconverged) + delta);
-      fin_reset_scratch(c);
+      f.unconverged = static_cast<unsigned>(static_cast<long long>(f.unconverged) + delta);
+      fin_reset_scratch(f);
       break;
     default:
       break;
   }
   // the graph loop also hands RnBP list mode over to the persistent kernel
-  const bool handover = c->persist_ok && c->cl_state == 2u;
-  if (handover && !c->handover_it) c->handover_it = c->iteration;
-  if (c->cond_handle && mode != kFinApply)
-    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(c->cond_handle), c->done || handover ? 0u : 1u);
+  const bool handover = f.persist_ok && f.cl_state == 2u;
+  if (handover && !f.handover_it) f.handover_it = f.iteration;
+  f.store(c);
+  if (f.cond_handle && mode != kFinApply)
+    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(f.cond_handle), f.done || handover ? 0u : 1u);
+}
+
+static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D,
+                                                          const unsigned long long* ext = nullptr) {
+  finalize_block(c, mode, D, ext);
+}
+
+// Kernel-fused loop control: the LAST block of a launch to finish runs the
+// finalize (or the RnBP retry) itself, so an iteration needs no extra
+// one-block launch.  threadFenceReduction pattern: the warp that issued the
+// block's slot atomics fences them before the block counts itself done, and
+// the block that takes the last count fences again before reading the slots.
+__device__ __forceinline__ bool last_block_done(Ctl* c) {
+  __shared__ unsigned s_last;
+  // the slot atomics of block_accumulate are issued by warp 0
+  if (threadIdx.x < 32) __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&c->blocks_done, 1u) == gridDim.x - 1u ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  if (threadIdx.x == 0) c->blocks_done = 0u;  // for the next launch (stream-ordered)
+  return true;
+}
+
+struct FinArgs {
+  int mode;    // kFinNone: no fused finalize
+  uint32_t D;  // directed edges counted by the finalize
+};
+
+__device__ __forceinline__ void fused_finalize(Ctl* c, const FinArgs& f) {
+  if (f.mode != kFinNone && last_block_done(c)) finalize_block(c, f.mode, f.D);
 }
 
 // ---------------------------------------------------------------------------
@@ -721,7 +843,7 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
 constexpr int kLatVPT = 1;  // measured at 1000^2: 4 -> 2 -> 1 vertices per thread, 23.0 -> 22.5 -> 22.4 us per LBP iteration
 constexpr uint32_t kLatTile = kBlock * kLatVPT;
 
-template <int MODE, bool CL, int VPT = kLatVPT>
+template <int MODE, bool CL, int VPT = kLatVPT, bool NC = true>
 __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const float* __restrict__ A,
                                                      float* __restrict__ B, float* __restrict__ res,
                                                      const uint32_t* __restrict__ vflag, uint32_t stamp,
@@ -769,22 +891,22 @@ __device__ __forceinline__ void lattice_binary_tiles(const DevGraph& g, const fl
       const uint32_t dn = c + 1u < C ? 1u : 0u;
       if (!first) {
         const uint32_t e = prow + 2u * c + dn;
-        pU[k] = __ldg(&A2[e]);
+        pU[k] = ldm<NC>(&A2[e]);
         aU[k] = __ldg(&ea[e]);
       }
       if (c > 0u) {
         const uint32_t e = last ? row + c - 1u : row + 2u * c - 2u;
-        pL[k] = __ldg(&A2[e]);
+        pL[k] = ldm<NC>(&A2[e]);
         aL[k] = __ldg(&ea[e]);
       }
       if (dn) {
         const uint32_t e = last ? row + c : row + 2u * c;
-        pR[k] = __ldg(&A2[e]);
+        pR[k] = ldm<NC>(&A2[e]);
         aR[k] = __ldg(&ea[e]);
       }
       if (!last) {
         const uint32_t e = row + 2u * c + dn;
-        pD[k] = __ldg(&A2[e]);
+        pD[k] = ldm<NC>(&A2[e]);
         aD[k] = __ldg(&ea[e]);
       }
       un[k] = __ldg(&g.unary_lo[r * C + c]);
@@ -888,12 +1010,14 @@ struct CandList {
   uint8_t* inlist;
 };
 
-template <int QS, int MODE, bool LIST, bool PINGPONG, bool CL>
-__global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const float* A0, float* B0,
-                                                          float* res, const uint32_t* vlist,
-                                                          const uint32_t* vflag, Ctl* ctl, float eps,
-                                                          CandList cand_list) {
-  if (run_done(ctl)) return;
+// One pass of the vertex update over the grid (every block of the launch
+// calls it): the body of k_vertex_update, also run inside the persistent loop
+// kernels (NC = false: messages change inside the launch, so they are read
+// with coherent loads).
+template <int QS, int MODE, bool LIST, bool PINGPONG, bool CL, bool NC = true>
+__device__ __forceinline__ void vertex_update_pass(const DevGraph& g, const float* A0, float* B0, float* res,
+                                                   const uint32_t* vlist, const uint32_t* vflag, Ctl* ctl,
+                                                   float eps, const CandList& cand_list) {
   const float* A = A0;
   float* B = B0;
   if (PINGPONG) {
@@ -917,8 +1041,8 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
   if (lattice)
     // one vertex per thread: more warps in flight (the delta-mode refresh
     // measured 63 -> 56 us per early RnBP iteration going from 2 to 1)
-    lattice_binary_tiles<MODE, CL, kLatVPT>(g, A, B, res, vflag, stamp, LIST, eps, &ctl->numeric_error, cnt, evals, visits,
-                                   cand_list.inlist, &cl, cl_on);
+    lattice_binary_tiles<MODE, CL, kLatVPT, NC>(g, A, B, res, vflag, stamp, LIST, eps, &ctl->numeric_error, cnt, evals,
+                                               visits, cand_list.inlist, &cl, cl_on);
   for (uint32_t base = lattice ? n : blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint32_t i = base + threadIdx.x;
     if (i < n) {
@@ -935,8 +1059,8 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
         go = row >= g.cnt_row0 && row < g.cnt_row1;
       }
       if (go) {
-        cnt += vertex_update<QS, MODE, CL>(g, v, A, B, res, eps, &ctl->numeric_error, evals, cand_list.inlist, &cl,
-                                           cl_on);
+        cnt += vertex_update<QS, MODE, CL, NC>(g, v, A, B, res, eps, &ctl->numeric_error, evals, cand_list.inlist,
+                                               &cl, cl_on);
         ++visits;
       }
     }
@@ -951,6 +1075,17 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
   c.evals = evals;
   c.visits = visits;
   block_accumulate(ctl, c);
+}
+
+// fin: the loop control of the iteration, run by the last block (FinArgs)
+template <int QS, int MODE, bool LIST, bool PINGPONG, bool CL>
+__global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const float* A0, float* B0,
+                                                          float* res, const uint32_t* vlist,
+                                                          const uint32_t* vflag, Ctl* ctl, float eps,
+                                                          CandList cand_list, FinArgs fin) {
+  if (run_done(ctl)) return;
+  vertex_update_pass<QS, MODE, LIST, PINGPONG, CL>(g, A0, B0, res, vlist, vflag, ctl, eps, cand_list);
+  fused_finalize(ctl, fin);
 }
 
 // ---------------------------------------------------------------------------
@@ -1030,11 +1165,9 @@ struct RnbpParams {
 // iteration follows the unconverged count instead of 2|E|.  The Bernoulli draw
 // is keyed by the edge id, so list order does not matter.
 template <int QS, bool CL>
-__global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live, const float* cand,
-                                                        float* res, uint32_t* vflag, uint32_t* vlist,
-                                                        uint8_t* sel, Ctl* ctl, float eps,
-                                                        RnbpParams prm, CandList cl) {
-  if (run_done(ctl)) return;
+__device__ __forceinline__ void rnbp_select_pass(const DevGraph& g, float* live, const float* cand, float* res,
+                                                 uint32_t* vflag, uint32_t* vlist, uint8_t* sel, Ctl* ctl,
+                                                 float eps, const RnbpParams& prm, const CandList& cl) {
   const double p = prm.fixed_p >= 0.0 ? prm.fixed_p : device_p_now(ctl, prm.low_p, prm.high_p, prm.thr);
   const unsigned long long thresh = static_cast<unsigned long long>(ceil(ldexp(p, 53)));
   const unsigned long long it = ctl->iteration;
@@ -1072,14 +1205,19 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
         }
         // binary: the four commits' operands (candidates, targets) in two
         // 16-byte loads, one round trip instead of one per commit
-        float4 cv4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 cv4 = make_float4(0.f, 0.f, 0.f, 0.f), lv4 = cv4;
         uint4 ep4 = make_uint4(0u, 0u, 0u, 0u);
-        if (QS == 1 && prm.commit && 4 * q + 3 < g.D &&
-            (rr[0] >= eps || rr[1] >= eps || rr[2] >= eps || rr[3] >= eps)) {
+        const bool quad = QS == 1 && prm.commit && 4 * q + 3 < g.D &&
+                          (rr[0] >= eps || rr[1] >= eps || rr[2] >= eps || rr[3] >= eps);
+        if (quad) {
           cv4 = reinterpret_cast<const float4*>(cand)[q];
+          lv4 = reinterpret_cast<const float4*>(live)[q];
           ep4 = __ldg(reinterpret_cast<const uint4*>(g.ep) + q);
         }
-        const float cvs[4] = {cv4.x, cv4.y, cv4.z, cv4.w};
+        float cvs[4] = {cv4.x, cv4.y, cv4.z, cv4.w};
+        float lvs[4] = {lv4.x, lv4.y, lv4.z, lv4.w};
+        float rvs[4] = {rr[0], rr[1], rr[2], rr[3]};
+        bool any = false;
         const uint32_t tgs[4] = {ep4.y, ep4.x, ep4.w, ep4.z};  // target of d = ep[d ^ 1]
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -1087,11 +1225,12 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
           if (rr[k] >= eps) {  // padding entries are 0
             c.survivors += 1;
             if (!draw || u53_of(ph[k >> 1], d) < thresh) {
-              if (QS == 1 && prm.commit && 4 * q + 3 < g.D) {  // commit_edge with the prefetched operands
+              if (quad) {  // commit_edge with the prefetched operands; the quad is stored whole below
                 c.delta -= 1;
                 c.frontier += 1;
-                res[d] = 0.f;
-                live[d] = cvs[k];
+                rvs[k] = 0.f;
+                lvs[k] = cvs[k];
+                any = true;
                 tg[k] = tgs[k];
                 if (dense) {
                   vflag[tg[k]] = stamp;
@@ -1109,6 +1248,10 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
               kp[k] = true;
             }
           }
+        }
+        if (any) {  // one 16-byte store per array instead of one 4-byte store per commit
+          reinterpret_cast<float4*>(live)[q] = make_float4(lvs[0], lvs[1], lvs[2], lvs[3]);
+          reinterpret_cast<float4*>(res)[q] = make_float4(rvs[0], rvs[1], rvs[2], rvs[3]);
         }
       }
       if (prm.commit && !dense) {
@@ -1157,6 +1300,7 @@ __global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live,
   if (prm.commit && !dense) fl.flush(0);
   block_accumulate(ctl, c);
 }
+
 
 // Retry + fallback of rnbp_frontier (schedulers.cpp:204-214), single block:
 // reduces the attempt-0 frontier and survivor counts; when the frontier came
@@ -1282,12 +1426,12 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
   }
 }
 
+// the retry decision + retry of one iteration, by ONE block (any size, a
+// multiple of 32): reduces the attempt-0 frontier / survivor slots
 template <int QS, bool CL>
-__global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, const float* cand,
-                                                     float* res, uint32_t* vflag, uint32_t* vlist,
-                                                     uint8_t* sel, Ctl* ctl, float eps, RnbpParams prm,
-                                                     CandList cl) {
-  if (run_done(ctl)) return;
+__device__ __forceinline__ void rnbp_retry_pass(const DevGraph& g, float* live, const float* cand, float* res,
+                                                uint32_t* vflag, uint32_t* vlist, uint8_t* sel, Ctl* ctl,
+                                                float eps, const RnbpParams& prm, const CandList& cl) {
   __shared__ unsigned long long s_f, s_s;
   if (threadIdx.x < 32) {
     unsigned long long f = 0, s = 0;
@@ -1306,6 +1450,28 @@ __global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, co
   __syncthreads();
   if (s_f > 0 || s_s == 0) return;
   rnbp_retry_block<QS, CL>(g, live, cand, res, vflag, vlist, sel, ctl, eps, prm, cl, s_s, &ctl->acc[0].delta);
+}
+
+// retry != 0: the last block runs the retry + fallback of the iteration
+// (rnbp_retry_pass; the lockstep frontier query); the run loop launches
+// k_rnbp_retry instead
+template <int QS, bool CL>
+__global__ void __launch_bounds__(kBlock) k_rnbp_select(DevGraph g, float* live, const float* cand,
+                                                        float* res, uint32_t* vflag, uint32_t* vlist,
+                                                        uint8_t* sel, Ctl* ctl, float eps,
+                                                        RnbpParams prm, CandList cl, int retry) {
+  if (run_done(ctl)) return;
+  rnbp_select_pass<QS, CL>(g, live, cand, res, vflag, vlist, sel, ctl, eps, prm, cl);
+  if (retry && last_block_done(ctl)) rnbp_retry_pass<QS, CL>(g, live, cand, res, vflag, vlist, sel, ctl, eps, prm, cl);
+}
+
+template <int QS, bool CL>
+__global__ void __launch_bounds__(1024) k_rnbp_retry(DevGraph g, float* live, const float* cand,
+                                                     float* res, uint32_t* vflag, uint32_t* vlist,
+                                                     uint8_t* sel, Ctl* ctl, float eps, RnbpParams prm,
+                                                     CandList cl) {
+  if (run_done(ctl)) return;
+  rnbp_retry_pass<QS, CL>(g, live, cand, res, vflag, vlist, sel, ctl, eps, prm, cl);
 }
 
 // Commit of a host-supplied frontier (lockstep apply_frontier).

@@ -122,7 +122,7 @@ class BandLBP:
 
     def __del__(self):
         e = getattr(self, "_e", None)
-        if e:
+        if e and _lib is not None:
             _lib.bp_engine_destroy(e)
             self._e = None
 

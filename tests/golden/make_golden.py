@@ -95,7 +95,7 @@ def suite(ref, workers, name):
         row = {"seed": s}
         for run_name, kw in sp["runs"]:
             kind = "lbp" if run_name == "lbp" else "rnbp"
-            reps = []
+            reps, conv = [], []
             for k in range(RNBP_REPLICATES if kind == "rnbp" else 1):
                 extra = dict(high_p=1.0, edge_ratio_threshold=0.9, seed=s - sp["seeds"][0] + 1000 * k) \
                     if kind == "rnbp" else {}
@@ -103,12 +103,32 @@ def suite(ref, workers, name):
                                              **kw, **extra), trace_cap=1)
                 reps.append({"converged": r.converged, "iterations": r.iterations, "wall_time": r.wall_time,
                              "messages_updated_total": r.messages_updated_total, "beliefs_sha": h(r.beliefs)})
-                if r.converged and k == 0:
-                    marg[f"{run_name}_{s}"] = r.beliefs[1::2].astype(np.float32)
+                if r.converged:
+                    conv.append(r.beliefs[1::2].copy())
             row[run_name] = dict(reps[0])
             if len(reps) > 1:
                 row[run_name]["replicates"] = [{"converged": x["converged"], "iterations": x["iterations"]}
                                                for x in reps]
+            # the distinct fixed points the converged replicates reached (max
+            # marginal difference < 1e-2 = same fixed point), one stored
+            # representative each, and the spread of converged marginals
+            # within a fixed point (the reference's own run-to-run precision)
+            clusters = []
+            for b in conv:
+                for cl in clusters:
+                    if np.max(np.abs(cl[0] - b)) < 1e-2:
+                        cl.append(b)
+                        break
+                else:
+                    clusters.append([b])
+            spread = 0.0
+            for j, cl in enumerate(clusters):
+                marg[f"{run_name}_{s}_fp{j}"] = cl[0].astype(np.float32)
+                for a in range(len(cl)):
+                    for b in range(a + 1, len(cl)):
+                        spread = max(spread, float(np.max(np.abs(cl[a] - cl[b]))))
+            row[run_name]["fixed_points"] = len(clusters)
+            row[run_name]["spread"] = spread
         print(name, s, {k: [x["iterations"] if x["converged"] else -1 for x in v.get("replicates", [v])]
                         for k, v in row.items() if k != "seed"}, flush=True)
         rows.append(row)
