@@ -50,7 +50,14 @@ struct DevGraph {
   unsigned long long edge_offset;         // global id of local edge 0 (band: RnBP draws use global ids)
   const float* __restrict__ ising_a;      // E  (binary, par_mode 1): a = e^J of the table {a, 1/a, 1/a, a}
   const float* __restrict__ pw;           // E  (generic, par_mode 1)
+  // 1: `table` holds log2 t (unscaled) and messages are contracted in the log
+  // domain (models whose messages can collapse in the reference, graph.cu)
+  uint32_t log_tables;
 };
+
+// numeric_error parity (normalize_in_place, messages.cpp:41-49): the reference
+// throws when a message's unnormalised mass falls below 1e-300.
+constexpr float kLog2MinMass = -996.578428f;  // log2(1e-300)
 
 constexpr uint32_t kUncl = 0xFFFFFFFFu;
 constexpr uint32_t kRsMaxDepth = 8;
@@ -355,6 +362,38 @@ __device__ __forceinline__ void generic_matvec(const DevGraph& g, uint32_t out, 
       o[xt] = acc;
     }
   }
+}
+
+// Log-domain update for collapse-checked models (log_tables): p = log2 of the
+// product psi_i * prod m (unshifted, messages.hpp:123-131), the contraction
+// with the table is a log-sum-exp per target state, lo = the normalised log2
+// message; returns log2 of the reference's unnormalised mass, so the caller
+// can raise numeric_error exactly where normalize_in_place would.  No value
+// is formed in linear fp32, so nothing under- or overflows.
+template <int QS>
+__device__ __forceinline__ float generic_logmatvec(const DevGraph& g, uint32_t out, const float* p, uint32_t ci,
+                                                   uint32_t cj, float* lo) {
+  const float* lt = g.table + static_cast<size_t>(out >> 1) * QS * QS;
+  float Mt = -INFINITY;
+  for (int xt = 0; xt < QS; ++xt) {
+    if (xt >= static_cast<int>(cj)) {
+      lo[xt] = -INFINITY;
+      continue;
+    }
+    float m = -INFINITY;
+    for (int xs = 0; xs < static_cast<int>(ci); ++xs)
+      m = fmaxf(m, p[xs] + __ldg(&lt[(out & 1u) ? xt * QS + xs : xs * QS + xt]));
+    float s = 0.f;
+    for (int xs = 0; xs < static_cast<int>(ci); ++xs)
+      s += fex2(p[xs] + __ldg(&lt[(out & 1u) ? xt * QS + xs : xs * QS + xt]) - m);
+    lo[xt] = m + flg2(s);
+    Mt = fmaxf(Mt, lo[xt]);
+  }
+  float S = 0.f;
+  for (int xt = 0; xt < static_cast<int>(cj); ++xt) S += fex2(lo[xt] - Mt);
+  const float tot = Mt + flg2(S);
+  for (int xt = 0; xt < static_cast<int>(cj); ++xt) lo[xt] -= tot;
+  return tot;
 }
 
 // ---------------------------------------------------------------------------

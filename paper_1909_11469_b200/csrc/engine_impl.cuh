@@ -161,7 +161,7 @@ class EngineT final : public EngineBase {
     }
     fetch_ctl_header();
     drain_trace(trace, trace_cap, copied);
-    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (total mass below 1e-300 or non-finite)");
 
     if (opts && opts->messages_host)  // LBP reports m_t, which lives in buf[t & 1]
       read_messages(opts->messages_host, cfg_.kind == BP_LBP && (hctl_->iteration & 1ull));
@@ -177,6 +177,10 @@ class EngineT final : public EngineBase {
     }
     cuda_check(cudaEventRecord(e1, s_), "event record");
     cuda_check(cudaStreamSynchronize(s_), "run");
+    if (g_.check_collapse) {  // compute_belief's mass check (k_beliefs) on collapse-checked models
+      fetch_ctl_header();
+      if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (total mass below 1e-300)");
+    }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
@@ -366,7 +370,7 @@ class EngineT final : public EngineBase {
     enqueue_refresh(kFinApply);
     sync();
     fetch_ctl_header();
-    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (total mass below 1e-300 or non-finite)");
   }
   // One fused LBP sweep exactly as run() executes it (the production kernel
   // for this graph, or the one the flags force): sweep t reads m_t, writes
@@ -388,7 +392,7 @@ class EngineT final : public EngineBase {
     enqueue_lbp_sweep(kFinLbp);
     sync();
     fetch_ctl_header();
-    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (total mass below 1e-300 or non-finite)");
     return lbp_kernel_;
   }
 
@@ -741,7 +745,7 @@ class EngineT final : public EngineBase {
     r->message_evaluations = hctl_->evals_total;
     r->vertex_visits = hctl_->vertex_visits;
     r->gpu_launches = launches_;
-    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (non-finite message)");
+    if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (total mass below 1e-300 or non-finite)");
   }
 
   void enqueue_init(bool lbp) {

@@ -149,6 +149,7 @@ DevGraph GraphImpl::dev() const {
   g.edge_offset = edge_offset;
   g.ising_a = ising_a.as<float>();
   g.pw = pw.as<float>();
+  g.log_tables = check_collapse ? 1u : 0u;
   return g;
 }
 
@@ -403,13 +404,66 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
       }
   }
   stage("csr");
+  // Can the reference's numeric_error (normalize_in_place: total mass below
+  // 1e-300, messages.cpp:41-49) ever fire on this model?  A lower bound of
+  // every message's unnormalised mass: a message m_k out of a table t_k has
+  // m_k(x) >= rho_k = min_{y,x} t_k(y,x) / sum_x' t_k(y,x') (any non-negative
+  // mixture of the rows; also the uniform initial messages), so the mass of
+  // d = (i -> j) is >= max_x psi_i(x) R_d(x) prod_{k in in(i), k != d^1} rho_k
+  // (R_d = row sums of t oriented i -> j), and a belief's is >= max_x psi_v(x)
+  // prod_{k in in(v)} rho_k.  Models where every bound clears 1e-290 (all
+  // generated instances, any sane input) never collapse in the reference; the
+  // others are built with the q-state layout and log-domain tables, and the
+  // device computes the reference's mass exactly (generic_logmatvec) to raise
+  // the same error.
+  bool collapse_free = true;
+  {
+    std::vector<size_t> uoff(static_cast<size_t>(V) + 1, 0);
+    for (uint32_t v = 0; v < V; ++v) uoff[v + 1] = uoff[v] + d->cardinalities[v];
+    std::vector<double> lrho(2ull * E), lrmax(2ull * E), LI(V, 0.0);
+    for (uint32_t e = 0; e < E; ++e) {
+      const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
+      const uint32_t ci = d->cardinalities[i], cj = d->cardinalities[j];
+      const double* t = d->pairwise_values + table_at(e);
+      double rho_f = 1.0, rho_b = 1.0, mf = 0.0, mb = 0.0;
+      for (uint32_t x = 0; x < ci; ++x) {  // d = 2e: rows x_i
+        double r = 0.0;
+        for (uint32_t y = 0; y < cj; ++y) r += t[static_cast<size_t>(x) * cj + y];
+        for (uint32_t y = 0; y < cj; ++y) rho_f = std::min(rho_f, t[static_cast<size_t>(x) * cj + y] / r);
+        mf = std::max(mf, d->unary_values[uoff[i] + x] * r);
+      }
+      for (uint32_t y = 0; y < cj; ++y) {  // d = 2e + 1: rows x_j
+        double r = 0.0;
+        for (uint32_t x = 0; x < ci; ++x) r += t[static_cast<size_t>(x) * cj + y];
+        for (uint32_t x = 0; x < ci; ++x) rho_b = std::min(rho_b, t[static_cast<size_t>(x) * cj + y] / r);
+        mb = std::max(mb, d->unary_values[uoff[j] + y] * r);
+      }
+      lrho[2ull * e] = std::log(rho_f);  // message into j
+      lrho[2ull * e + 1] = std::log(rho_b);  // message into i
+      lrmax[2ull * e] = std::log(mf);
+      lrmax[2ull * e + 1] = std::log(mb);
+      LI[j] += lrho[2ull * e];
+      LI[i] += lrho[2ull * e + 1];
+    }
+    const double floor = std::log(1e-290);
+    for (uint64_t dd = 0; dd < 2ull * E && collapse_free; ++dd) {
+      const uint32_t src = d->edge_endpoints[dd];  // ep[d] = source of d
+      collapse_free = lrmax[dd] + LI[src] - lrho[dd ^ 1ull] >= floor;
+    }
+    for (uint32_t v = 0; v < V && collapse_free; ++v) {
+      double mu = 0.0;
+      for (uint32_t x = 0; x < d->cardinalities[v]; ++x) mu = std::max(mu, d->unary_values[uoff[v] + x]);
+      collapse_free = std::log(mu) + LI[v] >= floor;
+    }
+  }
+  stage("collapse bound");
   auto g = std::make_unique<GraphImpl>();
   g->device = select_device(opts);
   g->V = V;
   g->E = E;
   g->D = 2 * E;
   g->maxq = maxq;
-  g->binary = V > 0 && maxq == 2 && usz == 2ull * V;
+  g->binary = V > 0 && maxq == 2 && usz == 2ull * V && collapse_free;
   bool uniform = true;
   for (uint32_t v = 1; v < V; ++v) uniform = uniform && d->cardinalities[v] == d->cardinalities[0];
   if (uniform && V) g->uniform_q = d->cardinalities[0];
@@ -475,7 +529,8 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
         ul[static_cast<size_t>(v) * qs + x] = static_cast<float>(std::log2(d->unary_values[o + x]));  // base 2
     }
     // Potts tables (a on the diagonal, d off it, square): one weight per edge
-    bool potts = E > 0;
+    // (not on collapse-checked models: their mass check uses the dense tables' scales)
+    bool potts = E > 0 && collapse_free;
     std::vector<float> w1(potts ? E : 0);
     for (uint32_t e = 0; e < E && potts; ++e) {
       const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
@@ -501,6 +556,13 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
       const double* t = d->pairwise_values + table_at(e);
       double mx = 0.0;
       for (size_t k = 0; k < static_cast<size_t>(ci) * cj; ++k) mx = std::max(mx, t[k]);
+      if (!collapse_free) {  // log-domain tables: log2 t, unscaled (generic_logmatvec)
+        for (uint32_t a = 0; a < ci; ++a)
+          for (uint32_t b = 0; b < cj; ++b)
+            tb[static_cast<size_t>(e) * qs * qs + static_cast<size_t>(a) * qs + b] =
+                static_cast<float>(std::log2(t[static_cast<size_t>(a) * cj + b]));
+        continue;
+      }
       for (uint32_t a = 0; a < ci; ++a)
         for (uint32_t b = 0; b < cj; ++b) {
           // max-scaled linear fp32; clamped so no entry underflows to 0
@@ -512,6 +574,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     g->card.upload(d->cardinalities, static_cast<size_t>(V) * 4);
     g->unary_log.upload(ul.data(), ul.size() * 4);
     if (!potts) g->table.upload(tb.data(), tb.size() * 4);
+    g->check_collapse = !collapse_free;
     g->bel_off.upload(bo.data(), bo.size() * 4);
   }
   g->lat_cols = lat_cols;

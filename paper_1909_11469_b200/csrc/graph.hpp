@@ -50,6 +50,9 @@ struct GraphImpl {
   uint32_t uniform_q = 0;  // all cardinalities equal to this (0 = mixed)
   bool binary = true;
   DevBuf in_off, in_adj, ep, unary_lo, epar, card, unary_log, table, bel_off, ising_a, pw;
+  // numeric_error parity on models whose messages can collapse (graph.cu):
+  // log-domain tables and the reference's mass computed on the device
+  bool check_collapse = false;
   uint32_t lat_rows = 0, lat_cols = 0;  // lattice topology detected / generated (0 = CSR only)
   uint32_t par_mode = 0;                // 1: Ising couplings (binary) / Potts weights (generic)
   // row-band partition (bp_graph_generate_ising_band): owned local rows

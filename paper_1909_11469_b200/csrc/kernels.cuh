@@ -741,14 +741,21 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
       p[x] = T[x] - mi[x];
       if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
     }
+    float o[QS], s, inv;
+    if (g.log_tables) {  // collapse-checked model: log-domain contraction (o = log2 message), exact mass
+      const float lm = generic_logmatvec<QS>(g, out, p, ci, cj, o);
+      if (!(lm >= kLog2MinMass)) *numeric_flag = 1u;
+      s = 1.f;
+      inv = 1.f;
+    } else {
 #pragma unroll (QS <= 8 ? QS : 2)
-    for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
-    float o[QS];
-    generic_matvec<QS>(g, out, p, o);
-    float s = 0.f;
+      for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
+      generic_matvec<QS>(g, out, p, o);
+      s = 0.f;
 #pragma unroll (QS <= 8 ? QS : 2)
-    for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
-    const float inv = frcp(s);
+      for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
+      inv = frcp(s);
+    }
     float r = 0.f;
     // the residual compares 2^(stored log) on both sides, so a bitwise fixed
     // point reports exactly 0 (as for the binary layout); states >= cj keep
@@ -756,7 +763,7 @@ __device__ __forceinline__ int vertex_update_generic(const DevGraph& g, uint32_t
 #pragma unroll (QS <= 8 ? QS : 2)
     for (int xt = 0; xt < QS; ++xt) {
       if (xt < static_cast<int>(cj)) {
-        const float ln = flg2(o[xt] * inv);
+        const float ln = g.log_tables ? o[xt] : flg2(o[xt] * inv);
         r = fmaxf(r, fabsf(fex2(ln) - fex2(mo[xt])));
         o[xt] = ln;
       } else {
@@ -1762,6 +1769,8 @@ __global__ void k_beliefs(DevGraph g, const float* A0, const float* A1, int ping
         p[x] = x < static_cast<int>(q) ? exp2(static_cast<double>(T[x] - M)) : 0.0;
         s += p[x];
       }
+      // compute_belief normalises too (messages.cpp:75-105): same mass check
+      if (g.log_tables && static_cast<double>(M) + log2(s) < static_cast<double>(kLog2MinMass)) ctl->numeric_error = 1u;
       double* o = out + g.bel_off[v];
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x)

@@ -297,6 +297,13 @@ __device__ __forceinline__ void splash_vertex_update(const DevGraph& g, uint32_t
         p[x] = T[x] - m_in[x];
         if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
       }
+      float* dst = shadow + static_cast<size_t>(out) * QS;
+      if (g.log_tables) {  // collapse-checked model (generic_logmatvec)
+        float lo[QS];
+        if (!(generic_logmatvec<QS>(g, out, p, ci, cj, lo) >= kLog2MinMass)) *nf = 1u;
+        for (int xt = 0; xt < static_cast<int>(cj); ++xt) dst[xt] = lo[xt];
+        continue;
+      }
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
       float o[QS], s = 0.f;
@@ -305,7 +312,6 @@ __device__ __forceinline__ void splash_vertex_update(const DevGraph& g, uint32_t
       for (int xt = 0; xt < QS; ++xt) s += xt < static_cast<int>(cj) ? o[xt] : 0.f;
       if (!(s > 0.f) || !(s < INFINITY)) *nf = 1u;
       const float inv = frcp(s);
-      float* dst = shadow + static_cast<size_t>(out) * QS;
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int xt = 0; xt < QS; ++xt)
         if (xt < static_cast<int>(cj)) dst[xt] = flg2(o[xt] * inv);
@@ -729,17 +735,23 @@ __global__ void __launch_bounds__(kBlock) k_splash_apply_edges(DevGraph g, const
 #pragma unroll (QS <= 8 ? QS : 2)
       for (int x = 0; x < QS; ++x)
         if (x < static_cast<int>(ci)) M = fmaxf(M, p[x]);
+      if (g.log_tables) {  // collapse-checked model (generic_logmatvec)
+        float lo[QS];
+        if (!(generic_logmatvec<QS>(g, d, p, ci, cj, lo) >= kLog2MinMass)) *nf = 1u;
+        for (int xt = 0; xt < static_cast<int>(cj); ++xt) shadow[static_cast<size_t>(d) * QS + xt] = lo[xt];
+      } else {
 #pragma unroll (QS <= 8 ? QS : 2)
-      for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
-      float o[QS], s2 = 0.f;
-      generic_matvec<QS>(g, d, p, o);
+        for (int x = 0; x < QS; ++x) p[x] = x < static_cast<int>(ci) ? fex2(p[x] - M) : 0.f;
+        float o[QS], s2 = 0.f;
+        generic_matvec<QS>(g, d, p, o);
 #pragma unroll (QS <= 8 ? QS : 2)
-      for (int xt = 0; xt < QS; ++xt) s2 += xt < static_cast<int>(cj) ? o[xt] : 0.f;
-      if (!(s2 > 0.f) || !(s2 < INFINITY)) *nf = 1u;
-      const float inv = frcp(s2);
+        for (int xt = 0; xt < QS; ++xt) s2 += xt < static_cast<int>(cj) ? o[xt] : 0.f;
+        if (!(s2 > 0.f) || !(s2 < INFINITY)) *nf = 1u;
+        const float inv = frcp(s2);
 #pragma unroll (QS <= 8 ? QS : 2)
-      for (int xt = 0; xt < QS; ++xt)
-        if (xt < static_cast<int>(cj)) shadow[static_cast<size_t>(d) * QS + xt] = flg2(o[xt] * inv);
+        for (int xt = 0; xt < QS; ++xt)
+          if (xt < static_cast<int>(cj)) shadow[static_cast<size_t>(d) * QS + xt] = flg2(o[xt] * inv);
+      }
     }
     written[d] = me;
   }
