@@ -20,6 +20,9 @@ PROG = r"""
 import ctypes, json, sys
 sys.path.insert(0, %r)
 from oracle import pyoracle as po
+# a C++ caller links the reference at link time; ctypes loads it RTLD_LOCAL
+# unless asked, which would hide the reference's symbols from the shim
+ctypes.CDLL(po.PATHS["ref"], mode=ctypes.RTLD_GLOBAL)
 ref = po.load("ref")
 out = {}
 for kind, n, c, seed in (("lbp", 20, 2.0, 3), ("rnbp", 16, 2.0, 1), ("srbp", 12, 2.0, 5)):
