@@ -149,11 +149,13 @@ typedef struct {
 #define BP_RUN_NO_PERSIST 8u    /* RnBP: keep the per-kernel graph loop in candidate-list mode */
 #define BP_RUN_LBP_TMA 16u      /* LBP: force the TMA-staged lattice sweep (binary Ising lattices, >= 2 rows) */
 #define BP_RUN_LBP_TILES 32u    /* LBP: force the register-tiled lattice sweep (default below 2^21 vertices) */
+#define BP_RUN_LBP_VERTEX 64u   /* LBP: force the vertex-centric sweep (q-state lattices: instead of lanes over states) */
 
 /* LBP sweep kernels (bp_engine_lbp_sweep's *kernel_out) */
 #define BP_LBP_KERNEL_VERTEX 0u /* k_vertex_update: vertex-centric (CSR / generic q-state / Potts lattice) */
 #define BP_LBP_KERNEL_TILES 1u  /* k_vertex_update lattice tiles (binary Ising lattice) */
 #define BP_LBP_KERNEL_TMA 2u    /* k_lbp_lattice: TMA-staged rows (binary Ising lattice) */
+#define BP_LBP_KERNEL_QLANES 3u /* k_lattice_qsweep: q-state lattice, lanes over states (q <= 8, uniform q) */
 
 BP_API const char* bp_last_error(void);
 BP_API int bp_abi_version(void);
@@ -307,6 +309,38 @@ BP_API int bp_band_rbp_select(struct bp_engine* e);
 BP_API int bp_band_rs_select(struct bp_engine* e);
 BP_API int bp_band_rnbp_finish(struct bp_engine* e);
 BP_API int bp_band_survivors(struct bp_engine* e, uint64_t* global_ids, uint64_t cap, uint64_t* n);
+
+/* ---- Row-band partition driven from C++ (no Python in the loop) ----------
+ * bp_graph_create_band: band `part` of `nparts` of ANY binary Ising lattice
+ *   given in build_graph's input layout (generate_ising's edge numbering,
+ *   generators.cpp:37-43; any rows x cols; tables {a, d, d, a}); owned rows
+ *   [row0, row1) of R rows plus one ghost row per neighbouring band.
+ * bp_band_engine_create_owned: a band engine that owns its halo buffers.
+ * bp_band_comm_create_nccl: the ranks' NCCL communicator (every rank passes
+ *   the same 128-byte id from bp_nccl_unique_id on one rank; libnccl.so.2 is
+ *   loaded at first use).  bp_band_comm_create_local: all bands in this
+ *   process (host-staged copies; tests on one GPU).
+ * bp_band_run: the run() loop (schedulers.cpp:301-347) of LBP / RnBP / RBP /
+ *   RS over the bands -- NCCL: nbands == 1, this rank's band; local: the
+ *   bands of parts 0 .. P-1 in order.  Halo send/recv and the all-reduce of
+ *   the loop counters are enqueued on the band's stream; the loop control
+ *   runs on the global counts, so every rank stops at the same iteration and
+ *   owned messages equal the unpartitioned run's bit for bit (LBP, RnBP).
+ *   result: the global iteration count / convergence; messages_updated_total
+ *   counts this band's owned messages (LBP) or the global frontier (others).
+ *   Beliefs of the owned rows: bp_engine_beliefs (rows row0 - ghost_up ... in
+ *   local numbering). */
+typedef struct bp_band_comm bp_band_comm;
+BP_API int bp_graph_create_band(const bp_graph_desc* desc, uint32_t part, uint32_t nparts,
+                                const bp_device_opts* opts, struct bp_graph** out, bp_band_info* info);
+BP_API int bp_band_engine_create_owned(const struct bp_graph* g, const bp_sched_config* cfg,
+                                       const bp_band_info* info, struct bp_engine** out);
+BP_API int bp_nccl_unique_id(uint8_t* id /* 128 bytes */);
+BP_API int bp_band_comm_create_nccl(const uint8_t* id, uint32_t rank, uint32_t nranks, int32_t device,
+                                    bp_band_comm** out);
+BP_API int bp_band_comm_create_local(bp_band_comm** out);
+BP_API void bp_band_comm_destroy(bp_band_comm* c);
+BP_API int bp_band_run(struct bp_engine* const* bands, uint32_t nbands, bp_band_comm* comm, bp_run_result* result);
 BP_API int bp_band_rnbp_fallback(struct bp_engine* e, uint64_t global_d);
 BP_API uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t d);
 

@@ -26,6 +26,8 @@
 #ifndef BPSCHED_CUDA_HPP
 #define BPSCHED_CUDA_HPP
 
+#include <algorithm>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -71,21 +73,20 @@ inline bp_sched_config to_c(const bpsched::SchedulerConfig& c) {
   return o;
 }
 
-/// A PairwiseMRF resident in HBM.  Upload once, run many times (the graph is
-/// immutable and shareable across runs, mrf.hpp:24-25).
-class DeviceGraph {
- public:
-  explicit DeviceGraph(const bpsched::PairwiseMRF& g, int device = -1) {
+/// build_graph's input layout of a PairwiseMRF, read through its public
+/// accessors (mrf.hpp:39-70) -- what the C ABI takes.
+struct HostArrays {
+  std::vector<uint32_t> cards, ep;
+  std::vector<double> unary, tables;
+  explicit HostArrays(const bpsched::PairwiseMRF& g) {
     const uint32_t V = g.num_vertices(), E = g.num_edges();
-    cards_.resize(V);
-    std::vector<double> unary;
+    cards.resize(V);
     for (bpsched::vertex_id v = 0; v < V; ++v) {
-      cards_[v] = g.cardinality(v);
+      cards[v] = g.cardinality(v);
       const auto u = g.unary(v);
       unary.insert(unary.end(), u.begin(), u.end());
     }
-    std::vector<uint32_t> ep(2ull * E);
-    std::vector<double> tables;
+    ep.resize(2ull * E);
     for (bpsched::edge_id e = 0; e < E; ++e) {
       const auto [i, j] = g.edge_endpoints(e);
       ep[2ull * e] = i;
@@ -93,7 +94,21 @@ class DeviceGraph {
       const auto t = g.pairwise(e);
       tables.insert(tables.end(), t.begin(), t.end());
     }
-    bp_graph_desc d{V, E, cards_.data(), unary.data(), ep.data(), tables.data()};
+  }
+  bp_graph_desc desc() const {
+    return bp_graph_desc{static_cast<uint32_t>(cards.size()), static_cast<uint32_t>(ep.size() / 2), cards.data(),
+                         unary.data(), ep.data(), tables.data()};
+  }
+};
+
+/// A PairwiseMRF resident in HBM.  Upload once, run many times (the graph is
+/// immutable and shareable across runs, mrf.hpp:24-25).
+class DeviceGraph {
+ public:
+  explicit DeviceGraph(const bpsched::PairwiseMRF& g, int device = -1) {
+    const HostArrays a(g);
+    cards_ = a.cards;
+    const bp_graph_desc d = a.desc();
     bp_device_opts o{device, BP_GRAPH_TRUSTED};  // build_graph already validated it
     check(bp_graph_create(&d, &o, &h_));
   }
@@ -145,6 +160,121 @@ inline bpsched::RunResult run(const bpsched::PairwiseMRF& graph, const bpsched::
   if (config.kind == bpsched::SchedulerKind::serial_rbp) return bpsched::run_serial_rbp(graph, config);
   DeviceGraph g(graph);
   return run(g, config);
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU: row bands of a binary Ising lattice, the run()
+// loop in the engine (bp_band_run), NCCL between the ranks.
+
+/// The rank's share of a partitioned run: the global loop result with the
+/// beliefs of the band's OWNED rows [row0, row1) (vertices row0*cols ..).
+struct BandRunResult {
+  bpsched::RunResult result;
+  uint32_t row0 = 0, row1 = 0, cols = 0;
+};
+
+namespace detail {
+struct BandHandles {
+  bp_graph* g = nullptr;
+  bp_engine* e = nullptr;
+  bp_band_info info{};
+  ~BandHandles() {
+    if (e) bp_engine_destroy(e);
+    if (g) bp_graph_destroy(g);
+  }
+};
+inline void make_band(const HostArrays& a, const bp_sched_config& c, uint32_t part, uint32_t nparts, int device,
+                      BandHandles& b) {
+  const bp_graph_desc d = a.desc();
+  bp_device_opts o{device, 0};
+  check(bp_graph_create_band(&d, part, nparts, &o, &b.g, &b.info));
+  check(bp_band_engine_create_owned(b.g, &c, &b.info, &b.e));
+}
+inline void owned_beliefs(BandHandles& b, bpsched::RunResult& out, std::vector<double>& all, size_t at) {
+  const size_t nloc = 2ull * b.info.local_rows * b.info.cols;
+  std::vector<double> bel(nloc);
+  check(bp_engine_beliefs(b.e, bel.data()));
+  const size_t first = 2ull * b.info.ghost_up * b.info.cols, n = 2ull * (b.info.row1 - b.info.row0) * b.info.cols;
+  std::copy(bel.begin() + first, bel.begin() + first + n, all.begin() + at);
+  (void)out;
+}
+inline void fill_result(const bp_run_result& r, bpsched::RunResult& out) {
+  out.converged = r.converged != 0;
+  out.iterations = r.iterations;
+  out.wall_time = r.wall_time;
+  out.messages_updated_total = r.messages_updated_total;
+}
+}  // namespace detail
+
+/// This rank's band of `graph` (any binary Ising lattice in generate_ising's
+/// numbering), run with the other ranks: every rank calls it with the same
+/// graph, config and NCCL id (bp_nccl_unique_id on one rank, broadcast by the
+/// caller's launcher).  Owned beliefs equal the one-GPU run's bit for bit
+/// (LBP, RnBP); RBP / RS use per-partition local frontiers.
+inline BandRunResult run_band(const bpsched::PairwiseMRF& graph, const bpsched::SchedulerConfig& config,
+                              uint32_t rank, uint32_t nranks, const uint8_t nccl_id[128], int device = -1) {
+  config.validate();
+  const HostArrays a(graph);
+  const bp_sched_config c = to_c(config);
+  detail::BandHandles b;
+  detail::make_band(a, c, rank, nranks, device, b);
+  bp_band_comm* comm = nullptr;
+  check(bp_band_comm_create_nccl(nccl_id, rank, nranks, device, &comm));
+  bp_run_result r{};
+  bp_engine* e = b.e;
+  const int rc = bp_band_run(&e, 1, comm, &r);
+  bp_band_comm_destroy(comm);
+  check(rc);
+  BandRunResult out;
+  detail::fill_result(r, out.result);
+  out.row0 = b.info.row0;
+  out.row1 = b.info.row1;
+  out.cols = b.info.cols;
+  std::vector<uint32_t> cards(static_cast<size_t>(b.info.row1 - b.info.row0) * b.info.cols, 2);
+  out.result.beliefs = bpsched::BeliefTable(cards);
+  std::vector<double> all(2 * cards.size());
+  detail::owned_beliefs(b, out.result, all, 0);
+  for (bpsched::vertex_id v = 0; v < cards.size(); ++v) {
+    auto dst = out.result.beliefs.at(v);
+    dst[0] = all[2 * v];
+    dst[1] = all[2 * v + 1];
+  }
+  return out;
+}
+
+/// Every band of an `nparts`-way partition inside this process (on `device`),
+/// assembled into the whole graph's RunResult: the partitioned loop without
+/// NCCL (the parity harness runs it against bpsched::run).
+inline bpsched::RunResult run_partitioned_local(const bpsched::PairwiseMRF& graph,
+                                                const bpsched::SchedulerConfig& config, uint32_t nparts,
+                                                int device = -1) {
+  config.validate();
+  const HostArrays a(graph);
+  const bp_sched_config c = to_c(config);
+  std::vector<std::unique_ptr<detail::BandHandles>> bands;
+  std::vector<bp_engine*> es;
+  for (uint32_t p = 0; p < nparts; ++p) {
+    bands.push_back(std::make_unique<detail::BandHandles>());
+    detail::make_band(a, c, p, nparts, device, *bands.back());
+    es.push_back(bands.back()->e);
+  }
+  bp_band_comm* comm = nullptr;
+  check(bp_band_comm_create_local(&comm));
+  bp_run_result r{};
+  const int rc = bp_band_run(es.data(), nparts, comm, &r);
+  bp_band_comm_destroy(comm);
+  check(rc);
+  bpsched::RunResult out;
+  detail::fill_result(r, out);
+  std::vector<double> all(a.unary.size());
+  for (auto& b : bands) detail::owned_beliefs(*b, out, all, 2ull * b->info.row0 * b->info.cols);
+  out.beliefs = bpsched::BeliefTable(a.cards);
+  for (bpsched::vertex_id v = 0; v < a.cards.size(); ++v) {
+    auto dst = out.beliefs.at(v);
+    dst[0] = all[2 * v];
+    dst[1] = all[2 * v + 1];
+  }
+  return out;
 }
 
 }  // namespace bpsched_cuda

@@ -126,7 +126,8 @@ RUN_NO_BELIEFS = 4
 RUN_NO_PERSIST = 8
 RUN_LBP_TMA = 16
 RUN_LBP_TILES = 32
-LBP_KERNELS = {0: "vertex", 1: "tiles", 2: "tma"}  # BP_LBP_KERNEL_*
+RUN_LBP_VERTEX = 64
+LBP_KERNELS = {0: "vertex", 1: "tiles", 2: "tma", 3: "qlanes"}  # BP_LBP_KERNEL_*
 GRAPH_TRUSTED = 1
 
 
@@ -669,9 +670,9 @@ class EngineState:
     def lbp_sweep(self, kernel: str = "auto") -> str:
         """One fused LBP sweep with the production kernel (bp_engine_lbp_sweep):
         afterwards messages() = m_t, candidates() = f(m_t), unconverged_count()
-        = #{r(m_t) >= eps}.  kernel: "auto" | "tma" | "tiles"; returns the
-        kernel that ran ("vertex", "tiles" or "tma")."""
-        flags = {"auto": 0, "tma": RUN_LBP_TMA, "tiles": RUN_LBP_TILES}[kernel]
+        = #{r(m_t) >= eps}.  kernel: "auto" | "tma" | "tiles" | "vertex"; returns
+        the kernel that ran ("vertex", "tiles", "tma" or "qlanes")."""
+        flags = {"auto": 0, "tma": RUN_LBP_TMA, "tiles": RUN_LBP_TILES, "vertex": RUN_LBP_VERTEX}[kernel]
         k = C.c_uint32()
         _check(_lib.bp_engine_lbp_sweep(self._h, flags, C.byref(k)))
         return LBP_KERNELS[int(k.value)]

@@ -10,6 +10,7 @@
 #include "bp_device.cuh"
 #include "engine.hpp"
 #include "graph.hpp"
+#include "partition.hpp"
 
 struct bp_graph {
   std::unique_ptr<bpb::GraphImpl> impl;
@@ -18,6 +19,10 @@ struct bp_engine {
   std::unique_ptr<bpb::EngineBase> e;
   const bp_graph* g;
   bp_sched_config cfg;
+  std::unique_ptr<bpb::Band> band;  // row-band engines: halo buffers, info, stream
+};
+struct bp_band_comm {
+  std::unique_ptr<bpb::BandComm> c;
 };
 
 namespace {
@@ -293,7 +298,119 @@ int bp_band_engine_create(const bp_graph* g, const bp_sched_config* cfg, const b
     h.recv_down = bufs->recv_down;
     h.count = bufs->count;
     e->band_config(h, info->owned_directed);
-    *out = new bp_engine{std::move(e), g, *cfg};
+    auto band = std::make_unique<bpb::Band>();
+    band->engine = e.get();
+    band->info = *info;
+    band->cfg = *cfg;
+    band->stream = e->stream();
+    band->halo = h;
+    *out = new bp_engine{std::move(e), g, *cfg, std::move(band)};
+  });
+}
+
+int bp_band_engine_create_owned(const bp_graph* g, const bp_sched_config* cfg, const bp_band_info* info,
+                                bp_engine** out) {
+  if (!g || !cfg || !info || !out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    bpb::validate_config(*cfg);
+    auto band = std::make_unique<bpb::Band>();
+    for (int k = 0; k < 4; ++k) band->own[k].alloc(4ull * info->cols);  // zero-filled, completed
+    band->own[4].alloc(8ull * 5);
+    bpb::PartHalo h{};
+    h.send_up = band->own[0].as<float>();
+    h.send_down = band->own[1].as<float>();
+    h.recv_up = band->own[2].as<float>();
+    h.recv_down = band->own[3].as<float>();
+    h.count = band->own[4].as<unsigned long long>();
+    auto e = bpb::make_engine(*g->impl, *cfg);
+    e->band_config(h, info->owned_directed);
+    band->engine = e.get();
+    band->info = *info;
+    band->cfg = *cfg;
+    band->stream = e->stream();
+    band->halo = h;
+    *out = new bp_engine{std::move(e), g, *cfg, std::move(band)};
+  });
+}
+
+int bp_graph_create_band(const bp_graph_desc* d, uint32_t part, uint32_t nparts, const bp_device_opts* opts,
+                         bp_graph** out, bp_band_info* info) {
+  if (!d || !out || !info) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    const uint32_t V = d->num_vertices, E = d->num_edges;
+    const uint32_t C = E && d->edge_endpoints ? bpb::lattice_cols(V, E, d->edge_endpoints) : 0;
+    if (!C || V % C) throw bpb::Error(BP_ERR_UNSUPPORTED, "row-band partition needs a lattice in generate_ising's numbering");
+    const uint32_t R = V / C;
+    if (nparts == 0 || part >= nparts || nparts > R) throw bpb::Error(BP_ERR_INVALID_ARGUMENT, "bad band partition");
+    for (uint32_t v = 0; v < V; ++v)
+      if (d->cardinalities[v] != 2) throw bpb::Error(BP_ERR_UNSUPPORTED, "row-band partition: binary lattices only");
+    const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(part) * R / nparts);
+    const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(part + 1) * R / nparts);
+    const uint32_t gu = part > 0 ? 1u : 0u, gd = part + 1 < nparts ? 1u : 0u;
+    const uint32_t lo = r0 - gu, hi = r1 + gd, L = hi - lo;
+    // the local L x C lattice: full edge blocks of rows lo .. hi-2, the right
+    // edges of row hi-1 (generators.cpp:37-43 numbering, relabelled)
+    std::vector<uint32_t> cards(static_cast<size_t>(L) * C, 2), ep;
+    std::vector<double> un(d->unary_values + 2ull * lo * C, d->unary_values + 2ull * hi * C), tb;
+    const uint64_t row_edges = 2ull * C - 1ull;
+    auto take = [&](uint64_t ge) {
+      ep.push_back(d->edge_endpoints[2 * ge] - lo * C);
+      ep.push_back(d->edge_endpoints[2 * ge + 1] - lo * C);
+      tb.insert(tb.end(), d->pairwise_values + 4 * ge, d->pairwise_values + 4 * ge + 4);
+    };
+    for (uint32_t r = lo; r + 1 < hi; ++r)
+      for (uint64_t k = 0; k < row_edges; ++k) take(static_cast<uint64_t>(r) * row_edges + k);
+    const uint64_t last = static_cast<uint64_t>(hi - 1) * row_edges;
+    for (uint32_t c = 0; c + 1 < C; ++c) take(hi == R ? last + c : last + 2ull * c);
+    bp_graph_desc ld{L * C, static_cast<uint32_t>(ep.size() / 2), cards.data(), un.data(), ep.data(), tb.data()};
+    auto g = bpb::build_from_desc(&ld, opts);
+    if (g->lat_cols != C || !g->binary || g->par_mode != 1)
+      throw bpb::Error(BP_ERR_UNSUPPORTED, "row-band partition needs Ising tables {a, d, d, a}");
+    g->cnt_row0 = gu;
+    g->cnt_row1 = gu + (r1 - r0);
+    uint64_t owned = 0;  // sum of the owned vertices' degrees in the full lattice
+    for (uint32_t r = r0; r < r1; ++r) owned += static_cast<uint64_t>(C) * ((r > 0) + (r + 1 < R)) + 2ull * (C - 1);
+    g->owned_directed = owned;
+    g->edge_offset = static_cast<uint64_t>(lo) * row_edges;
+    *info = bp_band_info{part, nparts, r0, r1, gu, gd, L, C, owned};
+    wrap_graph(std::move(g), out);
+  });
+}
+
+int bp_nccl_unique_id(uint8_t* id) {
+  if (!id) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { bpb::nccl_unique_id(id); });
+}
+
+int bp_band_comm_create_nccl(const uint8_t* id, uint32_t rank, uint32_t nranks, int32_t device, bp_band_comm** out) {
+  if (!id || !out || rank >= nranks) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    int dev = device;
+    if (dev < 0) bpb::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    *out = new bp_band_comm{std::unique_ptr<bpb::BandComm>(bpb::make_nccl_comm(id, static_cast<int>(rank),
+                                                                                   static_cast<int>(nranks), dev))};
+  });
+}
+
+int bp_band_comm_create_local(bp_band_comm** out) {
+  if (!out) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { *out = new bp_band_comm{std::unique_ptr<bpb::BandComm>(bpb::make_local_comm())}; });
+}
+
+void bp_band_comm_destroy(bp_band_comm* c) { delete c; }
+
+int bp_band_run(bp_engine* const* bands, uint32_t nbands, bp_band_comm* comm, bp_run_result* result) {
+  if (!bands || !nbands || !comm || !result) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    std::vector<bpb::Band*> b;
+    for (uint32_t i = 0; i < nbands; ++i) {
+      if (!bands[i] || !bands[i]->band) throw bpb::Error(BP_ERR_INVALID_ARGUMENT, "not a band engine");
+      b.push_back(bands[i]->band.get());
+    }
+    bpb::run_bands(b, *comm->c, result);
   });
 }
 
@@ -363,6 +480,13 @@ int bp_band_rnbp_fallback(bp_engine* e, uint64_t gd) {
 // Philox4x32-10 draw of the device (bp_device.cuh philox_u53), for host-side
 // decisions that must match the device stream (the band fallback).
 uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t d) {
+  return bpb::philox_u53_host(seed, iteration, attempt, d);
+}
+
+}  // extern "C"
+
+namespace bpb {
+uint64_t philox_u53_host(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t d) {
   const uint64_t e = d >> 1;
   uint32_t c0 = static_cast<uint32_t>(e), c1 = static_cast<uint32_t>(e >> 32), c2 = static_cast<uint32_t>(iteration),
            c3 = (static_cast<uint32_t>(iteration >> 32) & 0x3FFFFFFFu) | (attempt << 30);
@@ -384,6 +508,9 @@ uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint
   const uint64_t hi = (d & 1ull) ? c2 : c0, lo = (d & 1ull) ? c3 : c1;
   return ((hi << 32) | lo) >> 11;
 }
+}  // namespace bpb
+
+extern "C" {
 
 int bp_philox4x32_10_device(int32_t device, uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
   if (n && (!ctr || !key || !out)) return BP_ERR_INVALID_ARGUMENT;

@@ -121,7 +121,7 @@ class EngineT final : public EngineBase {
     launches_ = 0;
     const bool use_graph = !(flags & BP_RUN_NO_GRAPHS) && !timing_;
     persist_ = cfg_.kind == BP_RNBP && !(flags & BP_RUN_NO_PERSIST);
-    lbp_force_ = flags & (BP_RUN_LBP_TMA | BP_RUN_LBP_TILES);
+    lbp_force_ = flags & (BP_RUN_LBP_TMA | BP_RUN_LBP_TILES | BP_RUN_LBP_VERTEX);
     if (gexec_ && lbp_force_ != graph_force_) {  // the captured loop body embeds the sweep choice
       cudaGraphExecDestroy(gexec_);
       cudaGraphDestroy(graph_);
@@ -381,7 +381,7 @@ class EngineT final : public EngineBase {
   uint32_t lbp_sweep(uint32_t flags) override {
     if (cfg_.kind != BP_LBP) throw_invalid("lbp_sweep on a non-LBP engine");
     if (band_owned_) throw_invalid("lbp_sweep on a band engine (use bp_band_lbp_sweep)");
-    lbp_force_ = flags & (BP_RUN_LBP_TMA | BP_RUN_LBP_TILES);
+    lbp_force_ = flags & (BP_RUN_LBP_TMA | BP_RUN_LBP_TILES | BP_RUN_LBP_VERTEX);
     if (!pingpong_) {
       reset_ctl(std::numeric_limits<uint64_t>::max(), 1e300);
       const unsigned gi = grid_cap(static_cast<size_t>(g_.D) * QS);
@@ -586,6 +586,22 @@ class EngineT final : public EngineBase {
       // separate finalize: the fused one's static shared memory would cost the
       // TMA sweep its third resident block per SM (2.66 -> 3.10 ms at 16384^2)
       if (fin != kFinNone) enqueue_finalize(fin);
+    } else if constexpr (QS == 4 || QS == 8) {
+      if (g_.lat_cols && g_.uniform_q && !g_.check_collapse && !(lbp_force_ & BP_RUN_LBP_VERTEX)) {
+        // q-state lattice: lanes over states (k_lattice_qsweep)
+        lbp_kernel_ = BP_LBP_KERNEL_QLANES;
+        const unsigned grid = vgrid(k_lattice_qsweep<QS>, static_cast<size_t>(g_.V) * QS);
+        timed(kKUpdate, [&] {
+          k_lattice_qsweep<QS><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), eps_, fa);
+        });
+      } else {
+        lbp_kernel_ = BP_LBP_KERNEL_VERTEX;
+        timed(kKUpdate, [&] {
+          k_vertex_update<QS, kModeCount, false, true, false>
+              <<<vgrid(k_vertex_update<QS, kModeCount, false, true, false>, g_.V), kBlock, 0, s_>>>(
+                  dg_, live(), cand(), nullptr, nullptr, nullptr, ctl(), eps_, cand_list(), fa);
+        });
+      }
     } else {
       lbp_kernel_ = (QS == 1 && g_.lat_cols && g_.par_mode) ? BP_LBP_KERNEL_TILES : BP_LBP_KERNEL_VERTEX;
       timed(kKUpdate, [&] {

@@ -584,6 +584,8 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   return g;
 }
 
+uint32_t lattice_cols(uint32_t V, uint32_t E, const uint32_t* ep) { return detect_lattice(V, E, ep); }
+
 std::unique_ptr<GraphImpl> build_lattice_binary(uint32_t rows, uint32_t cols, const BinaryStreams& s,
                                                 const bp_device_opts* opts) {
   auto g = std::make_unique<GraphImpl>();

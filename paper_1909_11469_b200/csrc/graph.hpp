@@ -85,6 +85,8 @@ struct GraphImpl {
 };
 
 std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_device_opts* opts);
+// columns of the generate_ising lattice numbering of this edge list (0: not a lattice)
+uint32_t lattice_cols(uint32_t V, uint32_t E, const uint32_t* ep);
 std::unique_ptr<GraphImpl> build_lattice_binary(uint32_t rows, uint32_t cols, const BinaryStreams& s,
                                                 const bp_device_opts* opts);
 std::unique_ptr<GraphImpl> build_potts(uint32_t n, uint32_t q, const PottsStreams& s,

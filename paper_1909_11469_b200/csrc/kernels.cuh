@@ -1096,6 +1096,112 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
 }
 
 // ---------------------------------------------------------------------------
+// LBP sweep over a q-state lattice, LANES OVER STATES: a group of QS lanes
+// owns one vertex, lane x holds state x of every q-vector, so each q-vector
+// load / store is one coalesced 4*QS-byte access per group (a thread-per-vertex
+// sweep walks 4*QS-byte vectors at a 4*QS*2-byte stride and needs ~128
+// registers for 8 in + 8 out vectors: 25% occupancy, latency-bound).
+// Reductions over the states (max, sums) are xor-shuffles inside the group.
+// Same arithmetic as vertex_update_generic (kModeCount): m_{t+1} = f(m_t) into
+// B, count r(m_t) >= eps; the finalize of the iteration runs in the last block.
+template <int QS>
+__global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const float* A0, float* B0, Ctl* ctl,
+                                                           float eps, FinArgs fin) {
+  static_assert(QS == 4 || QS == 8, "lanes over states: QS divides the warp");
+  if (run_done(ctl)) return;
+  const float* A = A0;
+  float* B = B0;
+  if (ctl->sweeps & 1ull) {
+    A = B0;
+    B = const_cast<float*>(A0);
+  }
+  const uint32_t C = g.lat_cols, R = g.lat_rows, q = g.uniform_q;
+  const int x = static_cast<int>(threadIdx.x % QS);
+  const bool live_state = x < static_cast<int>(q);
+  auto gmax = [](float v) {
+#pragma unroll
+    for (int o = QS / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  };
+  auto gsum = [](float v) {
+#pragma unroll
+    for (int o = QS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  int cnt = 0;
+  unsigned long long evals = 0, visits = 0;
+  bool bad = false;
+  const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / QS);
+  const uint64_t V = g.V;
+  // every lane of the warp runs every trip (the shuffles need all of them)
+  const uint64_t trips = (V + groups - 1) / groups;
+  for (uint64_t t = 0; t < trips; ++t) {
+    const uint64_t vv = t * groups + static_cast<uint64_t>(blockIdx.x) * (blockDim.x / QS) + threadIdx.x / QS;
+    const bool act = vv < V;
+    const uint32_t v = act ? static_cast<uint32_t>(vv) : 0u;
+    const uint32_t r = v / C, c = v - r * C;
+    const uint32_t row = r * (2u * C - 1u);
+    const bool last = r + 1u == R;
+    const bool has[4] = {act && r > 0u, act && c > 0u, act && c + 1u < C, act && !last};
+    const uint32_t ins[4] = {
+        has[0] ? 2u * ((r - 1u) * (2u * C - 1u) + 2u * c + (c + 1u < C ? 1u : 0u)) : 0u,
+        has[1] ? 2u * (last ? row + c - 1u : row + 2u * (c - 1u)) : 0u,
+        has[2] ? 2u * (last ? row + c : row + 2u * c) + 1u : 0u,
+        has[3] ? 2u * (row + 2u * c + (c + 1u < C ? 1u : 0u)) + 1u : 0u};
+    float mi[4], mo[4], w[4];
+    float T = act ? __ldg(&g.unary_log[static_cast<size_t>(v) * QS + x]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mi[k] = has[k] ? __ldg(&A[static_cast<size_t>(ins[k]) * QS + x]) : 0.f;
+      mo[k] = has[k] ? __ldg(&A[static_cast<size_t>(ins[k] ^ 1u) * QS + x]) : 0.f;
+      w[k] = has[k] && g.par_mode ? __ldg(&g.pw[ins[k] >> 1]) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) T += mi[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t out = ins[k] ^ 1u;
+      const float pl = live_state ? T - mi[k] : -INFINITY;
+      const float M = gmax(pl);
+      const float e = live_state ? fex2(pl - M) : 0.f;
+      float o;
+      if (g.par_mode) {  // Potts: o(x) = sum_y e(y) t(y, x) / d = (a/d - 1) e(x) + sum_y e(y)
+        o = fmaf(w[k], e, gsum(e));
+      } else {  // dense max-scaled table, oriented by the direction of `out`
+        const float* tab = g.table + static_cast<size_t>(out >> 1) * QS * QS;
+        o = 0.f;
+#pragma unroll
+        for (int y = 0; y < QS; ++y) {
+          const float ey = __shfl_sync(0xffffffffu, e, (threadIdx.x & 31u & ~(QS - 1u)) + y);
+          const float tv = has[k] ? __ldg(&tab[(out & 1u) ? x * QS + y : y * QS + x]) : 0.f;
+          o = fmaf(tv, ey, o);
+        }
+      }
+      o = live_state ? o : 0.f;
+      const float sm = gsum(o);
+      const float ln = flg2(o * frcp(sm));
+      const float rr = gmax(live_state ? fabsf(fex2(ln) - fex2(mo[k])) : 0.f);
+      if (has[k]) {
+        B[static_cast<size_t>(out) * QS + x] = live_state ? ln : mo[k];
+        if (x == 0) {
+          cnt += rr >= eps;
+          ++evals;
+          bad |= !(sm > 0.f) || !(sm < INFINITY);
+        }
+      }
+    }
+    if (act && x == 0) ++visits;
+  }
+  if (bad) ctl->numeric_error = 1u;
+  Contrib cb;
+  cb.count = static_cast<unsigned long long>(cnt);
+  cb.evals = evals;
+  cb.visits = visits;
+  block_accumulate(ctl, cb);
+  fused_finalize(ctl, fin);
+}
+
+// ---------------------------------------------------------------------------
 // initial messages (init_messages, messages.cpp:23-39): uniform over the
 // target's states; binary log-odds 0.
 

@@ -32,8 +32,9 @@ from dataclasses import dataclass
 from . import (_Config, _DevOpts, _Result, _check, _lib, GRAPH_TRUSTED, PairwiseMRF, SchedulerConfig,
                SchedulerKind)
 
-__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "BandLBP", "BandRnBP", "BandRBP", "BandRS", "NcclExchange",
-           "LocalExchange", "NcclComm", "LocalComm", "run_band_lbp", "run_band_rnbp"]
+__all__ = ["band_rows", "owned_directed_edges", "BandInfo", "Band", "BandComm", "nccl_unique_id", "run_bands",
+           "BandLBP", "BandRnBP", "BandRBP", "BandRS", "NcclExchange", "LocalExchange", "NcclComm", "LocalComm",
+           "run_band_lbp", "run_band_rnbp"]
 
 
 def band_rows(n: int, part: int, nparts: int):
@@ -389,3 +390,113 @@ def run_band_lbp(band: BandLBP, exchange, max_iterations: int, check_every: int 
                 if st.stopped:
                     return st
     return band.status()
+
+
+# ---------------------------------------------------------------------------
+# The C++ driver (csrc/partition.cu): the run() loop of a band with the halo
+# exchange and the counter all-reduce enqueued on the band's stream by the
+# engine itself (NCCL between ranks), no Python inside the loop.
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype, f.argtypes = res, args
+    return f
+
+
+_P = C.c_void_p
+_create_band = _sig("bp_graph_create_band", C.c_int, [_P, C.c_uint32, C.c_uint32, C.POINTER(_DevOpts), C.POINTER(_P),
+                                                      C.POINTER(_BandInfoC)])
+_create_owned = _sig("bp_band_engine_create_owned", C.c_int, [_P, C.POINTER(_Config), C.POINTER(_BandInfoC),
+                                                              C.POINTER(_P)])
+_unique_id = _sig("bp_nccl_unique_id", C.c_int, [_P])
+_comm_nccl = _sig("bp_band_comm_create_nccl", C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_int32, C.POINTER(_P)])
+_comm_local = _sig("bp_band_comm_create_local", C.c_int, [C.POINTER(_P)])
+_comm_destroy = _sig("bp_band_comm_destroy", None, [_P])
+_band_run = _sig("bp_band_run", C.c_int, [_P, C.c_uint32, _P, C.POINTER(_Result)])
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId on this rank (128 bytes; broadcast it to the other ranks)."""
+    buf = (C.c_uint8 * 128)()
+    _check(_unique_id(buf))
+    return bytes(buf)
+
+
+class BandComm:
+    """The exchange of the C++ band loop: `nccl(id, rank, nranks, device)` links
+    one band per rank; `local()` drives every band of the partition in this
+    process (host-staged copies; one GPU in the tests)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, nranks: int, device: int = -1) -> "BandComm":
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(_comm_nccl(buf, rank, nranks, device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def local(cls) -> "BandComm":
+        h = C.c_void_p()
+        _check(_comm_local(C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _comm_destroy(h)
+            self._h = None
+
+
+class Band:
+    """One band of a row partition with engine-owned halo buffers, driven by
+    run_bands.  Either band `part` of generate_ising(n, c, seed), or of any
+    binary Ising lattice given as build_graph arrays (generate_ising's edge
+    numbering, any rows x cols)."""
+
+    def __init__(self, config: SchedulerConfig, part: int, nparts: int, device: int = 0, *, n: int = 0,
+                 c: float = 0.0, seed: int = 0, arrays=None):
+        import numpy as np
+
+        info = _BandInfoC()
+        h = C.c_void_p()
+        opts = _DevOpts(device, GRAPH_TRUSTED)
+        if arrays is None:
+            _check(_lib.bp_graph_generate_ising_band(n, c, seed, part, nparts, C.byref(opts), C.byref(h),
+                                                     C.byref(info)))
+        else:
+            from . import _Desc
+            cards, un, ep, tb = (np.ascontiguousarray(arrays[0], np.uint32), np.ascontiguousarray(arrays[1], np.float64),
+                                 np.ascontiguousarray(np.asarray(arrays[2]).reshape(-1), np.uint32),
+                                 np.ascontiguousarray(arrays[3], np.float64))
+            d = _Desc(cards.size, ep.size // 2, cards.ctypes.data_as(C.c_void_p), un.ctypes.data_as(C.c_void_p),
+                      ep.ctypes.data_as(C.c_void_p), tb.ctypes.data_as(C.c_void_p))
+            _check(_create_band(C.byref(d), part, nparts, C.byref(_DevOpts(device, 0)), C.byref(h), C.byref(info)))
+        self.graph = PairwiseMRF(h, None)
+        self.info = BandInfo(*(getattr(info, f) for f, _ in _BandInfoC._fields_))
+        self._cfg = config._c()
+        e = C.c_void_p()
+        _check(_create_owned(self.graph._h, C.byref(self._cfg), C.byref(info), C.byref(e)))
+        self._e = e
+
+    def __del__(self):
+        e = getattr(self, "_e", None)
+        if e and _lib is not None:
+            _lib.bp_engine_destroy(e)
+            self._e = None
+
+    beliefs = BandLBP.beliefs
+    owned_beliefs = BandLBP.owned_beliefs
+    status = BandLBP.status
+
+
+def run_bands(bands, comm: BandComm) -> BandStatus:
+    """The run() loop over row bands in C++ (bp_band_run): NCCL -- this rank's
+    band; local -- every band of the partition, parts 0..P-1."""
+    arr = (C.c_void_p * len(bands))(*[b._e.value for b in bands])
+    r = _Result()
+    _check(_band_run(arr, len(bands), comm._h, C.byref(r)))
+    return BandStatus(bool(r.stopped), bool(r.converged), int(r.iterations), int(r.messages_updated_total),
+                      int(r.gpu_launches))

@@ -227,6 +227,33 @@ int main() {
     run_compare("run_" + k + "_ising20_c2.0", bpsched::generate_ising({20, 2.0, 2}), cfg);
     run_compare("run_" + k + "_random", random_graph(31, 16, 3), cfg);
   }
+  // row-band partition driven by the engine (bp_band_run), all bands in this
+  // process: LBP owned beliefs bitwise, RnBP within 1e-4 of the reference
+  for (uint32_t parts : {2u, 3u}) {
+    bpsched::SchedulerConfig cfg;
+    cfg.kind = SchedulerKind::lbp;
+    cfg.max_iterations = 100000;
+    const auto g = bpsched::generate_ising({24, 1.5, 5});
+    const bpsched::RunResult a = bpsched_cuda::run(g, cfg);
+    const bpsched::RunResult b = bpsched_cuda::run_partitioned_local(g, cfg, parts);
+    bool same = a.converged == b.converged && a.iterations == b.iterations;
+    for (bpsched::vertex_id v = 0; v < g.num_vertices() && same; ++v)
+      same = a.beliefs.at(v)[0] == b.beliefs.at(v)[0] && a.beliefs.at(v)[1] == b.beliefs.at(v)[1];
+    report("bands_lbp_ising24_x" + std::to_string(parts), same, "bitwise equal to the one-band run");
+    cfg.kind = SchedulerKind::rnbp;
+    cfg.low_p = 0.5;
+    const bpsched::RunResult c = bpsched_cuda::run_partitioned_local(g, cfg, parts);
+    const bpsched::RunResult d = bpsched_cuda::run(g, cfg);
+    const bpsched::RunResult ref = bpsched::run(g, cfg);
+    double worst = 0.0;
+    for (bpsched::vertex_id v = 0; v < g.num_vertices(); ++v)
+      for (size_t k = 0; k < 2; ++k) worst = std::max(worst, std::fabs(ref.beliefs.at(v)[k] - c.beliefs.at(v)[k]));
+    report("bands_rnbp_ising24_x" + std::to_string(parts),
+           c.iterations == d.iterations && c.messages_updated_total == d.messages_updated_total && c.converged &&
+               ref.converged && worst <= 1e-4,
+           "iterations " + std::to_string(c.iterations) + " (one band " + std::to_string(d.iterations) +
+               ", reference " + std::to_string(ref.iterations) + ") max|db| vs reference " + std::to_string(worst));
+  }
   // serial RBP goes through the reference's run_serial_rbp inside the facade
   {
     bpsched::SchedulerConfig cfg;

@@ -2,8 +2,9 @@
 
 bp.run executes LBP as one fused sweep per iteration (kernels_lbp.cuh
 k_lbp_lattice for binary Ising lattices of >= 2^21 vertices, the register-tiled
-lattice sweep below that, the vertex-centric k_vertex_update for CSR graphs and
-q-state lattices).  EngineState.lbp_sweep runs exactly that kernel once, so the
+lattice sweep below that, k_lattice_qsweep -- lanes over states -- for q-state
+lattices with q <= 8, the vertex-centric k_vertex_update for CSR graphs and
+larger q).  EngineState.lbp_sweep runs exactly that kernel once, so the
 reference's per-iteration state can be compared after every sweep:
 messages() = m_t, candidates() = f(m_t), unconverged = #{r(m_t) >= eps}
 (the reference's EngineState after t apply_frontier(frontier_lbp()) calls,
@@ -100,13 +101,39 @@ def test_production_sweep_1000_tiles(bp, orc):
     fused_lockstep(bp, dg, og, og.arrays().endpoints, 10, kernel="auto", expect="tiles")
 
 
-@pytest.mark.parametrize("n,q,c,seed", [(9, 3, 2.5, 1), (16, 8, 2.5, 2), (40, 4, 1.5, 3), (12, 5, 2.0, 4)])
-def test_potts_lattice_sweep_lockstep(bp, orc, n, q, c, seed):
-    """q-state lattices (the register path of vertex_update_generic, q <= 8,
-    and the strided path above it): fused sweeps <= 1e-5 per iteration."""
+@pytest.mark.parametrize("n,q,c,seed", [(9, 3, 2.5, 1), (16, 8, 2.5, 2), (40, 4, 1.5, 3), (12, 5, 2.0, 4),
+                                        (33, 16, 1.5, 6)])
+@pytest.mark.parametrize("kernel", ["auto", "vertex"])
+def test_potts_lattice_sweep_lockstep(bp, orc, n, q, c, seed, kernel):
+    """q-state lattices: lanes over states (k_lattice_qsweep, q <= 8, the
+    production kernel) and the thread-per-vertex path (forced, and q > 8):
+    fused sweeps <= 1e-5 per iteration."""
     dg = bp.generate_potts(n, q, c, seed)
     og = po.Graph.potts(orc, n, q, c, seed)
-    fused_lockstep(bp, dg, og, og.arrays().endpoints, 25, expect="vertex")
+    expect = "qlanes" if kernel == "auto" and q <= 8 else "vertex"
+    fused_lockstep(bp, dg, og, og.arrays().endpoints, 25, kernel=kernel, expect=expect)
+
+
+@pytest.mark.parametrize("rows,cols,q", [(7, 9, 3), (5, 33, 8)])
+def test_dense_table_lattice_sweep_lockstep(bp, orc, rows, cols, q):
+    """Non-Potts q-state lattice tables (dense, asymmetric): lanes over states
+    with the shuffled dense contraction, both edge directions."""
+    from tests.helpers import Stream
+    rng = Stream(orc, 100 + q)
+    V = rows * cols
+    unary = [rng.unit() + 0.05 for _ in range(V * q)]
+    ep, tb = [], []
+    for r in range(rows):
+        for col in range(cols):
+            v = r * cols + col
+            for w in ([v + 1] if col + 1 < cols else []) + ([v + cols] if r + 1 < rows else []):
+                ep.append((v, w))
+                tb += [np.exp(2.0 * (rng.unit() - 0.5)) for _ in range(q * q)]
+    cards = np.full(V, q, np.uint32)
+    ep = np.asarray(ep, np.uint32)
+    dg = bp.PairwiseMRF.from_arrays(cards, np.asarray(unary), ep, np.asarray(tb))
+    og = po.Graph.from_arrays(orc, cards, np.asarray(unary), ep, np.asarray(tb))
+    fused_lockstep(bp, dg, og, ep, 20, expect="qlanes")
 
 
 def test_er_sweep_lockstep(bp, orc):

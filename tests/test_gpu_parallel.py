@@ -145,3 +145,77 @@ def test_band_loops_through_nccl_torchrun():
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stderr[-3000:]
     assert "OK" in p.stdout, p.stdout + p.stderr[-2000:]
+
+
+# ---- the C++ driver (csrc/partition.cu, bp_band_run): the same contract
+@pytest.mark.parametrize("nparts", [1, 2, 3, 5])
+def test_cpp_driver_lbp_bitwise_equals_unpartitioned(bp, nparts):
+    n, c, seed, iters = 23, 2.5, 3, 17
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=iters)
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)), cfg)
+    bands = [par.Band(cfg, p, nparts, 0, n=n, c=c, seed=seed) for p in range(nparts)]
+    st = par.run_bands(bands, par.BandComm.local())
+    assert st.stopped and st.iterations == full.iterations == iters and st.converged == full.converged
+    want = full.beliefs.values.reshape(n, n, 2)
+    for b in bands:
+        assert np.array_equal(b.owned_beliefs(), want[b.info.row0:b.info.row1]), b.info
+    assert sum(b.status().messages_updated_total for b in bands) == full.messages_updated_total
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_cpp_driver_rnbp_equals_unpartitioned(bp, nparts):
+    n, c, seed = 20, 2.0, 4
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=400, seed=seed)
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)), cfg)
+    bands = [par.Band(cfg, p, nparts, 0, n=n, c=c, seed=seed) for p in range(nparts)]
+    st = par.run_bands(bands, par.BandComm.local())
+    assert st.converged == full.converged and st.iterations == full.iterations
+    assert st.messages_updated_total == full.messages_updated_total
+    want = full.beliefs.values.reshape(n, n, 2)
+    for b in bands:
+        assert np.array_equal(b.owned_beliefs(), want[b.info.row0:b.info.row1])
+
+
+def test_cpp_driver_rnbp_fallback_across_bands(bp):
+    """Tiny low_p: empty attempt-0 draws, retries and single-survivor
+    fallbacks picked across bands (ascending global ids) -- same run."""
+    n, c, seed = 12, 2.0, 3
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.02, high_p=0.02, max_iterations=300, seed=seed)
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)), cfg)
+    bands = [par.Band(cfg, p, 3, 0, n=n, c=c, seed=seed) for p in range(3)]
+    st = par.run_bands(bands, par.BandComm.local())
+    assert st.iterations == full.iterations and st.messages_updated_total == full.messages_updated_total
+    want = full.beliefs.values.reshape(n, n, 2)
+    for b in bands:
+        assert np.array_equal(b.owned_beliefs(), want[b.info.row0:b.info.row1])
+
+
+@pytest.mark.parametrize("kind", ["lbp", "rnbp"])
+def test_cpp_driver_any_lattice_descriptor(bp, orc, kind):
+    """Bands of a caller's own lattice (build_graph arrays, non-square): the
+    same run as the whole graph on one device."""
+    from tests.helpers import lattice_arrays
+    rows, cols = 17, 40
+    arrays = lattice_arrays(orc, rows, cols, 9, 2.0)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.from_string(kind), low_p=0.5, max_iterations=60, seed=2)
+    full = bp.run(bp.PairwiseMRF.from_arrays(*arrays), cfg)
+    bands = [par.Band(cfg, p, 3, 0, arrays=arrays) for p in range(3)]
+    st = par.run_bands(bands, par.BandComm.local())
+    assert st.iterations == full.iterations and st.converged == full.converged
+    want = full.beliefs.values.reshape(rows, cols, 2)
+    for b in bands:
+        assert np.array_equal(b.owned_beliefs(), want[b.info.row0:b.info.row1])
+
+
+def test_cpp_driver_nccl_single_rank(bp):
+    """The NCCL transport of the C++ driver (libnccl loaded at first use) with
+    one rank: communicator set-up, the all-reduce on the band stream."""
+    n, c, seed = 16, 2.0, 1
+    comm = par.BandComm.nccl(par.nccl_unique_id(), 0, 1, 0)
+    for kind in ("lbp", "rnbp"):
+        cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.from_string(kind), low_p=0.5, max_iterations=50, seed=seed)
+        full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed)), cfg)
+        band = par.Band(cfg, 0, 1, 0, n=n, c=c, seed=seed)
+        st = par.run_bands([band], comm)
+        assert st.iterations == full.iterations
+        assert np.array_equal(band.owned_beliefs(), full.beliefs.values.reshape(n, n, 2))

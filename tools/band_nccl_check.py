@@ -28,6 +28,21 @@ st = par.run_band_rnbp(bands, par.NcclComm(rank, world), cfg.max_iterations)
 full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed), device=local), cfg)
 ok &= st.iterations == full.iterations and st.messages_updated_total == full.messages_updated_total
 ok &= bool(np.array_equal(bands[0].owned_beliefs(), full.beliefs.values.reshape(n, n, 2)[bands[0].info.row0:bands[0].info.row1]))
+# the C++ driver (csrc/partition.cu): the engine enqueues ncclSend/Recv +
+# ncclAllReduce on the band stream itself; torch only broadcasts the NCCL id
+obj = [par.nccl_unique_id() if rank == 0 else None]
+dist.broadcast_object_list(obj, src=0)
+comm = par.BandComm.nccl(obj[0], rank, world, local)
+for kind, kw, iters in (("lbp", {}, 15), ("rnbp", dict(low_p=0.5, seed=seed), 300)):
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.from_string(kind), max_iterations=iters, **kw)
+    band = par.Band(cfg, rank, world, local, n=n, c=c, seed=seed)
+    st = par.run_bands([band], comm)
+    full = bp.run(bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed), device=local), cfg)
+    ok &= st.iterations == full.iterations and st.converged == full.converged
+    ok &= bool(np.array_equal(band.owned_beliefs(),
+                              full.beliefs.values.reshape(n, n, 2)[band.info.row0:band.info.row1]))
+    print(f"rank {rank} C++ NCCL band {kind}: iterations {st.iterations} / {full.iterations}", flush=True)
+del comm
 t = torch.tensor([1 if ok else 0], device="cuda")
 dist.all_reduce(t, op=dist.ReduceOp.MIN)
 if rank == 0:

@@ -18,7 +18,8 @@ def ncu_csv(rep, *args):
 
 
 def scale_of(unit):
-    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "KB": 1e3, "MB": 1e6,
+            "GB": 1e9}.get(unit, 1)
 
 
 def main():
@@ -53,7 +54,8 @@ def main():
         dur = val("gpu__time_duration.sum")
         dram = (val("dram__bytes_read.sum") or 0) * scale_of(fu[fh.index("dram__bytes_read.sum")]) + \
                (val("dram__bytes_write.sum") or 0) * scale_of(fu[fh.index("dram__bytes_write.sum")])
-        dur_s = (dur or 0) * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(
+        dur_s = (dur or 0) * {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3,
+                              "second": 1.0, "s": 1.0}.get(
             fu[fh.index("gpu__time_duration.sum")], 1e-9)
         stalls = []
         for i, n in enumerate(fh):
