@@ -307,7 +307,7 @@ def run_b200(args):
         t1 = time.perf_counter()
         g = bp.PairwiseMRF.from_arrays(cards, un, ep, tb, device=local)
         r = bp.run(g, bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
-        _ = r.beliefs.values.sum()
+        _ = float(r.beliefs.values[-1])  # the beliefs are already in host memory (bp_run D2H)
         dt = time.perf_counter() - t1
         e2e_t += dt
         e2e_steps.append(round(dt * 1e3, 3))

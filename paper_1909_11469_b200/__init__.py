@@ -300,9 +300,15 @@ class Trace(Sequence):
 class BeliefTable:
     """BeliefTable (messages.hpp:83-107): per-vertex probability vectors."""
 
-    def __init__(self, values: np.ndarray, offsets: np.ndarray):
+    def __init__(self, values: np.ndarray, offsets):
         self.values = values
-        self.offsets = offsets
+        self._offsets = offsets  # array, or the graph (offsets built on first use)
+
+    @property
+    def offsets(self) -> np.ndarray:
+        if not isinstance(self._offsets, np.ndarray):
+            self._offsets = self._offsets.belief_offsets
+        return self._offsets
 
     def num_vertices(self) -> int:
         return len(self.offsets) - 1
@@ -364,15 +370,33 @@ class ChainParams:
 class PairwiseMRF:
     """Device-resident pairwise MRF (immutable; shareable across runs)."""
 
-    def __init__(self, handle, cardinalities: Optional[np.ndarray]):
+    def __init__(self, handle, cardinalities: Optional[np.ndarray], uniform: bool = False):
         self._h = handle
         info = _Info()
         _check(_lib.bp_graph_info_get(handle, C.byref(info)))
         self.info = info
-        if cardinalities is None:
-            cardinalities = np.full(info.num_vertices, info.max_cardinality, np.uint32)
-        self.cardinalities = np.asarray(cardinalities, np.uint32)
-        self.belief_offsets = np.concatenate([[0], np.cumsum(self.cardinalities, dtype=np.int64)])
+        # uniform cardinality: the per-vertex arrays are built on first use only
+        # (graph construction from host arrays is on the end-to-end path)
+        self._uniform = uniform or cardinalities is None
+        self._cards = None if cardinalities is None else np.asarray(cardinalities, np.uint32)
+        self._boff = None
+        if self._uniform:
+            self.unary_size = int(info.num_vertices) * int(info.max_cardinality)
+        else:
+            self._boff = np.concatenate([[0], np.cumsum(self._cards, dtype=np.int64)])
+            self.unary_size = int(self._boff[-1])
+
+    @property
+    def cardinalities(self) -> np.ndarray:
+        if self._cards is None:
+            self._cards = np.full(self.info.num_vertices, self.info.max_cardinality, np.uint32)
+        return self._cards
+
+    @property
+    def belief_offsets(self) -> np.ndarray:
+        if self._boff is None:
+            self._boff = np.arange(int(self.info.num_vertices) + 1, dtype=np.int64) * int(self.info.max_cardinality)
+        return self._boff
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -412,11 +436,12 @@ class PairwiseMRF:
         tb = np.ascontiguousarray(pairwise_values, np.float64)
         if ep.size % 2:
             raise ValueError("edge_endpoints must hold (i, j) pairs")
-        expected_unary = int(cards.astype(np.int64).sum())
+        uniform = bool(cards.size) and cards.min() == cards.max()
+        expected_unary = int(cards[0]) * cards.size if uniform else int(cards.sum(dtype=np.uint64))
         if un.size != expected_unary:
             raise ModelError(f"expected {expected_unary} unary entries, got {un.size}")
         E = ep.size // 2
-        if E and cards.size and cards.min() == cards.max():  # uniform cardinality: q^2 entries per table
+        if E and uniform:  # uniform cardinality: q^2 entries per table
             q = int(cards[0])
             if tb.size != E * q * q:
                 raise ModelError(f"pairwise tables hold {tb.size} entries, expected {E * q * q}")
@@ -431,7 +456,7 @@ class PairwiseMRF:
         o = _DevOpts(device, GRAPH_TRUSTED if trusted else 0)
         h = C.c_void_p()
         _check(_lib.bp_graph_create(C.byref(d), C.byref(o), C.byref(h)))
-        return cls(h, cards)
+        return cls(h, cards, uniform)
 
 
 def build_graph(cardinalities: Sequence[int], unary_tables: Sequence[Sequence[float]],
@@ -511,7 +536,7 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
     the run (RunResult.messages, fp64 probabilities in MessageStore order)."""
     c = config._c()
     msgs = np.empty(max(int(graph.info.message_values), 1)) if messages else None
-    nb = int(graph.belief_offsets[-1])
+    nb = graph.unary_size
     bel = np.empty(max(nb, 1)) if beliefs and not beliefs_device_ptr else None  # filled by bp_run_ex
     if trace_cap is None:
         trace_cap = int(min(config.max_iterations, 1 << 20)) + 1
@@ -524,7 +549,7 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
                           trace_cap))
     n = min(int(res.trace_len), trace_cap)
     trace = Trace(np.frombuffer(tr, dtype=_TRACE_DTYPE, count=n).copy())
-    bt = BeliefTable(bel[:nb], graph.belief_offsets) if bel is not None else None
+    bt = BeliefTable(bel[:nb], graph) if bel is not None else None
     return RunResult(bool(res.converged), int(res.iterations), float(res.wall_time),
                      int(res.messages_updated_total), bt, trace, float(res.device_ms),
                      int(res.message_evaluations), int(res.gpu_launches), int(res.vertex_visits),

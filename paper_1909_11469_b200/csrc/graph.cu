@@ -11,9 +11,12 @@
 #include <cstring>
 #include <limits>
 #include <thread>
+#include <unordered_set>
 
 #include "bp_device.cuh"
+#include "engine.hpp"
 #include "graph.hpp"
+#include "host_pool.hpp"
 
 namespace bpb {
 
@@ -71,6 +74,36 @@ void DevBuf::reset() {
   p = nullptr;
   bytes = 0;
   cap = 0;
+}
+void DevBuf::alloc_async(size_t n, cudaStream_t st) {
+  reset();
+  if (n == 0) n = 16;
+  const size_t want = n + 64;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.free.lower_bound(std::make_pair(dev, want));
+    if (it != c.free.end() && it->first.first == dev && it->first.second <= want + want / 4) {
+      p = it->second;
+      cap = it->first.second;
+      c.held -= cap;
+      c.free.erase(it);
+    }
+  }
+  if (!p) {
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      trim_cache();
+      e = cudaMalloc(&p, want);
+    }
+    cuda_check(e, "cudaMalloc");
+    cap = want;
+  }
+  bytes = n;
+  cuda_check(cudaMemsetAsync(static_cast<char*>(p) + n, 0, cap - n, st), "memset (slack)");
 }
 void DevBuf::alloc(size_t n) {
   reset();
@@ -239,27 +272,14 @@ __global__ void k_iota_mul(uint32_t* p, size_t n, uint32_t mul) {
     p[i] = static_cast<uint32_t>(i * mul);
 }
 
-// Host loops over vertices / edges, split over the host's cores (graph
-// construction from host arrays is on the end-to-end path).
+// smallest index in [0, n) with bad(i), or n (host pool, host_pool.hpp);
+// `heavy`: every index is a long scan (rows), so split even small n
 template <class F>
-void parallel_for(uint64_t n, F&& f) {
-  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  const unsigned nt = n < (1u << 16) ? 1u : hw;
-  if (nt == 1) {
-    f(uint64_t{0}, n);
-    return;
-  }
-  std::vector<std::thread> ts;
-  for (unsigned t = 0; t < nt; ++t)
-    ts.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt); });
-  for (auto& th : ts) th.join();
-}
-
-// smallest index in [0, n) with bad(i), or n
-template <class F>
-uint64_t first_bad(uint64_t n, F&& bad) {
+uint64_t first_bad(uint64_t n, F&& bad, bool heavy = false) {
   std::atomic<uint64_t> first{n};
-  parallel_for(n, [&](uint64_t a, uint64_t b) {
+  const unsigned chunks = heavy ? static_cast<unsigned>(std::min<uint64_t>(n, HostPool::get().size() * 2))
+                                : pool_chunks(n);
+  auto body = [&](uint64_t a, uint64_t b, unsigned) {
     for (uint64_t i = a; i < b && i < first.load(std::memory_order_relaxed); ++i)
       if (bad(i)) {
         uint64_t cur = first.load();
@@ -267,7 +287,9 @@ uint64_t first_bad(uint64_t n, F&& bad) {
         }
         return;
       }
-  });
+  };
+  if (chunks <= 1) body(0, n, 0);
+  else HostPool::get().run(chunks, [&](unsigned t) { body(n * t / chunks, n * (t + 1) / chunks, t); });
   return first.load();
 }
 
@@ -298,6 +320,7 @@ uint32_t detect_lattice(uint32_t V, uint32_t E, const uint32_t* ep) {
 }
 
 // a = e^J (a / d of the table), clamped so the device arithmetic stays finite
+const double kIsingAMax = std::exp(69.0), kIsingAMin = std::exp(-69.0);
 float ising_weight(double J) {
   const double j = std::min(69.0, std::max(-69.0, J));
   return static_cast<float>(std::exp(j));
@@ -307,6 +330,148 @@ void upload_ising_weights(GraphImpl& g, const std::vector<float>& J) {
   std::vector<float> a(J.size());
   for (size_t e = 0; e < J.size(); ++e) a[e] = ising_weight(static_cast<double>(J[e]));
   g.ising_a.upload(a.data(), a.size() * 4);
+}
+
+}  // namespace
+
+namespace {
+
+bool bad_entry(double u) { return !(u > 0.0) || !std::isfinite(u); }
+
+// build_graph's validation restated sequentially in the reference's order
+// (mrf.cpp:37-85: per vertex cardinality then entries; per edge range,
+// self-loop, order, duplicate, entries).  Runs only after the parallel passes
+// found a violation, so the error raised is the reference's first one.
+[[noreturn]] void throw_first_model_error(const bp_graph_desc* d) {
+  const uint32_t V = d->num_vertices, E = d->num_edges;
+  size_t o = 0;
+  for (uint32_t v = 0; v < V; ++v) {
+    const uint32_t q = d->cardinalities[v];
+    if (q == 0) throw_model("vertex " + std::to_string(v) + " has cardinality 0");
+    for (uint32_t x = 0; x < q; ++x)
+      if (bad_entry(d->unary_values[o + x]))
+        throw_model("unary(" + std::to_string(v) + ") entries must be strictly positive and finite");
+    o += q;
+  }
+  std::unordered_set<uint64_t> seen;
+  seen.reserve(static_cast<size_t>(E) * 2);
+  size_t t = 0;
+  for (uint32_t e = 0; e < E; ++e) {
+    const uint32_t i = d->edge_endpoints[2ull * e], j = d->edge_endpoints[2ull * e + 1];
+    if (i >= V || j >= V) throw_model("edge " + std::to_string(e) + " references a vertex out of range");
+    if (i == j) throw_model("edge " + std::to_string(e) + " is a self-loop on vertex " + std::to_string(i));
+    if (i > j) throw_model("edge " + std::to_string(e) + " endpoints must satisfy i < j");
+    if (!seen.insert((static_cast<uint64_t>(i) << 32) | j).second)
+      throw_model("duplicate edge (" + std::to_string(i) + ", " + std::to_string(j) + ")");
+    const size_t sz = static_cast<size_t>(d->cardinalities[i]) * d->cardinalities[j];
+    for (size_t k = 0; k < sz; ++k)
+      if (bad_entry(d->pairwise_values[t + k]))
+        throw_model("pairwise(" + std::to_string(i) + "," + std::to_string(j) +
+                    ") entries must be strictly positive and finite");
+    t += sz;
+  }
+  throw Error(BP_ERR_CUDA, "internal: graph validation passes disagree");
+}
+
+// Pinned host blocks (the process-wide pool, engine.cu) the conversion passes
+// write the device layout into; their H2D copies run on the build stream.
+struct Staging {
+  cudaStream_t st = nullptr;
+  std::vector<std::pair<void*, size_t>> blocks;  // size 0: plain heap block (no device present yet)
+  ~Staging() {
+    if (st) cudaStreamSynchronize(st);
+    for (auto& b : blocks)
+      if (b.second) pinned_release(b.first, b.second);
+      else std::free(b.first);
+    if (st) cudaStreamDestroy(st);
+  }
+  cudaStream_t stream() {
+    if (!st) cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    return st;
+  }
+  template <class T>
+  T* get(size_t n) {
+    const size_t bytes = ((std::max<size_t>(n * sizeof(T), 1) + (1u << 20) - 1) >> 20) << 20;  // 1 MiB classes
+    try {
+      void* p = pinned_acquire(bytes);
+      blocks.emplace_back(p, bytes);
+      return static_cast<T*>(p);
+    } catch (const Error&) {  // no usable device: validation still runs (and raises) on the host
+      cudaGetLastError();
+      void* p = std::malloc(bytes);
+      if (!p) throw Error(BP_ERR_OOM, "host staging");
+      blocks.emplace_back(p, 0);
+      return static_cast<T*>(p);
+    }
+  }
+  // buf <- host[0, n) (host: a staged block, or pageable memory)
+  void put(DevBuf& buf, const void* host, size_t n) {
+    buf.alloc_async(n, stream());
+    if (n) cuda_check(cudaMemcpyAsync(buf.p, host, n, cudaMemcpyHostToDevice, st), "h2d");
+  }
+  // pageable source: copied into a staged block by the pool first
+  void put_copy(DevBuf& buf, const void* host, size_t n) {
+    char* h = get<char>(n);
+    parallel_for(n, [&](uint64_t a, uint64_t b) { std::memcpy(h + a, static_cast<const char*>(host) + a, b - a); });
+    put(buf, h, n);
+  }
+};
+
+// generate_ising's lattice numbering, checked row by row on the pool
+uint32_t detect_lattice_parallel(uint32_t V, uint32_t E, const uint32_t* ep) {
+  if (V < 2 || E == 0) return 0;
+  uint32_t C = V;
+  if (E >= 2 && ep[0] == 0 && ep[1] == 1 && ep[2] == 0 && ep[3] > 1) C = ep[3];
+  if (V % C) return 0;
+  const uint64_t R = V / C;
+  if (static_cast<uint64_t>(E) != R * (C - 1) + (R - 1) * C) return 0;
+  const uint64_t bad = first_bad(R, [&](uint64_t r) {
+    uint64_t e = r * (2ull * C - 1);  // every earlier row holds C - 1 right + C down edges
+    for (uint64_t c = 0; c < C; ++c) {
+      const uint64_t v = r * C + c;
+      if (c + 1 < C) {
+        if (ep[2 * e] != v || ep[2 * e + 1] != v + 1) return true;
+        ++e;
+      }
+      if (r + 1 < R) {
+        if (ep[2 * e] != v || ep[2 * e + 1] != v + C) return true;
+        ++e;
+      }
+    }
+    return false;
+  }, C >= 64);
+  return bad == R ? C : 0;
+}
+
+struct VAcc {
+  uint32_t maxq = 0, minq = std::numeric_limits<uint32_t>::max();
+  uint64_t usz = 0;
+  bool zero = false, bad = false;
+  double min_mu = std::numeric_limits<double>::infinity();
+};
+struct EAcc {
+  bool bad = false, ising = true;
+  double min_rho = 1.0, min_m = std::numeric_limits<double>::infinity();
+};
+
+// collapse-bound minima of one table t (ci x cj, row-major) of edge (i, j):
+// rho = min t(y,x) / row sum, m = max_x psi(x) * row sum, both orientations
+inline void table_minima(const double* t, uint32_t ci, uint32_t cj, const double* ui, const double* uj,
+                         double& rho, double& m) {
+  double mf = 0.0, mb = 0.0;
+  for (uint32_t x = 0; x < ci; ++x) {
+    double r = 0.0;
+    for (uint32_t y = 0; y < cj; ++y) r += t[static_cast<size_t>(x) * cj + y];
+    for (uint32_t y = 0; y < cj; ++y) rho = std::min(rho, t[static_cast<size_t>(x) * cj + y] / r);
+    mf = std::max(mf, ui[x] * r);
+  }
+  for (uint32_t y = 0; y < cj; ++y) {
+    double r = 0.0;
+    for (uint32_t x = 0; x < ci; ++x) r += t[static_cast<size_t>(x) * cj + y];
+    for (uint32_t x = 0; x < ci; ++x) rho = std::min(rho, t[static_cast<size_t>(x) * cj + y] / r);
+    mb = std::max(mb, uj[y] * r);
+  }
+  m = std::min(m, std::min(mf, mb));
 }
 
 }  // namespace
@@ -325,83 +490,154 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   const uint32_t V = d->num_vertices, E = d->num_edges;
   if (E > (1u << 31) - 1) throw_model("too many edges for 32-bit directed edge ids");
   if (V && !d->cardinalities) throw_invalid("null cardinalities");
-  // --- validation (mrf.cpp:28-91) ---
-  uint32_t maxq = 0;
-  size_t usz = 0;
-  for (uint32_t v = 0; v < V; ++v) {
-    if (d->cardinalities[v] == 0) throw_model("vertex " + std::to_string(v) + " has cardinality 0");
-    maxq = std::max(maxq, d->cardinalities[v]);
-    usz += d->cardinalities[v];
-  }
-  stage("cards");
-  if (usz && !d->unary_values) throw_invalid("null unary values");
-  const bool all_binary = V > 0 && maxq == 2 && usz == 2ull * V;
-  auto bad_entry = [](double u) { return !(u > 0.0) || !std::isfinite(u); };
-  if (all_binary) {  // offsets 2v: checked in parallel, first offender reported
-    const uint64_t bv = first_bad(V, [&](uint64_t v) {
-      return bad_entry(d->unary_values[2 * v]) || bad_entry(d->unary_values[2 * v + 1]);
+  const uint32_t* cards = d->cardinalities;
+  // --- validation (mrf.cpp:28-91) and layout conversion: O(V + E) passes on
+  // the host pool; any violation re-runs the reference's sequential order
+  // (throw_first_model_error) so the first error and its message match ---
+  VAcc va;
+  {
+    const unsigned nch = pool_chunks(V);
+    std::vector<VAcc> acc(nch);
+    parallel_chunks(V, nch, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      VAcc& a = acc[t];
+      for (uint64_t v = lo; v < hi; ++v) {
+        const uint32_t q = cards[v];
+        a.zero |= q == 0;
+        a.maxq = std::max(a.maxq, q);
+        a.minq = std::min(a.minq, q);
+        a.usz += q;
+      }
     });
-    if (bv < V) throw_model("unary(" + std::to_string(bv) + ") entries must be strictly positive and finite");
-  } else {
-    for (uint32_t v = 0, o = 0; v < V; o += d->cardinalities[v], ++v)
-      for (uint32_t x = 0; x < d->cardinalities[v]; ++x)
-        if (bad_entry(d->unary_values[o + x]))
-          throw_model("unary(" + std::to_string(v) + ") entries must be strictly positive and finite");
+    for (const VAcc& a : acc) {
+      va.zero |= a.zero;
+      va.maxq = std::max(va.maxq, a.maxq);
+      va.minq = std::min(va.minq, a.minq);
+      va.usz += a.usz;
+    }
   }
-  stage("unary check");
+  if (va.zero) throw_first_model_error(d);
+  const uint32_t maxq = va.maxq;
+  const uint64_t usz = va.usz;
+  if (usz && !d->unary_values) throw_invalid("null unary values");
+  const bool uniform_cards = V == 0 || va.minq == va.maxq;
+  const bool bin_cards = V > 0 && uniform_cards && maxq == 2;
+  stage("cards");
+  Staging stg;
+  float* ulo = bin_cards ? stg.get<float>(V) : nullptr;
+  std::vector<size_t> uoff;  // mixed cardinalities: unary offsets
+  if (!uniform_cards) {
+    uoff.assign(static_cast<size_t>(V) + 1, 0);
+    for (uint32_t v = 0; v < V; ++v) uoff[v + 1] = uoff[v] + cards[v];
+  }
+  auto unary_at = [&](uint64_t v) -> size_t { return uniform_cards ? v * maxq : uoff[v]; };
+  {
+    const unsigned nch = pool_chunks(V);
+    std::vector<VAcc> acc(nch);
+    parallel_chunks(V, nch, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      VAcc& a = acc[t];
+      for (uint64_t v = lo; v < hi; ++v) {
+        const double* u = d->unary_values + unary_at(v);
+        double mu = 0.0;
+        for (uint32_t x = 0; x < cards[v]; ++x) {
+          a.bad |= bad_entry(u[x]);
+          mu = std::max(mu, u[x]);
+        }
+        a.min_mu = std::min(a.min_mu, mu);
+        if (bin_cards) {  // base-2 log-odds (one log of the ratio unless it leaves the double range)
+          const double r = u[1] / u[0];
+          ulo[v] = static_cast<float>(r > 0.0 && r <= std::numeric_limits<double>::max() ? std::log2(r)
+                                                                                    : std::log2(u[1]) - std::log2(u[0]));
+        }
+      }
+    });
+    for (const VAcc& a : acc) {
+      va.bad |= a.bad;
+      va.min_mu = std::min(va.min_mu, a.min_mu);
+    }
+  }
+  if (va.bad) throw_first_model_error(d);
+  stage("unary");
   if (E && (!d->edge_endpoints || !d->pairwise_values)) throw_invalid("null edge arrays");
-  // endpoint checks in parallel; the first offending edge gets the
-  // reference's message for its first failing test
-  const uint64_t bep = first_bad(E, [&](uint64_t e) {
-    const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
-    return i >= V || j >= V || i >= j;
-  });
-  if (bep < E) {
-    const uint32_t i = d->edge_endpoints[2 * bep], j = d->edge_endpoints[2 * bep + 1];
-    if (i >= V || j >= V) throw_model("edge " + std::to_string(bep) + " references a vertex out of range");
-    if (i == j) throw_model("edge " + std::to_string(bep) + " is a self-loop on vertex " + std::to_string(i));
-    throw_model("edge " + std::to_string(bep) + " endpoints must satisfy i < j");
-  }
-  // table offsets: e q^2 for a uniform cardinality q, else a prefix sum
-  const bool uniform_cards = V == 0 || (maxq * static_cast<uint64_t>(V) == usz);
+  const uint32_t* ep = d->edge_endpoints;
+  // table offsets: e q^2 for a uniform cardinality q, else a prefix sum (after
+  // the endpoints are known to be in range)
   std::vector<size_t> poff;
   if (!uniform_cards) {
+    if (first_bad(E, [&](uint64_t e) {
+          const uint32_t i = ep[2 * e], j = ep[2 * e + 1];
+          return i >= V || j >= V || i >= j;
+        }) < E)
+      throw_first_model_error(d);
     poff.assign(static_cast<size_t>(E) + 1, 0);
     for (uint32_t e = 0; e < E; ++e)
-      poff[e + 1] = poff[e] + static_cast<size_t>(d->cardinalities[d->edge_endpoints[2 * e]]) *
-                                  d->cardinalities[d->edge_endpoints[2 * e + 1]];
+      poff[e + 1] = poff[e] + static_cast<size_t>(cards[ep[2 * e]]) * cards[ep[2 * e + 1]];
   }
   auto table_at = [&](uint64_t e) -> size_t { return uniform_cards ? e * maxq * maxq : poff[e]; };
-  auto table_size = [&](uint64_t e) -> size_t { return uniform_cards ? size_t{maxq} * maxq : poff[e + 1] - poff[e]; };
-  stage("edge check");
-  const uint64_t be = first_bad(E, [&](uint64_t e) {
-    const size_t k0 = table_at(e), k1 = k0 + table_size(e);
-    for (size_t k = k0; k < k1; ++k)
-      if (bad_entry(d->pairwise_values[k])) return true;
-    return false;
-  });
-  if (be < E)
-    throw_model("pairwise(" + std::to_string(d->edge_endpoints[2 * be]) + "," +
-                std::to_string(d->edge_endpoints[2 * be + 1]) + ") entries must be strictly positive and finite");
-  // generate_ising's lattice numbering: the topology is generated on the
-  // device (no host CSR; the numbering has no duplicate edges by construction)
-  stage("pair check");
-  const uint32_t lat_cols = detect_lattice(V, E, d->edge_endpoints);
+  // one pass over the edges: endpoints, table entries, collapse-bound minima,
+  // and on binary graphs the Ising couplings a = e^J of tables {a, d, d, a}
+  float* isa = bin_cards ? stg.get<float>(E) : nullptr;
+  EAcc ea;
+  {
+    const unsigned nch = pool_chunks(E);
+    std::vector<EAcc> acc(nch);
+    parallel_chunks(E, nch, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      EAcc& a = acc[t];
+      for (uint64_t e = lo; e < hi; ++e) {
+        const uint32_t i = ep[2 * e], j = ep[2 * e + 1];
+        if (i >= V || j >= V || i >= j) {
+          a.bad = true;
+          continue;
+        }
+        const double* tb = d->pairwise_values + table_at(e);
+        const uint32_t ci = cards[i], cj = cards[j];
+        if (bin_cards) {
+          const double t0 = tb[0], t1 = tb[1], t2 = tb[2], t3 = tb[3];
+          a.bad |= bad_entry(t0) || bad_entry(t1) || bad_entry(t2) || bad_entry(t3);
+          // table_minima in closed form: row / column sums of the 2 x 2 table
+          const double r0 = t0 + t1, r1 = t2 + t3, c0 = t0 + t2, c1 = t1 + t3;
+          const double* ui = d->unary_values + 2ull * i;
+          const double* uj = d->unary_values + 2ull * j;
+          a.min_rho = std::min(a.min_rho, std::min(std::min(std::min(t0, t1) / r0, std::min(t2, t3) / r1),
+                                                   std::min(std::min(t0, t2) / c0, std::min(t1, t3) / c1)));
+          a.min_m = std::min(a.min_m, std::min(std::max(ui[0] * r0, ui[1] * r1), std::max(uj[0] * c0, uj[1] * c1)));
+          const bool is = t0 == t3 && t1 == t2;
+          a.ising &= is;
+          // a = e^J = t0 / t1, clamped to e^{+-69} as ising_weight
+          if (is) isa[e] = static_cast<float>(std::min(kIsingAMax, std::max(kIsingAMin, t0 / t1)));
+        } else {
+          const size_t sz = static_cast<size_t>(ci) * cj;
+          for (size_t k = 0; k < sz; ++k) a.bad |= bad_entry(tb[k]);
+          table_minima(tb, ci, cj, d->unary_values + unary_at(i), d->unary_values + unary_at(j), a.min_rho,
+                       a.min_m);
+        }
+      }
+    });
+    for (const EAcc& a : acc) {
+      ea.bad |= a.bad;
+      ea.ising &= a.ising;
+      ea.min_rho = std::min(ea.min_rho, a.min_rho);
+      ea.min_m = std::min(ea.min_m, a.min_m);
+    }
+  }
+  if (ea.bad) throw_first_model_error(d);
+  stage("edges");
+  const uint32_t lat_cols = detect_lattice_parallel(V, E, ep);
   stage("lattice");
   std::vector<uint32_t> off, adj;
-  if (!lat_cols) build_csr(V, E, d->edge_endpoints, off, adj);
-  if (!lat_cols && !(opts && (opts->flags & BP_GRAPH_TRUSTED))) {
-    // duplicate edges: two incoming edges of one vertex from the same source
-    std::vector<uint32_t> mark(V, std::numeric_limits<uint32_t>::max());
-    for (uint32_t v = 0; v < V; ++v)
-      for (uint32_t a = off[v]; a < off[v + 1]; ++a) {
-        const uint32_t s = d->edge_endpoints[adj[a]];
-        if (mark[s] == v) {
-          const uint32_t lo = std::min(s, v), hi = std::max(s, v);
-          throw_model("duplicate edge (" + std::to_string(lo) + ", " + std::to_string(hi) + ")");
+  uint32_t maxdeg = lat_cols ? 4 : 0;
+  if (!lat_cols) {
+    build_csr(V, E, ep, off, adj);
+    for (uint32_t v = 0; v < V; ++v) maxdeg = std::max(maxdeg, off[v + 1] - off[v]);
+    if (!(opts && (opts->flags & BP_GRAPH_TRUSTED))) {
+      // duplicate edges: two incoming edges of one vertex from the same source
+      std::vector<uint32_t> mark(V, std::numeric_limits<uint32_t>::max());
+      for (uint32_t v = 0; v < V; ++v)
+        for (uint32_t a = off[v]; a < off[v + 1]; ++a) {
+          const uint32_t src = ep[adj[a]];
+          if (mark[src] == v) throw_first_model_error(d);
+          mark[src] = v;
         }
-        mark[s] = v;
-      }
+    }
   }
   stage("csr");
   // Can the reference's numeric_error (normalize_in_place: total mass below
@@ -415,44 +651,49 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   // generated instances, any sane input) never collapse in the reference; the
   // others are built with the q-state layout and log-domain tables, and the
   // device computes the reference's mass exactly (generic_logmatvec) to raise
-  // the same error.
-  bool collapse_free = true;
+  // the same error.  First the bound from the global minima (rho, R psi, psi)
+  // and the maximum degree, with a margin of e; the per-message bound only
+  // when that one does not clear.
+  const double floor = std::log(1e-290);
+  bool collapse_free;
   {
-    std::vector<size_t> uoff(static_cast<size_t>(V) + 1, 0);
-    for (uint32_t v = 0; v < V; ++v) uoff[v + 1] = uoff[v] + d->cardinalities[v];
+    const double lr = std::log(ea.min_rho), lm = std::log(ea.min_m), lmu = std::log(va.min_mu);
+    collapse_free = lmu + maxdeg * lr >= floor + 1.0 && (E == 0 || lm + (maxdeg - 1.0) * lr >= floor + 1.0);
+  }
+  if (!collapse_free) {
+    collapse_free = true;
     std::vector<double> lrho(2ull * E), lrmax(2ull * E), LI(V, 0.0);
     for (uint32_t e = 0; e < E; ++e) {
-      const uint32_t i = d->edge_endpoints[2 * e], j = d->edge_endpoints[2 * e + 1];
-      const uint32_t ci = d->cardinalities[i], cj = d->cardinalities[j];
+      const uint32_t i = ep[2 * e], j = ep[2 * e + 1];
+      const uint32_t ci = cards[i], cj = cards[j];
       const double* t = d->pairwise_values + table_at(e);
       double rho_f = 1.0, rho_b = 1.0, mf = 0.0, mb = 0.0;
       for (uint32_t x = 0; x < ci; ++x) {  // d = 2e: rows x_i
         double r = 0.0;
         for (uint32_t y = 0; y < cj; ++y) r += t[static_cast<size_t>(x) * cj + y];
         for (uint32_t y = 0; y < cj; ++y) rho_f = std::min(rho_f, t[static_cast<size_t>(x) * cj + y] / r);
-        mf = std::max(mf, d->unary_values[uoff[i] + x] * r);
+        mf = std::max(mf, d->unary_values[unary_at(i) + x] * r);
       }
       for (uint32_t y = 0; y < cj; ++y) {  // d = 2e + 1: rows x_j
         double r = 0.0;
         for (uint32_t x = 0; x < ci; ++x) r += t[static_cast<size_t>(x) * cj + y];
         for (uint32_t x = 0; x < ci; ++x) rho_b = std::min(rho_b, t[static_cast<size_t>(x) * cj + y] / r);
-        mb = std::max(mb, d->unary_values[uoff[j] + y] * r);
+        mb = std::max(mb, d->unary_values[unary_at(j) + y] * r);
       }
-      lrho[2ull * e] = std::log(rho_f);  // message into j
+      lrho[2ull * e] = std::log(rho_f);      // message into j
       lrho[2ull * e + 1] = std::log(rho_b);  // message into i
       lrmax[2ull * e] = std::log(mf);
       lrmax[2ull * e + 1] = std::log(mb);
       LI[j] += lrho[2ull * e];
       LI[i] += lrho[2ull * e + 1];
     }
-    const double floor = std::log(1e-290);
     for (uint64_t dd = 0; dd < 2ull * E && collapse_free; ++dd) {
-      const uint32_t src = d->edge_endpoints[dd];  // ep[d] = source of d
+      const uint32_t src = ep[dd];  // ep[d] = source of d
       collapse_free = lrmax[dd] + LI[src] - lrho[dd ^ 1ull] >= floor;
     }
     for (uint32_t v = 0; v < V && collapse_free; ++v) {
       double mu = 0.0;
-      for (uint32_t x = 0; x < d->cardinalities[v]; ++x) mu = std::max(mu, d->unary_values[uoff[v] + x]);
+      for (uint32_t x = 0; x < cards[v]; ++x) mu = std::max(mu, d->unary_values[unary_at(v) + x]);
       collapse_free = std::log(mu) + LI[v] >= floor;
     }
   }
@@ -463,50 +704,31 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   g->E = E;
   g->D = 2 * E;
   g->maxq = maxq;
-  g->binary = V > 0 && maxq == 2 && usz == 2ull * V && collapse_free;
-  bool uniform = true;
-  for (uint32_t v = 1; v < V; ++v) uniform = uniform && d->cardinalities[v] == d->cardinalities[0];
-  if (uniform && V) g->uniform_q = d->cardinalities[0];
-  else g->cards_host.assign(d->cardinalities, d->cardinalities + V);
+  g->binary = bin_cards && collapse_free;
+  if (uniform_cards && V) g->uniform_q = cards[0];
+  else g->cards_host.assign(cards, cards + V);
   if (lat_cols) {
-    g->in_off.alloc((static_cast<size_t>(V) + 1) * 4);
-    g->in_adj.alloc(static_cast<size_t>(E) * 8);
-    g->ep.alloc(static_cast<size_t>(E) * 8);
-    k_lattice_topology<<<grid_for(V), 256>>>(V / lat_cols, lat_cols, g->in_off.as<uint32_t>(),
-                                             g->in_adj.as<uint32_t>(), g->ep.as<uint32_t>());
+    g->in_off.alloc_async((static_cast<size_t>(V) + 1) * 4, stg.stream());
+    g->in_adj.alloc_async(static_cast<size_t>(E) * 8, stg.st);
+    g->ep.alloc_async(static_cast<size_t>(E) * 8, stg.st);
+    k_lattice_topology<<<grid_for(V), 256, 0, stg.st>>>(V / lat_cols, lat_cols, g->in_off.as<uint32_t>(),
+                                                        g->in_adj.as<uint32_t>(), g->ep.as<uint32_t>());
     cuda_check(cudaGetLastError(), "lattice topology");
   } else {
-    g->in_off.upload(off.data(), off.size() * 4);
-    g->in_adj.upload(adj.data(), adj.size() * 4);
-    g->ep.upload(d->edge_endpoints, static_cast<size_t>(E) * 8);
+    stg.put_copy(g->in_off, off.data(), off.size() * 4);
+    stg.put_copy(g->in_adj, adj.data(), adj.size() * 4);
+    stg.put_copy(g->ep, ep, static_cast<size_t>(E) * 8);
   }
   stage("topology");
   if (g->binary || V == 0) {
     g->binary = true;
     g->qs = 1;
-    std::vector<float> ulo(V);
-    parallel_for(V, [&](uint64_t a, uint64_t b) {
-      for (uint64_t v = a; v < b; ++v)
-        ulo[v] = static_cast<float>(std::log2(d->unary_values[2 * v + 1]) - std::log2(d->unary_values[2 * v]));
-    });
-    g->unary_lo.upload(ulo.data(), ulo.size() * 4);
-    // Ising tables {a, d, d, a} (generators.cpp:18-22): one coupling per edge
-    const bool ising = E > 0 && first_bad(E, [&](uint64_t e) {
-                                  const double* t = d->pairwise_values + 4ull * e;
-                                  return !(t[0] == t[3] && t[1] == t[2]);
-                                }) == E;
-    if (ising) {
-      std::vector<float> a(E);
-      parallel_for(E, [&](uint64_t lo, uint64_t hi) {
-        for (uint64_t e = lo; e < hi; ++e) {
-          const double* t = d->pairwise_values + 4ull * e;
-          a[e] = ising_weight(std::log(t[0]) - std::log(t[1]));
-        }
-      });
-      g->ising_a.upload(a.data(), a.size() * 4);
+    stg.put(g->unary_lo, ulo, ulo ? static_cast<size_t>(V) * 4 : 0);
+    if (E > 0 && ea.ising) {  // Ising tables {a, d, d, a} (generators.cpp:18-22): one coupling per edge
+      stg.put(g->ising_a, isa, static_cast<size_t>(E) * 4);
       g->par_mode = 1;
     } else {
-      std::vector<float4> par(E);
+      float4* par = stg.get<float4>(E);
       parallel_for(E, [&](uint64_t lo, uint64_t hi) {
         for (uint64_t e = lo; e < hi; ++e) {
           const double* t = d->pairwise_values + 4ull * e;
@@ -516,7 +738,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
                                static_cast<float>(gg - beta));
         }
       });
-      g->epar.upload(par.data(), par.size() * 16);
+      stg.put(g->epar, par, static_cast<size_t>(E) * 16);
     }
   } else {
     const uint32_t qs = stride_for(maxq);
@@ -579,6 +801,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   }
   g->lat_cols = lat_cols;
   g->lat_rows = lat_cols ? V / lat_cols : 0;
+  cuda_check(cudaStreamSynchronize(stg.stream()), "graph upload");
   cuda_check(cudaDeviceSynchronize(), "graph upload");
   stage("potentials");
   return g;

@@ -28,6 +28,9 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf();
   void alloc(size_t n);
+  // no zero-fill and no device synchronisation: the caller overwrites [0, n)
+  // on stream st (only the 64-byte slack is zeroed there)
+  void alloc_async(size_t n, cudaStream_t st);
   void upload(const void* src, size_t n);
   void reset();
   static void trim_cache();  // cudaFree every cached block
