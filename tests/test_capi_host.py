@@ -77,6 +77,12 @@ def test_scheduler_kind_strings(bp):
     (([2, 2], [[1, 1, 1], [1, 1]], []), "entries"),
     (([2, 2], [[1, 1], [1, 1]], [(1, 0, [1, 1, 1, 1])]), "i < j"),
     (([0, 2], [[], [1, 1]], []), "cardinality 0"),
+    # several violations: the reference's first one (vertex order, then edge
+    # order with range / self-loop / order / duplicate / entries per edge)
+    (([2, 2, 2], [[1, 1]] * 3, [(0, 1, [1, 0.0, 1, 1]), (2, 2, [1] * 4)]), r"pairwise\(0,1\)"),
+    (([2, 2, 2], [[1, 1]] * 3, [(0, 1, [1] * 4), (0, 1, [1] * 4), (1, 2, [1, -1, 1, 1])]), "duplicate edge \\(0, 1\\)"),
+    (([2, 2, 2], [[1, 1], [1, float("inf")], [1, 1]], [(2, 2, [1] * 4)]), r"unary\(1\)"),
+    (([2, 3, 2], [[1, 1], [1, 1, 1], [1, 1]], [(0, 1, [1] * 6), (1, 2, [1] * 5 + [float("nan")])]), r"pairwise\(1,2\)"),
 ])
 def test_build_graph_validation_is_host_side(bp, bad, msg):
     """model_error cases of build_graph (mrf.cpp:28-91) are raised before any
