@@ -124,10 +124,10 @@ typedef struct {
 } bp_graph_info;
 
 /* Per-kernel-class device time, filled when BP_RUN_KERNEL_TIMING is set. */
-#define BP_KERNEL_CLASSES 8
+#define BP_KERNEL_CLASSES 9
 typedef struct {
   /* 0 sweep/refresh, 1 select, 2 radix/top-k, 3 splash, 4 init, 5 beliefs, 6 other,
-   * 7 persistent RnBP list-mode tail */
+   * 7 persistent RnBP list-mode tail, 8 fused dense RnBP sweep */
   double ms[BP_KERNEL_CLASSES];
   uint64_t launches[BP_KERNEL_CLASSES];
   uint64_t bytes[BP_KERNEL_CLASSES]; /* algorithmic bytes moved by the timed launches */
@@ -150,6 +150,7 @@ typedef struct {
 #define BP_RUN_LBP_TMA 16u      /* LBP: force the TMA-staged lattice sweep (binary Ising lattices, >= 2 rows) */
 #define BP_RUN_LBP_TILES 32u    /* LBP: force the register-tiled lattice sweep (default below 2^21 vertices) */
 #define BP_RUN_LBP_VERTEX 64u   /* LBP: force the vertex-centric sweep (q-state lattices: instead of lanes over states) */
+#define BP_RUN_NO_FUSED 128u    /* RnBP: run the dense iterations as select + refresh launches, not fused sweeps */
 
 /* LBP sweep kernels (bp_engine_lbp_sweep's *kernel_out) */
 #define BP_LBP_KERNEL_VERTEX 0u /* k_vertex_update: vertex-centric (CSR / generic q-state / Potts lattice) */

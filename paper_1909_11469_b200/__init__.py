@@ -106,9 +106,9 @@ class _Info(C.Structure):
 
 
 class KernelStats(C.Structure):
-    _fields_ = [("ms", C.c_double * 8), ("launches", C.c_uint64 * 8), ("bytes", C.c_uint64 * 8)]
+    _fields_ = [("ms", C.c_double * 9), ("launches", C.c_uint64 * 9), ("bytes", C.c_uint64 * 9)]
 
-    CLASSES = ("update", "select", "topk", "splash", "init", "beliefs", "other", "persist")
+    CLASSES = ("update", "select", "topk", "splash", "init", "beliefs", "other", "persist", "fused")
 
     def as_dict(self):
         return {n: {"ms": self.ms[i], "launches": int(self.launches[i]), "bytes": int(self.bytes[i])}
@@ -127,6 +127,7 @@ RUN_NO_PERSIST = 8
 RUN_LBP_TMA = 16
 RUN_LBP_TILES = 32
 RUN_LBP_VERTEX = 64
+RUN_NO_FUSED = 128
 LBP_KERNELS = {0: "vertex", 1: "tiles", 2: "tma", 3: "qlanes"}  # BP_LBP_KERNEL_*
 GRAPH_TRUSTED = 1
 

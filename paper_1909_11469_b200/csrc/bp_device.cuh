@@ -216,6 +216,8 @@ struct Ctl {
   unsigned long long handover_it;  // iteration at which the graph loop handed over to the persistent kernel
   unsigned int time_stop;
   unsigned int blocks_done;  // last-block-done counter of the kernel-fused finalize / retry (reset by the last block)
+  unsigned int fused_par;    // fused RnBP sweep (kernels_fused.cuh): the state lives in the scratch set when odd
+  unsigned int fused_abort;  // fused RnBP sweep: an empty attempt-0 frontier, the per-kernel loop redoes the iteration
   unsigned long long persist_bytes;  // algorithmic bytes moved by the persistent kernel
   unsigned long long vote_limit_ns;  // row-band partition: time limit, decided by an all-reduced vote
   unsigned long long phase_ns[8];    // persistent kernel phase clock (CTA 0)

@@ -18,6 +18,7 @@
 #include "kernels_rs.cuh"
 #include "kernels_persist.cuh"
 #include "kernels_lbp.cuh"
+#include "kernels_fused.cuh"
 
 namespace bpb {
 namespace {
@@ -52,7 +53,7 @@ unsigned grid_cap(size_t n, int per_sm = 8) {
 }
 
 enum KClass { kKUpdate = 0, kKSelect = 1, kKTopk = 2, kKSplash = 3, kKInit = 4, kKBeliefs = 5, kKOther = 6,
-              kKPersist = 7 };
+              kKPersist = 7, kKFused = 8 };
 
 template <int QS>
 class EngineT final : public EngineBase {
@@ -76,6 +77,12 @@ class EngineT final : public EngineBase {
       cstamp_.alloc(static_cast<size_t>(g.D ? g.D : 1) * 4);
     }
     vlist_.alloc(static_cast<size_t>(g.V) * 4);
+    if (fused_capable()) {  // scratch buffer set of the fused dense RnBP sweep (here, not mid-run)
+      fl_.alloc(msz);
+      fc_.alloc(msz);
+      fu_[0].alloc(g.D);
+      fu_[1].alloc(g.D);
+    }
     ctl_.alloc(sizeof(Ctl));
     hctl_ = static_cast<Ctl*>(pinned_acquire(sizeof(Ctl)));
     std::memset(hctl_, 0, sizeof(Ctl));
@@ -103,6 +110,8 @@ class EngineT final : public EngineBase {
   ~EngineT() override {
     if (gexec_) cudaGraphExecDestroy(gexec_);
     if (graph_) cudaGraphDestroy(graph_);
+    if (fgexec_) cudaGraphExecDestroy(fgexec_);
+    if (fgraph_) cudaGraphDestroy(fgraph_);
     for (auto& ev : evs_) cudaEventDestroy(ev);
     // back to the process-wide pool: cudaFreeHost was measured at 75-750 ms
     // on some calls (page unpinning), on the end-to-end path of every run
@@ -145,6 +154,9 @@ class EngineT final : public EngineBase {
       fetch_ctl_header();
       drain_trace(trace, trace_cap, copied);
     }
+    // RnBP on binary Ising lattices: the dense iterations as fused sweeps
+    if (fused_capable() && !(flags & BP_RUN_NO_FUSED) && prm_.fixed_p < 0.0 && !hctl_->done)
+      run_fused_phase(use_graph, opts, trace, trace_cap, copied);
     if (!hctl_->done) {
       if (use_graph) {
         run_graph_loop(trace, trace_cap, copied);
@@ -973,6 +985,99 @@ class EngineT final : public EngineBase {
   }
   void set_cond_handle(unsigned long long h) {
     k_set_u64<<<1, 1, 0, s_>>>(&ctl()->cond_handle, h);
+    launch_check();
+  }
+
+  // ---- fused dense RnBP sweeps (kernels_fused.cuh)
+  DevBuf fl_, fc_;  // scratch buffer set (live, candidates)
+  DevBuf fu_[2];    // unconverged predicates (r >= eps) of the canonical / scratch set
+  cudaGraph_t fgraph_ = nullptr;
+  cudaGraphExec_t fgexec_ = nullptr;
+  cudaGraphConditionalHandle fcond_{};
+  bool fused_capable() const {
+    return cfg_.kind == BP_RNBP && QS == 1 && g_.lat_cols && g_.par_mode == 1 && !g_.check_collapse &&
+           g_.cnt_row0 == 0 && g_.cnt_row1 >= g_.lat_rows && g_.edge_offset == 0;
+  }
+  void enqueue_fused(unsigned dir) {
+    const unsigned grid = vgrid(k_rnbp_fused, g_.V);
+    timed(kKFused, [&] {
+      if (dir == 0)
+        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), fu_[0].as<uint8_t>(), fl_.as<float>(),
+                                              fc_.as<float>(), fu_[1].as<uint8_t>(), ctl(), eps_, prm_, 0u);
+      else
+        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, fl_.as<float>(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(),
+                                              cand(), fu_[0].as<uint8_t>(), ctl(), eps_, prm_, 1u);
+    });
+    launch_check();
+  }
+  // The dense phase: WHILE(cond) { fused sweep A -> S, fused sweep S -> A } as
+  // one CUDA graph (the finalize of each sweep sets cond), chunked like
+  // run_graph_loop for the trace ring; then the state back in the canonical
+  // set.  Without graphs (kernel timing): batches of sweep pairs.
+  void run_fused_phase(bool use_graph, const bp_run_opts* opts, bp_iter_record* trace, uint64_t cap,
+                       uint64_t& copied) {
+    timed(kKOther, [&] {
+      k_fused_enter<<<grid_cap(g_.D), kBlock, 0, s_>>>(res_.as<float>(), fu_[0].as<uint8_t>(), g_.D, eps_);
+    });
+    launch_check();
+    if (use_graph) {
+      if (!fgexec_) {
+        cuda_check(cudaGraphCreate(&fgraph_, 0), "graph create");
+        cuda_check(cudaGraphConditionalHandleCreate(&fcond_, fgraph_, 1, cudaGraphCondAssignDefault), "cond handle");
+        cudaGraphNodeParams p{};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = fcond_;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        cuda_check(cudaGraphAddNode(&node, fgraph_, nullptr, 0, &p), "graph add conditional");
+        cuda_check(cudaStreamBeginCaptureToGraph(s_, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeRelaxed),
+                   "begin capture");
+        const uint64_t l0 = launches_;
+        enqueue_fused(0);
+        enqueue_fused(1);
+        launches_ = l0;
+        cudaGraph_t out_body;
+        cuda_check(cudaStreamEndCapture(s_, &out_body), "end capture");
+        cuda_check(cudaGraphInstantiate(&fgexec_, fgraph_, 0), "graph instantiate");
+      }
+      set_cond_handle(static_cast<unsigned long long>(fcond_));
+      uint64_t bodies = 0;
+      for (;;) {
+        const uint64_t start_it = hctl_->iteration, par0 = hctl_->fused_par;
+        set_iteration_budget(start_it + kTraceRing / 2);
+        cuda_check(cudaGraphLaunch(fgexec_, s_), "graph launch");
+        fetch_ctl_header();
+        drain_trace(trace, cap, copied);
+        // each body launches both sweeps; an aborted sweep ran without advancing the iteration
+        const uint64_t sweeps = hctl_->iteration - start_it + hctl_->fused_abort;
+        bodies += std::max<uint64_t>(1, (sweeps + par0 + 1) / 2);
+        if (hctl_->done && hctl_->stop_reason == kStopMaxIter && hctl_->iteration < cfg_.max_iterations &&
+            budget_stop_) {
+          clear_budget_stop();
+          if (hctl_->cl_state == 0u && !hctl_->fused_abort) continue;
+        }
+        break;
+      }
+      launches_ += 2 * bodies;
+      set_cond_handle(0);
+    } else {
+      uint32_t batch = opts && opts->batch ? opts->batch : 16;
+      while (!hctl_->done && hctl_->cl_state == 0u && !hctl_->fused_abort) {
+        for (uint32_t b = 0; b < (batch + 1) / 2; ++b) {
+          enqueue_fused(0);
+          enqueue_fused(1);
+        }
+        fetch_ctl_header();
+        drain_trace(trace, cap, copied);
+        if (!(opts && opts->batch)) batch = std::min<uint32_t>(batch * 2, 256);
+      }
+    }
+    timed(kKOther, [&] {
+      k_fused_exit<<<grid_cap(g_.D), kBlock, 0, s_>>>(ctl(), fl_.as<float>(), fc_.as<float>(), fu_[0].as<uint8_t>(),
+                                                      fu_[1].as<uint8_t>(), live(), cand(), res_.as<float>(), g_.D);
+    });
     launch_check();
   }
 

@@ -25,7 +25,7 @@ enum UpdateMode : int {
 };
 
 enum FinMode : int { kFinNone = 0, kFinLbp = 1, kFinInit = 2, kFinIter = 3, kFinApply = 4,
-                     kFinInitExt = 5, kFinIterExt = 6 };  // *Ext: RnBP band, all-reduced sums
+                     kFinInitExt = 5, kFinIterExt = 6, kFinFused = 7 };  // *Ext: RnBP band, all-reduced sums
 
 constexpr int kSinkCap = 4096;
 
@@ -205,7 +205,7 @@ __device__ __forceinline__ void fin_record(Ctl* c, unsigned long long it, unsign
 // control-block round trips would cost microseconds.
 struct FinRegs {
   unsigned done, converged, numeric_error, has_prev, unconverged, prev_unconverged, nflag, dense;
-  unsigned stamp, stop_reason, cl_cur, use_clist, cl_state, persist_ok, rx_prefix;
+  unsigned stamp, stop_reason, cl_cur, use_clist, cl_state, persist_ok, rx_prefix, fused_par, fused_abort;
   unsigned cl_n[2];
   unsigned long long iteration, sweeps, max_iterations, msgs_total, evals_total, vertex_visits, t0_ns,
       time_limit_ns, frontier, survivors, rx_above, trace_len, cond_handle, handover_it;
@@ -226,6 +226,8 @@ struct FinRegs {
     cl_state = c->cl_state;
     persist_ok = c->persist_ok;
     rx_prefix = c->rx_prefix;
+    fused_par = c->fused_par;
+    fused_abort = c->fused_abort;
     cl_n[0] = c->cl_n[0];
     cl_n[1] = c->cl_n[1];
     iteration = c->iteration;
@@ -257,6 +259,8 @@ struct FinRegs {
     c->cl_cur = cl_cur;
     c->cl_state = cl_state;
     c->rx_prefix = rx_prefix;
+    c->fused_par = fused_par;
+    c->fused_abort = fused_abort;
     c->cl_n[0] = cl_n[0];
     c->cl_n[1] = cl_n[1];
     c->iteration = iteration;
@@ -518,6 +522,13 @@ __device__ __forceinline__ void finalize_block(Ctl* c, int mode, uint32_t D, con
       f.unconverged = static_cast<unsigned>(static_cast<long long>(f.unconverged) + delta);
       fin_reset_scratch(f);
       break;
+    case kFinFused:  // one fused RnBP sweep wrote the other buffer set
+      f.fused_par ^= 1u;
+      if (frontier == 0 && v[3] > 0)
+        f.fused_abort = 1u;  // empty attempt-0 frontier: nothing changed, the retry path redoes the iteration
+      else
+        fin_iter(f, c->trace, delta, frontier, D);
+      break;
     default:
       break;
   }
@@ -525,8 +536,9 @@ __device__ __forceinline__ void finalize_block(Ctl* c, int mode, uint32_t D, con
   const bool handover = f.persist_ok && f.cl_state == 2u;
   if (handover && !f.handover_it) f.handover_it = f.iteration;
   f.store(c);
+  const bool stop = f.done || handover || (mode == kFinFused && (f.fused_abort || f.cl_state != 0u));
   if (f.cond_handle && mode != kFinApply)
-    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(f.cond_handle), f.done || handover ? 0u : 1u);
+    cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(f.cond_handle), stop ? 0u : 1u);
 }
 
 static __global__ void __launch_bounds__(kSlots) k_finalize(Ctl* c, int mode, uint32_t D,
