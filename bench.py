@@ -341,16 +341,20 @@ def run_b200(args):
         # select class = residual scan 4 B per directed edge per iteration + commit
         # of every selected edge (read candidate 4 B, write message 4 B, zero residual 4 B)
         sel_bytes = 4 * D * ri.iterations + 12 * ri.messages_updated_total
-        dom = "update" if ks["update"]["ms"] >= ks["select"]["ms"] else "select"
+        fb = ks["fused"]["bytes"]
+        cls_bytes = {"update": upd_bytes, "select": sel_bytes, "fused": fb}
+        cls_name = {"update": "k_vertex_update<Init/Delta> (dense touched refresh)",
+                    "select": "k_rnbp_select (filter + Bernoulli + commit)",
+                    "fused": "k_rnbp_fused (fused select + commit + refresh sweep, ping-pong lattice state)"}
+        dom = max(cls_bytes, key=lambda k: ks[k]["ms"])
         roof = _roofline(
-            "k_vertex_update<Init/Delta> (dense touched refresh)" if dom == "update" else
-            "k_rnbp_select (filter + Bernoulli + commit)", upd_bytes if dom == "update" else sel_bytes,
-            ks[dom]["ms"], peak, peak_src, launches=ks[dom]["launches"], kernel_shares=shares,
-            traffic=_read_traffic("rnbp_refresh" if dom == "update" else "rnbp_select"),
-            select={"bytes": sel_bytes, "ms": ks["select"]["ms"],
-                    "GBps": sel_bytes / (ks["select"]["ms"] / 1e3) / 1e9 if ks["select"]["ms"] else None},
-            regime="1000^2: the 70 MB working set is L2-resident within a window (L2 flushed between steps); "
-                   "the HBM-bound configs are config4_potts4096 and config5_16k below")
+            cls_name[dom], cls_bytes[dom], ks[dom]["ms"], peak, peak_src, launches=ks[dom]["launches"],
+            kernel_shares=shares, fused_iterations=ri.fused_iterations,
+            bytes_per_unit=("40 B per edge pair + 4 B per vertex per sweep (84 B/vertex on the grid)" if dom == "fused"
+                            else None),
+            traffic=_read_traffic({"update": "rnbp_refresh", "select": "rnbp_select", "fused": "rnbp_fused1000"}[dom]),
+            regime="1000^2: the 84 MB ping-pong working set mostly L2-resident within a window (L2 flushed between "
+                   "steps); the HBM-bound configs are config4_potts4096 and config5_16k below")
 
         cpu_head = _ref_headline(min(K, 3), 1) if ws == 1 else None
         extra = {
@@ -564,14 +568,24 @@ def _config5(bp, torch, device, peak, peak_src, cpu_head):
     r = bp.run_ex(g, cfg, beliefs=False)
     ri = bp.run_ex(g, cfg, beliefs=False, kernel_timing=True)
     ks = ri.kernel_stats
-    ub = refresh_bytes(ri.vertex_visits, ri.message_evaluations)
-    sb = 4 * D * ri.iterations + 12 * ri.messages_updated_total
     out["rnbp"] = {"value": r.messages_updated_total / (r.device_ms / 1e3), "unit": UNIT, "iterations": r.iterations,
                    "device_ms": round(r.device_ms, 3), "ms_per_iteration": round(r.device_ms / max(1, r.iterations), 4),
-                   "refresh": _roofline("k_vertex_update<Init/Delta> (dense touched refresh)", ub, ks["update"]["ms"],
-                                        peak, peak_src, launches=ks["update"]["launches"]),
-                   "select": _roofline("k_rnbp_select (filter + Bernoulli + commit)", sb, ks["select"]["ms"], peak,
-                                       peak_src, launches=ks["select"]["launches"])}
+                   "fused": _roofline("k_rnbp_fused (fused select + commit + refresh sweep)", ks["fused"]["bytes"],
+                                      ks["fused"]["ms"], peak, peak_src, launches=ks["fused"]["launches"],
+                                      sweeps=ri.fused_iterations, bytes_per_vertex=84,
+                                      ms_per_sweep=ks["fused"]["ms"] / max(1, ri.fused_iterations),
+                                      traffic=_read_traffic("rnbp_fused16k"))}
+    # the two-launch loop the fused sweep replaces (select + refresh), same window
+    rn = bp.run_ex(g, cfg, beliefs=False, flags=bp.RUN_NO_FUSED, kernel_timing=True)
+    kn = rn.kernel_stats
+    ub = refresh_bytes(rn.vertex_visits, rn.message_evaluations)
+    sb = 4 * D * rn.iterations + 12 * rn.messages_updated_total
+    out["rnbp"]["two_launch"] = {
+        "ms_per_iteration": round((kn["update"]["ms"] + kn["select"]["ms"]) / max(1, rn.iterations), 4),
+        "refresh": _roofline("k_vertex_update<Init/Delta> (dense touched refresh)", ub, kn["update"]["ms"],
+                             peak, peak_src, launches=kn["update"]["launches"]),
+        "select": _roofline("k_rnbp_select (filter + Bernoulli + commit)", sb, kn["select"]["ms"], peak,
+                            peak_src, launches=kn["select"]["launches"])}
     del g
     torch.cuda.empty_cache()
     if cpu_head:

@@ -110,6 +110,7 @@ typedef struct {
   uint64_t splashes;               /* residual splash: splashes applied (all iterations)    */
   uint64_t splash_rounds;          /* residual splash: parallel claiming rounds             */
   uint64_t persist_iterations;     /* RnBP: iterations run inside the persistent tail kernel */
+  uint64_t fused_iterations;       /* RnBP: dense iterations run as fused sweeps (k_rnbp_fused) */
 } bp_run_result;
 
 typedef struct {

@@ -96,7 +96,7 @@ class _Result(C.Structure):
                 ("trace_len", C.c_uint64), ("device_ms", C.c_double),
                 ("message_evaluations", C.c_uint64), ("gpu_launches", C.c_uint64),
                 ("vertex_visits", C.c_uint64), ("splashes", C.c_uint64), ("splash_rounds", C.c_uint64),
-                ("persist_iterations", C.c_uint64)]
+                ("persist_iterations", C.c_uint64), ("fused_iterations", C.c_uint64)]
 
 
 class _Info(C.Structure):
@@ -334,6 +334,7 @@ class RunResult:
     splashes: int = 0
     splash_rounds: int = 0
     persist_iterations: int = 0
+    fused_iterations: int = 0
     messages: Optional[np.ndarray] = field(default=None, repr=False)
 
     def trace_signature(self) -> str:
@@ -555,7 +556,7 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
                      int(res.messages_updated_total), bt, trace, float(res.device_ms),
                      int(res.message_evaluations), int(res.gpu_launches), int(res.vertex_visits),
                      stats.as_dict() if kernel_timing else None, int(res.splashes), int(res.splash_rounds),
-                     int(res.persist_iterations),
+                     int(res.persist_iterations), int(res.fused_iterations),
                      msgs[: int(graph.info.message_values)] if msgs is not None else None)
 
 

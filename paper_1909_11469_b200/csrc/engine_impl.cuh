@@ -125,6 +125,7 @@ class EngineT final : public EngineBase {
            uint64_t trace_cap) override {
     const uint32_t flags = opts ? opts->flags : 0u;
     timing_ = (flags & BP_RUN_KERNEL_TIMING) != 0;
+    fused_iters_ = fused_sweeps_ = 0;
     stats_ = opts ? opts->stats : nullptr;
     if (stats_) std::memset(stats_, 0, sizeof(*stats_));
     launches_ = 0;
@@ -198,7 +199,12 @@ class EngineT final : public EngineBase {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     collect_timing();
-    if (stats_) stats_->bytes[kKPersist] = hctl_->persist_bytes;
+    if (stats_) {
+      stats_->bytes[kKPersist] = hctl_->persist_bytes;
+      // fused sweep (kernels_fused.cuh): per edge pair live + candidate read and
+      // written (2 x 16 B), predicates (2 x 2 B), coupling 4 B; unary 4 B per vertex
+      stats_->bytes[kKFused] = fused_sweeps_ * (40ull * g_.E + 4ull * g_.V);
+    }
 
     std::memset(res, 0, sizeof(*res));
     res->converged = hctl_->converged ? 1 : 0;
@@ -212,6 +218,7 @@ class EngineT final : public EngineBase {
     res->splash_rounds = hctl_->rs_rounds;
     res->persist_iterations =
         persist_ && hctl_->handover_it && hctl_->iteration > hctl_->handover_it ? hctl_->iteration - hctl_->handover_it : 0;
+    res->fused_iterations = fused_iters_;
     res->gpu_launches = launches_;
     res->wall_time = std::chrono::duration<double>(Clock::now() - t0).count();
   }
@@ -991,6 +998,7 @@ class EngineT final : public EngineBase {
   // ---- fused dense RnBP sweeps (kernels_fused.cuh)
   DevBuf fl_, fc_;  // scratch buffer set (live, candidates)
   DevBuf fu_[2];    // unconverged predicates (r >= eps) of the canonical / scratch set
+  uint64_t fused_iters_ = 0, fused_sweeps_ = 0;  // iterations run fused; sweeps (an aborted one included)
   cudaGraph_t fgraph_ = nullptr;
   cudaGraphExec_t fgexec_ = nullptr;
   cudaGraphConditionalHandle fcond_{};
@@ -998,8 +1006,16 @@ class EngineT final : public EngineBase {
     return cfg_.kind == BP_RNBP && QS == 1 && g_.lat_cols && g_.par_mode == 1 && !g_.check_collapse &&
            g_.cnt_row0 == 0 && g_.cnt_row1 >= g_.lat_rows && g_.edge_offset == 0;
   }
+  unsigned fused_grid() {
+    // one resident wave; BPB_FUSED_TPB = n: ~n tiles per block instead (tuning)
+    static const char* e = std::getenv("BPB_FUSED_TPB");
+    const uint64_t ntiles = static_cast<uint64_t>(g_.lat_rows) * ((g_.lat_cols + kFusedStrip - 1) / kFusedStrip);
+    if (e && std::atoi(e) > 0)
+      return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles / std::atoi(e), 1u << 30)));
+    return vgrid(k_rnbp_fused, g_.V);
+  }
   void enqueue_fused(unsigned dir) {
-    const unsigned grid = vgrid(k_rnbp_fused, g_.V);
+    const unsigned grid = fused_grid();
     timed(kKFused, [&] {
       if (dir == 0)
         k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), fu_[0].as<uint8_t>(), fl_.as<float>(),
@@ -1016,6 +1032,7 @@ class EngineT final : public EngineBase {
   // set.  Without graphs (kernel timing): batches of sweep pairs.
   void run_fused_phase(bool use_graph, const bp_run_opts* opts, bp_iter_record* trace, uint64_t cap,
                        uint64_t& copied) {
+    const uint64_t it_in = hctl_->iteration;
     timed(kKOther, [&] {
       k_fused_enter<<<grid_cap(g_.D), kBlock, 0, s_>>>(res_.as<float>(), fu_[0].as<uint8_t>(), g_.D, eps_);
     });
@@ -1074,6 +1091,8 @@ class EngineT final : public EngineBase {
         if (!(opts && opts->batch)) batch = std::min<uint32_t>(batch * 2, 256);
       }
     }
+    fused_iters_ = hctl_->iteration - it_in;
+    fused_sweeps_ = fused_iters_ + hctl_->fused_abort;
     timed(kKOther, [&] {
       k_fused_exit<<<grid_cap(g_.D), kBlock, 0, s_>>>(ctl(), fl_.as<float>(), fc_.as<float>(), fu_[0].as<uint8_t>(),
                                                       fu_[1].as<uint8_t>(), live(), cand(), res_.as<float>(), g_.D);
