@@ -344,6 +344,35 @@ BP_API int bp_band_comm_create_local(bp_band_comm** out);
 BP_API void bp_band_comm_destroy(bp_band_comm* c);
 BP_API int bp_band_run(struct bp_engine* const* bands, uint32_t nbands, bp_band_comm* comm, bp_run_result* result);
 BP_API int bp_band_rnbp_fallback(struct bp_engine* e, uint64_t global_d);
+
+/* ---- Vertex-range partition of ANY binary pairwise MRF (north_star: LBP and
+ * RnBP on large grids and random graphs partitioned across GPUs) ------------
+ * bp_graph_create_part: part `part` of `nparts` owns global vertices
+ *   [v0, v1) = [V part / nparts, V (part + 1) / nparts) and every message whose
+ *   source it owns.  Its local graph holds the edges with an owned endpoint
+ *   (global order and orientation; build_graph's validation runs on the whole
+ *   model, mrf.cpp:28-91) with local vertices = the owned ones in order, then
+ *   one ghost per outside neighbour.  Every iteration the messages that cross
+ *   the cut move to the part that owns their target (one send / recv run per
+ *   peer part, ordered by global directed id on both sides).
+ * bp_part_engine_create: its engine with owned halo buffers; drive the parts
+ *   with bp_band_run (NCCL: one part per rank; local: parts 0 .. P-1 in this
+ *   process).  LBP owned messages and RnBP runs (draws keyed by GLOBAL edge
+ *   ids) are identical to the unpartitioned run; beliefs of local vertices
+ *   [0, v1 - v0) are the owned ones. */
+typedef struct {
+  uint32_t part, nparts;
+  uint32_t v0, v1;              /* owned global vertices [v0, v1) = local [0, v1 - v0) */
+  uint32_t ghost_vertices;      /* local [v1 - v0, v1 - v0 + ghost_vertices) */
+  uint32_t local_edges;
+  uint32_t peers;               /* parts exchanging cut messages with this one */
+  uint32_t _pad;
+  uint64_t send_messages, recv_messages;  /* cut messages per iteration (all peers) */
+  uint64_t owned_directed;      /* directed edges whose source is owned */
+} bp_part_info;
+BP_API int bp_graph_create_part(const bp_graph_desc* desc, uint32_t part, uint32_t nparts,
+                                const bp_device_opts* opts, struct bp_graph** out, bp_part_info* info);
+BP_API int bp_part_engine_create(const struct bp_graph* g, const bp_sched_config* cfg, struct bp_engine** out);
 BP_API uint64_t bp_philox_u53(uint64_t seed, uint64_t iteration, uint32_t attempt, uint64_t d);
 
 /* ---- Diagnostics: the DEVICE random stream, for known-answer tests ---------

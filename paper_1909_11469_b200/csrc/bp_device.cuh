@@ -53,7 +53,21 @@ struct DevGraph {
   // 1: `table` holds log2 t (unscaled) and messages are contracted in the log
   // domain (models whose messages can collapse in the reference, graph.cu)
   uint32_t log_tables;
+  // vertex-range partition (bp_graph_create_part): local vertices [0, own_v)
+  // are owned (the rest are ghosts, never updated); egid maps a local edge to
+  // its global id (RnBP draws use global ids).  own_v = UINT32_MAX, egid =
+  // nullptr: no such partition.
+  uint32_t own_v;
+  const uint32_t* __restrict__ egid;
 };
+
+// global id of local edge e (partitions draw with global ids)
+__device__ __forceinline__ unsigned long long global_edge(const DevGraph& g, uint32_t e) {
+  return g.egid ? static_cast<unsigned long long>(g.egid[e]) : e + g.edge_offset;
+}
+__device__ __forceinline__ unsigned long long global_directed(const DevGraph& g, uint32_t d) {
+  return 2ull * global_edge(g, d >> 1) + (d & 1u);
+}
 
 // numeric_error parity (normalize_in_place, messages.cpp:41-49): the reference
 // throws when a message's unnormalised mass falls below 1e-300.

@@ -304,6 +304,7 @@ int bp_band_engine_create(const bp_graph* g, const bp_sched_config* cfg, const b
     band->cfg = *cfg;
     band->stream = e->stream();
     band->halo = h;
+    band->lattice_peers();
     *out = new bp_engine{std::move(e), g, *cfg, std::move(band)};
   });
 }
@@ -330,6 +331,54 @@ int bp_band_engine_create_owned(const bp_graph* g, const bp_sched_config* cfg, c
     band->cfg = *cfg;
     band->stream = e->stream();
     band->halo = h;
+    band->lattice_peers();
+    *out = new bp_engine{std::move(e), g, *cfg, std::move(band)};
+  });
+}
+
+int bp_graph_create_part(const bp_graph_desc* d, uint32_t part, uint32_t nparts, const bp_device_opts* opts,
+                         bp_graph** out, bp_part_info* info) {
+  if (!d || !out || !info) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    bpb::PartLayout L{};
+    auto g = bpb::build_part(d, part, nparts, opts, L);
+    *info = bp_part_info{L.part, L.nparts, L.v0, L.v1, L.ghost_vertices, L.local_edges, L.peers, 0,
+                         L.send_messages, L.recv_messages, L.owned_directed};
+    *out = new bp_graph{std::move(g)};
+  });
+}
+
+int bp_part_engine_create(const bp_graph* g, const bp_sched_config* cfg, bp_engine** out) {
+  if (!g || !cfg || !out) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    const bpb::GraphImpl& gi = *g->impl;
+    if (!gi.nparts) throw bpb::Error(BP_ERR_INVALID_ARGUMENT, "not a partition graph (bp_graph_create_part)");
+    bpb::validate_config(*cfg);
+    uint64_t ns = 0, nr = 0;
+    for (const auto& p : gi.peers) {
+      ns += p.send_n;
+      nr += p.recv_n;
+    }
+    auto band = std::make_unique<bpb::Band>();
+    band->own[0].alloc(4 * std::max<uint64_t>(ns, 1));  // every peer's send run back to back
+    band->own[2].alloc(4 * std::max<uint64_t>(nr, 1));  // every peer's recv run back to back
+    band->own[4].alloc(8ull * 5);
+    bpb::PartHalo h{};
+    h.send_up = band->own[0].as<float>();
+    h.recv_up = band->own[2].as<float>();
+    h.count = band->own[4].as<unsigned long long>();
+    auto e = bpb::make_engine(gi, *cfg);
+    e->band_config(h, gi.owned_directed);
+    band->engine = e.get();
+    band->info = bp_band_info{gi.part, gi.nparts, 0, 0, 0, 0, 0, 0, gi.owned_directed};
+    band->cfg = *cfg;
+    band->stream = e->stream();
+    band->halo = h;
+    for (const auto& p : gi.peers)
+      band->peers.push_back({p.part, h.send_up + p.send_off, p.send_n, const_cast<float*>(h.recv_up) + p.recv_off,
+                             p.recv_n});
     *out = new bp_engine{std::move(e), g, *cfg, std::move(band)};
   });
 }

@@ -645,15 +645,36 @@ class EngineT final : public EngineBase {
   uint64_t band_owned_ = 0;
   bool pingpong_ = false;
   cudaStream_t stream() const override { return s_; }
+  // vertex-range partition of any binary graph (bp_graph_create_part): cut
+  // messages through the graph's index lists; halo_.send_up / recv_up hold
+  // every peer's run back to back
+  bool part_mode_ = false;
+  uint32_t part_ns_ = 0, part_nr_ = 0;
   void band_config(const PartHalo& h, uint64_t owned_directed) override {
-    if (QS != 1 || !g_.lat_cols || g_.par_mode != 1)
+    part_mode_ = g_.nparts != 0;
+    if (part_mode_) {
+      if (QS != 1) throw Error(BP_ERR_UNSUPPORTED, "vertex-range partition: binary graphs only");
+      if (cfg_.kind != BP_LBP && cfg_.kind != BP_RNBP)
+        throw Error(BP_ERR_UNSUPPORTED, "vertex-range partition: LBP and RnBP (RBP / RS: row bands of lattices)");
+      part_ns_ = part_nr_ = 0;
+      for (const auto& p : g_.peers) {
+        part_ns_ += p.send_n;
+        part_nr_ += p.recv_n;
+      }
+    } else if (QS != 1 || !g_.lat_cols || g_.par_mode != 1) {
       throw Error(BP_ERR_UNSUPPORTED, "row-band partition needs a binary Ising lattice band");
+    }
     if (cfg_.kind == BP_SERIAL_RBP) throw Error(BP_ERR_UNSUPPORTED, "row-band partition: not for serial RBP");
     halo_ = h;
     halo_.ghost_up = g_.cnt_row0 > 0 ? 1u : 0u;
     halo_.ghost_down = g_.cnt_row1 < g_.lat_rows ? 1u : 0u;
     band_owned_ = owned_directed;
     pingpong_ = false;
+  }
+  unsigned list_grid(uint32_t n) const { return grid_cap(std::max<uint32_t>(n, 1u), 4); }
+  void part_pack(bool pingpong) {
+    k_plist_pack<<<list_grid(part_ns_), kBlock, 0, s_>>>(live(), cand(), ctl(), pingpong ? 1 : 0,
+                                                         g_.send_idx.as<uint32_t>(), part_ns_, halo_.send_up);
   }
   void band_sweep() override {
     if (cfg_.kind != BP_LBP) throw_invalid("band_lbp_* on a non-LBP engine");
@@ -663,14 +684,19 @@ class EngineT final : public EngineBase {
     }
     enqueue_lbp_sweep(kFinNone);
     const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
-    k_part_pack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
+    if (part_mode_) part_pack(true);
+    else k_part_pack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
     k_part_count<<<1, kSlots, 0, s_>>>(ctl(), halo_);
     launch_check();
     launches_ += 2;
   }
   void band_finish() override {
     const unsigned gc = static_cast<unsigned>((g_.lat_cols + kBlock - 1) / kBlock);
-    k_part_unpack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
+    if (part_mode_)
+      k_plist_unpack<<<list_grid(part_nr_), kBlock, 0, s_>>>(live(), cand(), ctl(), 1, g_.recv_idx.as<uint32_t>(),
+                                                             part_nr_, halo_.recv_up);
+    else
+      k_part_unpack<<<gc, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), halo_);
     launch_check();
     ++launches_;
     enqueue_finalize(kFinLbp, static_cast<uint32_t>(band_owned_), halo_.count);
@@ -704,7 +730,8 @@ class EngineT final : public EngineBase {
     k_rnbp_select<QS, false><<<grid_cap(g_.D / 4 + 1), kBlock, 0, s_>>>(
         dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), nullptr, ctl(), eps_, q,
         cand_list(), 0);
-    k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
+    if (part_mode_) part_pack(false);
+    else k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
     launch_check();
     launches_ += 2;
   }
@@ -729,8 +756,13 @@ class EngineT final : public EngineBase {
     launches_ += 2;
   }
   void band_rnbp_refresh() override {
-    k_part_unpack_flag<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), ctl(), vflag_.as<uint32_t>(),
-                                                           vlist_.as<uint32_t>(), halo_);
+    if (part_mode_)
+      k_plist_unpack_flag<<<list_grid(part_nr_), kBlock, 0, s_>>>(dg_, live(), ctl(), vflag_.as<uint32_t>(),
+                                                                  vlist_.as<uint32_t>(), g_.recv_idx.as<uint32_t>(),
+                                                                  part_nr_, halo_.recv_up);
+    else
+      k_part_unpack_flag<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), ctl(), vflag_.as<uint32_t>(),
+                                                             vlist_.as<uint32_t>(), halo_);
     k_vertex_update<QS, kModeDelta, true, false, false>
         <<<vgrid(k_vertex_update<QS, kModeDelta, true, false, false>, g_.V), kBlock, 0, s_>>>(
             dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_,
@@ -748,17 +780,26 @@ class EngineT final : public EngineBase {
     if (g_.D) cuda_check(cudaMemcpy(r.data(), res_.p, 4ull * g_.D, cudaMemcpyDeviceToHost), "d2h");
     out.clear();
     for (uint32_t d = 0; d < g_.D; ++d)
-      if (r[d] >= eps_) out.push_back(d + 2ull * g_.edge_offset);
+      if (r[d] >= eps_)
+        out.push_back(part_mode_ ? 2ull * g_.egid_host[d >> 1] + (d & 1u) : d + 2ull * g_.edge_offset);
   }
   void band_rnbp_pack() override {
-    k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
+    if (part_mode_) part_pack(false);
+    else k_part_pack_live<<<band_cols_grid(), kBlock, 0, s_>>>(dg_, live(), halo_);
     launch_check();
     ++launches_;
   }
   void band_commit_global(uint64_t gd) override {
     if (gd == ~0ull) return;
-    const uint64_t d = gd - 2ull * g_.edge_offset;
-    if (gd < 2ull * g_.edge_offset || d >= g_.D) throw_invalid("edge not in this band");
+    uint64_t d = gd - 2ull * g_.edge_offset;
+    if (part_mode_) {  // the local copy of global edge gd >> 1 (its source is owned here)
+      d = g_.D;
+      for (uint32_t e = 0; e < g_.E && d == g_.D; ++e)
+        if (g_.egid_host[e] == (gd >> 1)) d = 2ull * e + (gd & 1u);
+      if (d == g_.D) throw_invalid("edge not in this part");
+    } else if (gd < 2ull * g_.edge_offset || d >= g_.D) {
+      throw_invalid("edge not in this band");
+    }
     const uint32_t d32 = static_cast<uint32_t>(d);
     DevBuf list;
     list.upload(&d32, 4);

@@ -183,12 +183,15 @@ DevGraph GraphImpl::dev() const {
   g.ising_a = ising_a.as<float>();
   g.pw = pw.as<float>();
   g.log_tables = check_collapse ? 1u : 0u;
+  g.own_v = own_v;
+  g.egid = egid.p ? egid.as<uint32_t>() : nullptr;
   return g;
 }
 
 uint64_t GraphImpl::device_bytes() const {
   return in_off.bytes + in_adj.bytes + ep.bytes + unary_lo.bytes + epar.bytes + card.bytes +
-         unary_log.bytes + table.bytes + bel_off.bytes + ising_a.bytes + pw.bytes;
+         unary_log.bytes + table.bytes + bel_off.bytes + ising_a.bytes + pw.bytes + egid.bytes + send_idx.bytes +
+         recv_idx.bytes;
 }
 
 namespace {
@@ -342,7 +345,7 @@ bool bad_entry(double u) { return !(u > 0.0) || !std::isfinite(u); }
 // (mrf.cpp:37-85: per vertex cardinality then entries; per edge range,
 // self-loop, order, duplicate, entries).  Runs only after the parallel passes
 // found a violation, so the error raised is the reference's first one.
-[[noreturn]] void throw_first_model_error(const bp_graph_desc* d) {
+void validate_sequential(const bp_graph_desc* d, bool check_duplicates) {
   const uint32_t V = d->num_vertices, E = d->num_edges;
   size_t o = 0;
   for (uint32_t v = 0; v < V; ++v) {
@@ -361,7 +364,7 @@ bool bad_entry(double u) { return !(u > 0.0) || !std::isfinite(u); }
     if (i >= V || j >= V) throw_model("edge " + std::to_string(e) + " references a vertex out of range");
     if (i == j) throw_model("edge " + std::to_string(e) + " is a self-loop on vertex " + std::to_string(i));
     if (i > j) throw_model("edge " + std::to_string(e) + " endpoints must satisfy i < j");
-    if (!seen.insert((static_cast<uint64_t>(i) << 32) | j).second)
+    if (check_duplicates && !seen.insert((static_cast<uint64_t>(i) << 32) | j).second)
       throw_model("duplicate edge (" + std::to_string(i) + ", " + std::to_string(j) + ")");
     const size_t sz = static_cast<size_t>(d->cardinalities[i]) * d->cardinalities[j];
     for (size_t k = 0; k < sz; ++k)
@@ -370,6 +373,9 @@ bool bad_entry(double u) { return !(u > 0.0) || !std::isfinite(u); }
                     ") entries must be strictly positive and finite");
     t += sz;
   }
+}
+[[noreturn]] void throw_first_model_error(const bp_graph_desc* d) {
+  validate_sequential(d, true);
   throw Error(BP_ERR_CUDA, "internal: graph validation passes disagree");
 }
 
@@ -491,6 +497,9 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   if (E > (1u << 31) - 1) throw_model("too many edges for 32-bit directed edge ids");
   if (V && !d->cardinalities) throw_invalid("null cardinalities");
   const uint32_t* cards = d->cardinalities;
+  // a partition's local graph keeps the global edge orientation (local ids
+  // need not satisfy i < j); its input was validated globally
+  const bool any_order = opts && (opts->flags & kBuildAnyOrder);
   // --- validation (mrf.cpp:28-91) and layout conversion: O(V + E) passes on
   // the host pool; any violation re-runs the reference's sequential order
   // (throw_first_model_error) so the first error and its message match ---
@@ -565,7 +574,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   if (!uniform_cards) {
     if (first_bad(E, [&](uint64_t e) {
           const uint32_t i = ep[2 * e], j = ep[2 * e + 1];
-          return i >= V || j >= V || i >= j;
+          return i >= V || j >= V || (any_order ? i == j : i >= j);
         }) < E)
       throw_first_model_error(d);
     poff.assign(static_cast<size_t>(E) + 1, 0);
@@ -584,7 +593,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
       EAcc& a = acc[t];
       for (uint64_t e = lo; e < hi; ++e) {
         const uint32_t i = ep[2 * e], j = ep[2 * e + 1];
-        if (i >= V || j >= V || i >= j) {
+        if (i >= V || j >= V || (any_order ? i == j : i >= j)) {
           a.bad = true;
           continue;
         }
@@ -804,6 +813,108 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
   cuda_check(cudaStreamSynchronize(stg.stream()), "graph upload");
   cuda_check(cudaDeviceSynchronize(), "graph upload");
   stage("potentials");
+  return g;
+}
+
+// Vertex-range partition of any binary model (north_star: LBP / RnBP on large
+// grids AND random graphs partitioned across GPUs).  Part g of P owns global
+// vertices [V g / P, V (g + 1) / P) and every message whose source it owns.
+// Its local graph: the global edges with an owned endpoint, in global order
+// and orientation; local vertices = owned ones (in order) then one ghost per
+// outside endpoint (ascending global id).  Ghosts are never updated: their
+// messages into owned vertices arrive from their owners every iteration
+// (recv lists), and the owned-source messages into ghosts leave for their
+// owners (send lists); both sides order a peer's run by global directed id.
+std::unique_ptr<GraphImpl> build_part(const bp_graph_desc* d, uint32_t part, uint32_t nparts,
+                                      const bp_device_opts* opts, PartLayout& out) {
+  if (!d) throw_invalid("null graph descriptor");
+  const uint32_t V = d->num_vertices, E = d->num_edges;
+  if (nparts == 0 || part >= nparts || (V && nparts > V)) throw_invalid("bad vertex-range partition");
+  if (V && !d->cardinalities) throw_invalid("null cardinalities");
+  if (E && (!d->edge_endpoints || !d->pairwise_values)) throw_invalid("null edge arrays");
+  validate_sequential(d, !(opts && (opts->flags & BP_GRAPH_TRUSTED)));  // build_graph's checks, globally
+  for (uint32_t v = 0; v < V; ++v)
+    if (d->cardinalities[v] != 2) throw Error(BP_ERR_UNSUPPORTED, "vertex-range partition: binary models only");
+  const uint32_t v0 = static_cast<uint32_t>(uint64_t{V} * part / nparts);
+  const uint32_t v1 = static_cast<uint32_t>(uint64_t{V} * (part + 1) / nparts);
+  const uint32_t nown = v1 - v0;
+  auto owner = [&](uint32_t v) {
+    uint32_t h = static_cast<uint32_t>(uint64_t{v} * nparts / V);
+    while (h + 1 < nparts && uint64_t{V} * (h + 1) / nparts <= v) ++h;
+    while (h > 0 && uint64_t{V} * h / nparts > v) --h;
+    return h;
+  };
+  const uint32_t* ep = d->edge_endpoints;
+  auto own = [&](uint32_t v) { return v >= v0 && v < v1; };
+  std::vector<uint32_t> gid, ghosts;
+  for (uint32_t e = 0; e < E; ++e) {
+    const uint32_t i = ep[2ull * e], j = ep[2ull * e + 1];
+    if (!own(i) && !own(j)) continue;
+    gid.push_back(e);
+    if (!own(i)) ghosts.push_back(i);
+    if (!own(j)) ghosts.push_back(j);
+  }
+  std::sort(ghosts.begin(), ghosts.end());
+  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+  auto loc = [&](uint32_t v) -> uint32_t {
+    return own(v) ? v - v0 : nown + static_cast<uint32_t>(std::lower_bound(ghosts.begin(), ghosts.end(), v) - ghosts.begin());
+  };
+  const uint32_t VL = nown + static_cast<uint32_t>(ghosts.size()), EL = static_cast<uint32_t>(gid.size());
+  std::vector<uint32_t> lcards(VL, 2), lep(2ull * EL);
+  std::vector<double> lun(2ull * VL), ltb(4ull * EL);
+  for (uint32_t v = 0; v < VL; ++v) {
+    const uint32_t gv = v < nown ? v0 + v : ghosts[v - nown];
+    lun[2ull * v] = d->unary_values[2ull * gv];
+    lun[2ull * v + 1] = d->unary_values[2ull * gv + 1];
+  }
+  for (uint32_t e = 0; e < EL; ++e) {
+    const uint64_t ge = gid[e];
+    lep[2ull * e] = loc(ep[2 * ge]);
+    lep[2ull * e + 1] = loc(ep[2 * ge + 1]);
+    for (int k = 0; k < 4; ++k) ltb[4ull * e + k] = d->pairwise_values[4 * ge + k];
+  }
+  const bp_graph_desc ld{VL, EL, lcards.data(), lun.data(), lep.data(), ltb.data()};
+  bp_device_opts lo{opts ? opts->device : -1, BP_GRAPH_TRUSTED | kBuildAnyOrder};
+  auto g = build_from_desc(&ld, &lo);
+  g->lat_cols = g->lat_rows = 0;  // the CSR is complete either way; ownership is by vertex id
+  g->own_v = nown;
+  g->part = part;
+  g->nparts = nparts;
+  g->v0 = v0;
+  g->v1 = v1;
+  g->egid_host = gid;
+  if (EL) g->egid.upload(gid.data(), 4ull * EL);
+  // cut-message lists per peer, each run sorted by global directed id
+  std::vector<std::vector<std::pair<uint64_t, uint32_t>>> snd(nparts), rcv(nparts);
+  uint64_t owned_directed = 0;
+  for (uint32_t e = 0; e < EL; ++e)
+    for (uint32_t b = 0; b < 2; ++b) {
+      const uint32_t dl = 2 * e + b;
+      const uint32_t src = lep[dl], tgt = lep[dl ^ 1u];
+      const uint64_t key = 2ull * gid[e] + b;
+      if (src < nown) {
+        ++owned_directed;
+        if (tgt >= nown) snd[owner(ghosts[tgt - nown])].emplace_back(key, dl);
+      } else if (tgt < nown) {
+        rcv[owner(ghosts[src - nown])].emplace_back(key, dl);
+      }
+    }
+  std::vector<uint32_t> sidx, ridx;
+  for (uint32_t h = 0; h < nparts; ++h) {
+    if (snd[h].empty() && rcv[h].empty()) continue;
+    std::sort(snd[h].begin(), snd[h].end());
+    std::sort(rcv[h].begin(), rcv[h].end());
+    GraphImpl::PartPeer p{h, static_cast<uint32_t>(sidx.size()), static_cast<uint32_t>(snd[h].size()),
+                          static_cast<uint32_t>(ridx.size()), static_cast<uint32_t>(rcv[h].size())};
+    for (auto& x : snd[h]) sidx.push_back(x.second);
+    for (auto& x : rcv[h]) ridx.push_back(x.second);
+    g->peers.push_back(p);
+  }
+  g->send_idx.upload(sidx.data(), 4ull * sidx.size());
+  g->recv_idx.upload(ridx.data(), 4ull * ridx.size());
+  g->owned_directed = owned_directed;
+  out = PartLayout{part, nparts, v0, v1, static_cast<uint32_t>(ghosts.size()), EL,
+                   static_cast<uint32_t>(g->peers.size()), sidx.size(), ridx.size(), owned_directed};
   return g;
 }
 

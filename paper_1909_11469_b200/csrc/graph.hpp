@@ -63,6 +63,19 @@ struct GraphImpl {
   uint32_t cnt_row0 = 0, cnt_row1 = 0xFFFFFFFFu;
   uint64_t owned_directed = 0;          // directed edges whose source is owned
   uint64_t edge_offset = 0;             // global id of local edge 0
+  // vertex-range partition (bp_graph_create_part): owned local vertices
+  // [0, own_v), local -> global edge ids, and the cut-message lists per peer
+  uint32_t own_v = 0xFFFFFFFFu;
+  DevBuf egid;                           // u32[E]
+  std::vector<uint32_t> egid_host;
+  struct PartPeer {
+    uint32_t part;
+    uint32_t send_off, send_n;  // into send_idx: owned-source messages whose target the peer owns
+    uint32_t recv_off, recv_n;  // into recv_idx: messages from the peer's vertices into owned ones
+  };
+  std::vector<PartPeer> peers;
+  DevBuf send_idx, recv_idx;             // local directed ids, each peer's run in global directed-id order
+  uint32_t part = 0, nparts = 0, v0 = 0, v1 = 0;
   std::vector<uint32_t> cards_host;  // mixed cardinalities only
 
   DevGraph dev() const;
@@ -87,7 +100,15 @@ struct GraphImpl {
   mutable std::vector<uint32_t> ep_host, in_off_host, in_adj_host;
 };
 
+// internal bp_device_opts flag: keep the given edge orientation (i > j allowed)
+constexpr uint32_t kBuildAnyOrder = 1u << 31;
 std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_device_opts* opts);
+struct PartLayout {
+  uint32_t part, nparts, v0, v1, ghost_vertices, local_edges, peers;
+  uint64_t send_messages, recv_messages, owned_directed;
+};
+std::unique_ptr<GraphImpl> build_part(const bp_graph_desc* d, uint32_t part, uint32_t nparts,
+                                      const bp_device_opts* opts, PartLayout& out);
 // columns of the generate_ising lattice numbering of this edge list (0: not a lattice)
 uint32_t lattice_cols(uint32_t V, uint32_t E, const uint32_t* ep);
 std::unique_ptr<GraphImpl> build_lattice_binary(uint32_t rows, uint32_t cols, const BinaryStreams& s,

@@ -433,6 +433,44 @@ static __global__ void k_part_unpack_flag(DevGraph g, float* M, Ctl* ctl, uint32
   }
 }
 
+// vertex-range partition (bp_graph_create_part): the cut messages of any
+// graph move through index lists -- send: owned-source messages whose target
+// a peer owns, recv: messages from a peer's vertices into owned ones, each
+// peer's run in global directed-id order on both sides.
+// pingpong: M = the buffer the LBP sweep just wrote (ctl->sweeps parity).
+static __global__ void k_plist_pack(const float* buf0, const float* buf1, const Ctl* ctl, int pingpong,
+                                    const uint32_t* __restrict__ idx, uint32_t n, float* __restrict__ out) {
+  const float* M = pingpong && !(ctl->sweeps & 1ull) ? buf1 : buf0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = M[idx[i]];
+}
+
+static __global__ void k_plist_unpack(float* buf0, float* buf1, const Ctl* ctl, int pingpong,
+                                      const uint32_t* __restrict__ idx, uint32_t n, const float* __restrict__ in) {
+  float* M = pingpong && !(ctl->sweeps & 1ull) ? buf1 : buf0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) M[idx[i]] = in[i];
+}
+
+// RnBP: a changed message from a peer flags the owned vertex it flows into
+// (collect_touched across the cut, schedulers.cpp:31-42)
+static __global__ void k_plist_unpack_flag(DevGraph g, float* M, Ctl* ctl, uint32_t* vflag, uint32_t* vlist,
+                                           const uint32_t* __restrict__ idx, uint32_t n, const float* __restrict__ in) {
+  if (run_done(ctl)) return;
+  const uint32_t stamp = ctl->stamp;
+  const bool dense = ctl->dense != 0u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t d = idx[i];
+    if (M[d] != in[i]) {
+      M[d] = in[i];
+      const uint32_t v = g.ep[d ^ 1u];  // target
+      if (dense) {
+        vflag[v] = stamp;
+      } else if (atomicMax(&vflag[v], stamp) < stamp) {
+        vlist[atomicAdd(&ctl->nflag, 1u)] = v;
+      }
+    }
+  }
+}
+
 // the band's contributions of the iteration -> h.count = {delta, frontier,
 // survivors, time vote, count (init)}; slots are left for the finalize
 static __global__ void __launch_bounds__(kSlots) k_part_count_rnbp(Ctl* c, PartHalo h) {
@@ -1077,6 +1115,7 @@ __device__ __forceinline__ void vertex_update_pass(const DevGraph& g, const floa
         const uint32_t row = v / g.lat_cols;
         go = row >= g.cnt_row0 && row < g.cnt_row1;
       }
+      go = go && v < g.own_v;  // vertex-range partition: ghosts' messages come from their owners
       if (go) {
         cnt += vertex_update<QS, MODE, CL, NC>(g, v, A, B, res, eps, &ctl->numeric_error, evals, cand_list.inlist,
                                                &cl, cl_on);
@@ -1324,9 +1363,9 @@ __device__ __forceinline__ void rnbp_select_pass(const DevGraph& g, float* live,
         uint4 ph[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
         if (draw) {
           // keyed by the GLOBAL edge id (edge_offset != 0 for a band of a partition)
-          if (rr[0] >= eps || rr[1] >= eps) ph[0] = philox_edge(prm.seed, it, prm.attempt, 2ull * q + g.edge_offset);
+          if (rr[0] >= eps || rr[1] >= eps) ph[0] = philox_edge(prm.seed, it, prm.attempt, global_edge(g, 2u * q));
           if (rr[2] >= eps || rr[3] >= eps)
-            ph[1] = philox_edge(prm.seed, it, prm.attempt, 2ull * q + 1ull + g.edge_offset);
+            ph[1] = philox_edge(prm.seed, it, prm.attempt, global_edge(g, 2u * q + 1u));
         }
         // binary: the four commits' operands (candidates, targets) in two
         // 16-byte loads, one round trip instead of one per commit
@@ -1403,7 +1442,7 @@ __device__ __forceinline__ void rnbp_select_pass(const DevGraph& g, float* live,
         const float r = res[d];
         if (r >= eps) {
           c.survivors += 1;
-          if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, d + 2ull * g.edge_offset) < thresh)) {
+          if ((thresh >= (1ull << 53) || philox_u53(prm.seed, it, 0u, global_directed(g, d)) < thresh)) {
             cl.inlist[d] = 0;
             commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, dense, c, nf, tg);
           } else {
@@ -1474,7 +1513,7 @@ __device__ __forceinline__ void rnbp_retry_block(const DevGraph& g, float* live,
     const uint32_t d = (use_list || slots) ? list[i] : i;
     if (d == kSlotEmpty) continue;
     const float r = res[d];
-    if (r >= eps && philox_u53(prm.seed, it, 1u, d + 2ull * g.edge_offset) < thresh) {
+    if (r >= eps && philox_u53(prm.seed, it, 1u, global_directed(g, d)) < thresh) {
       ++fr;
       if (prm.commit) {
         Contrib c;

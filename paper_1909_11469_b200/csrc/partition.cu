@@ -116,15 +116,10 @@ struct NcclComm final : BandComm {
     check_bands(bands);
     Band& b = *bands[0];
     const auto& a = nccl();
-    const size_t C = b.info.cols;
     nccl_check(a.group_start(), "ncclGroupStart");
-    if (b.info.ghost_up) {
-      nccl_check(a.send(b.send_up(), C, ncclFloat32, rank - 1, comm, b.stream), "ncclSend");
-      nccl_check(a.recv(b.recv_up(), C, ncclFloat32, rank - 1, comm, b.stream), "ncclRecv");
-    }
-    if (b.info.ghost_down) {
-      nccl_check(a.send(b.send_down(), C, ncclFloat32, rank + 1, comm, b.stream), "ncclSend");
-      nccl_check(a.recv(b.recv_down(), C, ncclFloat32, rank + 1, comm, b.stream), "ncclRecv");
+    for (const Band::Peer& p : b.peers) {
+      if (p.ns) nccl_check(a.send(p.send, p.ns, ncclFloat32, static_cast<int>(p.part), comm, b.stream), "ncclSend");
+      if (p.nr) nccl_check(a.recv(p.recv, p.nr, ncclFloat32, static_cast<int>(p.part), comm, b.stream), "ncclRecv");
     }
     nccl_check(a.group_end(), "ncclGroupEnd");
   }
@@ -178,14 +173,14 @@ struct LocalComm final : BandComm {
   }
   void halo(const std::vector<Band*>& bands) override {
     sync_all(bands);
-    for (size_t i = 0; i < bands.size(); ++i) {
-      Band& b = *bands[i];
-      const size_t nb = 4ull * b.info.cols;
-      if (b.info.ghost_up)
-        cuda_check(cudaMemcpy(b.recv_up(), bands[i - 1]->send_down(), nb, cudaMemcpyDefault), "halo copy");
-      if (b.info.ghost_down)
-        cuda_check(cudaMemcpy(b.recv_down(), bands[i + 1]->send_up(), nb, cudaMemcpyDefault), "halo copy");
-    }
+    for (Band* b : bands)
+      for (const Band::Peer& p : b->peers) {
+        if (p.part >= bands.size()) throw Error(BP_ERR_INVALID_ARGUMENT, "local partition: missing part");
+        const Band& o = *bands[p.part];  // bands are parts 0 .. P-1 in order
+        auto q = std::find_if(o.peers.begin(), o.peers.end(), [&](const Band::Peer& x) { return x.part == b->info.part; });
+        if (q == o.peers.end() || q->ns != p.nr) throw Error(BP_ERR_INVALID_ARGUMENT, "local partition: halo sizes disagree");
+        if (p.nr) cuda_check(cudaMemcpy(p.recv, q->send, 4ull * p.nr, cudaMemcpyDefault), "halo copy");
+      }
     cuda_check(cudaDeviceSynchronize(), "halo");
   }
   void all_reduce(const std::vector<Band*>& bands, uint32_t n) override {

@@ -16,6 +16,23 @@ struct Band {
   cudaStream_t stream = nullptr;
   PartHalo halo{};
   DevBuf own[5];  // halo buffers owned by the band (bp_band_engine_create_owned)
+  // the parts this band exchanges cut messages with: per peer, the run of the
+  // send buffer it receives and the run of the recv buffer it fills (row
+  // bands: the band above / below, cols floats each way; vertex-range parts:
+  // any peer, the graph's list lengths)
+  struct Peer {
+    uint32_t part;
+    float* send;
+    uint32_t ns;
+    float* recv;
+    uint32_t nr;
+  };
+  std::vector<Peer> peers;
+  void lattice_peers() {  // row bands: the band above and the band below
+    peers.clear();
+    if (info.ghost_up) peers.push_back({info.part - 1, halo.send_up, info.cols, recv_up(), info.cols});
+    if (info.ghost_down) peers.push_back({info.part + 1, halo.send_down, info.cols, recv_down(), info.cols});
+  }
   float* send_up() const { return halo.send_up; }
   float* send_down() const { return halo.send_down; }
   float* recv_up() const { return const_cast<float*>(halo.recv_up); }

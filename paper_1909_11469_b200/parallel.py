@@ -492,6 +492,77 @@ class Band:
     status = BandLBP.status
 
 
+class _PartInfoC(C.Structure):
+    _fields_ = [("part", C.c_uint32), ("nparts", C.c_uint32), ("v0", C.c_uint32), ("v1", C.c_uint32),
+                ("ghost_vertices", C.c_uint32), ("local_edges", C.c_uint32), ("peers", C.c_uint32),
+                ("_pad", C.c_uint32), ("send_messages", C.c_uint64), ("recv_messages", C.c_uint64),
+                ("owned_directed", C.c_uint64)]
+
+
+@dataclass
+class PartInfo:
+    part: int
+    nparts: int
+    v0: int
+    v1: int
+    ghost_vertices: int
+    local_edges: int
+    peers: int
+    send_messages: int
+    recv_messages: int
+    owned_directed: int
+
+
+_create_part = _sig("bp_graph_create_part", C.c_int, [_P, C.c_uint32, C.c_uint32, C.POINTER(_DevOpts), C.POINTER(_P),
+                                                      C.POINTER(_PartInfoC)])
+_part_engine = _sig("bp_part_engine_create", C.c_int, [_P, C.POINTER(_Config), C.POINTER(_P)])
+
+
+class Part:
+    """One part of a vertex-range partition of ANY binary model given as
+    build_graph arrays (random graphs included): vertices [v0, v1) and the
+    messages they send, ghosts for the outside neighbours, cut messages
+    exchanged with every peer part each iteration.  Driven by run_bands (LBP,
+    RnBP); the run is the unpartitioned one for any number of parts."""
+
+    def __init__(self, config: SchedulerConfig, part: int, nparts: int, arrays, device: int = 0,
+                 trusted: bool = False):
+        import numpy as np
+
+        from . import _Desc
+        cards, un, ep, tb = (np.ascontiguousarray(arrays[0], np.uint32), np.ascontiguousarray(arrays[1], np.float64),
+                             np.ascontiguousarray(np.asarray(arrays[2]).reshape(-1), np.uint32),
+                             np.ascontiguousarray(arrays[3], np.float64))
+        d = _Desc(cards.size, ep.size // 2, cards.ctypes.data_as(C.c_void_p), un.ctypes.data_as(C.c_void_p),
+                  ep.ctypes.data_as(C.c_void_p), tb.ctypes.data_as(C.c_void_p))
+        info = _PartInfoC()
+        h = C.c_void_p()
+        _check(_create_part(C.byref(d), part, nparts, C.byref(_DevOpts(device, GRAPH_TRUSTED if trusted else 0)),
+                            C.byref(h), C.byref(info)))
+        self.graph = PairwiseMRF(h, None)
+        self.info = PartInfo(*(getattr(info, f) for f, _ in _PartInfoC._fields_ if f != "_pad"))
+        self._cfg = config._c()
+        e = C.c_void_p()
+        _check(_part_engine(self.graph._h, C.byref(self._cfg), C.byref(e)))
+        self._e = e
+
+    def __del__(self):
+        e = getattr(self, "_e", None)
+        if e and _lib is not None:
+            _lib.bp_engine_destroy(e)
+            self._e = None
+
+    def owned_beliefs(self):
+        """Beliefs (v1 - v0, 2) of the owned vertices, global order."""
+        import numpy as np
+
+        out = np.zeros(2 * self.graph.num_vertices())
+        _check(_lib.bp_engine_beliefs(self._e, out.ctypes.data_as(C.c_void_p)))
+        return out.reshape(-1, 2)[: self.info.v1 - self.info.v0]
+
+    status = BandLBP.status
+
+
 def run_bands(bands, comm: BandComm) -> BandStatus:
     """The run() loop over row bands in C++ (bp_band_run): NCCL -- this rank's
     band; local -- every band of the partition, parts 0..P-1."""

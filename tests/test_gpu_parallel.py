@@ -219,3 +219,92 @@ def test_cpp_driver_nccl_single_rank(bp):
         st = par.run_bands([band], comm)
         assert st.iterations == full.iterations
         assert np.array_equal(band.owned_beliefs(), full.beliefs.values.reshape(n, n, 2))
+
+
+# ---- vertex-range partition of ANY binary model (bp_graph_create_part):
+# random graphs, cut messages exchanged with every peer part
+def _er(orc, n, m, c, seed):
+    from oracle import pyoracle as po
+    a = po.Graph.er(orc, n, m, c, seed).arrays()
+    return a.cardinalities, a.unary, a.endpoints, a.tables
+
+
+def _owned(parts):
+    return np.concatenate([p.owned_beliefs() for p in parts]).reshape(-1)
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 5])
+def test_parts_lbp_random_graph_bitwise_equals_unpartitioned(bp, orc, nparts):
+    arrays = _er(orc, 3000, 6000, 2.5, 1)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=25)
+    full = bp.run(bp.PairwiseMRF.from_arrays(*arrays), cfg)
+    parts = [par.Part(cfg, p, nparts, arrays) for p in range(nparts)]
+    infos = [p.info for p in parts]
+    assert sum(i.v1 - i.v0 for i in infos) == 3000
+    assert sum(i.send_messages for i in infos) == sum(i.recv_messages for i in infos)
+    assert sum(i.owned_directed for i in infos) == 2 * 6000
+    st = par.run_bands(parts, par.BandComm.local())
+    assert st.iterations == full.iterations == 25 and st.converged == full.converged
+    assert np.array_equal(_owned(parts), full.beliefs.values)
+    assert sum(p.status().messages_updated_total for p in parts) == full.messages_updated_total
+
+
+def test_parts_lbp_converges_like_unpartitioned(bp, orc):
+    arrays = _er(orc, 2000, 3000, 1.0, 2)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.lbp, max_iterations=2000)
+    full = bp.run(bp.PairwiseMRF.from_arrays(*arrays), cfg)
+    parts = [par.Part(cfg, p, 4, arrays) for p in range(4)]
+    st = par.run_bands(parts, par.BandComm.local())
+    assert full.converged and st.converged and st.iterations == full.iterations
+    assert np.array_equal(_owned(parts), full.beliefs.values)
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_parts_rnbp_random_graph_equals_unpartitioned(bp, orc, nparts):
+    """RnBP draws are keyed by GLOBAL edge ids, so the partitioned run commits
+    exactly the unpartitioned frontiers"""
+    arrays = _er(orc, 2000, 4000, 2.0, 3)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=400, seed=7)
+    full = bp.run(bp.PairwiseMRF.from_arrays(*arrays), cfg)
+    parts = [par.Part(cfg, p, nparts, arrays) for p in range(nparts)]
+    st = par.run_bands(parts, par.BandComm.local())
+    assert st.converged == full.converged and st.iterations == full.iterations
+    assert st.messages_updated_total == full.messages_updated_total
+    assert np.array_equal(_owned(parts), full.beliefs.values)
+
+
+def test_parts_rnbp_fallback_across_parts(bp, orc):
+    """low_p: empty attempt-0 draws, retries and single-survivor fallbacks
+    picked across parts (ascending global directed ids)"""
+    arrays = _er(orc, 60, 90, 2.0, 4)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.02, high_p=0.02, max_iterations=300, seed=3)
+    full = bp.run(bp.PairwiseMRF.from_arrays(*arrays), cfg)
+    parts = [par.Part(cfg, p, 3, arrays) for p in range(3)]
+    st = par.run_bands(parts, par.BandComm.local())
+    assert st.iterations == full.iterations and st.messages_updated_total == full.messages_updated_total
+    assert np.array_equal(_owned(parts), full.beliefs.values)
+
+
+def test_parts_generic_binary_tables_and_lattices(bp, orc):
+    """non-Ising binary tables (bptest::random_graph, test_helpers.hpp:90-132)
+    and a lattice given as arrays: vertex ranges partition any binary model"""
+    from tests.helpers import Stream, lattice_arrays, random_graph
+    cards, un, ed = random_graph(Stream(orc, 77), 300, 2, 0.02)
+    rg = (np.asarray(cards, np.uint32), np.concatenate([np.asarray(u, float) for u in un]),
+          np.asarray([(i, j) for i, j, _ in ed], np.uint32), np.concatenate([np.asarray(t, float) for _, _, t in ed]))
+    for arrays in (rg, lattice_arrays(orc, 13, 29, 5, 2.0)):
+        for kind in ("lbp", "rnbp"):
+            cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.from_string(kind), low_p=0.5, max_iterations=80, seed=1)
+            full = bp.run(bp.PairwiseMRF.from_arrays(*arrays), cfg)
+            parts = [par.Part(cfg, p, 3, arrays) for p in range(3)]
+            st = par.run_bands(parts, par.BandComm.local())
+            assert st.iterations == full.iterations and st.converged == full.converged
+            assert np.array_equal(_owned(parts), full.beliefs.values)
+
+
+def test_parts_reject_what_they_do_not_partition(bp, orc):
+    arrays = _er(orc, 100, 150, 2.0, 5)
+    with pytest.raises(Exception, match="LBP and RnBP"):
+        par.Part(bp.SchedulerConfig(kind=bp.SchedulerKind.rbp), 0, 2, arrays)
+    with pytest.raises(Exception):
+        par.Part(bp.SchedulerConfig(kind=bp.SchedulerKind.lbp), 2, 2, arrays)
