@@ -184,6 +184,10 @@ BP_API int bp_graph_generate_er(uint32_t n, uint32_t m, double c, uint64_t seed,
 BP_API int bp_generate_ising_arrays(uint32_t n, double c, uint64_t seed, uint32_t* cardinalities,
                                     double* unary_values, uint32_t* edge_endpoints,
                                     double* pairwise_values);
+/* The Erdos-Renyi G(n, m) instance of bp_graph_generate_er as build_graph
+ * input arrays (n cardinalities, 2n unaries, 2m endpoints, 4m tables). */
+BP_API int bp_generate_er_arrays(uint32_t n, uint32_t m, double c, uint64_t seed, uint32_t* cardinalities,
+                                 double* unary, uint32_t* endpoints, double* tables);
 
 BP_API void bp_graph_destroy(struct bp_graph* g);
 BP_API int bp_graph_info_get(const struct bp_graph* g, bp_graph_info* info);

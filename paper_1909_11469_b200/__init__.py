@@ -150,6 +150,7 @@ def _load():
                                            C.POINTER(P)]),
         "bp_graph_destroy": (None, [P]),
         "bp_generate_ising_arrays": (C.c_int, [C.c_uint32, C.c_double, C.c_uint64, P, P, P, P]),
+        "bp_generate_er_arrays": (C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, P, P, P, P]),
         "bp_graph_info_get": (C.c_int, [P, C.POINTER(_Info)]),
         "bp_run": (C.c_int, [P, C.POINTER(_Config), C.POINTER(_Result), P, P, C.c_uint64]),
         "bp_run_ex": (C.c_int, [P, C.POINTER(_Config), C.POINTER(_RunOpts), C.POINTER(_Result), P, P, C.c_uint64]),
@@ -511,6 +512,16 @@ def generate_ising_arrays(params: IsingParams):
     tb = np.zeros(max(4 * E, 1))
     _check(_lib.bp_generate_ising_arrays(n, params.c, params.seed, _ptr(cards), _ptr(un), _ptr(ep), _ptr(tb)))
     return cards[:V], un[: 2 * V], ep[: 2 * E].reshape(E, 2), tb[: 4 * E]
+
+
+def generate_er_arrays(n: int, m: int, c: float, seed: int):
+    """generate_er's instance as build_graph inputs on the host: (cards, unary, endpoints (m,2), tables)."""
+    cards = np.zeros(max(n, 1), np.uint32)
+    un = np.zeros(max(2 * n, 1))
+    ep = np.zeros(max(2 * m, 2), np.uint32)
+    tb = np.zeros(max(4 * m, 1))
+    _check(_lib.bp_generate_er_arrays(n, m, c, seed, _ptr(cards), _ptr(un), _ptr(ep), _ptr(tb)))
+    return cards[:n], un[: 2 * n], ep[: 2 * m].reshape(m, 2), tb[: 4 * m]
 
 
 def generate_chain(params: ChainParams, device: int = -1) -> PairwiseMRF:

@@ -59,6 +59,9 @@ struct ErInstance {
   std::vector<float> coupling;
 };
 ErInstance er_instance(uint32_t n, uint32_t m, double c, uint64_t seed);
+// the same instance as build_graph input arrays (unaries, Ising tables {a, d, d, a})
+void er_desc_arrays(uint32_t n, uint32_t m, double c, uint64_t seed, std::vector<uint32_t>& cards,
+                    std::vector<double>& unary, std::vector<uint32_t>& ep, std::vector<double>& tables);
 
 // Exact double-precision unary / table values of the same streams (for the
 // descriptor path and tests).

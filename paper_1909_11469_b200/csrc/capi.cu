@@ -123,6 +123,20 @@ int bp_generate_ising_arrays(uint32_t n, double c, uint64_t seed, uint32_t* card
   });
 }
 
+int bp_generate_er_arrays(uint32_t n, uint32_t m, double c, uint64_t seed, uint32_t* cards, double* unary,
+                          uint32_t* ep, double* tables) {
+  if ((n && (!cards || !unary)) || (m && (!ep || !tables))) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    std::vector<uint32_t> cv, ev;
+    std::vector<double> uv, tv;
+    bpb::er_desc_arrays(n, m, c, seed, cv, uv, ev, tv);
+    if (!cv.empty()) std::memcpy(cards, cv.data(), cv.size() * 4);
+    if (!uv.empty()) std::memcpy(unary, uv.data(), uv.size() * 8);
+    if (!ev.empty()) std::memcpy(ep, ev.data(), ev.size() * 4);
+    if (!tv.empty()) std::memcpy(tables, tv.data(), tv.size() * 8);
+  });
+}
+
 void bp_graph_destroy(bp_graph* g) { delete g; }
 
 int bp_graph_info_get(const bp_graph* g, bp_graph_info* info) {

@@ -116,39 +116,73 @@ PottsStreams potts_streams(uint32_t n, uint32_t q, double c, uint64_t seed) {
   return s;
 }
 
-ErInstance er_instance(uint32_t n, uint32_t m, double c, uint64_t seed) {
+// G(n, m) stream: unaries 2 x unit_open per vertex, then
+// (floor(u n), floor(u n)) pairs redrawn on self-loops / duplicates until m
+// distinct edges, sorted by (i, j), then one lambda per edge
+namespace {
+struct ErStream {
+  std::vector<double> u;         // 2n unaries
+  std::vector<uint64_t> keys;    // (i << 32) | j, sorted
+  std::vector<double> lambda;    // per edge
+};
+ErStream er_stream(uint32_t n, uint32_t m, uint64_t seed) {
   if (m > 0 && n < 2) throw_invalid("er: need n >= 2");
   if (static_cast<uint64_t>(m) > static_cast<uint64_t>(n) * (n - 1) / 2) throw_invalid("er: too many edges");
   Mt64 rng(seed);
-  std::vector<double> u(2 * static_cast<size_t>(n));
-  for (auto& x : u) x = rng.unit_open();
-  std::vector<uint64_t> keys;
-  keys.reserve(m);
+  ErStream st;
+  st.u.resize(2 * static_cast<size_t>(n));
+  for (auto& x : st.u) x = rng.unit_open();
+  st.keys.reserve(m);
   std::unordered_set<uint64_t> seen;
   seen.reserve(static_cast<size_t>(m) * 2);
-  while (keys.size() < m) {
+  while (st.keys.size() < m) {
     uint32_t a = static_cast<uint32_t>(rng.unit() * static_cast<double>(n));
     uint32_t b = static_cast<uint32_t>(rng.unit() * static_cast<double>(n));
     if (a == b) continue;
     if (a > b) std::swap(a, b);
     const uint64_t key = (static_cast<uint64_t>(a) << 32) | b;
     if (!seen.insert(key).second) continue;
-    keys.push_back(key);
+    st.keys.push_back(key);
   }
-  std::sort(keys.begin(), keys.end());
+  std::sort(st.keys.begin(), st.keys.end());
+  st.lambda.resize(m);
+  for (auto& l : st.lambda) l = rng.unit() - 0.5;
+  return st;
+}
+}  // namespace
+
+ErInstance er_instance(uint32_t n, uint32_t m, double c, uint64_t seed) {
+  const ErStream st = er_stream(n, m, seed);
   ErInstance inst;
   inst.endpoints.resize(2 * static_cast<size_t>(m));
   inst.coupling.resize(m);
   for (uint32_t k = 0; k < m; ++k) {
-    inst.endpoints[2 * k] = static_cast<uint32_t>(keys[k] >> 32);
-    inst.endpoints[2 * k + 1] = static_cast<uint32_t>(keys[k]);
-    const double lambda = rng.unit() - 0.5;
-    inst.coupling[k] = static_cast<float>(2.0 * (lambda * c));
+    inst.endpoints[2 * k] = static_cast<uint32_t>(st.keys[k] >> 32);
+    inst.endpoints[2 * k + 1] = static_cast<uint32_t>(st.keys[k]);
+    inst.coupling[k] = static_cast<float>(2.0 * (st.lambda[k] * c));
   }
   inst.unary_lo.resize(n);
   for (uint32_t v = 0; v < n; ++v)
-    inst.unary_lo[v] = static_cast<float>(std::log2(u[2 * v + 1]) - std::log2(u[2 * v]));
+    inst.unary_lo[v] = static_cast<float>(std::log2(st.u[2 * v + 1]) - std::log2(st.u[2 * v]));
   return inst;
+}
+
+void er_desc_arrays(uint32_t n, uint32_t m, double c, uint64_t seed, std::vector<uint32_t>& cards,
+                    std::vector<double>& unary, std::vector<uint32_t>& ep, std::vector<double>& tables) {
+  const ErStream st = er_stream(n, m, seed);
+  cards.assign(n, 2);
+  unary = st.u;
+  ep.resize(2 * static_cast<size_t>(m));
+  tables.resize(4 * static_cast<size_t>(m));
+  for (uint32_t k = 0; k < m; ++k) {
+    ep[2 * k] = static_cast<uint32_t>(st.keys[k] >> 32);
+    ep[2 * k + 1] = static_cast<uint32_t>(st.keys[k]);
+    const double agree = std::exp(st.lambda[k] * c), disagree = std::exp(-st.lambda[k] * c);
+    tables[4 * k] = agree;
+    tables[4 * k + 1] = disagree;
+    tables[4 * k + 2] = disagree;
+    tables[4 * k + 3] = agree;
+  }
 }
 
 void ising_desc_arrays(uint32_t rows, uint32_t cols, double c, uint64_t seed,

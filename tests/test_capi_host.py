@@ -121,3 +121,12 @@ def test_host_philox_known_answer(bp):
     iteration 0, attempt 0, seed 0; d = 0 takes words 0-1, d = 1 words 2-3."""
     assert bp.philox_u53(0, 0, 0, 0) == ((0x6627E8D5 << 32) | 0xE169C58D) >> 11
     assert bp.philox_u53(0, 0, 0, 1) == ((0xBC57AC4C << 32) | 0x9B00DBD8) >> 11
+
+
+def test_host_er_arrays_equal_reference_style_generator(bp, orc):
+    """bp_generate_er_arrays: the ER instance the oracle builds."""
+    for n, m, c, seed in ((10, 12, 2.5, 0), (500, 900, 2.0, 3)):
+        cards, un, ep, tb = bp.generate_er_arrays(n, m, c, seed)
+        a = po.Graph.er(orc, n, m, c, seed).arrays()
+        assert np.array_equal(cards, a.cardinalities) and np.array_equal(ep.reshape(-1), a.endpoints.reshape(-1))
+        assert np.array_equal(un, a.unary) and np.array_equal(tb, a.tables)
