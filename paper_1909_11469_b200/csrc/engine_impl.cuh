@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "engine.hpp"
+#include "host_pool.hpp"
 #include "kernels.cuh"
 #include "kernels_rs.cuh"
 #include "kernels_persist.cuh"
@@ -186,10 +187,27 @@ class EngineT final : public EngineBase {
         dst = bel_.as<double>();
       }
       enqueue_beliefs(dst, cfg_.kind == BP_LBP);
-      if (beliefs_host) cuda_check(cudaMemcpyAsync(beliefs_host, dst, nb * 8, cudaMemcpyDeviceToHost, s_), "beliefs d2h");
+      if (beliefs_host) {
+        // large tables through a pinned block (full-rate DMA), then copied out
+        // on the host pool; small ones straight into the caller's memory
+        if (nb * 8 >= kPinnedBeliefs) {
+          bel_pinned_bytes_ = ((nb * 8 + (1u << 20) - 1) >> 20) << 20;
+          bel_pinned_ = pinned_acquire(bel_pinned_bytes_);
+          cuda_check(cudaMemcpyAsync(bel_pinned_, dst, nb * 8, cudaMemcpyDeviceToHost, s_), "beliefs d2h");
+        } else {
+          cuda_check(cudaMemcpyAsync(beliefs_host, dst, nb * 8, cudaMemcpyDeviceToHost, s_), "beliefs d2h");
+        }
+      }
     }
     cuda_check(cudaEventRecord(e1, s_), "event record");
     cuda_check(cudaStreamSynchronize(s_), "run");
+    if (bel_pinned_) {
+      const char* src = static_cast<const char*>(bel_pinned_);
+      char* out = reinterpret_cast<char*>(beliefs_host);
+      parallel_for(nb * 8, [&](uint64_t a, uint64_t b) { std::memcpy(out + a, src + a, b - a); });
+      pinned_release(bel_pinned_, bel_pinned_bytes_);
+      bel_pinned_ = nullptr;
+    }
     if (g_.check_collapse) {  // compute_belief's mass check (k_beliefs) on collapse-checked models
       fetch_ctl_header();
       if (hctl_->numeric_error) throw Error(BP_ERR_NUMERIC, "probability vector collapsed (total mass below 1e-300)");
@@ -1035,6 +1053,10 @@ class EngineT final : public EngineBase {
     k_set_u64<<<1, 1, 0, s_>>>(&ctl()->cond_handle, h);
     launch_check();
   }
+
+  static constexpr size_t kPinnedBeliefs = size_t{1} << 20;
+  void* bel_pinned_ = nullptr;
+  size_t bel_pinned_bytes_ = 0;
 
   // ---- fused dense RnBP sweeps (kernels_fused.cuh)
   DevBuf fl_, fc_;  // scratch buffer set (live, candidates)

@@ -454,10 +454,13 @@ struct VAcc {
   uint64_t usz = 0;
   bool zero = false, bad = false;
   double min_mu = std::numeric_limits<double>::infinity();
+  double min_u = std::numeric_limits<double>::infinity();  // smallest unary entry
 };
 struct EAcc {
   bool bad = false, ising = true;
   double min_rho = 1.0, min_m = std::numeric_limits<double>::infinity();
+  // binary tables: the smallest entry and the extreme row / column sums
+  double tmin = std::numeric_limits<double>::infinity(), smin = std::numeric_limits<double>::infinity(), smax = 0.0;
 };
 
 // collapse-bound minima of one table t (ci x cj, row-major) of edge (i, j):
@@ -546,22 +549,28 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
       VAcc& a = acc[t];
       for (uint64_t v = lo; v < hi; ++v) {
         const double* u = d->unary_values + unary_at(v);
-        double mu = 0.0;
+        double mu = 0.0, mn = std::numeric_limits<double>::infinity();
         for (uint32_t x = 0; x < cards[v]; ++x) {
           a.bad |= bad_entry(u[x]);
           mu = std::max(mu, u[x]);
+          mn = std::min(mn, u[x]);
         }
         a.min_mu = std::min(a.min_mu, mu);
-        if (bin_cards) {  // base-2 log-odds (one log of the ratio unless it leaves the double range)
+        a.min_u = std::min(a.min_u, mn);
+        if (bin_cards) {
+          // base-2 log-odds, kept in fp32: the ratio's log in single precision
+          // when the ratio is a normal float (error below 1e-7 absolute), else
+          // the difference of double logs
           const double r = u[1] / u[0];
-          ulo[v] = static_cast<float>(r > 0.0 && r <= std::numeric_limits<double>::max() ? std::log2(r)
-                                                                                    : std::log2(u[1]) - std::log2(u[0]));
+          ulo[v] = r >= 1e-30 && r <= 1e30 ? log2f(static_cast<float>(r))
+                                           : static_cast<float>(std::log2(u[1]) - std::log2(u[0]));
         }
       }
     });
     for (const VAcc& a : acc) {
       va.bad |= a.bad;
       va.min_mu = std::min(va.min_mu, a.min_mu);
+      va.min_u = std::min(va.min_u, a.min_u);
     }
   }
   if (va.bad) throw_first_model_error(d);
@@ -602,13 +611,12 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
         if (bin_cards) {
           const double t0 = tb[0], t1 = tb[1], t2 = tb[2], t3 = tb[3];
           a.bad |= bad_entry(t0) || bad_entry(t1) || bad_entry(t2) || bad_entry(t3);
-          // table_minima in closed form: row / column sums of the 2 x 2 table
+          // collapse-bound inputs without per-edge divisions: rho >= tmin / smax
+          // and m >= (smallest unary entry) x smin over the whole model
           const double r0 = t0 + t1, r1 = t2 + t3, c0 = t0 + t2, c1 = t1 + t3;
-          const double* ui = d->unary_values + 2ull * i;
-          const double* uj = d->unary_values + 2ull * j;
-          a.min_rho = std::min(a.min_rho, std::min(std::min(std::min(t0, t1) / r0, std::min(t2, t3) / r1),
-                                                   std::min(std::min(t0, t2) / c0, std::min(t1, t3) / c1)));
-          a.min_m = std::min(a.min_m, std::min(std::max(ui[0] * r0, ui[1] * r1), std::max(uj[0] * c0, uj[1] * c1)));
+          a.tmin = std::min(a.tmin, std::min(std::min(t0, t1), std::min(t2, t3)));
+          a.smin = std::min(a.smin, std::min(std::min(r0, r1), std::min(c0, c1)));
+          a.smax = std::max(a.smax, std::max(std::max(r0, r1), std::max(c0, c1)));
           const bool is = t0 == t3 && t1 == t2;
           a.ising &= is;
           // a = e^J = t0 / t1, clamped to e^{+-69} as ising_weight
@@ -626,6 +634,13 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
       ea.ising &= a.ising;
       ea.min_rho = std::min(ea.min_rho, a.min_rho);
       ea.min_m = std::min(ea.min_m, a.min_m);
+      ea.tmin = std::min(ea.tmin, a.tmin);
+      ea.smin = std::min(ea.smin, a.smin);
+      ea.smax = std::max(ea.smax, a.smax);
+    }
+    if (bin_cards && E) {  // lower bounds of the per-edge minima (the exact bound runs if these do not clear)
+      ea.min_rho = std::min(1.0, ea.tmin / ea.smax);
+      ea.min_m = va.min_u * ea.smin;
     }
   }
   if (ea.bad) throw_first_model_error(d);
