@@ -625,12 +625,19 @@ class EngineT final : public EngineBase {
       if (fin != kFinNone) enqueue_finalize(fin);
     } else if constexpr (QS == 4 || QS == 8) {
       if (g_.lat_cols && g_.uniform_q && !g_.check_collapse && !(lbp_force_ & BP_RUN_LBP_VERTEX)) {
-        // q-state lattice: lanes over states (k_lattice_qsweep)
+        // q-state lattice: four states per lane (k_lattice_qsweep)
         lbp_kernel_ = BP_LBP_KERNEL_QLANES;
-        const unsigned grid = vgrid(k_lattice_qsweep<QS>, static_cast<size_t>(g_.V) * QS);
-        timed(kKUpdate, [&] {
-          k_lattice_qsweep<QS><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), eps_, fa);
-        });
+        if (g_.par_mode) {
+          const unsigned grid = vgrid(k_lattice_qsweep<QS, true>, static_cast<size_t>(g_.V) * (QS / 4));
+          timed(kKUpdate, [&] {
+            k_lattice_qsweep<QS, true><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), eps_, fa);
+          });
+        } else {
+          const unsigned grid = vgrid(k_lattice_qsweep<QS, false>, static_cast<size_t>(g_.V) * (QS / 4));
+          timed(kKUpdate, [&] {
+            k_lattice_qsweep<QS, false><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), eps_, fa);
+          });
+        }
       } else {
         lbp_kernel_ = BP_LBP_KERNEL_VERTEX;
         timed(kKUpdate, [&] {

@@ -1147,18 +1147,22 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
 }
 
 // ---------------------------------------------------------------------------
-// LBP sweep over a q-state lattice, LANES OVER STATES: a group of QS lanes
-// owns one vertex, lane x holds state x of every q-vector, so each q-vector
-// load / store is one coalesced 4*QS-byte access per group (a thread-per-vertex
-// sweep walks 4*QS-byte vectors at a 4*QS*2-byte stride and needs ~128
-// registers for 8 in + 8 out vectors: 25% occupancy, latency-bound).
-// Reductions over the states (max, sums) are xor-shuffles inside the group.
+// LBP sweep over a q-state lattice, FOUR STATES PER LANE: a group of QS / 4
+// lanes owns one vertex (q = 8: a lane pair), lane l holds states
+// [4l, 4l + 4) of every q-vector, so each q-vector moves as one 16-byte access
+// per lane (a 32-byte sector per pair) and a reduction over the states is
+// three in-register steps plus log2(QS / 4) xor-shuffles (one lane per state
+// needed three shuffles per reduction, ~12 per message: the sweep was
+// instruction-bound at 1.96G warp instructions per 4096^2 sweep; a thread per
+// vertex holding 8 in + 8 out vectors needs ~128 registers: latency-bound).
 // Same arithmetic as vertex_update_generic (kModeCount): m_{t+1} = f(m_t) into
 // B, count r(m_t) >= eps; the finalize of the iteration runs in the last block.
-template <int QS>
+// POTTS: Potts tables (par_mode 1, the O(q) contraction); else dense tables
+template <int QS, bool POTTS>
 __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const float* A0, float* B0, Ctl* ctl,
                                                            float eps, FinArgs fin) {
-  static_assert(QS == 4 || QS == 8, "lanes over states: QS divides the warp");
+  static_assert(QS == 4 || QS == 8, "four states per lane: QS = 4 or 8");
+  constexpr int SPL = 4, LPV = QS / SPL;  // states per lane, lanes per vertex
   if (run_done(ctl)) return;
   const float* A = A0;
   float* B = B0;
@@ -1167,27 +1171,31 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
     B = const_cast<float*>(A0);
   }
   const uint32_t C = g.lat_cols, R = g.lat_rows, q = g.uniform_q;
-  const int x = static_cast<int>(threadIdx.x % QS);
-  const bool live_state = x < static_cast<int>(q);
+  const int l = static_cast<int>(threadIdx.x % LPV);
+  const int x0 = l * SPL;
+  bool live_state[SPL];
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) live_state[j] = x0 + j < static_cast<int>(q);
   auto gmax = [](float v) {
 #pragma unroll
-    for (int o = QS / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = LPV / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
   };
   auto gsum = [](float v) {
 #pragma unroll
-    for (int o = QS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = LPV / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
+  auto ld4 = [](const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); };
   int cnt = 0;
   unsigned long long evals = 0, visits = 0;
   bool bad = false;
-  const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / QS);
+  const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / LPV);
   const uint64_t V = g.V;
   // every lane of the warp runs every trip (the shuffles need all of them)
   const uint64_t trips = (V + groups - 1) / groups;
   for (uint64_t t = 0; t < trips; ++t) {
-    const uint64_t vv = t * groups + static_cast<uint64_t>(blockIdx.x) * (blockDim.x / QS) + threadIdx.x / QS;
+    const uint64_t vv = t * groups + static_cast<uint64_t>(blockIdx.x) * (blockDim.x / LPV) + threadIdx.x / LPV;
     const bool act = vv < V;
     const uint32_t v = act ? static_cast<uint32_t>(vv) : 0u;
     const uint32_t r = v / C, c = v - r * C;
@@ -1199,49 +1207,93 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
         has[1] ? 2u * (last ? row + c - 1u : row + 2u * (c - 1u)) : 0u,
         has[2] ? 2u * (last ? row + c : row + 2u * c) + 1u : 0u,
         has[3] ? 2u * (row + 2u * c + (c + 1u < C ? 1u : 0u)) + 1u : 0u};
-    float mi[4], mo[4], w[4];
-    float T = act ? __ldg(&g.unary_log[static_cast<size_t>(v) * QS + x]) : 0.f;
+    float4 mi[4], mo[4];
+    float w[4];
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 T4 = act ? ld4(&g.unary_log[static_cast<size_t>(v) * QS + x0]) : z4;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      mi[k] = has[k] ? __ldg(&A[static_cast<size_t>(ins[k]) * QS + x]) : 0.f;
-      mo[k] = has[k] ? __ldg(&A[static_cast<size_t>(ins[k] ^ 1u) * QS + x]) : 0.f;
-      w[k] = has[k] && g.par_mode ? __ldg(&g.pw[ins[k] >> 1]) : 0.f;
+      mi[k] = has[k] ? ld4(&A[static_cast<size_t>(ins[k]) * QS + x0]) : z4;
+      mo[k] = has[k] ? ld4(&A[static_cast<size_t>(ins[k] ^ 1u) * QS + x0]) : z4;
+      w[k] = has[k] && POTTS ? __ldg(&g.pw[ins[k] >> 1]) : 0.f;
     }
+    float T[SPL] = {T4.x, T4.y, T4.z, T4.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) T += mi[k];
+    for (int k = 0; k < 4; ++k) {
+      T[0] += mi[k].x;
+      T[1] += mi[k].y;
+      T[2] += mi[k].z;
+      T[3] += mi[k].w;
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t out = ins[k] ^ 1u;
-      const float pl = live_state ? T - mi[k] : -INFINITY;
-      const float M = gmax(pl);
-      const float e = live_state ? fex2(pl - M) : 0.f;
-      float o;
-      if (g.par_mode) {  // Potts: o(x) = sum_y e(y) t(y, x) / d = (a/d - 1) e(x) + sum_y e(y)
-        o = fmaf(w[k], e, gsum(e));
+      const float mik[SPL] = {mi[k].x, mi[k].y, mi[k].z, mi[k].w};
+      const float mok[SPL] = {mo[k].x, mo[k].y, mo[k].z, mo[k].w};
+      float pl[SPL], e[SPL], o[SPL];
+      float M = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        pl[j] = live_state[j] ? T[j] - mik[j] : -INFINITY;
+        M = fmaxf(M, pl[j]);
+      }
+      M = gmax(M);
+      float S = 0.f;
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        e[j] = live_state[j] ? fex2(pl[j] - M) : 0.f;
+        S += e[j];
+      }
+      if constexpr (POTTS) {  // Potts: o(x) = sum_y e(y) t(y, x) / d = (a/d - 1) e(x) + sum_y e(y)
+        S = gsum(S);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) o[j] = fmaf(w[k], e[j], S);
       } else {  // dense max-scaled table, oriented by the direction of `out`
         const float* tab = g.table + static_cast<size_t>(out >> 1) * QS * QS;
-        o = 0.f;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) o[j] = 0.f;
 #pragma unroll
         for (int y = 0; y < QS; ++y) {
-          const float ey = __shfl_sync(0xffffffffu, e, (threadIdx.x & 31u & ~(QS - 1u)) + y);
-          const float tv = has[k] ? __ldg(&tab[(out & 1u) ? x * QS + y : y * QS + x]) : 0.f;
-          o = fmaf(tv, ey, o);
+          // e(y) lives in lane y / SPL of the group, slot y % SPL
+          const float ey = __shfl_sync(0xffffffffu, e[y % SPL], (threadIdx.x & 31u & ~(LPV - 1u)) + y / SPL);
+#pragma unroll
+          for (int j = 0; j < SPL; ++j) {
+            const int x = x0 + j;
+            const float tv = has[k] ? __ldg(&tab[(out & 1u) ? x * QS + y : y * QS + x]) : 0.f;
+            o[j] = fmaf(tv, ey, o[j]);
+          }
         }
       }
-      o = live_state ? o : 0.f;
-      const float sm = gsum(o);
-      const float ln = flg2(o * frcp(sm));
-      const float rr = gmax(live_state ? fabsf(fex2(ln) - fex2(mo[k])) : 0.f);
+      float sm = 0.f;
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        o[j] = live_state[j] ? o[j] : 0.f;
+        sm += o[j];
+      }
+      sm = gsum(sm);
+      const float inv = frcp(sm);
+      float ln[SPL], rr = 0.f;
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        ln[j] = flg2(o[j] * inv);
+        rr = fmaxf(rr, live_state[j] ? fabsf(fex2(ln[j]) - fex2(mok[j])) : 0.f);
+      }
+      rr = gmax(rr);
       if (has[k]) {
-        B[static_cast<size_t>(out) * QS + x] = live_state ? ln : mo[k];
-        if (x == 0) {
+        float4 st;
+        st.x = live_state[0] ? ln[0] : mok[0];
+        st.y = live_state[1] ? ln[1] : mok[1];
+        st.z = live_state[2] ? ln[2] : mok[2];
+        st.w = live_state[3] ? ln[3] : mok[3];
+        *reinterpret_cast<float4*>(&B[static_cast<size_t>(out) * QS + x0]) = st;
+        if (l == 0) {
           cnt += rr >= eps;
           ++evals;
           bad |= !(sm > 0.f) || !(sm < INFINITY);
         }
       }
     }
-    if (act && x == 0) ++visits;
+    if (act && l == 0) ++visits;
   }
   if (bad) ctl->numeric_error = 1u;
   Contrib cb;
