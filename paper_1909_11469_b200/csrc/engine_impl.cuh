@@ -628,14 +628,16 @@ class EngineT final : public EngineBase {
         // q-state lattice: four states per lane (k_lattice_qsweep)
         lbp_kernel_ = BP_LBP_KERNEL_QLANES;
         if (g_.par_mode) {
-          const unsigned grid = vgrid(k_lattice_qsweep<QS, true>, static_cast<size_t>(g_.V) * (QS / 4));
+          const unsigned grid = vgrid(k_lattice_qsweep<QS, true, kModeCount>, static_cast<size_t>(g_.V) * (QS / 4));
           timed(kKUpdate, [&] {
-            k_lattice_qsweep<QS, true><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), eps_, fa);
+            k_lattice_qsweep<QS, true, kModeCount><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr,
+                                                                          nullptr, ctl(), eps_, fa);
           });
         } else {
-          const unsigned grid = vgrid(k_lattice_qsweep<QS, false>, static_cast<size_t>(g_.V) * (QS / 4));
+          const unsigned grid = vgrid(k_lattice_qsweep<QS, false, kModeCount>, static_cast<size_t>(g_.V) * (QS / 4));
           timed(kKUpdate, [&] {
-            k_lattice_qsweep<QS, false><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), ctl(), eps_, fa);
+            k_lattice_qsweep<QS, false, kModeCount><<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), nullptr, nullptr,
+                                                                           nullptr, ctl(), eps_, fa);
           });
         }
       } else {
@@ -870,8 +872,31 @@ class EngineT final : public EngineBase {
   }
 
   // touched refresh; the iteration's loop control (fin) runs in its last block
+  // q-state lattices (q <= 8): the touched refresh with four states per lane
+  // outside RnBP list mode (k_lattice_qsweep<kModeDelta>); the vertex kernel
+  // after it is gated to list mode
+  bool qlanes_refresh() const {
+    static const bool off = std::getenv("BPB_NO_QLANES_REFRESH") != nullptr;  // tuning aid
+    return !off && (QS == 4 || QS == 8) && g_.lat_cols && g_.uniform_q && !g_.check_collapse && !band_owned_;
+  }
   void enqueue_refresh(int fin) {
-    const FinArgs fa{fin, g_.D};
+    FinArgs fa{fin, g_.D, 0};
+    if constexpr (QS == 4 || QS == 8) {
+      if (qlanes_refresh()) {
+        const unsigned grid = vgrid(k_lattice_qsweep<QS, true, kModeDelta>, static_cast<size_t>(g_.V) * (QS / 4));
+        timed(kKUpdate, [&] {
+          if (g_.par_mode)
+            k_lattice_qsweep<QS, true, kModeDelta><<<grid, kBlock, 0, s_>>>(
+                dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_, fa);
+          else
+            k_lattice_qsweep<QS, false, kModeDelta><<<grid, kBlock, 0, s_>>>(
+                dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_, fa);
+        });
+        launch_check();
+        if (!use_clist_) return;  // no list mode: the lanes kernel refreshes every iteration
+        fa.gate = 1;
+      }
+    }
     timed(kKUpdate, [&] {
       if (use_clist_)
         k_vertex_update<QS, kModeDelta, true, false, true><<<vgrid(k_vertex_update<QS, kModeDelta, true, false, true>, g_.V), kBlock, 0, s_>>>(

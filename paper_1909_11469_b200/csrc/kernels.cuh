@@ -605,6 +605,7 @@ __device__ __forceinline__ bool last_block_done(Ctl* c) {
 struct FinArgs {
   int mode;    // kFinNone: no fused finalize
   uint32_t D;  // directed edges counted by the finalize
+  int gate;    // 1: the launch runs only in RnBP list mode (k_lattice_qsweep refreshes the other iterations)
 };
 
 __device__ __forceinline__ void fused_finalize(Ctl* c, const FinArgs& f) {
@@ -1142,6 +1143,7 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
                                                           const uint32_t* vflag, Ctl* ctl, float eps,
                                                           CandList cand_list, FinArgs fin) {
   if (run_done(ctl)) return;
+  if (fin.gate && ctl->cl_state < 1u) return;
   vertex_update_pass<QS, MODE, LIST, PINGPONG, CL>(g, A0, B0, res, vlist, vflag, ctl, eps, cand_list);
   fused_finalize(ctl, fin);
 }
@@ -1157,19 +1159,29 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
 // vertex holding 8 in + 8 out vectors needs ~128 registers: latency-bound).
 // Same arithmetic as vertex_update_generic (kModeCount): m_{t+1} = f(m_t) into
 // B, count r(m_t) >= eps; the finalize of the iteration runs in the last block.
-// POTTS: Potts tables (par_mode 1, the O(q) contraction); else dense tables
-template <int QS, bool POTTS>
-__global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const float* A0, float* B0, Ctl* ctl,
+// POTTS: Potts tables (par_mode 1, the O(q) contraction); else dense tables.
+// MODE kModeCount: the LBP sweep (ping-pong buffers, count r >= eps).
+// MODE kModeDelta: refresh_residuals of the touched vertices (flagged in
+// vflag, or listed in vlist on sparse iterations) outside RnBP list mode:
+// candidates into B, residuals r / res[out] and the unconverged delta, as
+// vertex_update_generic<kModeDelta> (list mode runs that kernel, gated).
+template <int QS, bool POTTS, int MODE>
+__global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const float* A0, float* B0, float* res,
+                                                           const uint32_t* vlist, const uint32_t* vflag, Ctl* ctl,
                                                            float eps, FinArgs fin) {
   static_assert(QS == 4 || QS == 8, "four states per lane: QS = 4 or 8");
+  static_assert(MODE == kModeCount || MODE == kModeDelta, "sweep or touched refresh");
   constexpr int SPL = 4, LPV = QS / SPL;  // states per lane, lanes per vertex
   if (run_done(ctl)) return;
+  if (MODE == kModeDelta && ctl->cl_state >= 1u) return;  // list mode: the gated vertex kernel
   const float* A = A0;
   float* B = B0;
-  if (ctl->sweeps & 1ull) {
+  if (MODE == kModeCount && (ctl->sweeps & 1ull)) {
     A = B0;
     B = const_cast<float*>(A0);
   }
+  const bool dense_items = MODE == kModeCount || ctl->dense != 0u;
+  const uint32_t stamp = ctl->stamp;
   const uint32_t C = g.lat_cols, R = g.lat_rows, q = g.uniform_q;
   const int l = static_cast<int>(threadIdx.x % LPV);
   const int x0 = l * SPL;
@@ -1191,13 +1203,20 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
   unsigned long long evals = 0, visits = 0;
   bool bad = false;
   const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / LPV);
-  const uint64_t V = g.V;
+  const uint64_t V = dense_items ? g.V : ctl->nflag;  // items: vertices, or the touched list
   // every lane of the warp runs every trip (the shuffles need all of them)
   const uint64_t trips = (V + groups - 1) / groups;
   for (uint64_t t = 0; t < trips; ++t) {
     const uint64_t vv = t * groups + static_cast<uint64_t>(blockIdx.x) * (blockDim.x / LPV) + threadIdx.x / LPV;
-    const bool act = vv < V;
-    const uint32_t v = act ? static_cast<uint32_t>(vv) : 0u;
+    bool act = vv < V;
+    uint32_t v = act ? static_cast<uint32_t>(vv) : 0u;
+    if (MODE == kModeDelta && act) {
+      if (dense_items)
+        act = __ldg(&vflag[v]) == stamp;
+      else
+        v = __ldg(&vlist[v]);
+    }
+    if (!act) v = 0u;
     const uint32_t r = v / C, c = v - r * C;
     const uint32_t row = r * (2u * C - 1u);
     const bool last = r + 1u == R;
@@ -1217,6 +1236,11 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
       mo[k] = has[k] ? ld4(&A[static_cast<size_t>(ins[k] ^ 1u) * QS + x0]) : z4;
       w[k] = has[k] && POTTS ? __ldg(&g.pw[ins[k] >> 1]) : 0.f;
     }
+    // old residuals of the outgoing messages (refresh), issued with the
+    // message loads: a load after this thread's stores would wait in line
+    bool was[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) was[k] = MODE == kModeDelta && l == 0 && has[k] && res[ins[k] ^ 1u] >= eps;
     float T[SPL] = {T4.x, T4.y, T4.z, T4.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -1287,7 +1311,12 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
         st.w = live_state[3] ? ln[3] : mok[3];
         *reinterpret_cast<float4*>(&B[static_cast<size_t>(out) * QS + x0]) = st;
         if (l == 0) {
-          cnt += rr >= eps;
+          if (MODE == kModeDelta) {
+            cnt += (rr >= eps ? 1 : 0) - (was[k] ? 1 : 0);
+            res[out] = rr;
+          } else {
+            cnt += rr >= eps;
+          }
           ++evals;
           bad |= !(sm > 0.f) || !(sm < INFINITY);
         }
@@ -1297,7 +1326,10 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
   }
   if (bad) ctl->numeric_error = 1u;
   Contrib cb;
-  cb.count = static_cast<unsigned long long>(cnt);
+  if (MODE == kModeDelta)
+    cb.delta = cnt;
+  else
+    cb.count = static_cast<unsigned long long>(cnt);
   cb.evals = evals;
   cb.visits = visits;
   block_accumulate(ctl, cb);
@@ -1343,8 +1375,15 @@ __device__ __forceinline__ void commit_edge(const DevGraph& g, uint32_t d, float
   c.delta -= (r >= eps) ? 1 : 0;
   c.frontier += 1;
   res[d] = 0.f;
+  if constexpr (QS % 4 == 0) {  // q-vectors move as 16-byte loads / stores
+    float4* dst = reinterpret_cast<float4*>(live + static_cast<size_t>(d) * QS);
+    const float4* src = reinterpret_cast<const float4*>(cand + static_cast<size_t>(d) * QS);
+#pragma unroll (QS <= 16 ? QS / 4 : 2)
+    for (int x4 = 0; x4 < QS / 4; ++x4) dst[x4] = src[x4];
+  } else {
 #pragma unroll (QS <= 8 ? QS : 2)
-  for (int x = 0; x < QS; ++x) live[static_cast<size_t>(d) * QS + x] = cand[static_cast<size_t>(d) * QS + x];
+    for (int x = 0; x < QS; ++x) live[static_cast<size_t>(d) * QS + x] = cand[static_cast<size_t>(d) * QS + x];
+  }
   tgt = g.ep[d ^ 1u];
   if (dense) {
     vflag[tgt] = stamp;
