@@ -32,6 +32,7 @@ row-band partitioned 16384^2 grid (config 5) is reported under
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -305,9 +306,11 @@ def run_b200(args):
         r = bp.run(g, bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
         _ = float(r.beliefs.values[-1])
         del g, r
+    gc.disable()  # no collector pauses inside the timed steps (as timeit)
     for s in seeds:
         cards, un, ep, tb = host_arrays[s]
         flush_l2(torch, flush)
+        torch.cuda.synchronize()
         t1 = time.perf_counter()
         g = bp.PairwiseMRF.from_arrays(cards, un, ep, tb, device=local)
         r = bp.run(g, bp.SchedulerConfig(kind=kind, **rnbp_kw(s)))
@@ -319,6 +322,7 @@ def run_b200(args):
         h2d = cards.nbytes + un.nbytes + ep.nbytes + tb.nbytes
         d2h = r.beliefs.values.nbytes + 32 * len(r.trace)
         del g
+    gc.enable()
     del host_arrays
     if dist:
         tt = torch.tensor([e2e_t, float(e2e_updates)], dtype=torch.float64, device="cuda")
@@ -523,7 +527,8 @@ def _config4(bp, torch, device, peak, peak_src):
     k = r.kernel_stats["update"]
     sweeps = r.iterations + 1
     nbytes = qstate_sweep_bytes(V, D, 8) * sweeps
-    out["lbp"] = _roofline("k_vertex_update<Count> q-state lattice sweep (LBP), Potts 4096^2 q=8", nbytes, k["ms"],
+    out["lbp"] = _roofline("k_lattice_qsweep<8, Potts, Count> (LBP sweep, four states per lane), Potts 4096^2 q=8",
+                           nbytes, k["ms"],
                            peak, peak_src, launches=k["launches"], sweeps=sweeps, ms_per_sweep=k["ms"] / sweeps,
                            updates_per_s=r.messages_updated_total / (r.device_ms / 1e3),
                            bytes_per_directed_edge=round(qstate_sweep_bytes(V, D, 8) / D, 2),
@@ -538,6 +543,24 @@ def _config4(bp, torch, device, peak, peak_src):
                           "ms_per_iteration": round(r.device_ms / max(1, r.iterations), 4),
                           "unconverged_end": r.trace[-1].unconverged if len(r.trace) else None}
     out["rnbp_low_p_sweep"] = sweep
+    # the dense RnBP iteration at low_p 0.5 (the 20-iteration window): HBM
+    # rooflines of the touched refresh (four states per lane) and the select,
+    # unique bytes: refresh per touched vertex 4q + 4 (unary, flag), per
+    # refreshed directed edge 8q + 10 (message read + candidate write, coupling
+    # half, residual r/w); select 4 B per directed edge scanned + 8q + 4 per commit
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, high_p=1.0, max_iterations=20, time_limit=1e9,
+                             seed=1)
+    ri = bp.run_ex(g, cfg, beliefs=False, kernel_timing=True)
+    ks = ri.kernel_stats
+    q = POTTS_Q
+    rb = ri.vertex_visits * (4 * q + 4) + ri.message_evaluations * (8 * q + 10)
+    sb = 4 * D * ri.iterations + (8 * q + 4) * ri.messages_updated_total
+    out["rnbp_dense"] = {
+        "ms_per_iteration": round((ks["update"]["ms"] + ks["select"]["ms"]) / max(1, ri.iterations), 4),
+        "refresh": _roofline("k_lattice_qsweep<8, Potts, Delta> (touched refresh, four states per lane)", rb,
+                             ks["update"]["ms"], peak, peak_src, launches=ks["update"]["launches"]),
+        "select": _roofline("k_rnbp_select<8> (filter + Bernoulli + 16-byte commits)", sb, ks["select"]["ms"], peak,
+                            peak_src, launches=ks["select"]["launches"])}
     del g
     torch.cuda.empty_cache()
 

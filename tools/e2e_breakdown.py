@@ -11,11 +11,11 @@ import torch  # noqa: E402
 import paper_1909_11469_b200 as bp  # noqa: E402
 
 torch.cuda.set_device(0)
-arrs = {s: bp.generate_ising_arrays(bp.IsingParams(n=1000, c=2.5, seed=s)) for s in range(3)}
+arrs = {s: bp.generate_ising_arrays(bp.IsingParams(n=1000, c=2.5, seed=s)) for s in range(6)}
 cfg = lambda s, it=20: bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=0.5, max_iterations=it,
                                           time_limit=1e9, seed=s)
 bp.run(bp.PairwiseMRF.from_arrays(*arrs[0]), cfg(0, 2))
-for s in range(3):
+for s in range(6):
     t0 = time.perf_counter()
     g = bp.PairwiseMRF.from_arrays(*arrs[s])
     t1 = time.perf_counter()
