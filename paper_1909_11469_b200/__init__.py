@@ -304,12 +304,16 @@ class BeliefTable:
 
     def __init__(self, values: np.ndarray, offsets):
         self.values = values
-        self._offsets = offsets  # array, or the graph (offsets built on first use)
+        # an array, or (V, q) of a uniform-cardinality graph: offsets built on
+        # first use (no reference to the graph, whose device memory the table
+        # must not keep alive)
+        self._offsets = offsets
 
     @property
     def offsets(self) -> np.ndarray:
         if not isinstance(self._offsets, np.ndarray):
-            self._offsets = self._offsets.belief_offsets
+            V, q = self._offsets
+            self._offsets = np.arange(V + 1, dtype=np.int64) * q
         return self._offsets
 
     def num_vertices(self) -> int:
@@ -562,7 +566,8 @@ def run_ex(graph: PairwiseMRF, config: SchedulerConfig, flags: int = 0, batch: i
                           trace_cap))
     n = min(int(res.trace_len), trace_cap)
     trace = Trace(np.frombuffer(tr, dtype=_TRACE_DTYPE, count=n).copy())
-    bt = BeliefTable(bel[:nb], graph) if bel is not None else None
+    boff = graph._boff if graph._boff is not None else (int(graph.info.num_vertices), int(graph.info.max_cardinality))
+    bt = BeliefTable(bel[:nb], boff) if bel is not None else None
     return RunResult(bool(res.converged), int(res.iterations), float(res.wall_time),
                      int(res.messages_updated_total), bt, trace, float(res.device_ms),
                      int(res.message_evaluations), int(res.gpu_launches), int(res.vertex_visits),

@@ -511,7 +511,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     const unsigned nch = pool_chunks(V);
     std::vector<VAcc> acc(nch);
     parallel_chunks(V, nch, [&](uint64_t lo, uint64_t hi, unsigned t) {
-      VAcc& a = acc[t];
+      VAcc a;
       for (uint64_t v = lo; v < hi; ++v) {
         const uint32_t q = cards[v];
         a.zero |= q == 0;
@@ -519,6 +519,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
         a.minq = std::min(a.minq, q);
         a.usz += q;
       }
+      acc[t] = a;
     });
     for (const VAcc& a : acc) {
       va.zero |= a.zero;
@@ -546,7 +547,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     const unsigned nch = pool_chunks(V);
     std::vector<VAcc> acc(nch);
     parallel_chunks(V, nch, [&](uint64_t lo, uint64_t hi, unsigned t) {
-      VAcc& a = acc[t];
+      VAcc a;  // in registers; written back once
       for (uint64_t v = lo; v < hi; ++v) {
         const double* u = d->unary_values + unary_at(v);
         double mu = 0.0, mn = std::numeric_limits<double>::infinity();
@@ -566,6 +567,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
                                            : static_cast<float>(std::log2(u[1]) - std::log2(u[0]));
         }
       }
+      acc[t] = a;
     });
     for (const VAcc& a : acc) {
       va.bad |= a.bad;
@@ -599,7 +601,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
     const unsigned nch = pool_chunks(E);
     std::vector<EAcc> acc(nch);
     parallel_chunks(E, nch, [&](uint64_t lo, uint64_t hi, unsigned t) {
-      EAcc& a = acc[t];
+      EAcc a;  // in registers; written back once (the per-chunk slots share cache lines)
       for (uint64_t e = lo; e < hi; ++e) {
         const uint32_t i = ep[2 * e], j = ep[2 * e + 1];
         if (i >= V || j >= V || (any_order ? i == j : i >= j)) {
@@ -628,6 +630,7 @@ std::unique_ptr<GraphImpl> build_from_desc(const bp_graph_desc* d, const bp_devi
                        a.min_m);
         }
       }
+      acc[t] = a;
     });
     for (const EAcc& a : acc) {
       ea.bad |= a.bad;

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstdint>
 #include <functional>
 #include <mutex>
@@ -53,7 +54,9 @@ class HostPool {
  private:
   HostPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    nworkers_ = std::min(31u, hw) - 1;
+    unsigned n = std::min(32u, hw);
+    if (const char* e = std::getenv("BPB_HOST_THREADS")) n = std::max(1, std::min(64, std::atoi(e)));
+    nworkers_ = n - 1;
     for (unsigned i = 0; i < nworkers_; ++i)
       std::thread([this] { loop(); }).detach();
   }
