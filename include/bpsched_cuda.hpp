@@ -277,6 +277,50 @@ inline bpsched::RunResult run_partitioned_local(const bpsched::PairwiseMRF& grap
   return out;
 }
 
+/// Vertex-range partition of ANY binary model (random graphs included):
+/// every part of an `nparts`-way partition inside this process, assembled into
+/// the whole graph's RunResult (LBP, RnBP; bitwise the one-GPU run).  Part p
+/// owns vertices [V p / P, V (p + 1) / P) (bp_graph_create_part).
+inline bpsched::RunResult run_vertex_partitioned_local(const bpsched::PairwiseMRF& graph,
+                                                       const bpsched::SchedulerConfig& config, uint32_t nparts,
+                                                       int device = -1) {
+  config.validate();
+  const HostArrays a(graph);
+  const bp_sched_config c = to_c(config);
+  const bp_graph_desc d = a.desc();
+  bp_device_opts o{device, 0};
+  std::vector<std::unique_ptr<detail::BandHandles>> parts;
+  std::vector<bp_part_info> infos(nparts);
+  std::vector<bp_engine*> es;
+  for (uint32_t p = 0; p < nparts; ++p) {
+    parts.push_back(std::make_unique<detail::BandHandles>());
+    check(bp_graph_create_part(&d, p, nparts, &o, &parts.back()->g, &infos[p]));
+    check(bp_part_engine_create(parts.back()->g, &c, &parts.back()->e));
+    es.push_back(parts.back()->e);
+  }
+  bp_band_comm* comm = nullptr;
+  check(bp_band_comm_create_local(&comm));
+  bp_run_result r{};
+  const int rc = bp_band_run(es.data(), nparts, comm, &r);
+  bp_band_comm_destroy(comm);
+  check(rc);
+  bpsched::RunResult out;
+  detail::fill_result(r, out);
+  out.beliefs = bpsched::BeliefTable(a.cards);
+  for (uint32_t p = 0; p < nparts; ++p) {
+    bp_graph_info gi{};
+    check(bp_graph_info_get(parts[p]->g, &gi));
+    std::vector<double> bel(2ull * gi.num_vertices);
+    check(bp_engine_beliefs(parts[p]->e, bel.data()));
+    for (uint32_t v = infos[p].v0; v < infos[p].v1; ++v) {  // local ids [0, v1 - v0) are the owned vertices
+      auto dst = out.beliefs.at(v);
+      dst[0] = bel[2ull * (v - infos[p].v0)];
+      dst[1] = bel[2ull * (v - infos[p].v0) + 1];
+    }
+  }
+  return out;
+}
+
 }  // namespace bpsched_cuda
 
 #endif  // BPSCHED_CUDA_HPP

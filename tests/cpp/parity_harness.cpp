@@ -17,6 +17,8 @@
 //   run_<kind>        bpsched::run vs bpsched_cuda::run: same convergence
 //                     verdict, converged beliefs within 1e-4
 //   errors            std::invalid_argument / bpsched::model_error from both
+#include <set>
+#include <random>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -253,6 +255,47 @@ int main() {
                ref.converged && worst <= 1e-4,
            "iterations " + std::to_string(c.iterations) + " (one band " + std::to_string(d.iterations) +
                ", reference " + std::to_string(ref.iterations) + ") max|db| vs reference " + std::to_string(worst));
+  }
+  // vertex-range partition of a random binary model (bp_graph_create_part):
+  // bitwise the one-GPU run, and the reference's converged marginals
+  for (uint32_t parts : {2u, 3u}) {
+    std::vector<uint32_t> cards(400, 2);
+    std::vector<std::vector<double>> unary;
+    std::vector<bpsched::PairwiseMRF::EdgeSpec> edges;
+    std::mt19937_64 rng(77 + parts);
+    std::uniform_real_distribution<double> u(0.5, 1.5);
+    for (uint32_t v = 0; v < 400; ++v) unary.push_back({u(rng), u(rng)});
+    std::set<std::pair<uint32_t, uint32_t>> seen;
+    while (edges.size() < 700) {
+      uint32_t i = static_cast<uint32_t>(rng() % 400), j = static_cast<uint32_t>(rng() % 400);
+      if (i == j) continue;
+      if (i > j) std::swap(i, j);
+      if (!seen.insert({i, j}).second) continue;
+      edges.push_back({i, j, {u(rng), u(rng) * 0.3, u(rng) * 0.3, u(rng)}});
+    }
+    std::sort(edges.begin(), edges.end(), [](const auto& x, const auto& y) { return std::make_pair(x.i, x.j) < std::make_pair(y.i, y.j); });
+    const auto g = bpsched::build_graph(cards, unary, edges);
+    for (auto kind : {SchedulerKind::lbp, SchedulerKind::rnbp}) {
+      bpsched::SchedulerConfig cfg;
+      cfg.kind = kind;
+      cfg.low_p = 0.5;
+      cfg.max_iterations = 5000;
+      const bpsched::RunResult a = bpsched_cuda::run(g, cfg);
+      const bpsched::RunResult b = bpsched_cuda::run_vertex_partitioned_local(g, cfg, parts);
+      const bpsched::RunResult ref = bpsched::run(g, cfg);
+      bool same = a.converged == b.converged && a.iterations == b.iterations;
+      double worst = 0.0;
+      for (bpsched::vertex_id v = 0; v < g.num_vertices(); ++v)
+        for (size_t k = 0; k < 2; ++k) {
+          same = same && a.beliefs.at(v)[k] == b.beliefs.at(v)[k];
+          worst = std::max(worst, std::fabs(ref.beliefs.at(v)[k] - b.beliefs.at(v)[k]));
+        }
+      report(std::string("parts_") + (kind == SchedulerKind::lbp ? "lbp" : "rnbp") + "_random400_x" +
+                 std::to_string(parts),
+             same && b.converged && ref.converged && worst <= 1e-4,
+             "bitwise the one-GPU run; iterations " + std::to_string(b.iterations) + " (reference " +
+                 std::to_string(ref.iterations) + ") max|db| vs reference " + std::to_string(worst));
+    }
   }
   // serial RBP goes through the reference's run_serial_rbp inside the facade
   {
