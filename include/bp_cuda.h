@@ -42,7 +42,8 @@ typedef enum {
   BP_ERR_CUDA = 4,
   BP_ERR_NCCL = 5,
   BP_ERR_OOM = 6,
-  BP_ERR_UNSUPPORTED = 7
+  BP_ERR_UNSUPPORTED = 7,
+  BP_ERR_PARSE = 8             /* bpsched::parse_error (errors.hpp:29-38): message "line N: ..." */
 } bp_status;
 
 /* bpsched::SchedulerKind (schedulers.hpp:21-24), same numbering. */
@@ -188,6 +189,19 @@ BP_API int bp_generate_ising_arrays(uint32_t n, double c, uint64_t seed, uint32_
  * input arrays (n cardinalities, 2n unaries, 2m endpoints, 4m tables). */
 BP_API int bp_generate_er_arrays(uint32_t n, uint32_t m, double c, uint64_t seed, uint32_t* cardinalities,
                                  double* unary, uint32_t* endpoints, double* tables);
+
+/* The reference's text model format (.pgm; parse_model / serialize_model,
+ * model_io.cpp:98-181): bulk ingest on the host pool into build_graph's input
+ * arrays (BP_ERR_PARSE with the reference's first parse_error, "line N: ...").
+ * bp_pgm_*: host only (the arrays); bp_graph_create_pgm: parse + bp_graph_create. */
+typedef struct bp_pgm bp_pgm;
+BP_API int bp_pgm_parse(const char* text, uint64_t len, bp_pgm** out);
+BP_API int bp_pgm_info(const bp_pgm* m, uint32_t* num_vertices, uint32_t* num_edges, uint64_t* unary_len,
+                       uint64_t* table_len);
+BP_API int bp_pgm_arrays(const bp_pgm* m, uint32_t* cardinalities, double* unary_values, uint32_t* edge_endpoints,
+                         double* pairwise_values);
+BP_API void bp_pgm_destroy(bp_pgm* m);
+BP_API int bp_graph_create_pgm(const char* text, uint64_t len, const bp_device_opts* opts, struct bp_graph** out);
 
 BP_API void bp_graph_destroy(struct bp_graph* g);
 BP_API int bp_graph_info_get(const struct bp_graph* g, bp_graph_info* info);

@@ -110,6 +110,9 @@ class Lib:
             f("generate_potts", C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(_P)])
             f("generate_er", C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, C.POINTER(_P)])
             f("engine_set_messages", C.c_int, [_P, _f64p])
+        if which == "ref":
+            f("parse_model", C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(_P)])
+            f("serialize_model", C.c_uint64, [_P, C.c_char_p, C.c_uint64])
         f("mt_draws", None, [C.c_uint64, C.c_uint64, _u64p, _f64p])
         f("validate_config", C.c_int, [C.POINTER(OrcConfig)])
         f("select_parallelism", C.c_double, [C.c_uint32, C.c_uint32, C.POINTER(OrcConfig)])
@@ -198,6 +201,21 @@ class Graph:
         lib.check(lib.graph_create(cards.size, cards, unary, len(np.asarray(endpoints).reshape(-1)) // 2,
                                    ep, tables, C.byref(h)))
         return cls(lib, h)
+
+    @classmethod
+    def parse(cls, lib: Lib, text) -> "Graph":
+        """the reference's parse_model (model_io.cpp:98-150); ref only"""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        h = _P()
+        lib.check(lib.parse_model(data, len(data), C.byref(h)))
+        return cls(lib, h)
+
+    def serialize(self) -> str:
+        """the reference's serialize_model (model_io.cpp:152-181); ref only"""
+        n = self.lib.serialize_model(self.h, None, 0)
+        buf = C.create_string_buffer(n)
+        self.lib.serialize_model(self.h, buf, n)
+        return buf.raw[:n].decode()
 
     @classmethod
     def ising(cls, lib: Lib, n, c, seed) -> "Graph":

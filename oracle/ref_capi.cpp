@@ -10,6 +10,7 @@
 #include <bpsched/errors.hpp>
 #include <bpsched/generators.hpp>
 #include <bpsched/messages.hpp>
+#include <bpsched/model_io.hpp>
 #include <bpsched/mrf.hpp>
 #include <bpsched/schedulers.hpp>
 
@@ -35,6 +36,9 @@ int guarded(F&& f) {
   } catch (const numeric_error& e) {
     g_err = e.what();
     return ORC_NUMERIC;
+  } catch (const parse_error& e) {
+    g_err = e.what();
+    return 8;  // the engine's BP_ERR_PARSE
   } catch (const model_error& e) {
     g_err = e.what();
     return ORC_MODEL;
@@ -111,6 +115,17 @@ int ref_graph_create(uint32_t V, const uint32_t* cards, const double* unary, uin
 }
 
 void ref_graph_destroy(ref_graph* g) { delete g; }
+
+// parse_model / serialize_model (model_io.cpp:98-181), for the .pgm ingest tests
+int ref_parse_model(const char* text, uint64_t len, ref_graph** out) {
+  *out = nullptr;
+  return guarded([&] { *out = new ref_graph{parse_model(std::string_view(text, len))}; });
+}
+uint64_t ref_serialize_model(const ref_graph* g, char* buf, uint64_t cap) {
+  const std::string s = serialize_model(g->g);
+  if (buf && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+  return s.size();
+}
 uint32_t ref_graph_num_vertices(const ref_graph* g) { return g->g.num_vertices(); }
 uint32_t ref_graph_num_edges(const ref_graph* g) { return g->g.num_edges(); }
 

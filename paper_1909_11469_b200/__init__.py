@@ -56,12 +56,20 @@ class UnsupportedError(Error):
     pass
 
 
+class ParseError(Error):
+    """bpsched::parse_error (errors.hpp:29-38): the message starts with "line N: "."""
+
+    @property
+    def line(self) -> int:
+        return int(str(self).split(":", 1)[0].split()[1])
+
+
 class CudaError(Error):
     pass
 
 
 _CODES = {1: ValueError, 2: ModelError, 3: NumericError, 4: CudaError, 5: CudaError, 6: MemoryError,
-          7: UnsupportedError}
+          7: UnsupportedError, 8: ParseError}
 
 
 # --------------------------------------------------------------------------
@@ -151,6 +159,11 @@ def _load():
         "bp_graph_destroy": (None, [P]),
         "bp_generate_ising_arrays": (C.c_int, [C.c_uint32, C.c_double, C.c_uint64, P, P, P, P]),
         "bp_generate_er_arrays": (C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_uint64, P, P, P, P]),
+        "bp_pgm_parse": (C.c_int, [C.c_char_p, C.c_uint64, P]),
+        "bp_pgm_info": (C.c_int, [P, P, P, P, P]),
+        "bp_pgm_arrays": (C.c_int, [P, P, P, P, P]),
+        "bp_pgm_destroy": (None, [P]),
+        "bp_graph_create_pgm": (C.c_int, [C.c_char_p, C.c_uint64, P, P]),
         "bp_graph_info_get": (C.c_int, [P, C.POINTER(_Info)]),
         "bp_run": (C.c_int, [P, C.POINTER(_Config), C.POINTER(_Result), P, P, C.c_uint64]),
         "bp_run_ex": (C.c_int, [P, C.POINTER(_Config), C.POINTER(_RunOpts), C.POINTER(_Result), P, P, C.c_uint64]),
@@ -516,6 +529,32 @@ def generate_ising_arrays(params: IsingParams):
     tb = np.zeros(max(4 * E, 1))
     _check(_lib.bp_generate_ising_arrays(n, params.c, params.seed, _ptr(cards), _ptr(un), _ptr(ep), _ptr(tb)))
     return cards[:V], un[: 2 * V], ep[: 2 * E].reshape(E, 2), tb[: 4 * E]
+
+
+def parse_model_arrays(text):
+    """parse_model (model_io.cpp:98-150) up to build_graph: the reference's text
+    model as build_graph's input arrays (cards, unary, endpoints (E, 2), tables),
+    parsed on the host pool; ParseError as the reference's parse_error."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    _check(_lib.bp_pgm_parse(data, len(data), C.byref(h)))
+    try:
+        V, E, nu, nt = C.c_uint32(), C.c_uint32(), C.c_uint64(), C.c_uint64()
+        _check(_lib.bp_pgm_info(h, C.byref(V), C.byref(E), C.byref(nu), C.byref(nt)))
+        cards = np.zeros(max(V.value, 1), np.uint32)
+        un = np.zeros(max(nu.value, 1))
+        ep = np.zeros(max(2 * E.value, 2), np.uint32)
+        tb = np.zeros(max(nt.value, 1))
+        _check(_lib.bp_pgm_arrays(h, _ptr(cards), _ptr(un), _ptr(ep), _ptr(tb)))
+    finally:
+        _lib.bp_pgm_destroy(h)
+    return cards[: V.value], un[: nu.value], ep[: 2 * E.value].reshape(E.value, 2), tb[: nt.value]
+
+
+def parse_model(text, device: int = -1) -> "PairwiseMRF":
+    """parse_model (model_io.cpp:98-150): the text model on the device
+    (the arrays of parse_model_arrays through bp_graph_create)."""
+    return PairwiseMRF.from_arrays(*parse_model_arrays(text), device=device)
 
 
 def generate_er_arrays(n: int, m: int, c: float, seed: int):

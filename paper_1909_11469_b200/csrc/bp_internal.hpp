@@ -63,6 +63,15 @@ ErInstance er_instance(uint32_t n, uint32_t m, double c, uint64_t seed);
 void er_desc_arrays(uint32_t n, uint32_t m, double c, uint64_t seed, std::vector<uint32_t>& cards,
                     std::vector<double>& unary, std::vector<uint32_t>& ep, std::vector<double>& tables);
 
+// The reference's text model (.pgm, model_io.cpp:98-150) as build_graph's
+// input arrays (pgm.cpp); throws Error(BP_ERR_PARSE, "line N: ...") as
+// parse_model throws parse_error.
+struct PgmArrays {
+  std::vector<uint32_t> cards, ep;
+  std::vector<double> unary, tables;
+};
+void parse_pgm(const char* text, size_t len, PgmArrays& out);
+
 // Exact double-precision unary / table values of the same streams (for the
 // descriptor path and tests).
 void ising_desc_arrays(uint32_t rows, uint32_t cols, double c, uint64_t seed,

@@ -137,6 +137,50 @@ int bp_generate_er_arrays(uint32_t n, uint32_t m, double c, uint64_t seed, uint3
   });
 }
 
+struct bp_pgm {
+  bpb::PgmArrays a;
+};
+int bp_pgm_parse(const char* text, uint64_t len, bp_pgm** out) {
+  if (!out || (!text && len)) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    auto m = std::make_unique<bp_pgm>();
+    bpb::parse_pgm(text ? text : "", len, m->a);
+    *out = m.release();
+  });
+}
+int bp_pgm_info(const bp_pgm* m, uint32_t* V, uint32_t* E, uint64_t* nu, uint64_t* nt) {
+  if (!m) return BP_ERR_INVALID_ARGUMENT;
+  if (V) *V = static_cast<uint32_t>(m->a.cards.size());
+  if (E) *E = static_cast<uint32_t>(m->a.ep.size() / 2);
+  if (nu) *nu = m->a.unary.size();
+  if (nt) *nt = m->a.tables.size();
+  return BP_OK;
+}
+int bp_pgm_arrays(const bp_pgm* m, uint32_t* cards, double* unary, uint32_t* ep, double* tables) {
+  if (!m) return BP_ERR_INVALID_ARGUMENT;
+  auto put = [](auto* dst, const auto& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+  };
+  put(cards, m->a.cards);
+  put(unary, m->a.unary);
+  put(ep, m->a.ep);
+  put(tables, m->a.tables);
+  return BP_OK;
+}
+void bp_pgm_destroy(bp_pgm* m) { delete m; }
+int bp_graph_create_pgm(const char* text, uint64_t len, const bp_device_opts* opts, bp_graph** out) {
+  if (!out || (!text && len)) return BP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded([&] {
+    bpb::PgmArrays a;
+    bpb::parse_pgm(text ? text : "", len, a);
+    const bp_graph_desc d{static_cast<uint32_t>(a.cards.size()), static_cast<uint32_t>(a.ep.size() / 2),
+                          a.cards.data(), a.unary.data(), a.ep.data(), a.tables.data()};
+    *out = new bp_graph{bpb::build_from_desc(&d, opts)};
+  });
+}
+
 void bp_graph_destroy(bp_graph* g) { delete g; }
 
 int bp_graph_info_get(const bp_graph* g, bp_graph_info* info) {
