@@ -257,6 +257,9 @@ BP_API int bp_engine_step(struct bp_engine* e, uint64_t* frontier_size);
  * kernel_out (optional): BP_LBP_KERNEL_* that ran.  Residuals are not stored. */
 BP_API int bp_engine_lbp_sweep(struct bp_engine* e, uint32_t flags, uint32_t* kernel_out);
 BP_API int bp_engine_iteration(const struct bp_engine* e, uint64_t* out);
+/* EngineState::advance_iteration (schedulers.hpp:75): the next rnbp_frontier
+ * draws with the next iteration's Philox keys */
+BP_API int bp_engine_advance_iteration(struct bp_engine* e);
 
 /* ---- Row-band partition of a lattice across GPUs ----------
  * Rank `part` of `nparts` owns rows [row0, row1) of generate_ising(n, c, seed)

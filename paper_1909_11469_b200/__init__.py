@@ -173,6 +173,7 @@ def _load():
         "bp_engine_destroy": (None, [P]),
         "bp_engine_unconverged": (C.c_int, [P, C.POINTER(C.c_uint32)]),
         "bp_engine_iteration": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+        "bp_engine_advance_iteration": (C.c_int, [P]),
         "bp_engine_messages": (C.c_int, [P, P]),
         "bp_engine_candidates": (C.c_int, [P, P]),
         "bp_engine_residuals": (C.c_int, [P, P]),
@@ -743,6 +744,11 @@ class EngineState:
         eoff = np.ascontiguousarray(eoff, np.uint64)
         edges = np.ascontiguousarray(edges, np.uint32)
         _check(_lib.bp_engine_apply_splashes(self._h, roots.size, _ptr(roots), _ptr(eoff), _ptr(edges)))
+
+    def advance_iteration(self) -> None:
+        """EngineState::advance_iteration (schedulers.hpp:75): the Philox draws of
+        the next rnbp_frontier use the next iteration's keys."""
+        _check(_lib.bp_engine_advance_iteration(self._h))
 
     def step(self) -> int:
         n = C.c_uint64()

@@ -259,6 +259,10 @@ int bp_engine_unconverged(const bp_engine* e, uint32_t* out) {
   if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] { *out = e->e->unconverged(); });
 }
+int bp_engine_advance_iteration(bp_engine* e) {
+  if (!e) return BP_ERR_INVALID_ARGUMENT;
+  return guarded([&] { e->e->advance_iteration(); });
+}
 int bp_engine_iteration(const bp_engine* e, uint64_t* out) {
   if (!e || !out) return BP_ERR_INVALID_ARGUMENT;
   return guarded([&] { *out = e->e->iteration(); });

@@ -36,6 +36,7 @@ class EngineBase {
                               const uint32_t* edges) = 0;
   virtual uint64_t step() = 0;
   virtual uint32_t lbp_sweep(uint32_t flags) = 0;  // fused LBP sweep (lockstep of the production kernel)
+  virtual void advance_iteration() = 0;  // EngineState::advance_iteration (schedulers.hpp:75)
   // row-band partition (bp_band_*): LBP on a lattice band with ghost rows
   virtual void band_config(const PartHalo& h, uint64_t owned_directed) = 0;
   // RnBP on a band: begin = init + first refresh; select (attempt 0/1) =

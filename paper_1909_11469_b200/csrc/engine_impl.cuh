@@ -255,6 +255,14 @@ class EngineT final : public EngineBase {
     fetch_ctl_header();
     return hctl_->iteration;
   }
+  // the iteration keys the Philox draws of rnbp_frontier (the reference's
+  // draws advance with its mt19937_64 instead)
+  void advance_iteration() override {
+    fetch_ctl_header();
+    k_set_u64<<<1, 1, 0, s_>>>(&ctl()->iteration, hctl_->iteration + 1);
+    launch_check();
+    sync();
+  }
   void messages(double* out, bool candidates) override {
     // fused LBP sweeps (lockstep, bands) ping-pong like run()'s LBP: m_t lives in buf[t & 1]
     bool flip = false;

@@ -116,3 +116,19 @@ def test_device_edge_ratio_rule_from_traces(bp, n, c, seed, low_p):
         r = bp.run_ex(g, cfg, flags=flags)
         high, low = _edge_ratio_check(r.trace, low_p)
         assert high >= 1 and low >= 1
+
+
+def test_advance_iteration_rekeys_the_draws(bp):
+    """EngineState::advance_iteration (schedulers.hpp:75): each lockstep
+    iteration draws with its own Philox keys, so the frontier stays a
+    Bernoulli(p) sample of the survivors (without advancing, the edges left
+    out once would be left out again)."""
+    g = bp.generate_ising(bp.IsingParams(n=300, c=2.5, seed=4))
+    de = bp.EngineState(g, bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, seed=5))
+    for t in range(4):
+        s = de.unconverged_count()
+        f = de.rnbp_frontier(0.5)
+        assert abs(len(f) - s / 2) < 6 * np.sqrt(s / 4), (t, len(f), s)
+        assert de.iteration() == t
+        de.apply_frontier(f)
+        de.advance_iteration()
