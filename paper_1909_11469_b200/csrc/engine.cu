@@ -69,6 +69,8 @@ std::unique_ptr<EngineBase> make_engine_q4(const GraphImpl& g, const bp_sched_co
 std::unique_ptr<EngineBase> make_engine_q8(const GraphImpl& g, const bp_sched_config& cfg);
 std::unique_ptr<EngineBase> make_engine_q16(const GraphImpl& g, const bp_sched_config& cfg);
 std::unique_ptr<EngineBase> make_engine_q32(const GraphImpl& g, const bp_sched_config& cfg);
+std::unique_ptr<EngineBase> make_engine_q64(const GraphImpl& g, const bp_sched_config& cfg);
+std::unique_ptr<EngineBase> make_engine_q128(const GraphImpl& g, const bp_sched_config& cfg);
 
 std::unique_ptr<EngineBase> make_engine(const GraphImpl& g, const bp_sched_config& cfg) {
   switch (g.qs) {
@@ -76,6 +78,8 @@ std::unique_ptr<EngineBase> make_engine(const GraphImpl& g, const bp_sched_confi
     case 4: return make_engine_q4(g, cfg);
     case 8: return make_engine_q8(g, cfg);
     case 16: return make_engine_q16(g, cfg);
+    case 64: return make_engine_q64(g, cfg);
+    case 128: return make_engine_q128(g, cfg);
     case 32: return make_engine_q32(g, cfg);
     default: throw Error(BP_ERR_UNSUPPORTED, "unsupported message stride");
   }

@@ -1,0 +1,8 @@
+// EngineT<64> instantiation (see engine_impl.cuh).
+#include "engine_impl.cuh"
+
+namespace bpb {
+std::unique_ptr<EngineBase> make_engine_q64(const GraphImpl& g, const bp_sched_config& cfg) {
+  return std::make_unique<EngineT<64>>(g, cfg);
+}
+}  // namespace bpb

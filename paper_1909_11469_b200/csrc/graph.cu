@@ -212,7 +212,9 @@ uint32_t stride_for(uint32_t maxq) {
   if (maxq <= 8) return 8;
   if (maxq <= 16) return 16;
   if (maxq <= 32) return 32;
-  throw Error(BP_ERR_UNSUPPORTED, "cardinalities above 32 are not supported by the device kernels (max " +
+  if (maxq <= 64) return 64;  // q >= 33: q-vectors in local memory (correct, not tuned)
+  if (maxq <= 128) return 128;
+  throw Error(BP_ERR_UNSUPPORTED, "cardinalities above 128 are not supported by the device kernels (max " +
                                       std::to_string(maxq) + ")");
 }
 

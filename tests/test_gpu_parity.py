@@ -307,3 +307,22 @@ def test_rnbp_persistent_tail_potts_4096(bp):
     a = bp.run_ex(g, cfg, beliefs=False)
     b = bp.run_ex(g, cfg, beliefs=False, flags=bp.RUN_NO_PERSIST)
     assert a.trace_signature() == b.trace_signature()
+
+
+@pytest.mark.parametrize("maxq", [20, 40, 64, 100])
+def test_large_cardinalities(bp, orc, maxq):
+    """q up to 128 (message strides 64, 128): LBP lockstep and converged marginals
+    under RnBP / RBP / RS against the oracle."""
+    rng = Stream(orc, 300 + maxq)
+    cards, un, ed = random_graph(rng, 8, maxq, 0.3)
+    cards[0] = maxq  # at least one vertex at the maximum
+    un[0] = [rng.unit() + 0.5 for _ in range(maxq)]
+    ed = [(i, j, t if i != 0 else [rng.unit() + 0.5 for _ in range(cards[i] * cards[j])]) for i, j, t in ed]
+    dg, og, ep = both(bp, orc, cards, un, ed)
+    _lockstep_lbp(bp, orc, dg, og, ep, 12)
+    for kind in ("rnbp", "rbp", "rs"):
+        cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.from_string(kind), low_p=0.5, p=0.3, max_iterations=5000)
+        r = bp.run(dg, cfg)
+        o = po.run(og, oracle_config(cfg))
+        assert r.converged and o.converged, kind
+        assert float(np.max(np.abs(r.beliefs.values - o.beliefs))) <= BELIEF_TOL, kind
