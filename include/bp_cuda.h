@@ -153,6 +153,8 @@ typedef struct {
 #define BP_RUN_LBP_TILES 32u    /* LBP: force the register-tiled lattice sweep (default below 2^21 vertices) */
 #define BP_RUN_LBP_VERTEX 64u   /* LBP: force the vertex-centric sweep (q-state lattices: instead of lanes over states) */
 #define BP_RUN_NO_FUSED 128u    /* RnBP: run the dense iterations as select + refresh launches, not fused sweeps */
+#define BP_RUN_FUSED_TMA 256u   /* RnBP: the SMEM-staged fused sweep instead of the register one (slower: DESIGN.md 5) */
+#define BP_RUN_FUSED_REGS 512u  /* RnBP: the register fused sweep (the default) */
 
 /* LBP sweep kernels (bp_engine_lbp_sweep's *kernel_out) */
 #define BP_LBP_KERNEL_VERTEX 0u /* k_vertex_update: vertex-centric (CSR / generic q-state / Potts lattice) */

@@ -136,6 +136,8 @@ RUN_LBP_TMA = 16
 RUN_LBP_TILES = 32
 RUN_LBP_VERTEX = 64
 RUN_NO_FUSED = 128
+RUN_FUSED_TMA = 256
+RUN_FUSED_REGS = 512
 LBP_KERNELS = {0: "vertex", 1: "tiles", 2: "tma", 3: "qlanes"}  # BP_LBP_KERNEL_*
 GRAPH_TRUSTED = 1
 

@@ -20,6 +20,7 @@
 #include "kernels_persist.cuh"
 #include "kernels_lbp.cuh"
 #include "kernels_fused.cuh"
+#include "kernels_fused_tma.cuh"
 
 namespace bpb {
 namespace {
@@ -157,8 +158,17 @@ class EngineT final : public EngineBase {
       drain_trace(trace, trace_cap, copied);
     }
     // RnBP on binary Ising lattices: the dense iterations as fused sweeps
-    if (fused_capable() && !(flags & BP_RUN_NO_FUSED) && prm_.fixed_p < 0.0 && !hctl_->done)
+    if (fused_capable() && !(flags & BP_RUN_NO_FUSED) && prm_.fixed_p < 0.0 && !hctl_->done) {
+      const uint32_t ff = flags & (BP_RUN_FUSED_TMA | BP_RUN_FUSED_REGS);
+      if (fgexec_ && ff != fused_force_) {  // the captured body embeds the kernel choice
+        cudaGraphExecDestroy(fgexec_);
+        cudaGraphDestroy(fgraph_);
+        fgexec_ = nullptr;
+        fgraph_ = nullptr;
+      }
+      fused_force_ = ff;
       run_fused_phase(use_graph, opts, trace, trace_cap, copied);
+    }
     if (!hctl_->done) {
       if (use_graph) {
         run_graph_loop(trace, trace_cap, copied);
@@ -1117,7 +1127,38 @@ class EngineT final : public EngineBase {
       return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles / std::atoi(e), 1u << 30)));
     return vgrid(k_rnbp_fused, g_.V);
   }
+  // the SMEM-staged version only on request (BP_RUN_FUSED_TMA): it moves
+  // exactly the algorithmic bytes (23.4 GB per 16384^2 sweep against 26.6 GB)
+  // but measured slower (8.8 vs 7.0 ms): both versions are instruction-bound
+  // (~600 / ~780 instructions per vertex), and the staged one adds three
+  // block barriers per row tile
+  uint32_t fused_force_ = 0;
+  unsigned fused_tma_grid_ = 0;
+  bool fused_uses_tma() const { return (fused_force_ & BP_RUN_FUSED_TMA) != 0; }
   void enqueue_fused(unsigned dir) {
+    if (fused_uses_tma()) {
+      if (!fused_tma_grid_) {
+        cuda_check(cudaFuncSetAttribute(k_rnbp_fused_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(FusedSmem))),
+                   "smem attribute");
+        int per = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rnbp_fused_tma, kBlock, sizeof(FusedSmem)),
+                   "occupancy");
+        fused_tma_grid_ = static_cast<unsigned>(std::max(1, per) * sm_count());
+      }
+      timed(kKFused, [&] {
+        if (dir == 0)
+          k_rnbp_fused_tma<<<fused_tma_grid_, kBlock, sizeof(FusedSmem), s_>>>(
+              dg_, live(), cand(), fu_[0].as<uint8_t>(), fl_.as<float>(), fc_.as<float>(), fu_[1].as<uint8_t>(), ctl(),
+              eps_, prm_, 0u);
+        else
+          k_rnbp_fused_tma<<<fused_tma_grid_, kBlock, sizeof(FusedSmem), s_>>>(
+              dg_, fl_.as<float>(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(), cand(), fu_[0].as<uint8_t>(), ctl(),
+              eps_, prm_, 1u);
+      });
+      launch_check();
+      return;
+    }
     const unsigned grid = fused_grid();
     timed(kKFused, [&] {
       if (dir == 0)

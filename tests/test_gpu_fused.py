@@ -96,3 +96,28 @@ def test_fused_converged_marginals_match_oracle(bp, orc, n, c, seed):
                                                                seed=seed))
     assert r.converged and o.converged
     assert float(np.max(np.abs(r.beliefs.values - o.beliefs))) <= 1e-4
+
+
+# ---- the SMEM-staged fused sweep (kernels_fused_tma.cuh): bulk-copied rows,
+# strip boundaries, ragged strips, blocks starting mid-strip -- bit for bit
+@pytest.mark.parametrize("rows,cols", [(2, 5), (3, 257), (7, 600), (33, 256), (40, 513), (1, 300), (300, 7),
+                                       (64, 1000), (129, 255)])
+def test_fused_tma_equals_two_launch_loop(bp, orc, rows, cols):
+    cards, un, ep, tb = lattice_arrays(orc, rows, cols, rows + cols, 2.0)
+    g = bp.PairwiseMRF.from_arrays(cards, un, ep, tb)
+    for iters, lp in ((7, 0.5), (60, 0.3)):
+        cfg = _cfg(bp, seed=rows, low_p=lp, iters=iters)
+        a = bp.run_ex(g, cfg, flags=bp.RUN_FUSED_TMA, messages=True)
+        b = bp.run_ex(g, cfg, flags=bp.RUN_NO_FUSED, messages=True)
+        _assert_same(a, b)
+        assert a.fused_iterations > 0
+
+
+@pytest.mark.parametrize("n,iters", [(1000, 20), (2048, 9)])
+def test_fused_tma_windows(bp, n, iters):
+    """the staged sweep forced at 1000^2 and 2048^2"""
+    g = bp.generate_ising(bp.IsingParams(n=n, c=2.5, seed=1))
+    cfg = _cfg(bp, seed=1, iters=iters)
+    a = bp.run_ex(g, cfg, flags=bp.RUN_FUSED_TMA, messages=True)
+    b = bp.run_ex(g, cfg, flags=bp.RUN_NO_FUSED, messages=True)
+    _assert_same(a, b)
