@@ -312,7 +312,8 @@ static __global__ void __launch_bounds__(kBlock) k_fused_enter(const float* __re
 
 // End of the fused phase: the state back in the canonical set when the last
 // sweep left it in the scratch set (odd count), and the residual array
-// rematerialised from the predicate (1 = unconverged, 0 = converged).
+// rematerialised from the predicate (1 = unconverged, 0 = converged) -- for
+// the phases that follow; a finished run keeps only the live messages.
 static __global__ void __launch_bounds__(kBlock) k_fused_exit(const Ctl* ctl, const float* __restrict__ L1,
                                                               const float* __restrict__ C1,
                                                               const uint8_t* __restrict__ Ucur,
@@ -320,12 +321,14 @@ static __global__ void __launch_bounds__(kBlock) k_fused_exit(const Ctl* ctl, co
                                                               float* __restrict__ C0, float* __restrict__ res,
                                                               uint32_t D) {
   const bool odd = ctl->fused_par & 1u;
+  // a finished run needs only the live messages (beliefs, RunResult messages)
+  const bool done = ctl->done != 0u;
+  if (done && !odd) return;
   const uint8_t* __restrict__ U = odd ? Ualt : Ucur;
   for (uint32_t d = blockIdx.x * blockDim.x + threadIdx.x; d < D; d += gridDim.x * blockDim.x) {
-    if (odd) {
-      L0[d] = L1[d];
-      C0[d] = C1[d];
-    }
+    if (odd) L0[d] = L1[d];
+    if (done) continue;
+    if (odd) C0[d] = C1[d];
     res[d] = U[d] ? 1.f : 0.f;
   }
 }
