@@ -80,7 +80,6 @@ class EngineT final : public EngineBase {
     }
     vlist_.alloc(static_cast<size_t>(g.V) * 4);
     if (fused_capable()) {  // scratch buffer set of the fused dense RnBP sweep (here, not mid-run)
-      fl_.alloc(msz);
       fc_.alloc(msz);
       fu_[0].alloc(g.D);
       fu_[1].alloc(g.D);
@@ -1109,7 +1108,7 @@ class EngineT final : public EngineBase {
   size_t bel_pinned_bytes_ = 0;
 
   // ---- fused dense RnBP sweeps (kernels_fused.cuh)
-  DevBuf fl_, fc_;  // scratch buffer set (live, candidates)
+  DevBuf fc_;  // scratch candidate set (live messages are updated in place)
   DevBuf fu_[2];    // unconverged predicates (r >= eps) of the canonical / scratch set
   uint64_t fused_iters_ = 0, fused_sweeps_ = 0;  // iterations run fused; sweeps (an aborted one included)
   cudaGraph_t fgraph_ = nullptr;
@@ -1149,12 +1148,12 @@ class EngineT final : public EngineBase {
       timed(kKFused, [&] {
         if (dir == 0)
           k_rnbp_fused_tma<<<fused_tma_grid_, kBlock, sizeof(FusedSmem), s_>>>(
-              dg_, live(), cand(), fu_[0].as<uint8_t>(), fl_.as<float>(), fc_.as<float>(), fu_[1].as<uint8_t>(), ctl(),
-              eps_, prm_, 0u);
+              dg_, live(), cand(), fu_[0].as<uint8_t>(), live(), fc_.as<float>(), fu_[1].as<uint8_t>(), ctl(), eps_,
+              prm_, 0u);
         else
           k_rnbp_fused_tma<<<fused_tma_grid_, kBlock, sizeof(FusedSmem), s_>>>(
-              dg_, fl_.as<float>(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(), cand(), fu_[0].as<uint8_t>(), ctl(),
-              eps_, prm_, 1u);
+              dg_, live(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(), cand(), fu_[0].as<uint8_t>(), ctl(), eps_,
+              prm_, 1u);
       });
       launch_check();
       return;
@@ -1162,10 +1161,10 @@ class EngineT final : public EngineBase {
     const unsigned grid = fused_grid();
     timed(kKFused, [&] {
       if (dir == 0)
-        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), fu_[0].as<uint8_t>(), fl_.as<float>(),
+        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), fu_[0].as<uint8_t>(), live(),
                                               fc_.as<float>(), fu_[1].as<uint8_t>(), ctl(), eps_, prm_, 0u);
       else
-        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, fl_.as<float>(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(),
+        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, live(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(),
                                               cand(), fu_[0].as<uint8_t>(), ctl(), eps_, prm_, 1u);
     });
     launch_check();
@@ -1238,8 +1237,8 @@ class EngineT final : public EngineBase {
     fused_iters_ = hctl_->iteration - it_in;
     fused_sweeps_ = fused_iters_ + hctl_->fused_abort;
     timed(kKOther, [&] {
-      k_fused_exit<<<grid_cap(g_.D), kBlock, 0, s_>>>(ctl(), fl_.as<float>(), fc_.as<float>(), fu_[0].as<uint8_t>(),
-                                                      fu_[1].as<uint8_t>(), live(), cand(), res_.as<float>(), g_.D);
+      k_fused_exit<<<grid_cap(g_.D), kBlock, 0, s_>>>(ctl(), fc_.as<float>(), fu_[0].as<uint8_t>(),
+                                                      fu_[1].as<uint8_t>(), cand(), res_.as<float>(), g_.D);
     });
     launch_check();
   }

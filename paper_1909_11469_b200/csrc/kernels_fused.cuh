@@ -13,12 +13,14 @@
 // and then, when v is touched, recompute every outgoing candidate from the
 // post-commit messages (the cavity sum in the refresh's order), exactly as
 // k_rnbp_select + k_vertex_update<Delta> do in two launches with a touched-set
-// round trip in between.  The state is read from one buffer set (live,
-// candidates, unconverged predicates) and written to the other (ping-pong: a
-// neighbour's writes never race with this vertex's reads), so every directed
-// edge is written exactly once per iteration.  ctl->fused_par says which set
-// holds the state; k_fused_exit copies it back to the canonical set when the
-// fused phase ends on an odd count.
+// round trip in between.  Candidates and unconverged predicates are read from
+// one buffer set and written to the other (ping-pong: a neighbour's refresh
+// never races with this vertex's reads); live messages are updated in place --
+// a live message changes only when its edge is committed, and then its target
+// reads the candidate instead, so every other write stores the value already
+// there.  ctl->fused_par says which set holds the candidates / predicates;
+// k_fused_exit copies them back to the canonical set when the fused phase
+// ends on an odd count.
 //
 // Used while the run scans residuals (cl_state == 0, i.e. at least 1/16 of
 // the edges unconverged: the touched set covers most vertices).  An empty
@@ -84,11 +86,11 @@ __device__ __forceinline__ uint32_t pair_select(uint32_t u, unsigned long long e
   return s;
 }
 
-__device__ __forceinline__ FusedPair load_pair(const float2* __restrict__ L, const float2* __restrict__ Cn,
+__device__ __forceinline__ FusedPair load_pair(const float2* L, const float2* __restrict__ Cn,
                                                const uint16_t* __restrict__ U, const float* __restrict__ ea,
                                                uint32_t e) {
   FusedPair p;
-  p.l = __ldg(&L[e]);
+  p.l = L[e];  // coherent: the live set is updated in place
   p.c = __ldg(&Cn[e]);
   const uint32_t u = __ldg(&U[e]);  // bytes are 0 / 1
   p.u = (u & 1u) | ((u >> 7) & 2u);
@@ -129,9 +131,9 @@ constexpr uint32_t kFusedStrip = (kBlock / 32) * kFusedWarpCols;
 // neighbour lane's outgoing value (shuffle), vertical pairs one row later
 // with the lower vertex's.  Pairs split between warps / blocks leave as two
 // single-direction stores.
-static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const float* __restrict__ L0,
+static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const float* L0,
                                                               const float* __restrict__ C0,
-                                                              const uint8_t* __restrict__ U0, float* __restrict__ L1,
+                                                              const uint8_t* __restrict__ U0, float* L1,
                                                               float* __restrict__ C1, uint8_t* __restrict__ U1,
                                                               Ctl* ctl, float eps, RnbpParams prm, unsigned dir) {
   if (run_done(ctl)) return;
@@ -149,10 +151,13 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const 
   const uint32_t C = g.lat_cols, R = g.lat_rows;
   const uint32_t nstrips = (C + kFusedStrip - 1) / kFusedStrip;
   const uint64_t ntiles = static_cast<uint64_t>(R) * nstrips;
-  const float2* __restrict__ La = reinterpret_cast<const float2*>(L0);
+  // live messages IN PLACE (L0 == L1): a directed edge's live message changes
+  // only when it is committed, and then its target reads the candidate
+  // instead; every other write stores the value already there
+  const float2* La = reinterpret_cast<const float2*>(L0);
   const float2* __restrict__ Ca = reinterpret_cast<const float2*>(C0);
   const uint16_t* __restrict__ Ua = reinterpret_cast<const uint16_t*>(U0);
-  float2* __restrict__ Lb = reinterpret_cast<float2*>(L1);
+  float2* Lb = reinterpret_cast<float2*>(L1);
   float2* __restrict__ Cb = reinterpret_cast<float2*>(C1);
   uint16_t* __restrict__ Ub = reinterpret_cast<uint16_t*>(U1);
   const float* __restrict__ ea = g.ising_a;
@@ -314,20 +319,14 @@ static __global__ void __launch_bounds__(kBlock) k_fused_enter(const float* __re
 // sweep left it in the scratch set (odd count), and the residual array
 // rematerialised from the predicate (1 = unconverged, 0 = converged) -- for
 // the phases that follow; a finished run keeps only the live messages.
-static __global__ void __launch_bounds__(kBlock) k_fused_exit(const Ctl* ctl, const float* __restrict__ L1,
-                                                              const float* __restrict__ C1,
+static __global__ void __launch_bounds__(kBlock) k_fused_exit(const Ctl* ctl, const float* __restrict__ C1,
                                                               const uint8_t* __restrict__ Ucur,
-                                                              const uint8_t* __restrict__ Ualt, float* __restrict__ L0,
-                                                              float* __restrict__ C0, float* __restrict__ res,
-                                                              uint32_t D) {
+                                                              const uint8_t* __restrict__ Ualt, float* __restrict__ C0,
+                                                              float* __restrict__ res, uint32_t D) {
   const bool odd = ctl->fused_par & 1u;
-  // a finished run needs only the live messages (beliefs, RunResult messages)
-  const bool done = ctl->done != 0u;
-  if (done && !odd) return;
+  if (ctl->done != 0u) return;  // a finished run needs only the live messages (always in place)
   const uint8_t* __restrict__ U = odd ? Ualt : Ucur;
   for (uint32_t d = blockIdx.x * blockDim.x + threadIdx.x; d < D; d += gridDim.x * blockDim.x) {
-    if (odd) L0[d] = L1[d];
-    if (done) continue;
     if (odd) C0[d] = C1[d];
     res[d] = U[d] ? 1.f : 0.f;
   }

@@ -49,7 +49,7 @@ struct FusedSmem {
 
 // k of a strip row's pair e0 + k in slot arrays: L / C / S at k + aoff,
 // U at k + uoff, E at k + eoff; BL / BC at k + (e0 & 1), BU at k + (e0 & 7)
-static __global__ void __launch_bounds__(kBlock) k_rnbp_fused_tma(DevGraph g, const float* __restrict__ L0,
+static __global__ void __launch_bounds__(kBlock) k_rnbp_fused_tma(DevGraph g, const float* L0,
                                                                   const float* __restrict__ C0,
                                                                   const uint8_t* __restrict__ U0, float* L1, float* C1,
                                                                   uint8_t* U1, Ctl* ctl, float eps, RnbpParams prm,
@@ -68,7 +68,7 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused_tma(DevGraph g, co
   const bool draw = thresh < (1ull << 53);
   const unsigned long long it = ctl->iteration, eoffs = g.edge_offset;
   const PhiloxKeys pk(prm.seed);
-  const float2* __restrict__ La = reinterpret_cast<const float2*>(L0);
+  const float2* La = reinterpret_cast<const float2*>(L0);  // == L1: live messages in place (k_rnbp_fused)
   const float2* __restrict__ Ca = reinterpret_cast<const float2*>(C0);
   const uint16_t* __restrict__ Ua = reinterpret_cast<const uint16_t*>(U0);
   float2* Lb = reinterpret_cast<float2*>(L1);
