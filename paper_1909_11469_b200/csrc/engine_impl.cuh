@@ -1347,16 +1347,15 @@ class EngineT final : public EngineBase {
   }
   unsigned long long rs_k(double p) const { return rs_k_of(p, g_.V); }
   void ensure_rs(uint32_t h) {
-    if (h > kRsMaxDepth)
-      throw Error(BP_ERR_UNSUPPORTED, "splash_depth above " + std::to_string(kRsMaxDepth) +
-                                          " is not supported by the device splash builder");
-    (void)g_.balls(h);  // built here, never inside a graph capture
+    // any depth: above the walk stack the builder tests ball intersection by
+    // distance propagation instead of ball lists / walks (kernels_rs.cuh)
+    if (h <= kRsMaxDepth) (void)g_.balls(h);  // built here, never inside a graph capture
     if (rs_vres_.p) return;
     const size_t V = std::max<size_t>(g_.V, 1);
     for (DevBuf* b : {&rs_vres_, &rs_state_, &rs_claimed_, &rs_qnext_, &rs_spos_, &rs_depth_, &rs_clist_,
                       &rs_blist_, &rs_rlist_, &rs_klist_})
       b->alloc(V * 4);
-    rs_ballmax_.alloc(V * 8);
+    rs_ballmax_.alloc(V * 16);
     rs_hist_.alloc(4096 * 4);
     cuda_check(cudaMemset(rs_hist_.p, 0, 4096 * 4), "memset");
     int per_sm = 0;
@@ -1378,6 +1377,7 @@ class EngineT final : public EngineBase {
     b.spos = rs_spos_.as<uint32_t>();
     b.depth = rs_depth_.as<uint32_t>();
     b.ballmax = rs_ballmax_.as<unsigned long long>();
+    b.ballmax2 = b.ballmax + std::max<size_t>(g_.V, 1);
     b.clist = rs_clist_.as<uint32_t>();
     b.blist = rs_blist_.as<uint32_t>();
     b.rlist = rs_rlist_.as<uint32_t>();
@@ -1391,7 +1391,7 @@ class EngineT final : public EngineBase {
   void launch_rs(unsigned long long k, uint32_t h, int apply) {
     RsParams prm{k, h, apply};
     RsBufs bufs = rs_bufs();
-    if (const BallLists* bl = g_.balls(h)) {
+    if (const BallLists* bl = h <= kRsMaxDepth ? g_.balls(h) : nullptr) {
       bufs.boff = bl->off.as<unsigned long long>();
       bufs.bl = bl->list.as<uint32_t>();
     }

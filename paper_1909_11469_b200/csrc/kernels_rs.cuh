@@ -16,7 +16,11 @@
 //   * a candidate r is "ready" once no unresolved candidate of higher priority
 //     has a depth-h ball intersecting r's ball (ballmax: every candidate
 //     atomicMax-es its 64-bit priority key over its ball, r is ready iff it
-//     holds the max on its whole ball).  Ready roots have pairwise disjoint
+//     holds the max on its whole ball).  Deep splashes (h above the walk
+//     stack, no ball lists) use the equivalent distance test instead: balls
+//     intersect iff the roots are within 2h, so 2h max-propagation sweeps over
+//     the vertex graph give each root the highest key within 2h -- any depth,
+//     at O(h (V + E)) per round.  Ready roots have pairwise disjoint
 //     balls, so their BFS claims run concurrently without conflicts and give
 //     the claims of the sequential walk; candidates found claimed are the
 //     skipped roots of the walk (their claimer always has higher priority);
@@ -66,6 +70,7 @@ struct RsBufs {
   uint32_t* spos;
   uint32_t* depth;
   unsigned long long* ballmax;
+  unsigned long long* ballmax2;    // V more: the propagation ping-pong (deep splashes)
   uint32_t* clist;
   uint32_t* blist;
   uint32_t* rlist;
@@ -411,6 +416,7 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       // thread per candidate would serialise a load per ball vertex).
       unsigned unres = 0;
       const bool wl = b.boff != nullptr;
+      const bool prop = !wl && h > kRsMaxDepth;  // distance test by propagation
       const uint32_t lane = threadIdx.x & 31u, gw = tid >> 5, nw = stride >> 5;
       auto warp_ball = [&](uint32_t r, auto&& f) -> bool {  // all lanes; AND of f over the ball
         const unsigned long long e0 = b.boff[r], e1 = b.boff[r + 1];
@@ -430,7 +436,9 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
         }
         if (!wl || lane == 0) ++unres;
         const unsigned long long key = rs_key64(__ldcg(&b.vres[r]), r);
-        if (wl)
+        if (prop)
+          b.ballmax[r] = key;
+        else if (wl)
           warp_ball(r, [&](uint32_t w) {
             atomicMax(&b.ballmax[w], key);
             return true;
@@ -446,13 +454,29 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       if (tid == 0) rc->nready = 0;
       grid.sync();
       if (__ldcg(&rc->unres) == 0) break;
+      if (prop) {  // ballmax[v] = max key of the unresolved candidates within 2h of v
+        for (uint32_t t = 0; t < 2u * h; ++t) {
+          const unsigned long long* src = (t & 1u) ? b.ballmax2 : b.ballmax;
+          unsigned long long* dst = (t & 1u) ? b.ballmax : b.ballmax2;
+          for (uint32_t v = tid; v < V; v += stride) {
+            unsigned long long m = __ldcg(&src[v]);
+            for (uint32_t a = g.in_off[v]; a < g.in_off[v + 1]; ++a) {
+              const unsigned long long x = __ldcg(&src[g.ep[g.in_adj[a]]]);
+              m = x > m ? x : m;
+            }
+            dst[v] = m;
+          }
+          grid.sync();
+        }
+      }
       // A2: ready = maximum priority over the whole ball
       for (uint32_t i = wl ? gw : tid; i < nc; i += wl ? nw : stride) {
         const uint32_t r = __ldcg(&b.clist[i]);
         if (__ldcg(&b.state[r]) != kRsCand) continue;
         const unsigned long long key = rs_key64(__ldcg(&b.vres[r]), r);
-        const bool ready = wl ? warp_ball(r, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; })
-                              : ball_each(g, b, r, h, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; });
+        const bool ready = prop ? __ldcg(&b.ballmax[r]) <= key
+                           : wl ? warp_ball(r, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; })
+                                : ball_each(g, b, r, h, [&](uint32_t w) { return __ldcg(&b.ballmax[w]) <= key; });
         if (ready && (!wl || lane == 0)) b.rlist[atomicAdd(&rc->nready, 1u)] = r;
       }
       grid.sync();
@@ -539,14 +563,17 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
         }
         b.state[r] = kRsBuilt;
         b.blist[atomicAdd(&rc->nbuilt, 1u)] = r;
-        ball_each(g, b, r, h, [&](uint32_t w) {
-          b.ballmax[w] = 0ull;
-          return true;
-        });
+        if (!prop)
+          ball_each(g, b, r, h, [&](uint32_t w) {
+            b.ballmax[w] = 0ull;
+            return true;
+          });
       }
       // unresolved candidates clear their balls (a ready root racing to
       // kRsBuilt may be cleared twice: idempotent)
-      for (uint32_t i = wl ? gw : tid; i < nc; i += wl ? nw : stride) {
+      if (prop)  // the propagation filled every vertex: clear them all
+        for (uint32_t v = tid; v < V; v += stride) b.ballmax[v] = 0ull;
+      for (uint32_t i = wl ? gw : (prop ? nc : tid); i < nc; i += wl ? nw : stride) {
         const uint32_t r = __ldcg(&b.clist[i]);
         uint32_t st = __ldcg(&b.state[r]);
         // builders flip states concurrently in this phase: one read per warp

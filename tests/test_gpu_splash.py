@@ -76,7 +76,10 @@ def _check_rs_exact(de, og, p, h):
 
 
 @pytest.mark.parametrize("n,c,seed,p,h", [(12, 2.5, 1, 1 / 16, 2), (16, 2.5, 7, 1 / 128, 2), (10, 3.0, 3, 0.3, 1),
-                                          (9, 2.0, 5, 1.0, 0), (14, 2.5, 2, 1 / 8, 3)])
+                                          (9, 2.0, 5, 1.0, 0), (14, 2.5, 2, 1 / 8, 3),
+                                          # deep splashes: the distance-propagation ready test (h > 8)
+                                          (20, 2.5, 4, 1 / 64, 9), (24, 2.5, 6, 1 / 128, 12),
+                                          (16, 2.0, 8, 1 / 32, 25)])
 def test_rs_frontier_equals_sequential_walk_ising(bp, orc, n, c, seed, p, h):
     og = po.Graph.ising(orc, n, c, seed)
     a = og.arrays()
@@ -97,6 +100,18 @@ def test_rs_frontier_equals_sequential_walk_random_graphs(bp, orc):
         de.set_endpoints(ep)
         for p, h in ((0.25, 2), (0.1, 1), (0.5, 2)):
             _check_rs_exact(de, og, p, h)
+
+
+def test_deep_rs_frontier_random_graphs(bp, orc):
+    rng = Stream(orc, 91)
+    for rep in range(3):
+        cards, un, ed = random_graph(rng, 40 + 10 * rep, 4, 0.1)
+        dg, og, ep = both(bp, orc, cards, un, ed)
+        de = bp.EngineState(dg, bp.SchedulerConfig(kind=bp.SchedulerKind.rs))
+        de.set_endpoints(ep)
+        for p, h in ((0.05, 9), (0.1, 14)):
+            roots, eoff, edges = _check_rs_exact(de, og, p, h)
+            de.apply_splashes(roots, eoff, edges)
 
 
 def test_rs_frontier_matches_reference_when_order_is_unambiguous(bp, orc):
@@ -167,7 +182,8 @@ def test_splash_depth_zero_equals_apply_frontier(bp, orc):
     assert np.max(np.abs(d1.messages() - d2.messages())) <= 1e-6
 
 
-@pytest.mark.parametrize("n,c,seed,p,h", [(10, 2.0, 1, 1 / 16, 2), (20, 2.0, 2, 1 / 32, 2), (16, 2.5, 3, 1 / 8, 1)])
+@pytest.mark.parametrize("n,c,seed,p,h", [(10, 2.0, 1, 1 / 16, 2), (20, 2.0, 2, 1 / 32, 2), (16, 2.5, 3, 1 / 8, 1),
+                                          (16, 2.0, 5, 1 / 64, 10)])
 def test_rs_run_matches_reference(bp, orc, n, c, seed, p, h):
     g = bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed))
     og = po.Graph.ising(orc, n, c, seed)
