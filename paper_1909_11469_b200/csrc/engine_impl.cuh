@@ -1122,9 +1122,9 @@ class EngineT final : public EngineBase {
     // one resident wave; BPB_FUSED_TPB = n: ~n tiles per block instead (tuning)
     static const char* e = std::getenv("BPB_FUSED_TPB");
     const uint64_t ntiles = static_cast<uint64_t>(g_.lat_rows) * ((g_.lat_cols + kFusedStrip - 1) / kFusedStrip);
-    if (e && std::atoi(e) > 0)
+    if (e && std::atoi(e) > 0)  // ~n block-strip tiles per block
       return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles / std::atoi(e), 1u << 30)));
-    return vgrid(k_rnbp_fused, g_.V);
+    return fused_warp_tiles(g_.lat_cols) ? vgrid(k_rnbp_fused<true>, g_.V) : vgrid(k_rnbp_fused<false>, g_.V);
   }
   // the SMEM-staged version only on request (BP_RUN_FUSED_TMA): it moves
   // exactly the algorithmic bytes (23.4 GB per 16384^2 sweep against 26.6 GB)
@@ -1159,13 +1159,14 @@ class EngineT final : public EngineBase {
       return;
     }
     const unsigned grid = fused_grid();
+    const auto kern = fused_warp_tiles(g_.lat_cols) ? k_rnbp_fused<true> : k_rnbp_fused<false>;
     timed(kKFused, [&] {
       if (dir == 0)
-        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), fu_[0].as<uint8_t>(), live(),
-                                              fc_.as<float>(), fu_[1].as<uint8_t>(), ctl(), eps_, prm_, 0u);
+        kern<<<grid, kBlock, 0, s_>>>(dg_, live(), cand(), fu_[0].as<uint8_t>(), live(), fc_.as<float>(),
+                                      fu_[1].as<uint8_t>(), ctl(), eps_, prm_, 0u);
       else
-        k_rnbp_fused<<<grid, kBlock, 0, s_>>>(dg_, live(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(),
-                                              cand(), fu_[0].as<uint8_t>(), ctl(), eps_, prm_, 1u);
+        kern<<<grid, kBlock, 0, s_>>>(dg_, live(), fc_.as<float>(), fu_[1].as<uint8_t>(), live(), cand(),
+                                      fu_[0].as<uint8_t>(), ctl(), eps_, prm_, 1u);
     });
     launch_check();
   }

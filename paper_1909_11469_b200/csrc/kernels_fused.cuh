@@ -112,18 +112,29 @@ __device__ __forceinline__ FusedPair shfl_up_pair(const FusedPair& p) {
   return q;
 }
 
-// columns per warp / per block-wide strip: lane 0 of every warp is a halo
-// lane that only loads and draws the right pair of the column left of the
-// warp's first one (so every lane's left pair arrives by shuffle and the
-// draw costs no extra warp instruction)
+// columns per warp strip: lane 0 of every warp is a halo lane that only
+// loads and draws the right pair of the column left of the warp's first one
+// (so every lane's left pair arrives by shuffle and the draw costs no extra
+// warp instruction)
 constexpr uint32_t kFusedWarpCols = 31;
-constexpr uint32_t kFusedStrip = (kBlock / 32) * kFusedWarpCols;
+constexpr uint32_t kFusedStrip = (kBlock / 32) * kFusedWarpCols;  // block-wide strip
+
+// Tiles per warp (31-column strips) instead of per block (248-column strips)
+// when the block strips would leave a ragged end: a block walking the last
+// strip with most warps past the edge holds an SM slot for little work (20%
+// of the grid at 1000^2).  Block strips where they divide the lattice
+// evenly: their 8 warps read adjacent columns of one row, which keeps the
+// DRAM pages and partially used sectors shared (16384^2: 13% faster).
+__host__ __device__ inline bool fused_warp_tiles(uint32_t C) {
+  const uint32_t nb = (C + kFusedStrip - 1) / kFusedStrip;
+  return 20u * (nb * kFusedStrip - C) > nb * kFusedStrip;  // > 5% of the block strips' lanes idle
+}
 
 // dir: the parity this launch serves (0: canonical -> scratch, 1: back); a
 // launch of the wrong parity is a no-op (the loop body holds both).
 //
-// Lanes = columns, block = a contiguous run of (strip, row) tiles walked down
-// the strip.  Every edge pair is loaded and drawn once: a vertex owns its
+// Lanes = columns, block (or warp, fused_warp_tiles) = a contiguous run of
+// (strip, row) tiles walked down the strip.  Every edge pair is loaded and drawn once: a vertex owns its
 // right and down pairs; its left pair comes from lane - 1 (shuffle), its up
 // pair is the down pair the same thread held one row ago (carried in
 // registers; loaded at the start of the block's run).  A pair leaves as one
@@ -131,6 +142,7 @@ constexpr uint32_t kFusedStrip = (kBlock / 32) * kFusedWarpCols;
 // neighbour lane's outgoing value (shuffle), vertical pairs one row later
 // with the lower vertex's.  Pairs split between warps / blocks leave as two
 // single-direction stores.
+template <bool WT>  // fused_warp_tiles(lat_cols)
 static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const float* L0,
                                                               const float* __restrict__ C0,
                                                               const uint8_t* __restrict__ U0, float* L1,
@@ -149,7 +161,9 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const 
   const unsigned long long it = ctl->iteration, eoff = g.edge_offset;
   const PhiloxKeys pk(prm.seed);
   const uint32_t C = g.lat_cols, R = g.lat_rows;
-  const uint32_t nstrips = (C + kFusedStrip - 1) / kFusedStrip;
+  constexpr bool wt = WT;
+  constexpr uint32_t SW = wt ? kFusedWarpCols : kFusedStrip;  // strip width
+  const uint32_t nstrips = (C + SW - 1) / SW;
   const uint64_t ntiles = static_cast<uint64_t>(R) * nstrips;
   // live messages IN PLACE (L0 == L1): a directed edge's live message changes
   // only when it is committed, and then its target reads the candidate
@@ -164,7 +178,7 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const 
   const uint32_t lane = threadIdx.x & 31u;
   const bool halo = lane == 0u;
   // column of this lane within a strip (the halo lane: the column before the warp's first)
-  const uint32_t col_in_strip = (threadIdx.x >> 5) * kFusedWarpCols + lane - 1u;  // wraps for halo of warp 0
+  const uint32_t col_in_strip = (wt ? 0u : (threadIdx.x >> 5) * kFusedWarpCols) + lane - 1u;  // wraps for halo of warp 0
   // per-thread counts in 32 bits (a thread sees at most a few thousand tiles)
   int n_delta = 0;
   uint32_t n_surv = 0, n_front = 0, n_evals = 0, n_visits = 0;
@@ -174,10 +188,12 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const 
   FusedPair dprev{};
   float dl_new = 0.f, dc_new = 0.f;
   uint32_t du_new = 0u;
-  const uint64_t t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t gw = wt ? static_cast<uint64_t>(blockIdx.x) * (kBlock / 32) + (threadIdx.x >> 5) : blockIdx.x;
+  const uint64_t nw = wt ? static_cast<uint64_t>(gridDim.x) * (kBlock / 32) : gridDim.x;
+  const uint64_t t_begin = ntiles * gw / nw, t_end = ntiles * (gw + 1) / nw;
   uint32_t strip = static_cast<uint32_t>(t_begin / R), r = static_cast<uint32_t>(t_begin - static_cast<uint64_t>(strip) * R);
   for (uint64_t t = t_begin; t < t_end; ++t) {
-    const uint32_t c = strip * kFusedStrip + col_in_strip;  // halo of the first warp of strip 0: 0xffffffff
+    const uint32_t c = strip * SW + col_in_strip;  // halo of the first warp of strip 0: 0xffffffff
     const bool inb = c < C;                                  // a real column (the halo lane's included)
     if (__all_sync(0xffffffffu, !inb || (halo && c + 1u >= C))) {  // a warp past the ragged end: no vertex
       if (++r == R) {
