@@ -222,7 +222,7 @@ struct Ctl {
   unsigned int use_clist;
   unsigned int cl_state;      // 0 scan residuals, 1 build the list this iteration, 2 walk the list
   unsigned int persist_ok;    // RnBP: hand list mode over to the persistent kernel (graph loop exits)
-  unsigned int pad3_;
+  unsigned int rx_n;          // RBP top-k: entries of the compacted candidate list (k_rx_compact)
   // persistent kernel: per-iteration sums (delta, count, frontier, survivors,
   // evals, visits), triple-buffered by iteration; the time-limit verdict of
   // the bookkeeping thread

@@ -92,6 +92,7 @@ class EngineT final : public EngineBase {
       cuda_check(cudaMemset(hist_.p, 0, kRadixBins * 4), "memset");
       nchunks_ = std::max<uint32_t>(1, (g.D + kTieChunk - 1) / kTieChunk);
       chunk_.alloc(static_cast<size_t>(nchunks_) * 4);
+      rx_list_.alloc(std::max<size_t>(g.D, 1) * 4);
       const long long kr = std::llround(cfg.p * static_cast<double>(g.D));  // schedulers.cpp:124
       k_ = kr < 1 ? 1 : static_cast<uint64_t>(kr);
     }
@@ -937,6 +938,7 @@ class EngineT final : public EngineBase {
       nchunks_ = std::max<uint32_t>(1, (g_.D + kTieChunk - 1) / kTieChunk);
       chunk_.alloc(static_cast<size_t>(nchunks_) * 4);
     }
+    if (!rx_list_.p) rx_list_.alloc(std::max<size_t>(g_.D, 1) * 4);
   }
 
   // select_all commit (|F| = 2|E|)
@@ -960,19 +962,27 @@ class EngineT final : public EngineBase {
       launch_check();
       return;
     }
+    // radix select over a compacted candidate list (kernels.cuh k_rx_*):
+    // five launches, two full passes over the residuals
     const unsigned gh = grid_cap(g_.D / 4 + 1, 4);
-    for (int pass = 0; pass < 3; ++pass) {
-      timed(kKTopk, [&] {
-        k_radix_hist<<<gh, kBlock, 0, s_>>>(dg_, res_.as<float>(), g_.D, pass, hist_.as<unsigned>(), ctl());
-      });
-      timed(kKTopk, [&] { k_radix_scan<<<1, 1024, 0, s_>>>(hist_.as<unsigned>(), pass, k, ctl()); });
-    }
-    timed(kKTopk, [&] { k_tie_count<<<nchunks_, kBlock, 0, s_>>>(dg_, res_.as<float>(), g_.D, chunk_.as<unsigned>(), ctl()); });
-    timed(kKTopk, [&] { k_tie_scan<<<1, 1024, 0, s_>>>(chunk_.as<unsigned>(), nchunks_, ctl()); });
+    float* res = res_.as<float>();
+    unsigned* hist = hist_.as<unsigned>();
+    uint32_t* list = rx_list_.as<uint32_t>();
+    timed(kKTopk, [&] { k_rx_hist0<<<gh, kBlock, 0, s_>>>(dg_, res, g_.D, hist, ctl(), k); });
+    timed(kKTopk, [&] { k_rx_compact<<<gh, kBlock, 0, s_>>>(dg_, res, g_.D, hist, list, ctl(), k); });
+    // the list (k .. a few k entries; its length lives on the device): one
+    // resident wave, so each thread's dependent list -> residual -> commit
+    // round trips happen once, not once per grid-stride step
+    const unsigned gl = grid_cap(std::min<uint64_t>(4 * k, g_.D), 2);
+    timed(kKTopk, [&] { k_rx_hist2<<<gl, kBlock, 0, s_>>>(res, list, hist, ctl(), k); });
+    timed(kKTopk, [&] {
+      k_rx_ties<<<std::min<unsigned>(nchunks_, 2 * sm_count()), kBlock, 0, s_>>>(dg_, res, g_.D,
+                                                                                 chunk_.as<unsigned>(), nchunks_, ctl());
+    });
     timed(kKSelect, [&] {
-      k_rbp_commit<QS><<<nchunks_, kBlock, 0, s_>>>(dg_, live(), cand(), res_.as<float>(), vflag_.as<uint32_t>(),
-                                                    vlist_.as<uint32_t>(), sel_.as<uint8_t>(), chunk_.as<unsigned>(),
-                                                    ctl(), eps_, 0, commit, dense);
+      k_rbp_commit_list<QS><<<gl, kBlock, 0, s_>>>(
+          dg_, live(), cand(), res, vflag_.as<uint32_t>(), vlist_.as<uint32_t>(), sel_.as<uint8_t>(), list,
+          chunk_.as<unsigned>(), nchunks_, ctl(), eps_, commit, dense);
     });
     launch_check();
   }
@@ -1449,6 +1459,7 @@ class EngineT final : public EngineBase {
   cudaStream_t s_ = nullptr;
   DevBuf bufA_, bufB_, res_, vflag_, vlist_, ctl_, hist_, chunk_, sel_, bel_, inlist_;
   DevBuf clist_[2];
+  DevBuf rx_list_;  // RBP top-k candidate list (k_rx_compact)
   DevBuf rs_vres_, rs_state_, rs_claimed_, rs_qnext_, rs_spos_, rs_depth_, rs_clist_, rs_blist_, rs_rlist_,
       rs_klist_, rs_ballmax_, rs_hist_, rs_blk_, rs_ctl_, rs_shadow_, rs_written_;
   unsigned rs_grid_ = 1;

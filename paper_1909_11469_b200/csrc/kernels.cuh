@@ -1761,159 +1761,15 @@ __global__ void __launch_bounds__(kBlock) k_commit_list(DevGraph g, const uint32
 // RBP top-k (select_top_k, schedulers.cpp:105-116): exact radix select of the
 // k-th largest residual over the 32-bit float pattern (residuals are >= +0,
 // so the unsigned order equals the float order), three passes of 12/12/8
-// bits, then a commit pass; ties at the threshold go to the lowest ids via
-// per-chunk tie counts.
+// bits (k_rx_* below), then a commit pass; ties at the threshold go to the
+// lowest ids via per-chunk tie counts.  k_rbp_commit is the select-all commit
+// (k >= the directed edges).
 
 constexpr int kRadixBins = 4096;
 
 __device__ __forceinline__ uint32_t float_key(float r) { return __float_as_uint(r); }
 
-// pass 0: bins key>>20; pass 1: (key>>8)&0xfff for key>>20 == prefix;
-// pass 2: key&0xff for key>>8 == prefix
-// band graphs: only the band's own edges compete (per-partition local top-k)
-static __global__ void __launch_bounds__(kBlock) k_radix_hist(DevGraph g, const float* res, uint32_t D, int pass,
-                                                       unsigned* hist, Ctl* ctl) {
-  if (run_done(ctl)) return;
-  const bool band = band_graph(g);
-  __shared__ unsigned sh[kRadixBins];
-  const int nb = pass == 2 ? 256 : kRadixBins;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
-  const uint32_t prefix = ctl->rx_prefix;
-  const uint32_t D4 = (D + 3) / 4;
-  const float4* res4 = reinterpret_cast<const float4*>(res);
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < D4; q += gridDim.x * blockDim.x) {
-    const float4 r4 = res4[q];
-    const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (4 * q + k >= D) break;
-      if (band && !edge_owned(g, 4 * q + k)) continue;
-      const uint32_t key = float_key(rr[k]);
-      if (pass == 0) {
-        atomicAdd(&sh[key >> 20], 1u);
-      } else if (pass == 1) {
-        if ((key >> 20) == prefix) atomicAdd(&sh[(key >> 8) & 0xfffu], 1u);
-      } else {
-        if ((key >> 8) == prefix) atomicAdd(&sh[key & 0xffu], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nb; i += blockDim.x)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-
-// Single block of 1024: find the bin holding the k-th largest key (counting
-// from the top), extend the prefix, accumulate the count strictly above it and
-// clear the histogram for the next use.
-static __global__ void __launch_bounds__(1024) k_radix_scan(unsigned* hist, int pass, unsigned long long k,
-                                                     Ctl* ctl) {
-  if (run_done(ctl)) return;
-  __shared__ unsigned long long wsum[32];
-  const int nb = pass == 2 ? 256 : kRadixBins;
-  const int per = nb / 1024 > 0 ? nb / 1024 : 1;
-  const int t = threadIdx.x;
-  // thread t owns bins [lo, lo+per) counted from the TOP: bin index nb-1-(t*per+j)
-  unsigned long long mine = 0;
-  if (t * per < nb)
-    for (int j = 0; j < per; ++j) mine += hist[nb - 1 - (t * per + j)];
-  // exclusive scan of `mine` across the block (in top-down order)
-  unsigned long long v = mine;
-  const unsigned lane = t & 31, wid = t >> 5;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long n = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= static_cast<unsigned>(o)) v += n;
-  }
-  if (lane == 31) wsum[wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    unsigned long long w = wsum[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long n = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= static_cast<unsigned>(o)) w += n;
-    }
-    wsum[lane] = w;  // inclusive
-  }
-  __syncthreads();
-  const unsigned long long excl = v - mine + (wid ? wsum[wid - 1] : 0ull);
-  const unsigned long long above0 = ctl->rx_above;
-  const unsigned long long need = k - above0;  // >= 1
-  if (t * per < nb && excl < need && need <= excl + mine) {
-    unsigned long long acc = excl;
-    for (int j = 0; j < per; ++j) {
-      const int bin = nb - 1 - (t * per + j);
-      const unsigned c = hist[bin];
-      if (acc < need && need <= acc + c) {
-        const int bits = pass == 2 ? 8 : 12;
-        ctl->rx_prefix = (pass == 0 ? 0u : (ctl->rx_prefix << bits)) | static_cast<unsigned>(bin);
-        ctl->rx_above = above0 + acc;
-        ctl->rx_ties = c;
-        ctl->rx_need = static_cast<unsigned>(need - acc);
-        break;
-      }
-      acc += c;
-    }
-  }
-  __syncthreads();
-  for (int i = t; i < nb; i += blockDim.x) hist[i] = 0;
-}
-
 constexpr uint32_t kTieChunk = 8192;
-
-// per-chunk count of keys equal to the threshold (only when not all ties are taken)
-static __global__ void __launch_bounds__(kBlock) k_tie_count(DevGraph g, const float* res, uint32_t D,
-                                                      unsigned* chunk_cnt, Ctl* ctl) {
-  const bool band = band_graph(g);
-  if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
-  const uint32_t key = ctl->rx_prefix;
-  const size_t c0 = static_cast<size_t>(blockIdx.x) * kTieChunk;
-  unsigned n = 0;
-  for (size_t d = c0 + threadIdx.x; d < c0 + kTieChunk && d < D; d += blockDim.x)
-    n += float_key(res[d]) == key && (!band || edge_owned(g, static_cast<uint32_t>(d)));
-  __shared__ unsigned sh[kBlock / 32];
-  const unsigned tot = block_sum(n, sh);
-  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = tot;
-}
-
-// exclusive prefix over chunk counts (single block)
-static __global__ void __launch_bounds__(1024) k_tie_scan(unsigned* chunk_cnt, uint32_t nchunks, Ctl* ctl) {
-  if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
-  __shared__ unsigned wsum[32];
-  __shared__ unsigned carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (uint32_t base = 0; base < nchunks; base += blockDim.x) {
-    const uint32_t i = base + threadIdx.x;
-    const unsigned c = i < nchunks ? chunk_cnt[i] : 0u;
-    unsigned v = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned n = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= static_cast<unsigned>(o)) v += n;
-    }
-    if (lane == 31) wsum[wid] = v;
-    __syncthreads();
-    if (wid == 0) {
-      unsigned w = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned n = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= static_cast<unsigned>(o)) w += n;
-      }
-      wsum[lane] = w;
-    }
-    __syncthreads();
-    const unsigned excl = v - c + (wid ? wsum[wid - 1] : 0u) + carry;
-    if (i < nchunks) chunk_cnt[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += wsum[(blockDim.x >> 5) - 1];
-    __syncthreads();
-  }
-}
 
 // Commit the top-k: key > K*, or key == K* with tie rank < need.
 // One block per tie chunk so tie ranks follow ascending edge id.
@@ -1976,6 +1832,346 @@ __global__ void __launch_bounds__(kBlock) k_rbp_commit(DevGraph g, float* live, 
     if (commit && !dense) {
       fl.push_warp(nf, tgt);
       fl.flush(kBlock);
+    }
+  }
+  if (commit && !dense) fl.flush(0);
+  block_accumulate(ctl, c);
+}
+
+// ---------------------------------------------------------------------------
+// RBP top-k over a compacted candidate list: the same exact radix select in
+// five launches and two full passes over the residuals (instead of eight
+// launches and five passes):
+//   k_rx_hist0    pass-0 histogram (top 12 bits) of every residual; the last
+//                 block scans it (bin of the k-th key)
+//   k_rx_compact  edges whose top 12 bits reach that bin join a list; the
+//                 bin's own members feed the pass-1 histogram; last block: scan 1
+//   k_rx_hist2    pass-2 histogram over the list; last block: scan 2 = K*
+//   k_rx_ties     only when K* is shared and not every tie is taken: per-chunk
+//                 tie counts over all edges, prefix summed by the last block
+//   k_rbp_commit_list  the list's keys >= K* -- or, when ties are ranked,
+//                 every chunk of edges with k_rbp_commit's ascending-id rank
+// Outcome (frontier, commits, touched vertices) is identical to the
+// eight-launch path; only the order of the touched list differs.
+
+// k_radix_scan for one block of any size (a multiple of 32, <= 1024): the bin
+// holding the k-th largest key counted from the top, the prefix extended,
+// the count strictly above it accumulated, the histogram cleared.
+static __device__ void radix_scan_block(unsigned* hist, int pass, unsigned long long k, Ctl* ctl) {
+  __shared__ unsigned long long wsum[32];
+  const int nb = pass == 2 ? 256 : kRadixBins;
+  const int nt = static_cast<int>(blockDim.x);
+  const int per = (nb + nt - 1) / nt;
+  const int t = threadIdx.x;
+  unsigned long long mine = 0;
+  for (int j = 0; j < per; ++j)
+    if (t * per + j < nb) mine += __ldcg(&hist[nb - 1 - (t * per + j)]);
+  unsigned long long v = mine;
+  const unsigned lane = t & 31, wid = t >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= static_cast<unsigned>(o)) v += n;
+  }
+  if (lane == 31) wsum[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < static_cast<unsigned>(nt >> 5) ? wsum[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long n = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= static_cast<unsigned>(o)) w += n;
+    }
+    wsum[lane] = w;  // inclusive
+  }
+  __syncthreads();
+  const unsigned long long excl = v - mine + (wid ? wsum[wid - 1] : 0ull);
+  const unsigned long long above0 = pass == 0 ? 0ull : ctl->rx_above;
+  const unsigned long long need = k - above0;  // >= 1
+  if (excl < need && need <= excl + mine) {
+    unsigned long long acc = excl;
+    for (int j = 0; j < per && t * per + j < nb; ++j) {
+      const int bin = nb - 1 - (t * per + j);
+      const unsigned c = __ldcg(&hist[bin]);
+      if (acc < need && need <= acc + c) {
+        const int bits = pass == 2 ? 8 : 12;
+        ctl->rx_prefix = (pass == 0 ? 0u : (ctl->rx_prefix << bits)) | static_cast<unsigned>(bin);
+        ctl->rx_above = above0 + acc;
+        ctl->rx_ties = c;
+        ctl->rx_need = static_cast<unsigned>(need - acc);
+        break;
+      }
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int i = t; i < nb; i += nt) hist[i] = 0;
+}
+
+// block histogram -> global (every thread fences its own atomics), then the
+// last block to finish scans
+// (a release fence only in the threads that issued bin atomics: a full
+// __threadfence in every thread was a fifth of the pass-0 kernel's stalls)
+__device__ __forceinline__ void rx_flush_and_scan(const unsigned* sh, int nb, unsigned* hist, int pass,
+                                                  unsigned long long k, Ctl* ctl) {
+  __syncthreads();
+  bool any = false;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (sh[i]) {
+      atomicAdd(&hist[i], sh[i]);
+      any = true;
+    }
+  if (any) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (last_block_done(ctl)) radix_scan_block(hist, pass, k, ctl);
+}
+
+constexpr int kRxUnroll = 2;
+
+// exclusive scan over the block (kBlock threads); *total the sum; ends behind a barrier
+__device__ __forceinline__ unsigned block_excl_scan_u32(unsigned x, unsigned* total) {
+  __shared__ unsigned ws[kBlock / 32];
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  unsigned v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= static_cast<unsigned>(o)) v += n;
+  }
+  __syncthreads();  // ws is reused across calls
+  if (lane == 31) ws[wid] = v;
+  __syncthreads();
+  unsigned before = 0, tot = 0;
+#pragma unroll
+  for (unsigned w = 0; w < kBlock / 32; ++w) {
+    const unsigned c = ws[w];
+    before += w < wid ? c : 0u;
+    tot += c;
+  }
+  *total = tot;
+  return before + v - x;
+}
+
+static __global__ void __launch_bounds__(kBlock) k_rx_hist0(DevGraph g, const float* res, uint32_t D,
+                                                     unsigned* hist, Ctl* ctl, unsigned long long k) {
+  if (run_done(ctl)) return;
+  const bool band = band_graph(g);
+  __shared__ unsigned sh[kRadixBins];
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t D4 = (D + 3) / 4;
+  const float4* res4 = reinterpret_cast<const float4*>(res);
+  // kRxUnroll float4 loads in flight per thread (the pass is latency-bound)
+  for (uint32_t q0 = blockIdx.x * blockDim.x * kRxUnroll + threadIdx.x; q0 < D4;
+       q0 += gridDim.x * blockDim.x * kRxUnroll) {
+    float4 r4[kRxUnroll];
+#pragma unroll
+    for (int u = 0; u < kRxUnroll; ++u) {
+      const uint32_t q = q0 + u * blockDim.x;
+      r4[u] = q < D4 ? res4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kRxUnroll; ++u) {
+      const uint32_t q = q0 + u * blockDim.x;
+      const float rr[4] = {r4[u].x, r4[u].y, r4[u].z, r4[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (q >= D4 || 4 * q + j >= D) continue;
+        if (band && !edge_owned(g, 4 * q + j)) continue;
+        atomicAdd(&sh[float_key(rr[j]) >> 20], 1u);
+      }
+    }
+  }
+  rx_flush_and_scan(sh, kRadixBins, hist, 0, k, ctl);
+  if (threadIdx.x == 0 && blockIdx.x == 0) ctl->rx_n = 0u;  // read by k_rx_compact only (next launch)
+}
+
+static __global__ void __launch_bounds__(kBlock) k_rx_compact(DevGraph g, const float* res, uint32_t D,
+                                                       unsigned* hist, uint32_t* list, Ctl* ctl,
+                                                       unsigned long long k) {
+  if (run_done(ctl)) return;
+  const bool band = band_graph(g);
+  __shared__ unsigned sh[kRadixBins];
+  __shared__ unsigned s_base;
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t p0 = ctl->rx_prefix;
+  const uint32_t D4 = (D + 3) / 4;
+  const float4* res4 = reinterpret_cast<const float4*>(res);
+  for (uint32_t base = blockIdx.x * blockDim.x * kRxUnroll; base < D4; base += gridDim.x * blockDim.x * kRxUnroll) {
+    float4 r4[kRxUnroll];
+#pragma unroll
+    for (int u = 0; u < kRxUnroll; ++u) {
+      const uint32_t q = base + u * blockDim.x + threadIdx.x;
+      r4[u] = q < D4 ? res4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // this thread's candidates as a bit mask, one block scan, one global
+    // reservation per block and step
+    uint32_t m = 0u;
+#pragma unroll
+    for (int u = 0; u < kRxUnroll; ++u) {
+      const uint32_t q = base + u * blockDim.x + threadIdx.x;
+      const float rr[4] = {r4[u].x, r4[u].y, r4[u].z, r4[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t d = 4 * q + j;
+        const bool ok = q < D4 && d < D && (!band || edge_owned(g, d));
+        const uint32_t key = float_key(rr[j]);
+        if (ok && (key >> 20) == p0) atomicAdd(&sh[(key >> 8) & 0xfffu], 1u);
+        if (ok && (key >> 20) >= p0) m |= 1u << (4 * u + j);
+      }
+    }
+    unsigned tot;
+    const unsigned pre = block_excl_scan_u32(__popc(m), &tot);
+    if (tot == 0u) continue;  // block-uniform
+    if (threadIdx.x == 0) s_base = atomicAdd(&ctl->rx_n, tot);
+    __syncthreads();
+    unsigned o = s_base + pre;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1u;
+      list[o++] = 4 * (base + (b >> 2) * blockDim.x + threadIdx.x) + (b & 3);
+    }
+    __syncthreads();  // s_base is rewritten by the next step
+  }
+  rx_flush_and_scan(sh, kRadixBins, hist, 1, k, ctl);
+}
+
+static __global__ void __launch_bounds__(kBlock) k_rx_hist2(const float* res, const uint32_t* list, unsigned* hist,
+                                                     Ctl* ctl, unsigned long long k) {
+  if (run_done(ctl)) return;
+  __shared__ unsigned sh[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t n = __ldcg(&ctl->rx_n), p01 = ctl->rx_prefix;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t key = float_key(res[__ldcg(&list[i])]);
+    if ((key >> 8) == p01) atomicAdd(&sh[key & 0xffu], 1u);
+  }
+  rx_flush_and_scan(sh, 256, hist, 2, k, ctl);
+}
+
+// k_tie_count + k_tie_scan in one launch (the last block prefix-sums the chunk counts)
+static __global__ void __launch_bounds__(kBlock) k_rx_ties(DevGraph g, const float* res, uint32_t D,
+                                                    unsigned* chunk_cnt, uint32_t nchunks, Ctl* ctl) {
+  const bool band = band_graph(g);
+  if (run_done(ctl) || ctl->rx_need == ctl->rx_ties) return;
+  const uint32_t key = ctl->rx_prefix;
+  __shared__ unsigned sh[kBlock / 32];
+  for (uint32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {  // grid-stride: a no-op launch stays small
+    const size_t c0 = static_cast<size_t>(ch) * kTieChunk;
+    unsigned n = 0;
+    for (size_t d = c0 + threadIdx.x; d < c0 + kTieChunk && d < D; d += blockDim.x)
+      n += float_key(res[d]) == key && (!band || edge_owned(g, static_cast<uint32_t>(d)));
+    const unsigned tot = block_sum(n, sh);
+    if (threadIdx.x == 0) chunk_cnt[ch] = tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) __threadfence();
+  if (!last_block_done(ctl)) return;
+  __shared__ unsigned wsum[kBlock / 32];
+  __shared__ unsigned carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < nchunks; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const unsigned c = i < nchunks ? __ldcg(&chunk_cnt[i]) : 0u;
+    unsigned v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned x = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= static_cast<unsigned>(o)) v += x;
+    }
+    if (lane == 31) wsum[wid] = v;
+    __syncthreads();
+    unsigned before = 0, total = 0;
+    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
+      if (w < wid) before += wsum[w];
+      total += wsum[w];
+    }
+    if (i < nchunks) chunk_cnt[i] = carry + before + v - c;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+}
+
+// Commit (or mark, commit == 0) the top-k: the list's keys >= K* when every
+// tie is taken; otherwise k_rbp_commit's chunk walk (key > K*, or a tie whose
+// ascending-id rank is below need) over every chunk -- grid-stride over the
+// chunks, since the list pass would change residuals a tie walk reads.
+template <int QS>
+__global__ void __launch_bounds__(kBlock) k_rbp_commit_list(DevGraph g, float* live, const float* cand, float* res,
+                                                            uint32_t* vflag, uint32_t* vlist, uint8_t* sel,
+                                                            const uint32_t* list, const unsigned* chunk_off,
+                                                            uint32_t nchunks, Ctl* ctl, float eps, int commit,
+                                                            int dense) {
+  if (run_done(ctl)) return;
+  BPB_STAGER(fl, 2048, vlist, &ctl->nflag);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && commit) ctl->dense = dense;
+  fl.init();
+  const uint32_t key = ctl->rx_prefix;
+  const bool band = band_graph(g);
+  const bool rank_ties = ctl->rx_need != ctl->rx_ties;
+  const unsigned need = ctl->rx_need;
+  const uint32_t stamp = ctl->stamp;
+  Contrib c;
+  auto take_edge = [&](uint32_t d, float r, bool take) {
+    bool nf = false;
+    uint32_t tgt = 0;
+    if (take) {
+      if (commit) {
+        commit_edge<QS>(g, d, r, live, cand, res, eps, vflag, stamp, dense != 0, c, nf, tgt);
+      } else {
+        sel[d] = 1;
+        c.frontier += 1;
+      }
+    }
+    if (commit && !dense) {
+      fl.push_warp(nf, tgt);
+      fl.flush(kBlock);
+    }
+  };
+  if (!rank_ties) {
+    const uint32_t n = __ldcg(&ctl->rx_n);
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      uint32_t d = 0;
+      float r = 0.f;
+      if (i < n) {
+        d = __ldcg(&list[i]);
+        r = res[d];
+      }
+      take_edge(d, r, i < n && float_key(r) >= key);
+    }
+  } else {
+    __shared__ unsigned wt[kBlock / 32];
+    __shared__ unsigned running;
+    const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    for (uint32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+      __syncthreads();
+      if (threadIdx.x == 0) running = __ldcg(&chunk_off[ch]);
+      __syncthreads();
+      const size_t c0 = static_cast<size_t>(ch) * kTieChunk;
+      for (size_t base = c0; base < c0 + kTieChunk && base < g.D; base += blockDim.x) {
+        const size_t di = base + threadIdx.x;
+        const bool valid = di < g.D && di < c0 + kTieChunk && (!band || edge_owned(g, static_cast<uint32_t>(di)));
+        const float r = valid ? res[di] : 0.f;
+        const uint32_t kk = float_key(r);
+        const bool tie = valid && kk == key;
+        const unsigned m = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) wt[wid] = __popc(m);
+        __syncthreads();
+        unsigned before = 0, total = 0;
+        for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
+          if (w < wid) before += wt[w];
+          total += wt[w];
+        }
+        const unsigned rank = running + before + __popc(m & ((1u << lane) - 1u));
+        __syncthreads();
+        if (threadIdx.x == 0) running += total;
+        take_edge(static_cast<uint32_t>(di), r, (valid && kk > key) || (tie && rank < need));
+      }
     }
   }
   if (commit && !dense) fl.flush(0);

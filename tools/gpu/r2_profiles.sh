@@ -13,5 +13,5 @@ timeout 600 $NCU -k regex:k_vertex_update -s 4 -c 1 -o gpurun_out/r2_prof_lbp100
 timeout 600 $NCU -k regex:k_vertex_update -s 2 -c 1 -o gpurun_out/r2_prof_potts $P --n 4096 --potts 8 --kind lbp --iters 3 > /dev/null 2>&1; echo potts=$?
 timeout 600 $NCU -k regex:k_rnbp_persist -c 1 -o gpurun_out/r2_prof_persist python tools/rnbp_trace.py 1000 > /dev/null 2>&1; echo persist=$?
 timeout 600 $NCU -k regex:k_rs_iteration -s 1 -c 1 -o gpurun_out/r2_prof_rs $P --n 1000000 --er --kind rs --iters 3 > /dev/null 2>&1; echo rs=$?
-timeout 600 $NCU -k regex:k_radix_hist -s 3 -c 1 -o gpurun_out/r2_prof_radix $P --n 1000 --kind rbp --iters 3 > /dev/null 2>&1; echo radix=$?
+timeout 600 $NCU -k regex:k_rx_compact -s 3 -c 1 -o gpurun_out/r2_prof_radix $P --n 1000 --kind rbp --iters 3 > /dev/null 2>&1; echo radix=$?
 ls -la gpurun_out/*.ncu-rep
