@@ -232,6 +232,8 @@ struct Ctl {
   unsigned int blocks_done;  // last-block-done counter of the kernel-fused finalize / retry (reset by the last block)
   unsigned int fused_par;    // fused RnBP sweep (kernels_fused.cuh): the state lives in the scratch set when odd
   unsigned int fused_abort;  // fused RnBP sweep: an empty attempt-0 frontier, the per-kernel loop redoes the iteration
+  unsigned int band_poll;    // band RnBP driven by a polling host (partition.cu): an empty attempt-0 frontier waits
+  unsigned int band_wait;    // ... for the host's retry: every kernel is a no-op until the host clears it
   unsigned long long persist_bytes;  // algorithmic bytes moved by the persistent kernel
   unsigned long long vote_limit_ns;  // row-band partition: time limit, decided by an all-reduced vote
   unsigned long long phase_ns[8];    // persistent kernel phase clock (CTA 0)

@@ -55,6 +55,11 @@ class EngineBase {
   virtual void band_sweep() = 0;
   virtual void band_finish() = 0;
   virtual void band_status(bp_run_result* r) = 0;
+  // polling host (partition.cu): RnBP iterations run back to back on the
+  // device; one whose attempt-0 frontier is empty parks the band (band_wait)
+  virtual void band_set_poll(bool on) = 0;
+  virtual bool band_waiting() = 0;  // after band_status (reads the fetched header)
+  virtual void band_clear_wait() = 0;
   virtual cudaStream_t stream() const = 0;
 };
 

@@ -855,6 +855,14 @@ class EngineT final : public EngineBase {
     sync();
   }
 
+  void ctl_put_u32(size_t off, unsigned v) {
+    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(ctl_.p) + off, &v, 4, cudaMemcpyHostToDevice, s_), "ctl h2d");
+    sync();  // v lives on this stack frame
+  }
+  void band_set_poll(bool on) override { ctl_put_u32(offsetof(Ctl, band_poll), on ? 1u : 0u); }
+  bool band_waiting() override { return hctl_->band_wait != 0u; }
+  void band_clear_wait() override { ctl_put_u32(offsetof(Ctl, band_wait), 0u); }
+
   void band_status(bp_run_result* r) override {
     fetch_ctl_header();
     std::memset(r, 0, sizeof(*r));

@@ -179,7 +179,7 @@ static __global__ void k_set_u32(unsigned* p, unsigned v) { *p = v; }
 // Early exit of every loop kernel once the run is over; inside the device-side
 // WHILE loop it also clears the loop condition.
 __device__ __forceinline__ bool run_done(Ctl* c) {
-  if (!c->done) return false;
+  if (!c->done && !c->band_wait) return false;
   if (c->cond_handle && blockIdx.x == 0 && threadIdx.x == 0)
     cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(c->cond_handle), 0u);
   return true;
@@ -474,6 +474,10 @@ static __global__ void k_plist_unpack_flag(DevGraph g, float* M, Ctl* ctl, uint3
 // the band's contributions of the iteration -> h.count = {delta, frontier,
 // survivors, time vote, count (init)}; slots are left for the finalize
 static __global__ void __launch_bounds__(kSlots) k_part_count_rnbp(Ctl* c, PartHalo h) {
+  if (c->band_wait) {  // waiting for the host's retry: zeros keep the in-place all-reduce bounded
+    if (threadIdx.x < 5) h.count[threadIdx.x] = 0ull;
+    return;
+  }
   __shared__ unsigned long long sh[5][kSlots / 32];
   const Accum a = c->acc[threadIdx.x];
   unsigned long long v[4] = {static_cast<unsigned long long>(a.delta), a.frontier, a.survivors, a.count};
@@ -504,6 +508,13 @@ static __global__ void __launch_bounds__(kSlots) k_part_count_rnbp(Ctl* c, PartH
 __device__ __forceinline__ void finalize_block(Ctl* c, int mode, uint32_t D, const unsigned long long* ext = nullptr) {
   if (run_done(c)) return;
   const int t = threadIdx.x;
+  // band RnBP under a polling host: an empty attempt-0 frontier with survivors
+  // (the GLOBAL sums) leaves the iteration open -- slots and state untouched --
+  // until the host runs the retry / single-survivor fallback (schedulers.cpp:204-214)
+  if (mode == kFinIterExt && ext && c->band_poll && ext[1] == 0ull && ext[2] > 0ull) {
+    if (t == 0) c->band_wait = 1u;
+    return;
+  }
   // thread 0's control-block loads are issued with the slot loads
   FinRegs f;
   if (t == 0) f.load(c);

@@ -9,9 +9,12 @@
 //         flag every kPollEvery iterations (later iterations are no-ops).
 //   RnBP  per iteration: select attempt 0 (Philox keyed by GLOBAL edge ids) +
 //   RBP   commit + pack | halo | ghost unpack + flagged refresh | all-reduce
-//   RS    {delta, frontier, survivors, time vote, count}; RnBP's retry and
-//         single-survivor fallback (schedulers.cpp:204-214) need the GLOBAL
-//         frontier, read once per iteration (one 40-byte D2H).
+//   RS    {delta, frontier, survivors, time vote, count}; the loop control
+//         runs on the device from the all-reduced sums and the host polls
+//         every kPollEvery iterations.  RnBP's retry and single-survivor
+//         fallback (schedulers.cpp:204-214) need the host: an iteration with
+//         an empty attempt-0 frontier parks the bands (Ctl::band_wait) until
+//         the next poll runs them.
 //
 // Transports: NcclTransport (one band per rank, ncclSend/ncclRecv/ncclAllReduce
 // on the band stream; libnccl is loaded at first use, so single-GPU users need
@@ -238,15 +241,21 @@ void frontier_loop(std::vector<Band*>& bands, BandComm& comm, int kind, uint64_t
   for (Band* b : bands) b->engine->band_rnbp_begin();
   comm.all_reduce(bands, 5);
   for (Band* b : bands) b->engine->band_rnbp_finish_init();
-  for (uint64_t k = 0; k <= max_iterations; ++k) {
+  // RnBP: an iteration whose attempt-0 frontier is empty parks every band on
+  // the device (the finalize sees the all-reduced sums, so all ranks park at
+  // the same iteration); the iterations enqueued behind it are no-ops -- their
+  // collectives still run, on zeroed sums -- until the next poll runs the retry
+  if (kind == BP_RNBP)
+    for (Band* b : bands) b->engine->band_set_poll(true);
+  const uint64_t max_polls = max_iterations / kPollEvery + 2;
+  for (uint64_t poll = 0; poll <= max_polls + 2 * (max_iterations + 1); ++poll) {
     bp_run_result st;
-    bands[0]->engine->band_status(&st);
-    if (st.stopped) return;
-    phase(0);
-    uint64_t c[5];
-    read_counts(c);
-    if (kind == BP_RNBP && c[1] == 0 && c[2] > 0) {  // retry once, then one survivor (schedulers.cpp:204-214)
-      phase(1);
+    bands[0]->engine->band_status(&st);  // one D2H + sync per kPollEvery iterations
+    if (st.stopped) break;
+    if (kind == BP_RNBP && bands[0]->engine->band_waiting()) {
+      for (Band* b : bands) b->engine->band_clear_wait();
+      phase(1);  // retry once, then one survivor (schedulers.cpp:204-214)
+      uint64_t c[5];
       read_counts(c);
       if (c[1] == 0) {
         std::vector<std::vector<uint64_t>> local(bands.size());
@@ -265,9 +274,16 @@ void frontier_loop(std::vector<Band*>& bands, BandComm& comm, int kind, uint64_t
           comm.all_reduce(bands, 5);
         }
       }
+      for (Band* b : bands) b->engine->band_rnbp_finish();
+      continue;  // poll again: the retried iteration may have been the last
     }
-    for (Band* b : bands) b->engine->band_rnbp_finish();
+    for (int j = 0; j < kPollEvery; ++j) {
+      phase(0);
+      for (Band* b : bands) b->engine->band_rnbp_finish();
+    }
   }
+  if (kind == BP_RNBP)
+    for (Band* b : bands) b->engine->band_set_poll(false);
 }
 }  // namespace
 
