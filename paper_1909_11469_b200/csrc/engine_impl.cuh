@@ -1152,6 +1152,53 @@ class EngineT final : public EngineBase {
   uint32_t fused_force_ = 0;
   unsigned fused_tma_grid_ = 0;
   bool fused_uses_tma() const { return (fused_force_ & BP_RUN_FUSED_TMA) != 0; }
+  // small lattices run the dense phase as ONE persistent launch
+  // (k_rnbp_fused_persist): 0 = per-sweep launches, 1 = 16-CTA cluster,
+  // 2 = cooperative grid (BPB_FUSED_PERSIST: tuning override)
+  // (measured, whole 10k-cap runs: 100^2 4.71 -> 4.48 ms with the cluster,
+  // 128^2 5.93 -> 5.58; 200^2 12.51 -> 11.94 with the grid, where the cluster
+  // was slower: 16 SMs for 1300 warp tiles)
+  static constexpr uint32_t kFusedPersistClusterV = 16384, kFusedPersistGridV = 48000;
+  unsigned fused_persist_mode() const {
+    static const char* e = std::getenv("BPB_FUSED_PERSIST");
+    if (fused_uses_tma()) return 0;
+    if (e) return static_cast<unsigned>(std::atoi(e));
+    return g_.V <= kFusedPersistClusterV ? 1u : g_.V <= kFusedPersistGridV ? 2u : 0u;
+  }
+  void launch_fused_persist(bool cluster) {
+    static std::map<int, bool> attr_set;  // per device
+    if (!attr_set[g_.device]) {
+      cuda_check(cudaFuncSetAttribute(k_rnbp_fused_persist<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                 "cluster attribute");
+      attr_set[g_.device] = true;
+    }
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(cluster ? 16u : static_cast<unsigned>(sm_count()));
+    lc.blockDim = dim3(kFusedPersistBlock);
+    lc.stream = s_;
+    cudaLaunchAttribute at[1];
+    if (cluster) {
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 16;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+    } else {
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+    }
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    float* L = live();
+    float* CA = cand();
+    float* CB = fc_.as<float>();
+    uint8_t* UA = fu_[0].as<uint8_t>();
+    uint8_t* UB = fu_[1].as<uint8_t>();
+    timed(kKFused, [&] {
+      auto k = cluster ? k_rnbp_fused_persist<true> : k_rnbp_fused_persist<false>;
+      cuda_check(cudaLaunchKernelEx(&lc, k, dg_, L, CA, UA, CB, UB, ctl(), eps_, prm_), "fused persistent launch");
+    });
+    ++launches_;
+  }
   void enqueue_fused(unsigned dir) {
     if (fused_uses_tma()) {
       if (!fused_tma_grid_) {
@@ -1199,7 +1246,20 @@ class EngineT final : public EngineBase {
       k_fused_enter<<<grid_cap(g_.D), kBlock, 0, s_>>>(res_.as<float>(), fu_[0].as<uint8_t>(), g_.D, eps_);
     });
     launch_check();
-    if (use_graph) {
+    if (const unsigned pm = fused_persist_mode()) {
+      for (;;) {
+        set_iteration_budget(hctl_->iteration + kTraceRing / 2);
+        launch_fused_persist(pm == 1);
+        fetch_ctl_header();
+        drain_trace(trace, cap, copied);
+        if (hctl_->done && hctl_->stop_reason == kStopMaxIter && hctl_->iteration < cfg_.max_iterations &&
+            budget_stop_) {
+          clear_budget_stop();
+          if (hctl_->cl_state == 0u && !hctl_->fused_abort) continue;
+        }
+        break;
+      }
+    } else if (use_graph) {
       if (!fgexec_) {
         cuda_check(cudaGraphCreate(&fgraph_, 0), "graph create");
         cuda_check(cudaGraphConditionalHandleCreate(&fcond_, fgraph_, 1, cudaGraphCondAssignDefault), "cond handle");

@@ -29,9 +29,13 @@
 // iteration with the retry / single-survivor fallback (:204-214).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace bpb {
+
+namespace cgp_fused = cooperative_groups;
 
 // The per-edge state the sweep carries: live and candidate messages (float2
 // per edge pair, both directions) and the unconverged predicate r >= eps as
@@ -86,13 +90,17 @@ __device__ __forceinline__ uint32_t pair_select(uint32_t u, unsigned long long e
   return s;
 }
 
+// NC: candidates / predicates through the read-only path (one launch per
+// sweep); the persistent variant rereads buffers other CTAs rewrote, so it
+// loads them coherently (behind the barrier's L1 invalidation)
+template <bool NC = true>
 __device__ __forceinline__ FusedPair load_pair(const float2* L, const float2* __restrict__ Cn,
                                                const uint16_t* __restrict__ U, const float* __restrict__ ea,
                                                uint32_t e) {
   FusedPair p;
   p.l = L[e];  // coherent: the live set is updated in place
-  p.c = __ldg(&Cn[e]);
-  const uint32_t u = __ldg(&U[e]);  // bytes are 0 / 1
+  p.c = NC ? __ldg(&Cn[e]) : Cn[e];
+  const uint32_t u = NC ? __ldg(&U[e]) : U[e];  // bytes are 0 / 1
   p.u = (u & 1u) | ((u >> 7) & 2u);
   p.a = __ldg(&ea[e]);
   p.sel = 0u;
@@ -142,24 +150,23 @@ __host__ __device__ inline bool fused_warp_tiles(uint32_t C) {
 // neighbour lane's outgoing value (shuffle), vertical pairs one row later
 // with the lower vertex's.  Pairs split between warps / blocks leave as two
 // single-direction stores.
-template <bool WT>  // fused_warp_tiles(lat_cols)
-static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const float* L0,
-                                                              const float* __restrict__ C0,
-                                                              const uint8_t* __restrict__ U0, float* L1,
-                                                              float* __restrict__ C1, uint8_t* __restrict__ U1,
-                                                              Ctl* ctl, float eps, RnbpParams prm, unsigned dir) {
-  if (run_done(ctl)) return;
-  if (ctl->cl_state != 0u || ctl->fused_abort) {  // the fused phase is over: leave the loop
-    if (ctl->cond_handle && blockIdx.x == 0 && threadIdx.x == 0)
-      cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(ctl->cond_handle), 0u);
-    return;
-  }
-  if (ctl->fused_par != dir) return;
-  const double p = device_p_now(ctl, prm.low_p, prm.high_p, prm.thr);
-  const unsigned long long thresh = static_cast<unsigned long long>(ceil(ldexp(p, 53)));
-  const bool draw = thresh < (1ull << 53);
-  const unsigned long long it = ctl->iteration, eoff = g.edge_offset;
-  const PhiloxKeys pk(prm.seed);
+// Per-thread sums of one sweep.
+struct FusedSums {
+  int n_delta = 0;
+  uint32_t n_surv = 0, n_front = 0, n_evals = 0, n_visits = 0;
+  bool bad = false;
+};
+
+// One fused sweep over this unit's tiles (unit = warp when WT, else block;
+// units = the grid's warps / blocks): the body of k_rnbp_fused and of its
+// persistent variant.
+template <bool WT, bool NC>
+__device__ __forceinline__ void fused_sweep(const DevGraph& g, const float* L0, const float* __restrict__ C0,
+                                            const uint8_t* __restrict__ U0, float* L1, float* __restrict__ C1,
+                                            uint8_t* __restrict__ U1, float eps, bool draw,
+                                            unsigned long long thresh, unsigned long long it,
+                                            const PhiloxKeys& pk, FusedSums& sums) {
+  const unsigned long long eoff = g.edge_offset;
   const uint32_t C = g.lat_cols, R = g.lat_rows;
   constexpr bool wt = WT;
   constexpr uint32_t SW = wt ? kFusedWarpCols : kFusedStrip;  // strip width
@@ -180,16 +187,17 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const 
   // column of this lane within a strip (the halo lane: the column before the warp's first)
   const uint32_t col_in_strip = (wt ? 0u : (threadIdx.x >> 5) * kFusedWarpCols) + lane - 1u;  // wraps for halo of warp 0
   // per-thread counts in 32 bits (a thread sees at most a few thousand tiles)
-  int n_delta = 0;
-  uint32_t n_surv = 0, n_front = 0, n_evals = 0, n_visits = 0;
-  bool bad = false;
+  int& n_delta = sums.n_delta;
+  uint32_t &n_surv = sums.n_surv, &n_front = sums.n_front, &n_evals = sums.n_evals, &n_visits = sums.n_visits;
+  bool& bad = sums.bad;
   // carried from the row above (same column): its down pair (old state +
   // draws) and the upper vertex's new outgoing message on it
   FusedPair dprev{};
   float dl_new = 0.f, dc_new = 0.f;
   uint32_t du_new = 0u;
-  const uint64_t gw = wt ? static_cast<uint64_t>(blockIdx.x) * (kBlock / 32) + (threadIdx.x >> 5) : blockIdx.x;
-  const uint64_t nw = wt ? static_cast<uint64_t>(gridDim.x) * (kBlock / 32) : gridDim.x;
+  // (warp tiles: any block size; block strips: kBlock threads)
+  const uint64_t gw = wt ? static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5) : blockIdx.x;
+  const uint64_t nw = wt ? static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32) : gridDim.x;
   const uint64_t t_begin = ntiles * gw / nw, t_end = ntiles * (gw + 1) / nw;
   uint32_t strip = static_cast<uint32_t>(t_begin / R), r = static_cast<uint32_t>(t_begin - static_cast<uint64_t>(strip) * R);
   for (uint64_t t = t_begin; t < t_end; ++t) {
@@ -211,10 +219,10 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const 
     const bool hasR = inb && dn, hasU = act && !first, hasL = act && c > 0u, hasD = act && !last;
     const uint32_t eR = last ? row + c : row + 2u * c, eD = row + 2u * c + dn;
     FusedPair pr{}, pd{}, pu{};
-    if (hasR) pr = load_pair(La, Ca, Ua, ea, eR);
-    if (hasD) pd = load_pair(La, Ca, Ua, ea, eD);
+    if (hasR) pr = load_pair<NC>(La, Ca, Ua, ea, eR);
+    if (hasD) pd = load_pair<NC>(La, Ca, Ua, ea, eD);
     const uint32_t eU = first ? 0u : (r - 1u) * (2u * C - 1u) + 2u * c + dn;
-    if (hasU) pu = carry ? dprev : load_pair(La, Ca, Ua, ea, eU);
+    if (hasU) pu = carry ? dprev : load_pair<NC>(La, Ca, Ua, ea, eU);
     const float un = act ? __ldg(&g.unary_lo[r * C + c]) : 0.f;
     if (hasR) pr.sel = pair_select(pr.u, eR + eoff, draw, pk, it, thresh);
     if (hasD) pd.sel = pair_select(pd.u, eD + eoff, draw, pk, it, thresh);
@@ -313,16 +321,85 @@ static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const 
       ++strip;
     }
   }
-  if (bad) ctl->numeric_error = 1u;
+}
+
+__device__ __forceinline__ void fused_accumulate(Ctl* ctl, const FusedSums& s) {
+  if (s.bad) ctl->numeric_error = 1u;
   Contrib acc;
-  acc.delta = n_delta;
-  acc.survivors = n_surv;
-  acc.frontier = n_front;
-  acc.evals = n_evals;
-  acc.visits = n_visits;
+  acc.delta = s.n_delta;
+  acc.survivors = s.n_surv;
+  acc.frontier = s.n_front;
+  acc.evals = s.n_evals;
+  acc.visits = s.n_visits;
   block_accumulate(ctl, acc);
+}
+
+// p_now -> Bernoulli threshold of the iteration (uniform_unit < p <=> u53 < ceil(p 2^53))
+__device__ __forceinline__ unsigned long long fused_thresh(const Ctl* ctl, const RnbpParams& prm) {
+  const double p = device_p_now(ctl, prm.low_p, prm.high_p, prm.thr);
+  return static_cast<unsigned long long>(ceil(ldexp(p, 53)));
+}
+
+// dir: the parity this launch serves (0: canonical -> scratch, 1: back); a
+// launch of the wrong parity is a no-op (the loop body holds both).  The last
+// block to finish runs the loop control (finalize kFinFused).
+template <bool WT>  // fused_warp_tiles(lat_cols)
+static __global__ void __launch_bounds__(kBlock) k_rnbp_fused(DevGraph g, const float* L0,
+                                                              const float* __restrict__ C0,
+                                                              const uint8_t* __restrict__ U0, float* L1,
+                                                              float* __restrict__ C1, uint8_t* __restrict__ U1,
+                                                              Ctl* ctl, float eps, RnbpParams prm, unsigned dir) {
+  if (run_done(ctl)) return;
+  if (ctl->cl_state != 0u || ctl->fused_abort) {  // the fused phase is over: leave the loop
+    if (ctl->cond_handle && blockIdx.x == 0 && threadIdx.x == 0)
+      cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(ctl->cond_handle), 0u);
+    return;
+  }
+  if (ctl->fused_par != dir) return;
+  const unsigned long long thresh = fused_thresh(ctl, prm);
+  const PhiloxKeys pk(prm.seed);
+  FusedSums sums;
+  fused_sweep<WT, true>(g, L0, C0, U0, L1, C1, U1, eps, thresh < (1ull << 53), thresh, ctl->iteration, pk, sums);
+  fused_accumulate(ctl, sums);
   if (last_block_done(ctl)) finalize_block(ctl, kFinFused, g.D);
 }
+
+// The dense phase of a SMALL lattice inside one launch: sweeps back to back,
+// each followed by a barrier, the loop control in CTA 0 (finalize kFinFused)
+// and a second barrier -- a 16-CTA cluster (hardware barrier) or a
+// cooperative grid.  One launch per 100x100 dense phase instead of one per
+// sweep, whose launch gap and last-block finalize chain (~13 us at 100^2)
+// were most of the iteration.  Same sweeps, same finalize: the same run.
+constexpr int kFusedPersistBlock = 512;  // warp tiles, 16 warps per CTA
+
+template <bool CLUSTER>
+static __global__ void __launch_bounds__(kFusedPersistBlock) k_rnbp_fused_persist(DevGraph g, float* L, float* CA,
+                                                                                  uint8_t* UA,
+                                                                      float* CB, uint8_t* UB, Ctl* ctl, float eps,
+                                                                      RnbpParams prm) {
+  auto sync_all = [] {
+    if constexpr (CLUSTER)
+      cgp_fused::this_cluster().sync();
+    else
+      cgp_fused::this_grid().sync();
+  };
+  const PhiloxKeys pk(prm.seed);
+  for (;;) {
+    // loop state: written by CTA 0's finalize before the last barrier (whose
+    // acquire invalidated L1: plain loads see it)
+    if (ctl->done || ctl->cl_state != 0u || ctl->fused_abort) break;
+    const bool odd = ctl->fused_par & 1u;
+    const unsigned long long thresh = fused_thresh(ctl, prm);
+    FusedSums sums;
+    fused_sweep<true, false>(g, L, odd ? CB : CA, odd ? UB : UA, L, odd ? CA : CB, odd ? UA : UB, eps,
+                           thresh < (1ull << 53), thresh, ctl->iteration, pk, sums);
+    fused_accumulate(ctl, sums);
+    sync_all();
+    if (blockIdx.x == 0) finalize_block(ctl, kFinFused, g.D);
+    sync_all();
+  }
+}
+
 
 // Start of the fused phase: the unconverged predicate of every directed edge.
 static __global__ void __launch_bounds__(kBlock) k_fused_enter(const float* __restrict__ res, uint8_t* __restrict__ U,
