@@ -35,8 +35,11 @@ def _assert_same(a, b):
     assert np.array_equal(a.beliefs.values, b.beliefs.values)
 
 
+# (lattices up to 16K vertices run the dense phase in one 16-CTA cluster
+# launch, up to 48K in one cooperative-grid launch: k_rnbp_fused_persist)
 @pytest.mark.parametrize("n,c,seed,low_p", [(30, 2.5, 1, 0.5), (64, 2.5, 7, 0.3), (100, 2.5, 500, 0.5),
-                                            (100, 1.0, 3, 0.7)])
+                                            (100, 1.0, 3, 0.7), (150, 2.5, 9, 0.5), (200, 2.5, 11, 0.3),
+                                            (260, 2.5, 2, 0.5)])
 def test_fused_run_equals_two_launch_loop(bp, n, c, seed, low_p):
     g = bp.generate_ising(bp.IsingParams(n=n, c=c, seed=seed))
     a, b = _pair(bp, g, _cfg(bp, seed=seed, low_p=low_p))
@@ -52,6 +55,17 @@ def test_fused_window_parity_fixup(bp, iters):
     a, b = _pair(bp, g, _cfg(bp, seed=0, iters=iters))
     _assert_same(a, b)
     assert a.iterations == iters and a.messages_updated_total > 0
+
+
+@pytest.mark.parametrize("n", [100, 180])
+@pytest.mark.parametrize("iters", [1, 2, 3, 21])
+def test_fused_persistent_windows(bp, n, iters):
+    """capped windows inside the persistent dense launch (cluster at 100^2,
+    grid at 180^2): odd and even sweep counts leave the canonical state"""
+    g = bp.generate_ising(bp.IsingParams(n=n, c=2.5, seed=4))
+    a, b = _pair(bp, g, _cfg(bp, seed=4, iters=iters))
+    _assert_same(a, b)
+    assert a.iterations == iters
 
 
 def test_fused_nonsquare_and_descriptor_lattices(bp, orc):
