@@ -60,39 +60,43 @@ enum KClass { kKUpdate = 0, kKSelect = 1, kKTopk = 2, kKSplash = 3, kKInit = 4, 
 template <int QS>
 class EngineT final : public EngineBase {
  public:
+  // engine buffers: zero-filled on the engine stream (a cached block's
+  // synchronous memset + device sync per buffer was ~0.3 ms of every run)
+  void zalloc(DevBuf& b, size_t n) {
+    b.alloc_async(n, s_);
+    cuda_check(cudaMemsetAsync(b.p, 0, b.bytes, s_), "memset");
+  }
   EngineT(const GraphImpl& g, const bp_sched_config& cfg) : g_(g), cfg_(cfg) {
     cuda_check(cudaSetDevice(g.device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
     dg_ = g.dev();
     eps_ = eps_ceil(cfg.epsilon);
     const size_t msz = static_cast<size_t>(g.D) * QS * sizeof(float);
-    bufA_.alloc(msz);
-    bufB_.alloc(msz);
-    res_.alloc((static_cast<size_t>(g.D) + 3) / 4 * 16);  // padded to float4, tail stays 0
-    cuda_check(cudaMemset(res_.p, 0, res_.bytes), "memset res");
-    vflag_.alloc(static_cast<size_t>(g.V) * 4);
+    zalloc(bufA_, msz);
+    zalloc(bufB_, msz);
+    zalloc(res_, (static_cast<size_t>(g.D) + 3) / 4 * 16);  // padded to float4, tail stays 0
+    zalloc(vflag_, static_cast<size_t>(g.V) * 4);
     if (cfg.kind == BP_RNBP) {  // candidate list (run mode)
-      clist_[0].alloc(static_cast<size_t>(g.D) * 4);
-      clist_[1].alloc(static_cast<size_t>(g.D) * 4);
-      inlist_.alloc(g.D ? g.D : 1);
-      vslot_.alloc(static_cast<size_t>(g.D ? g.D : 1) * 4);  // here, not mid-run: cudaMalloc can stall the device
-      cstamp_.alloc(static_cast<size_t>(g.D ? g.D : 1) * 4);
+      zalloc(clist_[0], static_cast<size_t>(g.D) * 4);
+      zalloc(clist_[1], static_cast<size_t>(g.D) * 4);
+      zalloc(inlist_, g.D ? g.D : 1);
+      zalloc(vslot_, static_cast<size_t>(g.D ? g.D : 1) * 4);  // here, not mid-run: cudaMalloc can stall the device
+      zalloc(cstamp_, static_cast<size_t>(g.D ? g.D : 1) * 4);
     }
-    vlist_.alloc(static_cast<size_t>(g.V) * 4);
+    zalloc(vlist_, static_cast<size_t>(g.V) * 4);
     if (fused_capable()) {  // scratch buffer set of the fused dense RnBP sweep (here, not mid-run)
-      fc_.alloc(msz);
-      fu_[0].alloc(g.D);
-      fu_[1].alloc(g.D);
+      zalloc(fc_, msz);
+      zalloc(fu_[0], g.D);
+      zalloc(fu_[1], g.D);
     }
-    ctl_.alloc(sizeof(Ctl));
+    zalloc(ctl_, sizeof(Ctl));
     hctl_ = static_cast<Ctl*>(pinned_acquire(sizeof(Ctl)));
     std::memset(hctl_, 0, sizeof(Ctl));
     if (cfg.kind == BP_RBP) {
-      hist_.alloc(kRadixBins * 4);
-      cuda_check(cudaMemset(hist_.p, 0, kRadixBins * 4), "memset");
+      zalloc(hist_, kRadixBins * 4);
       nchunks_ = std::max<uint32_t>(1, (g.D + kTieChunk - 1) / kTieChunk);
-      chunk_.alloc(static_cast<size_t>(nchunks_) * 4);
-      rx_list_.alloc(std::max<size_t>(g.D, 1) * 4);
+      zalloc(chunk_, static_cast<size_t>(nchunks_) * 4);
+      zalloc(rx_list_, std::max<size_t>(g.D, 1) * 4);
       const long long kr = std::llround(cfg.p * static_cast<double>(g.D));  // schedulers.cpp:124
       k_ = kr < 1 ? 1 : static_cast<uint64_t>(kr);
     }
