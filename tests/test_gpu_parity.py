@@ -174,6 +174,30 @@ def test_rbp_topk_exact_against_select_top_k(bp, orc):
         de.apply_frontier(de.rbp_frontier(0.3))
 
 
+def test_rbp_topk_ties_across_chunks(bp, orc):
+    """select_top_k's id order among equal keys across tie chunks and list
+    blocks: a 100^2 grid (5 chunks of 8192 edges) whose residuals go to
+    exactly 0 as edges commit (K* = 0 with partial ties), and a coupling-free
+    grid whose residuals are all 0 (the k lowest ids)."""
+    og = po.Graph.ising(orc, 100, 2.5, 8)
+    a = og.arrays()
+    dg = bp.PairwiseMRF.from_arrays(a.cardinalities, a.unary, a.endpoints, a.tables)
+    de = bp.EngineState(dg, bp.SchedulerConfig(kind=bp.SchedulerKind.rbp))
+    D = dg.num_directed_edges()
+    for step in range(4):
+        r = de.residuals().astype(np.float32).astype(np.float64)
+        for p in (1.0 / 64, 0.5, 0.9):
+            k = max(1, int(np.floor(p * D + 0.5)))
+            want = np.sort(po.select_top_k(orc, r, k))
+            assert np.array_equal(de.rbp_frontier(p), want), (step, p)
+        de.apply_frontier(de.rbp_frontier(0.6))
+    flat = bp.generate_ising(bp.IsingParams(n=60, c=0.0, seed=3))
+    fe = bp.EngineState(flat, bp.SchedulerConfig(kind=bp.SchedulerKind.rbp))
+    assert not np.any(fe.residuals())
+    k = int(np.floor(0.3 * flat.num_directed_edges() + 0.5))
+    assert np.array_equal(fe.rbp_frontier(0.3), np.arange(k))
+
+
 def test_rbp_frontier_size_rounding(bp, orc):
     """k = max(1, llround(p * 2|E|)): round(12.5) = 13 (test_schedulers.cpp:76-84)."""
     cards, un, ed = path_graph(101)
