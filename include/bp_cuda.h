@@ -349,8 +349,11 @@ BP_API int bp_band_survivors(struct bp_engine* e, uint64_t* global_ids, uint64_t
  *   RS over the bands -- NCCL: nbands == 1, this rank's band; local: the
  *   bands of parts 0 .. P-1 in order.  Halo send/recv and the all-reduce of
  *   the loop counters are enqueued on the band's stream; the loop control
- *   runs on the global counts, so every rank stops at the same iteration and
- *   owned messages equal the unpartitioned run's bit for bit (LBP, RnBP).
+ *   runs on the device from the global counts, so every rank stops at the
+ *   same iteration and owned messages equal the unpartitioned run's bit for
+ *   bit (LBP, RnBP).  The host polls every 16 iterations; an RnBP iteration
+ *   with an empty global attempt-0 frontier parks the bands until the poll
+ *   runs the retry / single-survivor fallback (schedulers.cpp:204-214).
  *   result: the global iteration count / convergence; messages_updated_total
  *   counts this band's owned messages (LBP) or the global frontier (others).
  *   Beliefs of the owned rows: bp_engine_beliefs (rows row0 - ghost_up ... in
