@@ -1217,15 +1217,26 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
   const uint64_t V = dense_items ? g.V : ctl->nflag;  // items: vertices, or the touched list
   // every lane of the warp runs every trip (the shuffles need all of them)
   const uint64_t trips = (V + groups - 1) / groups;
+  const uint64_t item0 = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / LPV) + threadIdx.x / LPV;
+  // refresh: the touched flag (dense) or list entry (sparse) of the NEXT
+  // trip is loaded one trip ahead, so a trip's message loads do not wait
+  // behind a flag round trip (k_rnbp_select wrote both in the previous launch)
+  auto item_word = [&](uint64_t vv) -> uint32_t {
+    if (MODE != kModeDelta || vv >= V) return 0u;
+    return dense_items ? __ldg(&vflag[vv]) : __ldg(&vlist[vv]);
+  };
+  uint32_t next_word = item_word(item0);
   for (uint64_t t = 0; t < trips; ++t) {
-    const uint64_t vv = t * groups + static_cast<uint64_t>(blockIdx.x) * (blockDim.x / LPV) + threadIdx.x / LPV;
+    const uint64_t vv = t * groups + item0;
     bool act = vv < V;
     uint32_t v = act ? static_cast<uint32_t>(vv) : 0u;
+    const uint32_t word = next_word;
+    if (MODE == kModeDelta) next_word = item_word(vv + groups);
     if (MODE == kModeDelta && act) {
       if (dense_items)
-        act = __ldg(&vflag[v]) == stamp;
+        act = word == stamp;
       else
-        v = __ldg(&vlist[v]);
+        v = word;
     }
     if (!act) v = 0u;
     const uint32_t r = v / C, c = v - r * C;
@@ -1404,6 +1415,52 @@ __device__ __forceinline__ void commit_edge(const DevGraph& g, uint32_t d, float
   }
 }
 
+// commit_edge for the committed edges of one quad of directed edges
+// 4q .. 4q + 3 (all < D) with q-vectors of QS = 4 / 8 floats: every load
+// (candidate q-vectors, the quad's endpoint ids) is issued before the first
+// store -- commit_edge one edge after another serialised a candidate round
+// trip and a target round trip per commit behind the previous commit's
+// stores.  Same stores, same values, same counts.
+template <int QS>
+__device__ __forceinline__ void commit_quad_qvec(const DevGraph& g, uint32_t q, const bool (&com)[4],
+                                                 const float (&r)[4], float* __restrict__ live,
+                                                 const float* __restrict__ cand, float* __restrict__ res, float eps,
+                                                 uint32_t* __restrict__ vflag, uint32_t stamp, bool dense,
+                                                 Contrib& c, bool (&new_flag)[4], uint32_t (&tgt)[4]) {
+  static_assert(QS % 4 == 0 && QS <= 8, "two 16-byte halves at most per q-vector");
+  constexpr int H = QS / 4;
+  const uint4 ep4 = __ldg(reinterpret_cast<const uint4*>(g.ep) + q);
+  const uint32_t tgs[4] = {ep4.y, ep4.x, ep4.w, ep4.z};  // target of d = ep[d ^ 1]
+  float4 v[4][H];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (com[k]) {
+      const float4* src = reinterpret_cast<const float4*>(cand + static_cast<size_t>(4 * q + k) * QS);
+#pragma unroll
+      for (int h = 0; h < H; ++h) v[k][h] = src[h];
+    }
+  float rv[4] = {r[0], r[1], r[2], r[3]};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (com[k]) {
+      c.delta -= (r[k] >= eps) ? 1 : 0;
+      c.frontier += 1;
+      rv[k] = 0.f;
+      float4* dst = reinterpret_cast<float4*>(live + static_cast<size_t>(4 * q + k) * QS);
+#pragma unroll
+      for (int h = 0; h < H; ++h) dst[h] = v[k][h];
+      tgt[k] = tgs[k];
+      if (dense) {
+        vflag[tgt[k]] = stamp;
+        new_flag[k] = false;
+      } else {
+        new_flag[k] = atomicMax(&vflag[tgt[k]], stamp) < stamp;
+      }
+    }
+  // res is padded to a multiple of four floats: the quad leaves as one store
+  reinterpret_cast<float4*>(res)[q] = make_float4(rv[0], rv[1], rv[2], rv[3]);
+}
+
 // select_parallelism (schedulers.cpp:218-224)
 __device__ __forceinline__ double device_p_now(const Ctl* c, double low_p, double high_p,
                                                double thr) {
@@ -1480,6 +1537,12 @@ __device__ __forceinline__ void rnbp_select_pass(const DevGraph& g, float* live,
           lv4 = reinterpret_cast<const float4*>(live)[q];
           ep4 = __ldg(reinterpret_cast<const uint4*>(g.ep) + q);
         }
+        // q-vectors (QS = 4 / 8): the quad's commits are decided first and
+        // committed together (commit_quad_qvec), so their candidate loads are
+        // one round trip instead of one per commit
+        constexpr bool kQBatch = QS == 4 || QS == 8;
+        const bool qbatch = kQBatch && prm.commit && 4 * q + 3 < g.D;
+        bool com[4] = {false, false, false, false};
         float cvs[4] = {cv4.x, cv4.y, cv4.z, cv4.w};
         float lvs[4] = {lv4.x, lv4.y, lv4.z, lv4.w};
         float rvs[4] = {rr[0], rr[1], rr[2], rr[3]};
@@ -1503,6 +1566,8 @@ __device__ __forceinline__ void rnbp_select_pass(const DevGraph& g, float* live,
                 } else {
                   nf[k] = atomicMax(&vflag[tg[k]], stamp) < stamp;
                 }
+              } else if (qbatch) {  // committed below, the quad's loads first
+                com[k] = true;
               } else if (prm.commit) {
                 commit_edge<QS>(g, d, rr[k], live, cand, res, eps, vflag, stamp, dense, c, nf[k], tg[k]);
               } else {
@@ -1518,6 +1583,10 @@ __device__ __forceinline__ void rnbp_select_pass(const DevGraph& g, float* live,
         if (any) {  // one 16-byte store per array instead of one 4-byte store per commit
           reinterpret_cast<float4*>(live)[q] = make_float4(lvs[0], lvs[1], lvs[2], lvs[3]);
           reinterpret_cast<float4*>(res)[q] = make_float4(rvs[0], rvs[1], rvs[2], rvs[3]);
+        }
+        if constexpr (kQBatch) {
+          if (com[0] || com[1] || com[2] || com[3])
+            commit_quad_qvec<QS>(g, q, com, rr, live, cand, res, eps, vflag, stamp, dense, c, nf, tg);
         }
       }
       if (prm.commit && !dense) {

@@ -79,14 +79,18 @@ struct PhiloxKeys {
 };
 
 // the draws of one edge pair (one Philox block serves both directions):
-// committed = unconverged && u53 < thresh (attempt 0, global edge id)
+// committed = unconverged && u53 < thresh (attempt 0, global edge id), with
+// u53 = X >> 11 of the 64-bit word X: u53 < thresh <=> X < thresh << 11
+// (thresh < 2^53 whenever draw is set, so the shifted bound fits), one
+// 64-bit compare per direction instead of a 64-bit shift and compare
 __device__ __forceinline__ uint32_t pair_select(uint32_t u, unsigned long long e, bool draw, const PhiloxKeys& pk,
                                                 unsigned long long it, unsigned long long thresh) {
   if (!draw) return u;
   const uint4 ph = pk.edge(it, e);
+  const unsigned long long bound = thresh << 11;
   uint32_t s = 0u;
-  if ((u & 1u) && ((((static_cast<unsigned long long>(ph.x) << 32) | ph.y) >> 11) < thresh)) s |= 1u;
-  if ((u & 2u) && ((((static_cast<unsigned long long>(ph.z) << 32) | ph.w) >> 11) < thresh)) s |= 2u;
+  if ((u & 1u) && ((static_cast<unsigned long long>(ph.x) << 32) | ph.y) < bound) s |= 1u;
+  if ((u & 2u) && ((static_cast<unsigned long long>(ph.z) << 32) | ph.w) < bound) s |= 2u;
   return s;
 }
 
