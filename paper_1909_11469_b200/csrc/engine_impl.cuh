@@ -913,14 +913,17 @@ class EngineT final : public EngineBase {
     FinArgs fa{fin, g_.D, 0};
     if constexpr (QS == 4 || QS == 8) {
       if (qlanes_refresh()) {
+        // with a candidate list the gated vertex kernel below runs the
+        // iteration's finalize (its refresh only in list mode)
+        const FinArgs fq{use_clist_ ? static_cast<int>(kFinNone) : fin, g_.D, 0};
         const unsigned grid = vgrid(k_lattice_qsweep<QS, true, kModeDelta>, static_cast<size_t>(g_.V) * (QS / 4));
         timed(kKUpdate, [&] {
           if (g_.par_mode)
             k_lattice_qsweep<QS, true, kModeDelta><<<grid, kBlock, 0, s_>>>(
-                dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_, fa);
+                dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_, fq);
           else
             k_lattice_qsweep<QS, false, kModeDelta><<<grid, kBlock, 0, s_>>>(
-                dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_, fa);
+                dg_, live(), cand(), res_.as<float>(), vlist_.as<uint32_t>(), vflag_.as<uint32_t>(), ctl(), eps_, fq);
         });
         launch_check();
         if (!use_clist_) return;  // no list mode: the lanes kernel refreshes every iteration

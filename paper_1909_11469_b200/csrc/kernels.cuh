@@ -616,7 +616,7 @@ __device__ __forceinline__ bool last_block_done(Ctl* c) {
 struct FinArgs {
   int mode;    // kFinNone: no fused finalize
   uint32_t D;  // directed edges counted by the finalize
-  int gate;    // 1: the launch runs only in RnBP list mode (k_lattice_qsweep refreshes the other iterations)
+  int gate;    // 1: the launch refreshes only in RnBP list mode (k_lattice_qsweep refreshes the other iterations)
 };
 
 __device__ __forceinline__ void fused_finalize(Ctl* c, const FinArgs& f) {
@@ -1154,8 +1154,13 @@ __global__ void __launch_bounds__(kBlock) k_vertex_update(DevGraph g, const floa
                                                           const uint32_t* vflag, Ctl* ctl, float eps,
                                                           CandList cand_list, FinArgs fin) {
   if (run_done(ctl)) return;
-  if (fin.gate && ctl->cl_state < 1u) return;
-  vertex_update_pass<QS, MODE, LIST, PINGPONG, CL>(g, A0, B0, res, vlist, vflag, ctl, eps, cand_list);
+  // gated (after k_lattice_qsweep's refresh): outside list mode the lanes
+  // kernel refreshed this iteration, so only the loop control runs here --
+  // the iteration's ONE finalize, after both launches (a finalize in the lanes
+  // kernel could enter list mode mid-iteration and make this launch refresh
+  // and finalize the same iteration a second time)
+  if (!(fin.gate && ctl->cl_state < 1u))
+    vertex_update_pass<QS, MODE, LIST, PINGPONG, CL>(g, A0, B0, res, vlist, vflag, ctl, eps, cand_list);
   fused_finalize(ctl, fin);
 }
 

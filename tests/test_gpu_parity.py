@@ -350,3 +350,22 @@ def test_large_cardinalities(bp, orc, maxq):
         o = po.run(og, oracle_config(cfg))
         assert r.converged and o.converged, kind
         assert float(np.max(np.abs(r.beliefs.values - o.beliefs))) <= BELIEF_TOL, kind
+
+
+@pytest.mark.parametrize("n,q,c,seed,low_p", [(16, 3, 1.0, 1, 0.5), (20, 8, 1.0, 2, 0.5), (24, 4, 1.5, 5, 0.7),
+                                              (40, 8, 1.0, 3, 0.3)])
+def test_potts_rnbp_run_matches_oracle(bp, orc, n, q, c, seed, low_p):
+    """RnBP on Potts lattices with q-vectors of 4 / 8 floats (the select's
+    quad commits, the lanes-over-states touched refresh): converges like the
+    reference, converged marginals within 1e-4 (north_star), and the
+    per-kernel graph loop gives the same run as the default path."""
+    g = bp.generate_potts(n, q, c, seed)
+    og = po.Graph.potts(orc, n, q, c, seed)
+    cfg = bp.SchedulerConfig(kind=bp.SchedulerKind.rnbp, low_p=low_p, max_iterations=5000, seed=seed)
+    r = bp.run(g, cfg)
+    o = po.run(og, oracle_config(cfg))
+    assert o.converged, "instance chosen to converge"
+    assert r.converged
+    assert np.max(np.abs(r.beliefs.values - o.beliefs)) <= BELIEF_TOL
+    b = bp.run_ex(g, cfg, flags=bp.RUN_NO_PERSIST)
+    assert r.trace_signature() == b.trace_signature()
