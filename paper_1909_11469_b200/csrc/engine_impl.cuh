@@ -889,6 +889,24 @@ class EngineT final : public EngineBase {
       enqueue_lbp_sweep(kFinLbp);
     } else {
       const FinArgs fa{kFinInit, g_.D};
+      if constexpr (QS == 4 || QS == 8) {
+        // q-state lattices: the initial candidates / residuals with four
+        // states per lane (the candidate list starts empty: cl_state is 0
+        // until this launch's finalize)
+        if (qlanes_refresh()) {
+          const unsigned grid = vgrid(k_lattice_qsweep<QS, true, kModeInit>, static_cast<size_t>(g_.V) * (QS / 4));
+          timed(kKUpdate, [&] {
+            if (g_.par_mode)
+              k_lattice_qsweep<QS, true, kModeInit><<<grid, kBlock, 0, s_>>>(
+                  dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, fa);
+            else
+              k_lattice_qsweep<QS, false, kModeInit><<<grid, kBlock, 0, s_>>>(
+                  dg_, live(), cand(), res_.as<float>(), nullptr, nullptr, ctl(), eps_, fa);
+          });
+          launch_check();
+          return;
+        }
+      }
       timed(kKUpdate, [&] {
         if (use_clist_)
           k_vertex_update<QS, kModeInit, false, false, true><<<vgrid(k_vertex_update<QS, kModeInit, false, false, true>, g_.V), kBlock, 0, s_>>>(

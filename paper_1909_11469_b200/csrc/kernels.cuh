@@ -1186,7 +1186,7 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
                                                            const uint32_t* vlist, const uint32_t* vflag, Ctl* ctl,
                                                            float eps, FinArgs fin) {
   static_assert(QS == 4 || QS == 8, "four states per lane: QS = 4 or 8");
-  static_assert(MODE == kModeCount || MODE == kModeDelta, "sweep or touched refresh");
+  static_assert(MODE == kModeCount || MODE == kModeDelta || MODE == kModeInit, "sweep, touched refresh or init");
   constexpr int SPL = 4, LPV = QS / SPL;  // states per lane, lanes per vertex
   if (run_done(ctl)) return;
   if (MODE == kModeDelta && ctl->cl_state >= 1u) return;  // list mode: the gated vertex kernel
@@ -1196,7 +1196,7 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
     A = B0;
     B = const_cast<float*>(A0);
   }
-  const bool dense_items = MODE == kModeCount || ctl->dense != 0u;
+  const bool dense_items = MODE != kModeDelta || ctl->dense != 0u;
   const uint32_t stamp = ctl->stamp;
   const uint32_t C = g.lat_cols, R = g.lat_rows, q = g.uniform_q;
   const int l = static_cast<int>(threadIdx.x % LPV);
@@ -1342,6 +1342,7 @@ __global__ void __launch_bounds__(kBlock) k_lattice_qsweep(DevGraph g, const flo
             cnt += (rr >= eps ? 1 : 0) - (was[k] ? 1 : 0);
             res[out] = rr;
           } else {
+            if (MODE == kModeInit) res[out] = rr;
             cnt += rr >= eps;
           }
           ++evals;
@@ -1376,9 +1377,9 @@ __global__ void k_init_messages(DevGraph g, float* M, Ctl* ctl, int set_t0) {
     if (QS == 1) {
       M[i] = 0.f;
     } else {
-      const uint32_t d = static_cast<uint32_t>(i / QS);
       const uint32_t x = static_cast<uint32_t>(i % QS);
-      const uint32_t q = g.card[g.ep[d ^ 1u]];
+      // uniform cardinality: no per-message lookup of the target's q
+      const uint32_t q = g.uniform_q ? g.uniform_q : g.card[g.ep[static_cast<uint32_t>(i / QS) ^ 1u]];
       M[i] = x < q ? -log2f(static_cast<float>(q)) : 0.f;  // base-2 log-probabilities
     }
   }
