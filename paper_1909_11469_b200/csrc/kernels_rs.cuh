@@ -483,8 +483,18 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
       // B: build the ready splashes (build_splash, schedulers.cpp:136-167); clear the balls
       const uint32_t nr = __ldcg(&rc->nready);
       if (wl) {
-        // one warp per ready root: the lanes scan a vertex's CSR neighbours and
-        // claim in lane (= CSR) order, so the visit order is build_splash's
+        // one warp per ready root, level by level: the lanes flatten the
+        // (frontier vertex, CSR neighbour) pairs of a BFS level in queue x CSR
+        // order and claim the first occurrence of every unclaimed neighbour in
+        // that order -- build_splash's visit order, with a handful of dependent
+        // round trips per LEVEL instead of per queued vertex (the walk one
+        // vertex at a time was the round's critical path: ~5 round trips per
+        // ball vertex).  A level wider than the warp's SMEM frontier finishes
+        // with the vertex-by-vertex walk from the level's first vertex.
+        constexpr uint32_t kFront = 64;
+        __shared__ uint32_t s_front[kRsBlock / 32][2][kFront];
+        const uint32_t wib = threadIdx.x >> 5;
+        const unsigned lt_mask = (1u << lane) - 1u;
         for (uint32_t i = gw; i < nr; i += nw) {
           const uint32_t r = __ldcg(&b.rlist[i]);
           if (lane == 0) {
@@ -492,10 +502,78 @@ __global__ void __launch_bounds__(kRsBlock) k_rs_iteration(DevGraph g, float* li
             b.spos[r] = 0;
             b.depth[r] = 0;
             b.qnext[r] = kUncl;
+            s_front[wib][0][0] = r;
           }
           __syncwarp();
-          uint32_t tail = r, n = 1;
-          for (uint32_t v = r; v != kUncl;) {
+          uint32_t tail = r, n = 1, nf = 1, cur = 0, dlev = 0, seq_from = kUncl;
+          while (nf && dlev < h) {
+            uint32_t nn = 0, head = kUncl;
+            for (uint32_t f0 = 0; f0 < nf; f0 += 32) {
+              const uint32_t fi = f0 + lane;
+              uint32_t a0 = 0, deg = 0;
+              if (fi < nf) {
+                const uint32_t v = s_front[wib][cur][fi];
+                a0 = g.in_off[v];
+                deg = g.in_off[v + 1] - a0;
+              }
+              uint32_t incl = deg;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (static_cast<int>(lane) >= o) incl += t;
+              }
+              const uint32_t total = __shfl_sync(0xffffffffu, incl, 31), excl = incl - deg;
+              for (uint32_t p0 = 0; p0 < total; p0 += 32) {
+                const uint32_t p = p0 + lane;
+                // owner = the last lane whose exclusive prefix is <= p
+                uint32_t lo = 0;
+#pragma unroll
+                for (uint32_t step = 16; step > 0; step >>= 1) {
+                  const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + step);
+                  if (ex <= p) lo += step;
+                }
+                const uint32_t a0o = __shfl_sync(0xffffffffu, a0, lo), exo = __shfl_sync(0xffffffffu, excl, lo);
+                uint32_t w = kUncl;
+                bool cand = false;
+                if (p < total) {
+                  w = g.ep[g.in_adj[a0o + (p - exo)]];
+                  cand = __ldcg(&b.claimed[w]) == kUncl && vown(w);
+                }
+                // two frontier vertices can share a neighbour: the first pair wins
+                const unsigned cm = __ballot_sync(0xffffffffu, cand);
+                const unsigned same = __match_any_sync(0xffffffffu, w) & cm;
+                const bool win = cand && lane == static_cast<uint32_t>(__ffs(same) - 1);
+                const unsigned m = __ballot_sync(0xffffffffu, win);
+                if (m) {
+                  const unsigned below = m & lt_mask;
+                  const int prev_lane = below ? 31 - __clz(below) : 0;
+                  const uint32_t wp = __shfl_sync(0xffffffffu, w, prev_lane);
+                  if (win) {
+                    b.claimed[w] = r;
+                    b.depth[w] = dlev + 1;
+                    b.spos[w] = n + __popc(below);
+                    b.qnext[w] = kUncl;
+                    b.qnext[below ? wp : tail] = w;
+                    const uint32_t pos = nn + __popc(below);
+                    if (pos < kFront) s_front[wib][cur ^ 1u][pos] = w;
+                  }
+                  if (head == kUncl) head = __shfl_sync(0xffffffffu, w, __ffs(m) - 1);
+                  tail = __shfl_sync(0xffffffffu, w, 31 - __clz(m));
+                  n += __popc(m);
+                  nn += __popc(m);
+                }
+                __syncwarp();
+              }
+            }
+            ++dlev;
+            cur ^= 1u;
+            nf = nn;
+            if (nn > kFront) {  // too wide for the SMEM frontier: walk on from the level's first vertex
+              seq_from = head;
+              break;
+            }
+          }
+          for (uint32_t v = seq_from; v != kUncl;) {
             const uint32_t dv = b.depth[v];
             if (dv < h) {
               const uint32_t a0 = g.in_off[v], a1 = g.in_off[v + 1];
