@@ -189,14 +189,19 @@ __device__ __forceinline__ bool run_done(Ctl* c) {
 // finalize: one block reduces the slots and restates the loop control of
 // run() (schedulers.cpp:301-347).
 
+// (t0_ns: the run's start, Ctl::t0_ns, passed in by callers that hold it in a register)
 __device__ __forceinline__ void fin_record(Ctl* c, unsigned long long it, unsigned long long fs,
-                                           unsigned un) {
+                                           unsigned un, unsigned long long t0_ns) {
   TraceRec& r = c->trace[it % kTraceRing];
   r.iteration = it;
   r.frontier_size = fs;
   r.unconverged = un;
-  r.elapsed_seconds = 1e-9 * static_cast<double>(globaltimer_ns() - c->t0_ns);
+  r.elapsed_seconds = 1e-9 * static_cast<double>(globaltimer_ns() - t0_ns);
   c->trace_len = it + 1;
+}
+__device__ __forceinline__ void fin_record(Ctl* c, unsigned long long it, unsigned long long fs,
+                                           unsigned un) {
+  fin_record(c, it, fs, un, c->t0_ns);
 }
 
 // The loop-control fields of Ctl the finalize touches, loaded into registers

@@ -120,6 +120,11 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
   const unsigned long long th_low = static_cast<unsigned long long>(ceil(ldexp(prm.low_p, 53)));
   const unsigned long long th_high = static_cast<unsigned long long>(ceil(ldexp(prm.high_p, 53)));
   unsigned long long msgs = ctl->msgs_total;
+  // the bookkeeping thread's per-launch constants and running sums, kept in
+  // registers (written back when the launch returns): no Ctl round trip on
+  // its path between the barriers
+  const unsigned long long t0_ns = lead ? ctl->t0_ns : 0ull, tlim_ns = lead ? ctl->time_limit_ns : 0ull;
+  unsigned long long evals_sum = 0ull, visits_sum = 0ull, bytes_sum = 0ull;
   // reduction buffers indexed by iteration: pacc3[it % 3]
   unsigned long long* pacc3 = ctl->pacc3[0];
   if (lead) {
@@ -135,11 +140,15 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
   // phase clock of CTA 0, the CTA that holds the most list work (profiling
   // aid, one timer read per phase)
   const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
+  // (accumulated in registers and written once when the launch returns: a
+  // read-modify-write of Ctl per phase put a dependent global round trip on
+  // CTA 0's critical path eight times per iteration)
   unsigned long long tclk = clk ? globaltimer_ns() : 0ull;
+  unsigned long long ph[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
   auto mark = [&](int k) {
     if (clk) {
       const unsigned long long t = globaltimer_ns();
-      ctl->phase_ns[k] += t - tclk;
+      ph[k] += t - tclk;
       tclk = t;
     }
   };
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
       mark(5);
       pacc_push(s_pacc, acc);
       mark(6);
-      if (lead && globaltimer_ns() - ctl->t0_ns >= ctl->time_limit_ns) ctl->time_stop = 1u;
+      if (lead && globaltimer_ns() - t0_ns >= tlim_ns) ctl->time_stop = 1u;
     }
     mark(2);
     sync_all();
@@ -306,10 +315,10 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     const bool numeric = ctl->numeric_error != 0u;
     const bool tstop = ctl->time_stop != 0u;
     if (lead) {
-      fin_record(ctl, it, frontier, unc);
-      ctl->evals_total += acc[4];
-      ctl->vertex_visits += acc[5];
-      ctl->persist_bytes += acc[1];
+      fin_record(ctl, it, frontier, unc, t0_ns);
+      evals_sum += acc[4];
+      visits_sum += acc[5];
+      bytes_sum += acc[1];
       ctl->survivors = acc[3];
     }
     it += 1;
@@ -337,7 +346,13 @@ __global__ void __launch_bounds__(kPersistBlock) k_rnbp_persist(DevGraph g, floa
     list_n = next_n;
     const bool switch_mode = CLUSTER ? next_n > 2u * kPersistClusterList : next_n < kPersistClusterList / 2u;
     if (done || switch_mode) {
+      if (clk)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ctl->phase_ns[k] += ph[k];
       if (lead) {  // mirror the loop state for the host
+        ctl->evals_total += evals_sum;
+        ctl->vertex_visits += visits_sum;
+        ctl->persist_bytes += bytes_sum;
         ctl->iteration = it;
         ctl->unconverged = unc;
         ctl->prev_unconverged = prev;
